@@ -1,0 +1,381 @@
+"""Benchmark: causal linear-attention fwd+bwd (f(x) = a + b*x) on B200.
+
+Default workload = BASELINE.json configs[1], the north star:
+B=4 H=16 N=65536 D=128, bf16, causal, a=b=1, one fwd+bwd per step.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Our arm: inputs resident in HBM (each input tensor is 1.07 GB, far above the
+126 MB L2, so no flush is needed between steps); K steps timed with CUDA events
+on the launching stream between barriers; max over ranks. N>1 ranks each run
+their own batch x head shard (weak scaling, no collective on the data path).
+`e2e` repeats the step through the host-buffer C-ABI (la_host_forward /
+la_host_backward: pinned host -> HBM -> host every step). `cpu_baseline` and
+`--impl reference` time the reference's own CPU path (oracle/_ref, compiled from
+the reference sources; else the oracle port) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "causal LA fwd+bwd tokens/s at N=64K D=128"
+UNIT = "tokens/s"
+CFG = dict(batch=4, heads=16, seq_len=65536, dim=128, dtype="bf16", causal=True, a=1.0, b=1.0)
+# CPU sample for the reference arm / cpu_baseline: 8 heads x 16384 rows of the same
+# shape family (f32 fast path, as the reference bench times it, bench.cpp:111-191).
+CPU_SAMPLE = dict(groups=8, seq_len=16384, dim=128)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- CPU arms
+def cpu_inputs(seed=0):
+    import numpy as np
+    G, N, D = CPU_SAMPLE["groups"], CPU_SAMPLE["seq_len"], CPU_SAMPLE["dim"]
+    rng = np.random.default_rng(seed)
+    q = rng.uniform(-1, 1, (G, N, D)).astype(np.float32)
+    k = rng.uniform(-1, 1, (G, N, D)).astype(np.float32)
+    q /= np.linalg.norm(q, axis=2, keepdims=True)
+    k /= np.linalg.norm(k, axis=2, keepdims=True)
+    # canonical reference layouts: q,k SequenceMajor; v, omega FeatureMajor ([g][j][i])
+    v = rng.uniform(-1, 1, (G, D, N)).astype(np.float32)
+    w = rng.uniform(-1, 1, (G, D, N)).astype(np.float32)
+    return q, k, v, w
+
+
+def cpu_runner():
+    """(kind, fn) timing one fwd+bwd of the CPU sample with all host threads."""
+    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    q, k, v, w = cpu_inputs()
+    shp = lambda x: x.reshape(CPU_SAMPLE["groups"], CPU_SAMPLE["seq_len"], CPU_SAMPLE["dim"])
+    if O.ref_lib() is not None:
+        def fn():
+            O.ref_fwd_bwd_f32(q, k, shp(v), shp(w), workers=cores)
+        return "reference", cores, fn
+    def fn():
+        O.fwd_bwd_f32_threads(q, k, shp(v), shp(w), threads=cores)
+    return "port", min(cores, CPU_SAMPLE["groups"]), fn
+
+
+def cpu_sample_desc(kind):
+    s = CPU_SAMPLE
+    src = ("reference la_core detail::run_forward<float> + run_backward<float> (oracle/_ref, built from "
+           "/root/reference/proj/src)" if kind == "reference" else "oracle/oracle.c f32 port")
+    return (f"{src}; {s['groups']} heads x N={s['seq_len']} x D={s['dim']} f32 causal, U(-1,1) with "
+            f"row-normalised q,k; tokens/s scaled to the config as (heads_sample*N_sample/H)/t, "
+            f"valid because cost is linear in N and in heads (acceptance.cpp:118)")
+
+
+def cpu_tokens_per_s(t):
+    return CPU_SAMPLE["groups"] * CPU_SAMPLE["seq_len"] / CFG["heads"] / t
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    kind, cores, fn = cpu_runner()
+    for _ in range(args.warmup):
+        fn()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        fn()
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    val = cpu_tokens_per_s(t)
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3 * (
+                CFG["batch"] * CFG["seq_len"]) / (CPU_SAMPLE["groups"] * CPU_SAMPLE["seq_len"] / CFG["heads"]),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "causal LA fwd+bwd B=4 H=16 N=65536 D=128 (reference CPU path, sampled)",
+                       "global_batch": CFG["batch"], "seq_len": CFG["seq_len"], "parallelism": "cpu"},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": cpu_sample_desc(kind)},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+ALG_BYTES = {  # algorithmic bytes per processed row (D, element bytes e), SURVEY §8(d)
+    "fwd": lambda D, e: 4 * D * e + 4,
+    "bwd": lambda D, e: 8 * D * e + 4,
+}
+
+
+def kernel_bytes(name, rows, D, e):
+    """Algorithmic bytes one launch of `name` must move (reads + writes of its own tensors)."""
+    table = {
+        "la_fwd_causal": 4 * D * e + 4, "la_bwd_causal": 8 * D * e + 4,
+        "k_fwd_rows": 4 * D * e + 4, "k_bwd_rows_dq": 4 * D * e + 8, "k_bwd_rows_dk": 4 * D * e + 8,
+        "k_bwd_rows_dv": 4 * D * e + 4, "k_seg_sums": 2 * D * e, "k_row_s": 2 * D * e + 8,
+    }
+    for key, per_row in table.items():
+        if name.startswith(key):
+            return per_row * rows
+    return None
+
+
+def run_our_arm(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2510_21956_b200 as la  # noqa: F401  (loads the CUDA library)
+    from paper_2510_21956_b200 import _abi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L = _abi.lib()
+    B, H, N, D = CFG["batch"], CFG["heads"], CFG["seq_len"], CFG["dim"]
+    G = B * H
+    e = 2
+    p = _abi.make_problem(G, N, D, CFG["dtype"], CFG["a"], CFG["b"], CFG["causal"], impl=args.kernel)
+
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+
+    def unit_rows(shape):
+        x = torch.rand(shape, device=dev, generator=gen, dtype=torch.float32) * 2 - 1
+        return (x / x.norm(dim=-1, keepdim=True)).to(torch.bfloat16)
+
+    def uni(shape):
+        return (torch.rand(shape, device=dev, generator=gen, dtype=torch.float32) * 2 - 1).to(torch.bfloat16)
+
+    q = unit_rows((G, N, D))       # SequenceMajor
+    k = unit_rows((G, N, D))       # SequenceMajor
+    v = uni((G, D, N))             # FeatureMajor
+    w = uni((G, D, N))             # FeatureMajor (cotangent dO)
+    out = torch.empty((G, D, N), device=dev, dtype=torch.bfloat16)
+    g = torch.empty((G, N), device=dev, dtype=torch.float32)
+    dq = torch.empty((G, N, D), device=dev, dtype=torch.bfloat16)
+    dk = torch.empty((G, D, N), device=dev, dtype=torch.bfloat16)
+    dv = torch.empty((G, D, N), device=dev, dtype=torch.bfloat16)
+    wsf = torch.empty(L.la_forward_workspace_bytes(C.byref(p)), device=dev, dtype=torch.uint8)
+    wsb = torch.empty(L.la_backward_workspace_bytes(C.byref(p)), device=dev, dtype=torch.uint8)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    FMj, SMj = 0, 1
+
+    def step():
+        st = L.la_forward(C.byref(p), q.data_ptr(), SMj, k.data_ptr(), SMj, v.data_ptr(), FMj,
+                          out.data_ptr(), g.data_ptr(), wsf.data_ptr(), wsf.numel(), sp, None)
+        assert st == 0, _abi.STATUS_NAMES[st]
+        st = L.la_backward(C.byref(p), q.data_ptr(), SMj, k.data_ptr(), SMj, v.data_ptr(), FMj,
+                           out.data_ptr(), w.data_ptr(), FMj, g.data_ptr(), dq.data_ptr(), dk.data_ptr(),
+                           dv.data_ptr(), wsb.data_ptr(), wsb.numel(), sp, None)
+        assert st == 0, _abi.STATUS_NAMES[st]
+
+    for _ in range(args.warmup):
+        step()
+    err = _abi.ErrorInfo()
+    st = L.la_query_status(wsf.data_ptr(), sp, C.byref(err))
+    assert st == 0, f"forward status {_abi.STATUS_NAMES[st]}: {err.message}"
+    torch.cuda.synchronize()
+
+    # ---- timed region
+    L.la_profile_enable(1)
+    _abi.profile_read()
+    launches0 = L.la_launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = L.la_launch_count() - launches0
+    L.la_profile_enable(0)
+    prof = _abi.profile_read()
+    ms = t0.elapsed_time(t1) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    tokens_step = B * N * world
+    value = tokens_step / (ms / 1e3)
+
+    # ---- per-kernel roofline from the in-region events
+    hbm, tf, src = peaks()
+    per = {}
+    for r in prof:
+        per.setdefault(r["name"], []).append(r["ms"])
+    kstats = {n: {"ms": sum(v_) / len(v_), "launches_per_step": len(v_) / args.steps,
+                  "share": sum(v_) / args.steps / ms} for n, v_ in per.items()}
+    top = max(kstats, key=lambda n: kstats[n]["ms"] * kstats[n]["launches_per_step"]) if kstats else None
+    roof = None
+    if top:
+        rows = G * N
+        alg = kernel_bytes(top, rows, D, e)
+        kms = kstats[top]["ms"]
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            traffic = json.load(open(tpath)).get(top)
+        if alg:
+            ach = alg / (kms / 1e3) / 1e9
+            roof = {"bound": "hbm", "kernel": top, "achieved": ach, "peak": hbm, "unit": "GB/s",
+                    "frac": ach / hbm, "traffic": traffic, "peak_source": src,
+                    "alg_bytes_per_launch": alg, "kernel_ms": kms}
+    step_bytes = G * N * (ALG_BYTES["fwd"](D, e) + ALG_BYTES["bwd"](D, e))
+    step_gbs = step_bytes / (ms / 1e3) / 1e9
+    flops = G * N * 14 * D * D
+    clocks = clk.summary()
+
+    # ---- e2e through the host-buffer C-ABI (pinned host memory, copies every step)
+    e2e = None
+    if not args.no_e2e:
+        pin = dict(device="cpu", dtype=torch.bfloat16, pin_memory=True)
+        hq, hk, hv, hw = (x.cpu().pin_memory() for x in (q, k, v, w))
+        hout, hdq, hdk, hdv = (torch.empty(x.shape, **pin) for x in (out, dq, dk, dv))
+        hg = torch.empty((G, N), dtype=torch.float32, pin_memory=True)
+
+        def e2e_step():
+            st = L.la_host_forward(C.byref(p), hq.data_ptr(), SMj, hk.data_ptr(), SMj, hv.data_ptr(), FMj,
+                                   hout.data_ptr(), hg.data_ptr(), C.byref(err))
+            assert st == 0, err.message
+            st = L.la_host_backward(C.byref(p), hq.data_ptr(), SMj, hk.data_ptr(), SMj, hv.data_ptr(), FMj,
+                                    hout.data_ptr(), hw.data_ptr(), FMj, hg.data_ptr(), hdq.data_ptr(),
+                                    hdk.data_ptr(), hdv.data_ptr(), C.byref(err))
+            assert st == 0, err.message
+
+        e2e_step()
+        if world > 1:
+            dist.barrier()
+        te = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        et = (time.perf_counter() - te) / args.e2e_steps
+        if world > 1:
+            tt = torch.tensor([et], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            et = float(tt.item())
+        T = G * N * D * e
+        e2e = {"value": tokens_step / et, "unit": UNIT, "h2d_bytes_per_step": 8 * T + 4 * G * N,
+               "d2h_bytes_per_step": 4 * T + 4 * G * N, "ms_per_step": et * 1e3,
+               "api": "la_host_forward + la_host_backward (pinned host buffers)"}
+        L.la_host_release()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        kind, cores, fn = cpu_runner()
+        fn()
+        ts = []
+        for _ in range(3):
+            t_ = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t_)
+        cpu = {"value": cpu_tokens_per_s(statistics.median(ts)), "unit": UNIT, "cores": cores,
+               "kind": kind, "sample": cpu_sample_desc(kind)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (U(-1,1), unit-norm q/k rows)",
+                "config": {"workload": "causal LA fwd+bwd B=4 H=16 N=65536 D=128 bf16 a=b=1 per GPU "
+                                       "(BASELINE configs[1])",
+                           "global_batch": B * world, "seq_len": N, "heads": H, "dim": D,
+                           "parallelism": f"batch_head{world}", "l2": "inputs 1.07 GB each >> 126 MB L2; no flush",
+                           "kernel_impl": args.kernel},
+                "roofline": roof,
+                "step_roofline": {"alg_bytes": step_bytes, "achieved_gbs": step_gbs, "frac_hbm": step_gbs / hbm,
+                                  "alg_tflops": flops / (ms / 1e3) / 1e12,
+                                  "frac_bf16": flops / (ms / 1e3) / 1e12 / tf},
+                "kernels": kstats, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "tcgen05"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_our_arm(args)
+
+
+if __name__ == "__main__":
+    main()

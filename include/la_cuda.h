@@ -1,0 +1,178 @@
+/*
+ * la_cuda.h — C-ABI of the B200 (sm_100a) linear-attention library.
+ *
+ * Drop-in for the reference library's forward/backward path
+ * (/root/reference/proj/include/la/forward.hpp, backward.hpp): same entry
+ * points, same (G = B*H, N, D) tensors and FeatureMajor/SequenceMajor layouts,
+ * same coefficients f(x) = a + b*x, same BlockPlan validation, same error
+ * taxonomy (error.hpp:10-75) as status codes. Plain pointers and sizes only.
+ *
+ * Entry point                      replaces (reference file:line)
+ * -------------------------------  ---------------------------------------------
+ * la_forward(causal=1)             la::forward_causal   src/forward.cpp:133-137
+ * la_forward(causal=0)             la::forward_full     src/forward.cpp:139-142
+ * la_backward(causal=1)            la::backward_causal  src/backward.cpp:93-96
+ * la_backward(causal=0)            la::backward_full    src/backward.cpp:98-101
+ * la_host_forward / _backward      the same, over host buffers (copies in/out)
+ * la_forward_shard_state           (new) per-shard (S,z,sigma,count) totals for
+ * la_backward_shard_state          (new) sequence sharding, exchanged by the
+ *                                  caller over NCCL, fed back as carry-in/out
+ * la_validate_plan                 la::validate_plan    src/plan.cpp:49-62
+ * la_default_plan                  la::default_plan     src/plan.cpp:24-47
+ *
+ * Device buffers are caller-owned. Calls are stream-ordered; argument errors
+ * return synchronously. The degenerate-denominator check (forward_kernels.hpp:53)
+ * runs on the device: when `err` is non-NULL the call synchronises its stream and
+ * reports the lexicographically first (group, position), like the reference's
+ * first-item rethrow (pool.hpp:36-42); with err == NULL it stays asynchronous and
+ * la_query_status() reads the flag later.
+ */
+#ifndef LA_CUDA_H
+#define LA_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LA_OK = 0,
+  LA_ERR_INVALID_SHAPE = 1,          /* la::InvalidShape */
+  LA_ERR_SHAPE_MISMATCH = 2,         /* la::ShapeMismatch */
+  LA_ERR_INVALID_ARGUMENT = 3,       /* la::InvalidArgument */
+  LA_ERR_INVALID_PLAN = 4,           /* la::InvalidPlan */
+  LA_ERR_MISSING_FORWARD_STATE = 5,  /* la::MissingForwardState */
+  LA_ERR_DEGENERATE_DENOMINATOR = 6, /* la::DegenerateDenominator(group, position) */
+  LA_ERR_CUDA = 7,                   /* CUDA runtime failure */
+  LA_ERR_UNSUPPORTED = 8,            /* dtype/shape the device path does not provide */
+  LA_ERR_WORKSPACE = 9               /* workspace too small or misaligned */
+} la_status;
+
+typedef enum { LA_FEATURE_MAJOR = 0, LA_SEQUENCE_MAJOR = 1 } la_layout; /* tensor.hpp:15 */
+typedef enum { LA_F32 = 0, LA_BF16 = 1, LA_F16 = 2 } la_dtype;
+
+typedef enum { /* fault.hpp:7-15 */
+  LA_FAULT_NONE = 0,
+  LA_FAULT_FLIP_BETA_K_SIGN = 1,
+  LA_FAULT_CAUSAL_PREFIX_OFF_BY_ONE = 2,
+  LA_FAULT_DROP_GRAD_V_CONSTANT_TERM = 3
+} la_fault;
+
+typedef enum { /* device path selection; AUTO picks tcgen05 when the shape allows */
+  LA_IMPL_AUTO = 0,
+  LA_IMPL_SIMT = 1,   /* CUDA-core fp32 path: every dtype/D, exact sweep order */
+  LA_IMPL_TCGEN05 = 2 /* sm_100a tensor-core chunked path (bf16/fp16) */
+} la_impl;
+
+typedef struct { /* la::BlockPlan, plan.hpp:15-21 */
+  int64_t groups;
+  int64_t reduction_blocks; /* L; must divide lanes. Advisory on the GPU. */
+  int64_t lanes;            /* must equal D */
+  int32_t workers;          /* must be >= 1. Advisory on the GPU. */
+  int32_t deterministic;
+} la_block_plan;
+
+typedef struct {
+  int64_t groups; /* G = batch * heads */
+  int64_t seq_len;
+  int64_t dim;
+  la_dtype dtype;
+  double a, b; /* la::LinearKernelCoeffs, tensor.hpp:30-35 */
+  int32_t causal;
+  la_fault fault;
+  la_impl impl;
+  la_block_plan plan;
+} la_problem;
+
+typedef struct {
+  la_status code;
+  int64_t group;    /* DegenerateDenominator::group() */
+  int64_t position; /* DegenerateDenominator::position() */
+  char message[256];
+} la_error_info;
+
+/* Per-shard carry for sequence sharding (row range [row_offset, row_offset + N)
+ * of a longer sequence). Each pointer is a device array of G * (D*D + 2*D + 1)
+ * fp32 values in the layout documented in DESIGN.md; NULL means "no carry". */
+typedef struct {
+  int64_t row_offset;      /* global index of this shard's first row */
+  const float* carry_in;   /* forward: exclusive prefix (S, z, sigma, count) */
+  const float* carry_suffix; /* backward: exclusive suffix (R, u, c) */
+} la_shard;
+
+/* ---------------------------------------------------------------- queries */
+const char* la_version(void);
+const char* la_status_name(la_status s);
+size_t la_forward_workspace_bytes(const la_problem* p);
+size_t la_backward_workspace_bytes(const la_problem* p);
+size_t la_shard_state_floats(const la_problem* p); /* G * (D*D + 2*D + 1) */
+la_status la_validate_plan(const la_block_plan* plan, int64_t groups, int64_t dim,
+                           la_error_info* err);
+la_status la_default_plan(int64_t groups, int64_t dim, int32_t workers, la_block_plan* out);
+/* Kernel launches issued by this library since load (for bench accounting). */
+uint64_t la_launch_count(void);
+/* Per-kernel device timing: while enabled, every kernel this library launches
+ * is bracketed by CUDA events on its stream. la_profile_read synchronises and
+ * writes a JSON array [{"name": ..., "ms": ...}, ...] of the launches since the
+ * last read, then clears the list. Returns the number of records. */
+void la_profile_enable(int32_t on);
+int32_t la_profile_read(char* json, size_t cap);
+
+/* ---------------------------------------------------------------- device API */
+la_status la_forward(const la_problem* p, const void* q, la_layout lq, const void* k, la_layout lk,
+                     const void* v, la_layout lv, void* out /* FeatureMajor */,
+                     float* g /* G*N */, void* workspace, size_t ws_bytes, void* stream,
+                     la_error_info* err);
+
+la_status la_backward(const la_problem* p, const void* q, la_layout lq, const void* k,
+                      la_layout lk, const void* v, la_layout lv, const void* o /* FeatureMajor */,
+                      const void* omega, la_layout lw, const float* g,
+                      void* dq /* SequenceMajor */, void* dk /* FeatureMajor */,
+                      void* dv /* FeatureMajor */, void* workspace, size_t ws_bytes,
+                      void* stream, la_error_info* err);
+
+/* Sequence-sharded variants: same as above on one shard, with carries. */
+la_status la_forward_sharded(const la_problem* p, const la_shard* shard, const void* q,
+                             la_layout lq, const void* k, la_layout lk, const void* v,
+                             la_layout lv, void* out, float* g, void* workspace, size_t ws_bytes,
+                             void* stream, la_error_info* err);
+la_status la_backward_sharded(const la_problem* p, const la_shard* shard, const void* q,
+                              la_layout lq, const void* k, la_layout lk, const void* v,
+                              la_layout lv, const void* o, const void* omega, la_layout lw,
+                              const float* g, void* dq, void* dk, void* dv, void* workspace,
+                              size_t ws_bytes, void* stream, la_error_info* err);
+/* Shard totals to exchange: forward (S=sum k^T v, z=sum k, sigma=sum v, count);
+ * backward (R=sum q^T w_hat, u=sum s q, c=sum w_hat). Written to `state_out`
+ * (la_shard_state_floats(p) fp32 values, device). */
+la_status la_forward_shard_state(const la_problem* p, const void* k, la_layout lk, const void* v,
+                                 la_layout lv, float* state_out, void* stream);
+la_status la_backward_shard_state(const la_problem* p, const void* q, la_layout lq,
+                                  const void* o, const void* omega, la_layout lw, const float* g,
+                                  float* state_out, void* stream);
+/* Exclusive prefix (forward) / suffix (backward) of `nshards` gathered shard
+ * states for shard `rank`, in fp32 on the device: the local step of the
+ * NCCL all-gather scan. */
+la_status la_combine_shard_states(const la_problem* p, const float* gathered, int32_t nshards,
+                                  int32_t rank, int32_t suffix, float* carry_out, void* stream);
+
+la_status la_query_status(const void* workspace, void* stream, la_error_info* err);
+
+/* ---------------------------------------------------------------- host API */
+/* End-to-end over host buffers: copies inputs to the device, runs, copies the
+ * results back (device arena cached per thread). Used by the reference-facing
+ * shim and the e2e bench. */
+la_status la_host_forward(const la_problem* p, const void* q, la_layout lq, const void* k,
+                          la_layout lk, const void* v, la_layout lv, void* out, float* g,
+                          la_error_info* err);
+la_status la_host_backward(const la_problem* p, const void* q, la_layout lq, const void* k,
+                           la_layout lk, const void* v, la_layout lv, const void* o,
+                           const void* omega, la_layout lw, const float* g, void* dq, void* dk,
+                           void* dv, la_error_info* err);
+void la_host_release(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LA_CUDA_H */

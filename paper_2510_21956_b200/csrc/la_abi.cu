@@ -1,0 +1,500 @@
+// C-ABI layer (include/la_cuda.h): argument validation with the reference's
+// error taxonomy, path selection, workspace carving, the device-side
+// degenerate-denominator report, and the host-buffer entry points.
+#include <atomic>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/la_cuda.h"
+#include "internal.h"
+
+#include <string>
+#include <vector>
+
+namespace lab {
+static std::atomic<uint64_t> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+struct ProfRec {
+  std::string name;
+  cudaEvent_t a, b;
+};
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof;
+
+ProfScope::ProfScope(const char* name, cudaStream_t s) : idx(-1), stream(s) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (!g_prof_on) return;
+  ProfRec r;
+  r.name = name;
+  cudaEventCreate(&r.a);
+  cudaEventCreate(&r.b);
+  cudaEventRecord(r.a, s);
+  g_prof.push_back(r);
+  idx = (int)g_prof.size() - 1;
+}
+ProfScope::~ProfScope() {
+  if (idx < 0) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (idx < (int)g_prof.size()) cudaEventRecord(g_prof[idx].b, stream);
+}
+}  // namespace lab
+
+using namespace lab;
+
+namespace {
+
+constexpr size_t kFlagBytes = 256;
+
+la_status fail(la_error_info* err, la_status code, const char* msg, int64_t grp = -1,
+               int64_t pos = -1) {
+  if (err) {
+    err->code = code;
+    err->group = grp;
+    err->position = pos;
+    std::snprintf(err->message, sizeof(err->message), "%s", msg);
+  }
+  return code;
+}
+
+la_status ok(la_error_info* err) {
+  if (err) {
+    err->code = LA_OK;
+    err->group = err->position = -1;
+    err->message[0] = 0;
+  }
+  return LA_OK;
+}
+
+la_status cuda_fail(la_error_info* err, cudaError_t e) {
+  char buf[200];
+  std::snprintf(buf, sizeof(buf), "CUDA error: %s", cudaGetErrorString(e));
+  return fail(err, LA_ERR_CUDA, buf);
+}
+
+// check_forward_inputs (forward.cpp:13-25) + validate_plan (plan.cpp:49-62).
+la_status check_problem(const la_problem* p, la_error_info* err) {
+  if (!p) return fail(err, LA_ERR_INVALID_ARGUMENT, "null problem");
+  if (p->groups <= 0 || p->seq_len <= 0 || p->dim <= 0)
+    return fail(err, LA_ERR_INVALID_SHAPE, "forward requires non-empty Q, K, V");
+  if (p->a == 0.0 && p->b == 0.0)
+    return fail(err, LA_ERR_INVALID_ARGUMENT, "kernel coefficients (a, b) must not both be zero");
+  la_status s = la_validate_plan(&p->plan, p->groups, p->dim, err);
+  if (s != LA_OK) return s;
+  if (p->dtype != LA_F32 && p->dtype != LA_BF16 && p->dtype != LA_F16)
+    return fail(err, LA_ERR_INVALID_ARGUMENT, "unknown dtype");
+  if (p->dim > 256) return fail(err, LA_ERR_UNSUPPORTED, "head dimension above 256");
+  if (p->fault < LA_FAULT_NONE || p->fault > LA_FAULT_DROP_GRAD_V_CONSTANT_TERM)
+    return fail(err, LA_ERR_INVALID_ARGUMENT, "unknown fault");
+  return LA_OK;
+}
+
+bool layout_ok(int l) { return l == LA_FEATURE_MAJOR || l == LA_SEQUENCE_MAJOR; }
+
+Launch make_launch(const la_problem* p, const la_shard* sh, void* stream) {
+  Launch L;
+  L.G = p->groups;
+  L.N = p->seq_len;
+  L.D = p->dim;
+  L.dtype = p->dtype;
+  L.a = (float)p->a;
+  L.b = (float)p->b;
+  L.causal = p->causal ? 1 : 0;
+  L.fault = p->fault;
+  L.row_offset = sh ? sh->row_offset : 0;
+  L.n_total = p->seq_len;
+  L.carry_prefix = sh ? sh->carry_in : nullptr;
+  L.carry_suffix = sh ? sh->carry_suffix : nullptr;
+  L.stream = (cudaStream_t)stream;
+  return L;
+}
+
+bool use_tc(const la_problem* p, bool supported) {
+  if (p->impl == LA_IMPL_SIMT) return false;
+  return supported;
+}
+
+size_t ws_bytes_for(size_t floats) { return kFlagBytes + floats * sizeof(float); }
+
+Workspace carve(void* ws, size_t bytes) {
+  Workspace w;
+  w.flag = (unsigned long long*)ws;
+  w.base = (float*)((char*)ws + kFlagBytes);
+  w.floats = bytes > kFlagBytes ? (bytes - kFlagBytes) / sizeof(float) : 0;
+  return w;
+}
+
+la_status finish(void* ws, cudaStream_t s, la_error_info* err) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(err, e);
+  if (!err) return LA_OK;  // asynchronous mode: la_query_status later
+  return la_query_status(ws, s, err);
+}
+
+size_t fwd_floats(const la_problem* p) {
+  size_t a = simt_forward_ws_floats(p->groups, p->seq_len, p->dim, p->fault);
+  size_t b = tc_forward_ws_floats(p->groups, p->seq_len, p->dim);
+  return a > b ? a : b;
+}
+size_t bwd_floats(const la_problem* p) {
+  size_t a = simt_backward_ws_floats(p->groups, p->seq_len, p->dim, p->fault);
+  size_t b = tc_backward_ws_floats(p->groups, p->seq_len, p->dim);
+  size_t c = (size_t)(p->groups * p->seq_len);  // backward shard state scratch
+  size_t m = a > b ? a : b;
+  return m > c ? m : c;
+}
+
+la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, la_layout lq,
+                       const void* k, la_layout lk, const void* v, la_layout lv, void* out,
+                       float* g, void* ws, size_t ws_bytes, void* stream, la_error_info* err) {
+  la_status s = check_problem(p, err);
+  if (s != LA_OK) return s;
+  if (!q || !k || !v || !out || !g)
+    return fail(err, LA_ERR_INVALID_SHAPE, "forward requires non-empty Q, K, V and outputs");
+  if (!layout_ok(lq) || !layout_ok(lk) || !layout_ok(lv))
+    return fail(err, LA_ERR_INVALID_ARGUMENT, "unknown layout");
+  if (!ws || ws_bytes < la_forward_workspace_bytes(p))
+    return fail(err, LA_ERR_WORKSPACE, "workspace smaller than la_forward_workspace_bytes");
+  if (sh && !p->causal && (sh->carry_in || sh->row_offset))
+    return fail(err, LA_ERR_UNSUPPORTED, "sequence sharding is defined for the causal mask");
+  Launch L = make_launch(p, sh, stream);
+  Tensors t{q, lq, k, lk, v, lv, nullptr, 0, nullptr, 0, nullptr};
+  Workspace w = carve(ws, ws_bytes);
+  cudaMemsetAsync(w.flag, 0xFF, sizeof(unsigned long long), L.stream);
+  cudaError_t e;
+  if (use_tc(p, tc_forward_supported(L, t)))
+    e = tc_forward(L, t, out, g, w);
+  else if (p->impl == LA_IMPL_TCGEN05)
+    return fail(err, LA_ERR_UNSUPPORTED, "tcgen05 path needs bf16/fp16, D=128, canonical layouts");
+  else
+    e = simt_forward(L, t, out, g, w);
+  if (e != cudaSuccess) return cuda_fail(err, e);
+  return finish(ws, L.stream, err);
+}
+
+la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, la_layout lq,
+                        const void* k, la_layout lk, const void* v, la_layout lv, const void* o,
+                        const void* omega, la_layout lw, const float* g, void* dq, void* dk,
+                        void* dv, void* ws, size_t ws_bytes, void* stream, la_error_info* err) {
+  // check_backward_inputs (backward.cpp:13-28)
+  if (p && (!o || !q || !k || !v))
+    return fail(err, LA_ERR_MISSING_FORWARD_STATE,
+                "backward requires the forward artifacts (Q, K, V, O)");
+  if (p && !g)
+    return fail(err, LA_ERR_MISSING_FORWARD_STATE, "backward requires the retained denominator vector g");
+  if (p && !omega) return fail(err, LA_ERR_SHAPE_MISMATCH, "cotangent shape must match the forward output");
+  la_status s = check_problem(p, err);
+  if (s != LA_OK) return s;
+  if (!dq || !dk || !dv) return fail(err, LA_ERR_INVALID_SHAPE, "null gradient buffer");
+  if (!layout_ok(lq) || !layout_ok(lk) || !layout_ok(lv) || !layout_ok(lw))
+    return fail(err, LA_ERR_INVALID_ARGUMENT, "unknown layout");
+  if (!ws || ws_bytes < la_backward_workspace_bytes(p))
+    return fail(err, LA_ERR_WORKSPACE, "workspace smaller than la_backward_workspace_bytes");
+  if (sh && !p->causal && (sh->carry_in || sh->carry_suffix || sh->row_offset))
+    return fail(err, LA_ERR_UNSUPPORTED, "sequence sharding is defined for the causal mask");
+  Launch L = make_launch(p, sh, stream);
+  Tensors t{q, lq, k, lk, v, lv, o, LA_FEATURE_MAJOR, omega, lw, g};
+  Workspace w = carve(ws, ws_bytes);
+  cudaMemsetAsync(w.flag, 0xFF, sizeof(unsigned long long), L.stream);
+  cudaError_t e;
+  if (use_tc(p, tc_backward_supported(L, t)))
+    e = tc_backward(L, t, dq, dk, dv, w);
+  else if (p->impl == LA_IMPL_TCGEN05)
+    return fail(err, LA_ERR_UNSUPPORTED, "tcgen05 path needs bf16/fp16, D=128, canonical layouts");
+  else
+    e = simt_backward(L, t, dq, dk, dv, w);
+  if (e != cudaSuccess) return cuda_fail(err, e);
+  return finish(ws, L.stream, err);
+}
+
+size_t elem_bytes(la_dtype d) { return d == LA_F32 ? 4 : 2; }
+
+// Per-thread device arena for the host-buffer API.
+struct Arena {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaStream_t stream = nullptr;
+  ~Arena() { release(); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    if (stream) cudaStreamDestroy(stream);
+    ptr = nullptr;
+    bytes = 0;
+    stream = nullptr;
+  }
+  cudaError_t reserve(size_t want) {
+    if (!stream) {
+      cudaError_t e = cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return e;
+    }
+    if (want <= bytes) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&ptr, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+};
+thread_local Arena t_arena;
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+}  // namespace
+
+extern "C" {
+
+const char* la_version(void) { return "la-b200 0.1 (sm_100a)"; }
+
+const char* la_status_name(la_status s) {
+  switch (s) {
+    case LA_OK: return "ok";
+    case LA_ERR_INVALID_SHAPE: return "InvalidShape";
+    case LA_ERR_SHAPE_MISMATCH: return "ShapeMismatch";
+    case LA_ERR_INVALID_ARGUMENT: return "InvalidArgument";
+    case LA_ERR_INVALID_PLAN: return "InvalidPlan";
+    case LA_ERR_MISSING_FORWARD_STATE: return "MissingForwardState";
+    case LA_ERR_DEGENERATE_DENOMINATOR: return "DegenerateDenominator";
+    case LA_ERR_CUDA: return "CudaError";
+    case LA_ERR_UNSUPPORTED: return "Unsupported";
+    case LA_ERR_WORKSPACE: return "WorkspaceError";
+  }
+  return "unknown";
+}
+
+uint64_t la_launch_count(void) { return g_launches.load(); }
+
+void la_profile_enable(int32_t on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_on = on != 0;
+}
+
+int32_t la_profile_read(char* json, size_t cap) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  std::string out = "[";
+  for (size_t i = 0; i < g_prof.size(); ++i) {
+    float ms = -1.f;
+    cudaEventSynchronize(g_prof[i].b);
+    cudaEventElapsedTime(&ms, g_prof[i].a, g_prof[i].b);
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "%s{\"name\": \"%s\", \"ms\": %.6f}", i ? ", " : "",
+                  g_prof[i].name.c_str(), ms);
+    out += buf;
+    cudaEventDestroy(g_prof[i].a);
+    cudaEventDestroy(g_prof[i].b);
+  }
+  out += "]";
+  const int32_t n = (int32_t)g_prof.size();
+  g_prof.clear();
+  if (json && cap) {
+    std::snprintf(json, cap, "%s", out.c_str());
+  }
+  return n;
+}
+
+size_t la_shard_state_floats(const la_problem* p) {
+  return p ? (size_t)(p->groups * state_floats(p->dim)) : 0;
+}
+
+size_t la_forward_workspace_bytes(const la_problem* p) {
+  if (!p || p->groups <= 0 || p->seq_len <= 0 || p->dim <= 0) return kFlagBytes;
+  return ws_bytes_for(fwd_floats(p));
+}
+
+size_t la_backward_workspace_bytes(const la_problem* p) {
+  if (!p || p->groups <= 0 || p->seq_len <= 0 || p->dim <= 0) return kFlagBytes;
+  return ws_bytes_for(bwd_floats(p));
+}
+
+// validate_plan (plan.cpp:49-62), same order of checks and messages.
+la_status la_validate_plan(const la_block_plan* plan, int64_t groups, int64_t dim,
+                           la_error_info* err) {
+  if (!plan) return fail(err, LA_ERR_INVALID_PLAN, "null plan");
+  if (plan->groups != groups)
+    return fail(err, LA_ERR_INVALID_PLAN, "plan group count does not match the tensors");
+  if (plan->lanes != dim)
+    return fail(err, LA_ERR_INVALID_PLAN, "plan lane count does not match the head dimension");
+  if (plan->reduction_blocks < 1 || plan->lanes % plan->reduction_blocks != 0)
+    return fail(err, LA_ERR_INVALID_PLAN,
+                "reduction block count must be >= 1 and divide the head dimension");
+  if (plan->workers < 1) return fail(err, LA_ERR_INVALID_PLAN, "worker count must be >= 1");
+  return ok(err);
+}
+
+// default_plan (plan.cpp:24-47): L = largest divisor of D not above D/32.
+la_status la_default_plan(int64_t groups, int64_t dim, int32_t workers, la_block_plan* out) {
+  if (groups <= 0 || dim <= 0 || !out) return LA_ERR_INVALID_SHAPE;
+  int64_t target = dim / 32;
+  if (target < 1) target = 1;
+  int64_t l = 1;
+  for (int64_t c = target; c >= 1; --c)
+    if (dim % c == 0) {
+      l = c;
+      break;
+    }
+  out->groups = groups;
+  out->reduction_blocks = l;
+  out->lanes = dim;
+  out->workers = workers > 0 ? workers : 1;
+  out->deterministic = 1;
+  return LA_OK;
+}
+
+la_status la_query_status(const void* workspace, void* stream, la_error_info* err) {
+  unsigned long long flag = ULLONG_MAX;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(&flag, workspace, sizeof(flag), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(err, e);
+  if (flag != ULLONG_MAX) {
+    const int64_t grp = (int64_t)(flag >> 32), pos = (int64_t)(flag & 0xFFFFFFFFull);
+    char msg[160];
+    std::snprintf(msg, sizeof(msg), "degenerate attention denominator at group %lld, position %lld",
+                  (long long)grp, (long long)pos);
+    return fail(err, LA_ERR_DEGENERATE_DENOMINATOR, msg, grp, pos);
+  }
+  return ok(err);
+}
+
+la_status la_forward(const la_problem* p, const void* q, la_layout lq, const void* k, la_layout lk,
+                     const void* v, la_layout lv, void* out, float* g, void* workspace,
+                     size_t ws_bytes, void* stream, la_error_info* err) {
+  return forward_impl(p, nullptr, q, lq, k, lk, v, lv, out, g, workspace, ws_bytes, stream, err);
+}
+
+la_status la_backward(const la_problem* p, const void* q, la_layout lq, const void* k,
+                      la_layout lk, const void* v, la_layout lv, const void* o, const void* omega,
+                      la_layout lw, const float* g, void* dq, void* dk, void* dv, void* workspace,
+                      size_t ws_bytes, void* stream, la_error_info* err) {
+  return backward_impl(p, nullptr, q, lq, k, lk, v, lv, o, omega, lw, g, dq, dk, dv, workspace,
+                       ws_bytes, stream, err);
+}
+
+la_status la_forward_sharded(const la_problem* p, const la_shard* shard, const void* q,
+                             la_layout lq, const void* k, la_layout lk, const void* v,
+                             la_layout lv, void* out, float* g, void* workspace, size_t ws_bytes,
+                             void* stream, la_error_info* err) {
+  return forward_impl(p, shard, q, lq, k, lk, v, lv, out, g, workspace, ws_bytes, stream, err);
+}
+
+la_status la_backward_sharded(const la_problem* p, const la_shard* shard, const void* q,
+                              la_layout lq, const void* k, la_layout lk, const void* v,
+                              la_layout lv, const void* o, const void* omega, la_layout lw,
+                              const float* g, void* dq, void* dk, void* dv, void* workspace,
+                              size_t ws_bytes, void* stream, la_error_info* err) {
+  return backward_impl(p, shard, q, lq, k, lk, v, lv, o, omega, lw, g, dq, dk, dv, workspace,
+                       ws_bytes, stream, err);
+}
+
+la_status la_forward_shard_state(const la_problem* p, const void* k, la_layout lk, const void* v,
+                                 la_layout lv, float* state_out, void* stream) {
+  la_status s = check_problem(p, nullptr);
+  if (s != LA_OK) return s;
+  if (!k || !v || !state_out) return LA_ERR_INVALID_SHAPE;
+  Launch L = make_launch(p, nullptr, stream);
+  Tensors t{nullptr, 0, k, lk, v, lv, nullptr, 0, nullptr, 0, nullptr};
+  return simt_forward_shard_state(L, t, state_out) == cudaSuccess ? LA_OK : LA_ERR_CUDA;
+}
+
+la_status la_backward_shard_state(const la_problem* p, const void* q, la_layout lq,
+                                  const void* o, const void* omega, la_layout lw, const float* g,
+                                  float* state_out, void* stream) {
+  la_status s = check_problem(p, nullptr);
+  if (s != LA_OK) return s;
+  if (!q || !o || !omega || !g || !state_out) return LA_ERR_MISSING_FORWARD_STATE;
+  Launch L = make_launch(p, nullptr, stream);
+  Tensors t{q, lq, nullptr, 0, nullptr, 0, o, LA_FEATURE_MAJOR, omega, lw, g};
+  // scratch for s_i: G*N floats, allocated stream-ordered
+  float* scratch = nullptr;
+  if (cudaMallocAsync((void**)&scratch, sizeof(float) * p->groups * p->seq_len, L.stream) !=
+      cudaSuccess)
+    return LA_ERR_CUDA;
+  Workspace w{nullptr, scratch, (size_t)(p->groups * p->seq_len)};
+  cudaError_t e = simt_backward_shard_state(L, t, state_out, w);
+  cudaFreeAsync(scratch, L.stream);
+  return e == cudaSuccess ? LA_OK : LA_ERR_CUDA;
+}
+
+la_status la_combine_shard_states(const la_problem* p, const float* gathered, int32_t nshards,
+                                  int32_t rank, int32_t suffix, float* carry_out, void* stream) {
+  if (!p || !gathered || !carry_out || nshards < 1 || rank < 0 || rank >= nshards)
+    return LA_ERR_INVALID_ARGUMENT;
+  return combine_shard_states(p->groups, p->dim, gathered, nshards, rank, suffix, carry_out,
+                              (cudaStream_t)stream) == cudaSuccess
+             ? LA_OK
+             : LA_ERR_CUDA;
+}
+
+la_status la_host_forward(const la_problem* p, const void* q, la_layout lq, const void* k,
+                          la_layout lk, const void* v, la_layout lv, void* out, float* g,
+                          la_error_info* err) {
+  la_status s = check_problem(p, err);
+  if (s != LA_OK) return s;
+  if (!q || !k || !v || !out || !g) return fail(err, LA_ERR_INVALID_SHAPE, "null host buffer");
+  const size_t tb = (size_t)(p->groups * p->seq_len * p->dim) * elem_bytes(p->dtype);
+  const size_t gb = sizeof(float) * (size_t)(p->groups * p->seq_len);
+  const size_t wb = la_forward_workspace_bytes(p);
+  const size_t need = 4 * align256(tb) + align256(gb) + align256(wb);
+  cudaError_t e = t_arena.reserve(need);
+  if (e != cudaSuccess) return cuda_fail(err, e);
+  char* base = (char*)t_arena.ptr;
+  void* dq_ = base;
+  void* dk_ = base + align256(tb);
+  void* dv_ = base + 2 * align256(tb);
+  void* dout = base + 3 * align256(tb);
+  float* dg = (float*)(base + 4 * align256(tb));
+  void* dws = base + 4 * align256(tb) + align256(gb);
+  cudaStream_t st = t_arena.stream;
+  cudaMemcpyAsync(dq_, q, tb, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(dk_, k, tb, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(dv_, v, tb, cudaMemcpyHostToDevice, st);
+  s = la_forward(p, dq_, lq, dk_, lk, dv_, lv, dout, dg, dws, wb, st, nullptr);
+  if (s != LA_OK) return fail(err, s, "device forward failed");
+  cudaMemcpyAsync(out, dout, tb, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(g, dg, gb, cudaMemcpyDeviceToHost, st);
+  return la_query_status(dws, st, err);
+}
+
+la_status la_host_backward(const la_problem* p, const void* q, la_layout lq, const void* k,
+                           la_layout lk, const void* v, la_layout lv, const void* o,
+                           const void* omega, la_layout lw, const float* g, void* dq, void* dk,
+                           void* dv, la_error_info* err) {
+  if (p && (!o || !g))
+    return fail(err, LA_ERR_MISSING_FORWARD_STATE, "backward requires the forward artifacts");
+  la_status s = check_problem(p, err);
+  if (s != LA_OK) return s;
+  if (!q || !k || !v || !omega || !dq || !dk || !dv)
+    return fail(err, LA_ERR_INVALID_SHAPE, "null host buffer");
+  const size_t tb = (size_t)(p->groups * p->seq_len * p->dim) * elem_bytes(p->dtype);
+  const size_t gb = sizeof(float) * (size_t)(p->groups * p->seq_len);
+  const size_t wb = la_backward_workspace_bytes(p);
+  const size_t need = 8 * align256(tb) + align256(gb) + align256(wb);
+  cudaError_t e = t_arena.reserve(need);
+  if (e != cudaSuccess) return cuda_fail(err, e);
+  char* base = (char*)t_arena.ptr;
+  void* b[8];
+  for (int i = 0; i < 8; ++i) b[i] = base + i * align256(tb);
+  float* dg = (float*)(base + 8 * align256(tb));
+  void* dws = base + 8 * align256(tb) + align256(gb);
+  cudaStream_t st = t_arena.stream;
+  cudaMemcpyAsync(b[0], q, tb, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(b[1], k, tb, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(b[2], v, tb, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(b[3], o, tb, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(b[4], omega, tb, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(dg, g, gb, cudaMemcpyHostToDevice, st);
+  s = la_backward(p, b[0], lq, b[1], lk, b[2], lv, b[3], b[4], lw, dg, b[5], b[6], b[7], dws, wb,
+                  st, nullptr);
+  if (s != LA_OK) return fail(err, s, "device backward failed");
+  cudaMemcpyAsync(dq, b[5], tb, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(dk, b[6], tb, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(dv, b[7], tb, cudaMemcpyDeviceToHost, st);
+  return la_query_status(dws, st, err);
+}
+
+void la_host_release(void) { t_arena.release(); }
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+"""C-ABI surface checks that need no GPU: the library loads, exports every
+symbol include/la_cuda.h declares, and rejects bad arguments synchronously with
+the reference's error taxonomy (error.hpp, forward.cpp:13-25, plan.cpp:49-62)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2510_21956_b200 as la
+from paper_2510_21956_b200 import _abi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "la_cuda.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:la_status|size_t|const char\s*\*|uint64_t|void|int32_t)\s+(la_\w+)\s*\(",
+                                 src, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _abi.lib()
+    names = declared_symbols()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_abi.EXPORTS)
+
+
+def test_library_is_sm100a():
+    # the cubin in the .so targets sm_100a (cuobjdump lists the ELF arch)
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([exe, "--list-elf", _abi.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_default_and_validate_plan_follow_reference():
+    # plan.cpp:24-47: L = largest divisor of D not above D/32
+    for d, want in ((128, 4), (64, 2), (96, 3), (24, 1), (100, 2), (256, 8)):
+        assert la.default_plan(la.Shape(1, 1, 4, d)).reduction_blocks == want
+    p = la.default_plan(la.Shape(2, 3, 4, 8))
+    la.validate_plan(p, 6, 8)
+    with pytest.raises(la.InvalidPlan):
+        la.validate_plan(p, 5, 8)
+    with pytest.raises(la.InvalidPlan):
+        la.validate_plan(p, 6, 9)
+    p.reduction_blocks = 3
+    with pytest.raises(la.InvalidPlan):
+        la.validate_plan(p, 6, 8)
+    p.reduction_blocks = 1
+    p.workers = 0
+    with pytest.raises(la.InvalidPlan):
+        la.validate_plan(p, 6, 8)
+
+
+def _ht(G, N, D, layout=la.Layout.SequenceMajor):
+    return la.HeadTensor.from_logical(np.zeros((G, N, D)), layout)
+
+
+def test_forward_argument_errors_are_synchronous():
+    q, k, v = _ht(1, 4, 4), _ht(1, 4, 4), _ht(1, 4, 4, la.Layout.FeatureMajor)
+    other = _ht(1, 4, 5, la.Layout.FeatureMajor)
+    with pytest.raises(la.ShapeMismatch):
+        la.forward_causal(q, k, other)
+    with pytest.raises(la.InvalidArgument):
+        la.forward_causal(q, k, v, la.LinearKernelCoeffs(0.0, 0.0))
+    plan = la.default_plan(la.Shape(1, 1, 4, 4))
+    plan.reduction_blocks = 3
+    with pytest.raises(la.InvalidPlan):
+        la.forward_causal(q, k, v, la.LinearKernelCoeffs(), plan)
+
+
+def test_c_abi_rejects_before_touching_the_device():
+    lib = _abi.lib()
+    err = _abi.ErrorInfo()
+    p = _abi.make_problem(2, 8, 4)
+    p.groups = 0
+    assert lib.la_forward(C.byref(p), 1, 1, 1, 1, 1, 0, 1, 1, 1, 1 << 20, None, C.byref(err)) == 1
+    p = _abi.make_problem(2, 8, 4, a=0.0, b=0.0)
+    assert lib.la_forward(C.byref(p), 1, 1, 1, 1, 1, 0, 1, 1, 1, 1 << 20, None, C.byref(err)) == 3
+    p = _abi.make_problem(2, 8, 4)
+    assert lib.la_forward(C.byref(p), 1, 1, 1, 1, 1, 0, 1, 1, 1, 0, None, C.byref(err)) == 9
+    # backward without forward artifacts -> MissingForwardState (backward.cpp:15-20)
+    assert lib.la_backward(C.byref(p), 1, 1, 1, 1, 1, 0, None, 1, 0, 1, 1, 1, 1, 1, 1 << 20, None,
+                           C.byref(err)) == 5
+    assert lib.la_backward(C.byref(p), 1, 1, 1, 1, 1, 0, 1, 1, 0, None, 1, 1, 1, 1, 1 << 20, None,
+                           C.byref(err)) == 5
+    p = _abi.make_problem(2, 8, 300)
+    assert lib.la_forward(C.byref(p), 1, 1, 1, 1, 1, 0, 1, 1, 1, 1 << 30, None, C.byref(err)) in (4, 8)
+
+
+def test_backward_argument_errors():
+    art = la.ForwardArtifacts()
+    with pytest.raises(la.MissingForwardState):
+        la.backward_causal(art, _ht(1, 4, 2))
+    art = la.ForwardArtifacts(out=_ht(1, 4, 2, la.Layout.FeatureMajor), g=np.ones(3),
+                              q=_ht(1, 4, 2), k=_ht(1, 4, 2), v=_ht(1, 4, 2))
+    with pytest.raises(la.MissingForwardState):
+        la.backward_causal(art, _ht(1, 4, 2))
+    art.g = np.ones(4)
+    with pytest.raises(la.ShapeMismatch):
+        la.backward_causal(art, _ht(1, 4, 3))
+
+
+def test_workspace_is_flat_in_sequence_length():
+    # O(ND) memory: the workspace depends on the segment count, not on N
+    # (test_backward.cpp:329-347 "backward memory bound is flat in N").
+    lib = _abi.lib()
+    sizes = set()
+    for n in (1 << 16, 1 << 18, 1 << 20):
+        p = _abi.make_problem(64, n, 128, "bf16")
+        sizes.add(lib.la_forward_workspace_bytes(C.byref(p)))
+    assert len(sizes) == 1

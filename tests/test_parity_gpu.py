@@ -1,0 +1,223 @@
+"""GPU parity: the CUDA library (through the reference-mirroring API over the
+C-ABI) against the CPU oracle on identical inputs.
+
+Tolerances (BASELINE.json north_star): fp32 <= 1e-5 relative (max|x-y|/max|y|)
+against the f64 oracle on the fp32 inputs; bf16 <= 2e-2 max-abs against the f64
+oracle on the bf16-rounded inputs."""
+import numpy as np
+import pytest
+
+import paper_2510_21956_b200 as la
+from oracle import oracle as O
+from tests._util import FM, SM, bench_inputs, fast_inputs, max_abs, rel_err, round_to
+
+pytestmark = pytest.mark.gpu
+
+FP32_REL = 1e-5
+BF16_ABS = 2e-2
+
+
+def dev(x, dtype, layout, cuda):
+    t, r = round_to(x, dtype)
+    return la.HeadTensor.from_logical(t.to(cuda), la.Layout(layout)), r
+
+
+def run_dev(q, k, v, w, dtype, cuda, causal=True, a=1.0, b=1.0, impl="auto", fault=la.Fault.None_,
+            lq=SM, lk=SM, lv=FM, lw=FM):
+    qt, qr = dev(q, dtype, lq, cuda)
+    kt, kr = dev(k, dtype, lk, cuda)
+    vt, vr = dev(v, dtype, lv, cuda)
+    c = la.LinearKernelCoeffs(a, b)
+    fwd = la.forward_causal if causal else la.forward_full
+    bwd = la.backward_causal if causal else la.backward_full
+    art = fwd(qt, kt, vt, c, None, fault, impl=impl)
+    res = {"out": art.out.logical(), "g": art.g.cpu().numpy().reshape(q.shape[0], q.shape[1]),
+           "rounded": (qr, kr, vr)}
+    if w is not None:
+        wt, wr = dev(w, dtype, lw, cuda)
+        gr = bwd(art, wt, c, None, fault, impl=impl)
+        res.update(dq=gr.dq.logical(), dk=gr.dk.logical(), dv=gr.dv.logical(), w=wr)
+    return res
+
+
+def oracle_all(res, causal, a=1.0, b=1.0, fault=0, dtype=np.float64):
+    qr, kr, vr = res["rounded"]
+    out, g = O.forward(qr, kr, vr, a, b, causal=causal, fault=fault, dtype=dtype)
+    ref = {"out": out, "g": g}
+    if "w" in res:
+        # the backward consumes the device forward's o and g, as the reference's
+        # backward consumes its own ForwardArtifacts
+        dq, dk, dv = O.backward(qr, kr, vr, res["out"], res["w"], res["g"], a, b, causal=causal,
+                                fault=fault, dtype=dtype)
+        ref.update(dq=dq, dk=dk, dv=dv)
+    return ref
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_config1_fp32_parity(cuda, causal):
+    # BASELINE config 1: fp32 B=1 H=4 N=2048 D=64 a=b=1, reference inputs (bench.cpp:75-97)
+    q, k, v, w = bench_inputs(4, 2048, 64)
+    res = run_dev(q, k, v, w, "f32", cuda, causal=causal)
+    ref = oracle_all(res, causal)
+    for key in ("out", "g", "dq", "dk", "dv"):
+        assert rel_err(res[key], ref[key]) <= FP32_REL, key
+
+
+def test_seed3_forward_goldens_on_gpu(cuda):
+    q = O.seeded(1, 3, 2, 3, SM)
+    k = O.seeded(1, 3, 2, 4, SM)
+    v = O.seeded(1, 3, 2, 5, FM)
+    res = run_dev(q, k, v, None, "f32", cuda)
+    golden_o = np.array([[0.34612980794285586, -0.92301077838464207],
+                         [-0.13319984306864124, -0.24065510636744042],
+                         [-0.37239006181521767, -0.43676585673830626]])
+    golden_g = np.array([1.1233087720476638, 2.4344381472035654, 3.6168703758830461])
+    assert rel_err(res["out"][0], golden_o) <= FP32_REL
+    assert rel_err(res["g"][0], golden_g) <= FP32_REL
+
+
+def test_seed11_backward_goldens_on_gpu(cuda):
+    q = O.seeded(1, 4, 3, 11, SM)
+    k = O.seeded(1, 4, 3, 12, SM)
+    v = O.seeded(1, 4, 3, 13, FM)
+    w = O.seeded(1, 4, 3, 14, FM)
+    res = run_dev(q, k, v, w, "f32", cuda)
+    gq = np.array([[0.0, 0.0, 0.0], [0.2610970160077386, 0.2013241874321281, 0.21024364305066712],
+                   [-0.13182186642257676, -0.28236676963278029, 0.22961200862869902],
+                   [-0.091971119497991083, 0.080342248132136973, 0.12996088871730649]])
+    gv = np.array([[0.42000940503328366, -0.78945868081659043, -0.31639909331415694],
+                   [0.36274863224328158, -0.25156616106913887, 0.41217273516469533],
+                   [0.1195796959230222, -0.029249696442690265, 0.066468620774084997],
+                   [0.00075433592705564934, -0.0089216108389855719, -0.0039506778404252429]])
+    assert max_abs(res["dq"][0], gq) <= 1e-5
+    assert max_abs(res["dv"][0], gv) <= 1e-5
+
+
+def test_randomized_shapes_fp32_mixed_layouts(cuda):
+    # test_forward.cpp:284-317: random N, D, both masks, coefficient table, mixed layouts
+    rng = np.random.default_rng(777)
+    table = [(1.0, 1.0), (1.0, 0.5), (0.3, 1.0)]
+    for case in range(24):
+        N, D = int(rng.integers(1, 200)), int(rng.integers(1, 40))
+        G = int(rng.integers(1, 3))
+        causal = bool(case % 2)
+        a, b = table[case % 3]
+        q = O.normalize_rows(O.seeded(G, N, D, int(rng.integers(1 << 40)), SM))
+        k = O.normalize_rows(O.seeded(G, N, D, int(rng.integers(1 << 40)), FM))
+        v = O.seeded(G, N, D, int(rng.integers(1 << 40)), FM)
+        w = O.seeded(G, N, D, int(rng.integers(1 << 40)), SM)
+        try:
+            _, qg = O.quadratic(q, k, v, a, b, causal=causal)
+        except O.OracleDegenerate:
+            continue
+        if np.min(np.abs(qg)) < 0.25:
+            continue
+        res = run_dev(q, k, v, w, "f32", cuda, causal=causal, a=a, b=b, lk=FM, lw=SM)
+        ref = oracle_all(res, causal, a, b)
+        for key in ("out", "g", "dq", "dk", "dv"):
+            assert rel_err(res[key], ref[key]) <= FP32_REL, (case, key, N, D)
+
+
+@pytest.mark.parametrize("fault", [1, 2, 3])
+def test_fault_variants_match_oracle(cuda, fault):
+    # Fault mutations are honoured on the device (fault.hpp:7-15, acceptance.cpp:195-217)
+    q, k, v, w = bench_inputs(2, 96, 16, seed=5)
+    res = run_dev(q, k, v, w, "f32", cuda, fault=la.Fault(fault))
+    ref = oracle_all(res, True, fault=fault)
+    clean = oracle_all(run_dev(q, k, v, w, "f32", cuda), True)
+    for key in ("out", "dq", "dk", "dv"):
+        assert rel_err(res[key], ref[key]) <= FP32_REL, key
+    changed = {1: "dk", 2: "out", 3: "dv"}[fault]
+    assert max_abs(res[changed], clean[changed]) > 1e-3
+
+
+def test_degenerate_denominator_reported(cuda):
+    import torch
+    q = np.array([[[1.0, 0.0], [-1.0, 0.0]]])
+    k = np.array([[[1.0, 0.0], [1.0, 0.0]]])
+    v = O.seeded(1, 2, 2, 88, FM)
+    with pytest.raises(la.DegenerateDenominator) as e:
+        run_dev(q, k, v, None, "f32", cuda)
+    assert (e.value.group(), e.value.position()) == (0, 1)
+    # lexicographically first offender across groups (pool.hpp:36-42)
+    q2 = np.concatenate([np.array([[[1.0, 0.0], [1.0, 0.0], [1.0, 0.0]]]),
+                         np.array([[[1.0, 0.0], [-1.0, 0.0], [-1.0, 0.0]]])])
+    k2 = np.ones((2, 3, 2)) * np.array([1.0, 0.0])
+    v2 = O.seeded(2, 3, 2, 89, FM)
+    with pytest.raises(la.DegenerateDenominator) as e:
+        run_dev(q2, k2, v2, None, "f32", cuda)
+    assert (e.value.group(), e.value.position()) == (1, 1)
+    torch.cuda.synchronize()
+
+
+def test_host_buffer_api_matches_device_api(cuda):
+    q, k, v, w = bench_inputs(2, 300, 32, seed=9)
+    c = la.LinearKernelCoeffs()
+    hq = la.HeadTensor.from_logical(q, la.Layout.SequenceMajor)
+    hk = la.HeadTensor.from_logical(k, la.Layout.SequenceMajor)
+    hv = la.HeadTensor.from_logical(v, la.Layout.FeatureMajor)
+    hw = la.HeadTensor.from_logical(w, la.Layout.FeatureMajor)
+    art = la.forward_causal(hq, hk, hv, c, dtype="f32")
+    gr = la.backward_causal(art, hw, c, dtype="f32")
+    res = run_dev(q, k, v, w, "f32", cuda)
+    assert np.array_equal(art.out.logical(), res["out"])
+    assert np.array_equal(gr.dk.logical(), res["dk"])
+
+
+@pytest.mark.parametrize("impl", ["simt", "auto"])
+def test_bf16_causal_d128_parity(cuda, impl):
+    # north-star dtype/head-dim at a size the f64 oracle finishes in seconds
+    q, k, v, w = fast_inputs(2, 4096, 128, seed=1)
+    res = run_dev(q, k, v, w, "bf16", cuda, impl=impl)
+    ref = oracle_all(res, True)
+    for key in ("out", "dq", "dk", "dv"):
+        assert max_abs(res[key], ref[key]) <= BF16_ABS, key
+    assert rel_err(res["g"], ref["g"]) <= 1e-3
+
+
+@pytest.mark.parametrize("D", [64, 128, 256])
+def test_bf16_noncausal_head_dim_sweep(cuda, D):
+    # BASELINE config 4 shape family (non-causal, D sweep) at reduced N
+    q, k, v, w = fast_inputs(2, 2048, D, seed=D)
+    res = run_dev(q, k, v, w, "bf16", cuda, causal=False)
+    ref = oracle_all(res, False)
+    for key in ("out", "dq", "dk", "dv"):
+        assert max_abs(res[key], ref[key]) <= BF16_ABS, (D, key)
+
+
+def test_north_star_sampled_groups_full_n(cuda):
+    # BASELINE config 2 at full N=65536, D=128, bf16: two groups checked against
+    # the oracle (groups are independent, forward_kernels.hpp:221-235)
+    q, k, v, w = fast_inputs(2, 65536, 128, seed=3)
+    res = run_dev(q, k, v, w, "bf16", cuda)
+    ref = oracle_all(res, True, dtype=np.float32)
+    for key in ("out", "dq", "dk", "dv"):
+        assert max_abs(res[key], ref[key]) <= BF16_ABS, key
+
+
+def test_bitwise_deterministic(cuda):
+    q, k, v, w = fast_inputs(3, 1000, 128, seed=4)
+    r1 = run_dev(q, k, v, w, "bf16", cuda)
+    r2 = run_dev(q, k, v, w, "bf16", cuda)
+    for key in ("out", "g", "dq", "dk", "dv"):
+        assert np.array_equal(r1[key], r2[key]), key
+
+
+def test_prefix_extensional(cuda):
+    # test_forward.cpp:256-282: rows of a causal run on a prefix match the full run
+    q, k, v, w = fast_inputs(2, 2048, 128, seed=6)
+    full = run_dev(q, k, v, None, "f32", cuda)
+    pre = run_dev(q[:, :700], k[:, :700], v[:, :700], None, "f32", cuda)
+    assert rel_err(pre["out"], full["out"][:, :700]) <= FP32_REL
+    assert rel_err(pre["g"], full["g"][:, :700]) <= FP32_REL
+
+
+def test_backward_linear_in_cotangent(cuda):
+    # test_backward.cpp:230-261 as a size-independent property
+    q, k, v, w1 = fast_inputs(2, 4096, 64, seed=8)
+    w2 = np.random.default_rng(9).uniform(-1, 1, w1.shape)
+    r1 = run_dev(q, k, v, w1, "f32", cuda)
+    r2 = run_dev(q, k, v, w2, "f32", cuda)
+    rs = run_dev(q, k, v, w1 + w2, "f32", cuda)
+    for key in ("dq", "dk", "dv"):
+        assert rel_err(r1[key] + r2[key], rs[key]) <= 1e-5, key
