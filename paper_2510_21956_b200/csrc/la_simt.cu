@@ -198,10 +198,9 @@ __global__ void __launch_bounds__(512) k_fwd_rows(const T* q, Strides sq, const 
                                                    int64_t seg_len, int P, float a, float b,
                                                    int causal, int fault, int64_t row_offset,
                                                    int64_t n_total,
-                                                   unsigned long long* flag) {
+                                                   unsigned long long* flag, int nsl) {
   extern __shared__ float sm[];
   const int rb = (int)lmin(D, kRB);  // output features per CTA
-  const int nsl = blockDim.x / rb;
   const int TRA = kTR + 1;
   float* qt = sm;                    // [kTR][D]
   float* kt = qt + kTR * D;          // [TRA][D]  (b * k)
@@ -215,9 +214,11 @@ __global__ void __launch_bounds__(512) k_fwd_rows(const T* q, Strides sq, const 
   const int p = blockIdx.x;
   const int64_t grp = blockIdx.y;
   const int64_t s0 = (int64_t)p * seg_len, s1 = lmin(N, s0 + seg_len);
-  const int jl = threadIdx.x % rb, sl = threadIdx.x / rb;
+  // blockDim is rounded up to whole warps; threads past nsl*rb only help load
+  const bool act = (int)threadIdx.x < nsl * rb;
+  const int jl = act ? (int)threadIdx.x % rb : 0, sl = act ? (int)threadIdx.x / rb : nsl;
   const int64_t j0 = (int64_t)blockIdx.z * rb;
-  const bool jok = j0 + jl < D;
+  const bool jok = act && j0 + jl < D;
   const int64_t j = jok ? j0 + jl : 0;
   const int64_t SZ = D * D + 2 * D + 1;
   const float* st = states + (grp * P + p) * SZ;
@@ -298,9 +299,9 @@ __global__ void __launch_bounds__(512) k_fwd_rows(const T* q, Strides sq, const 
         const int64_t m = (int64_t)sl * MPT + r;
         if (m < D) acc += qt[li * D + m] * X[r];
       }
-      part[((li & 1) * nsl + sl) * rb + jl] = acc;
+      if (act) part[((li & 1) * nsl + sl) * rb + jl] = acc;
       __syncthreads();
-      if (sl == 0) {
+      if (act && sl == 0) {
         if (causal) sigma += a * vt[li * D + j];
         float f = sigma;
         for (int s = 0; s < nsl; ++s) f += part[((li & 1) * nsl + s) * rb + jl];
@@ -332,10 +333,9 @@ __global__ void __launch_bounds__(512) k_bwd_rows(const T* q, Strides sq, const 
                                                    const float* gvec, const float* svec, T* outp,
                                                    Strides so, const float* states, int64_t N,
                                                    int64_t D, int64_t seg_len, int P, float a,
-                                                   float b, int causal, int fault) {
+                                                   float b, int causal, int fault, int nsl) {
   extern __shared__ float sm[];
   const int rb = (int)lmin(D, kRB);
-  const int nsl = blockDim.x / rb;
   float* At = sm;               // [kTR][D]
   float* Bt = At + kTR * D;     // [kTR][D]
   float* Ct = Bt + kTR * D;     // [kTR][D]
@@ -347,9 +347,10 @@ __global__ void __launch_bounds__(512) k_bwd_rows(const T* q, Strides sq, const 
   const int p = blockIdx.x;
   const int64_t grp = blockIdx.y;
   const int64_t s0 = (int64_t)p * seg_len, s1 = lmin(N, s0 + seg_len);
-  const int rl = threadIdx.x % rb, sl = threadIdx.x / rb;
+  const bool act = (int)threadIdx.x < nsl * rb;
+  const int rl = act ? (int)threadIdx.x % rb : 0, sl = act ? (int)threadIdx.x / rb : nsl;
   const int64_t r0b = (int64_t)blockIdx.z * rb;
-  const bool rok = r0b + rl < D;
+  const bool rok = act && r0b + rl < D;
   const int r = rok ? (int)(r0b + rl) : 0;
   const int64_t SZ = D * D + 2 * D + 1;
   const float* st = states + (grp * P + p) * SZ;
@@ -411,9 +412,9 @@ __global__ void __launch_bounds__(512) k_bwd_rows(const T* q, Strides sq, const 
         const int64_t c = (int64_t)sl * MPT + cc;
         if (c < D) acc += X[cc] * Ct[li * D + c];
       }
-      part[((step & 1) * nsl + sl) * rb + rl] = acc;
+      if (act) part[((step & 1) * nsl + sl) * rb + rl] = acc;
       __syncthreads();
-      if (sl == 0) {
+      if (act && sl == 0) {
         float dot = 0.f;
         for (int s = 0; s < nsl; ++s) dot += part[((step & 1) * nsl + s) * rb + rl];
         float res;
@@ -482,7 +483,7 @@ cudaError_t forward_t(const Launch& L, const Tensors& t, void* out, float* g, Wo
   }
   note_launch(2);
   const int nsl = nsl_for(D);
-  const int threads = (int)(nsl * rb_for(D));
+  const int threads = (int)((nsl * rb_for(D) + 31) / 32 * 32);
   const int nrb = (int)((D + rb_for(D) - 1) / rb_for(D));
   const size_t smem = fwd_rows_smem(D, nsl);
   const int64_t ntot = L.n_total > 0 ? L.n_total : N;
@@ -493,7 +494,7 @@ cudaError_t forward_t(const Launch& L, const Tensors& t, void* out, float* g, Wo
       ProfScope ps_("k_fwd_rows", L.stream);
       kern<<<dim3(P, G, nrb), threads, smem, L.stream>>>(
         (const T*)t.q, sq, (const T*)t.k, sk, (const T*)t.v, sv, (T*)out, g, states, N, D, seg,
-        P, L.a, L.b, L.causal, L.fault, L.row_offset, ntot, ws.flag);
+        P, L.a, L.b, L.causal, L.fault, L.row_offset, ntot, ws.flag, nsl);
     }
   } else {
     auto kern = k_fwd_rows<T, 64>;
@@ -502,7 +503,7 @@ cudaError_t forward_t(const Launch& L, const Tensors& t, void* out, float* g, Wo
       ProfScope ps_("k_fwd_rows", L.stream);
       kern<<<dim3(P, G, nrb), threads, smem, L.stream>>>(
         (const T*)t.q, sq, (const T*)t.k, sk, (const T*)t.v, sv, (T*)out, g, states, N, D, seg,
-        P, L.a, L.b, L.causal, L.fault, L.row_offset, ntot, ws.flag);
+        P, L.a, L.b, L.causal, L.fault, L.row_offset, ntot, ws.flag, nsl);
     }
   }
   note_launch(1);
@@ -520,10 +521,10 @@ void launch_bwd_rows(const Launch& L, const Tensors& t, const float* svec, void*
   const int nrb = (int)((D + rb_for(D) - 1) / rb_for(D));
   {
     ProfScope ps_(MODE == 0 ? "k_bwd_rows_dq" : MODE == 1 ? "k_bwd_rows_dk" : "k_bwd_rows_dv", L.stream);
-    kern<<<dim3(P, L.G, nrb), (int)(nsl * rb_for(D)), smem, L.stream>>>(
+    kern<<<dim3(P, L.G, nrb), (int)((nsl * rb_for(D) + 31) / 32 * 32), smem, L.stream>>>(
       (const T*)t.q, strides_of(t.lq, N, D), (const T*)t.k, strides_of(t.lk, N, D),
       (const T*)t.v, strides_of(t.lv, N, D), (const T*)t.w, strides_of(t.lw, N, D), t.g, svec,
-      (T*)outp, strides_of(lout, N, D), states, N, D, seg, P, L.a, L.b, L.causal, L.fault);
+      (T*)outp, strides_of(lout, N, D), states, N, D, seg, P, L.a, L.b, L.causal, L.fault, nsl);
   }
   note_launch(1);
 }
