@@ -1,17 +1,544 @@
-// sm_100a tcgen05/TMEM/TMA chunked kernels (bf16/fp16). Placeholder until the
-// tensor-core path lands: everything routes to the SIMT path.
+// sm_100a tensor-core path: chunked causal linear attention, f(x) = a + b*x.
+//
+// Forward (replaces forward_kernels.hpp run_forward<T>, causal, D = 128):
+//   the sequence of each group g is cut into P segments; a segment is walked in
+//   chunks of C = 128 rows with the running state S^T = sum v k^T (fp32, TMEM),
+//   z = sum k and sigma = sum v (fp32). Per chunk (rows i, t in the chunk):
+//     T1  = Q K^T                                  tcgen05, TMEM   (lanes i)
+//     P'  = tril(a + b T1) -> bf16 smem; g_i = rowsum(P') + a*row0 + b q_i.z
+//     O^T = V^T P'^T + bf16(b S^T) Q^T             tcgen05, TMEM   (lanes j)
+//     S^T += V^T K                                 tcgen05, TMEM   (lanes j)
+//     o_ij = (O^T[j][i] + a sigma_j) / g_i -> bf16 -> TMA store (FeatureMajor)
+//   Warp roles: warp 0 TMA producer, warp 1 MMA issuer (+TMEM owner), warps 2-5
+//   the TMEM<->register epilogue. Q/K/V tiles arrive by TMA (128B swizzle) in a
+//   2-stage ring. Segment carries come from an aggregate pass (S, z, sigma per
+//   segment via the same tcgen05 state MMA) and an exclusive scan.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "common.cuh"
 #include "internal.h"
+#include "sm100.cuh"
 
 namespace lab {
-bool tc_forward_supported(const Launch&, const Tensors&) { return false; }
-bool tc_backward_supported(const Launch&, const Tensors&) { return false; }
-size_t tc_forward_ws_floats(int64_t, int64_t, int64_t) { return 0; }
-size_t tc_backward_ws_floats(int64_t, int64_t, int64_t) { return 0; }
-cudaError_t tc_forward(const Launch&, const Tensors&, void*, float*, Workspace) {
-  return cudaErrorNotSupported;
+
+using namespace sm100;
+
+namespace {
+
+constexpr int kC = 128;          // chunk rows
+constexpr int kD = 128;          // head dim handled here
+constexpr int kTile = kC * kD * 2;  // 32 KB: one 128x128 16-bit tile (2 SW128 panels)
+constexpr int kPanel = 128 * 128;   // bytes per 64-column panel of 128 rows
+
+// TMEM columns (forward main)
+constexpr uint32_t kT1 = 0, kOT = 128, kST = 256, kSB = 384;
+
+// ---------------------------------------------------------------- host TMA maps
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  });
+  return fn;
 }
+
+// A (rows x 128) 16-bit tile of a row-major [R][inner] matrix, as two 64-column
+// SW128 panels: dims {64, R, inner/64}, box {64, 128, 2}.
+bool make_map(CUtensorMap* m, const void* base, bool bf16, uint64_t rows, uint64_t inner) {
+  cuuint64_t dims[3] = {64, rows, inner / 64};
+  cuuint64_t strides[2] = {inner * 2, 128};
+  cuuint32_t box[3] = {64, 128, 2};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode_fn()(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                           3, const_cast<void*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// K-major SW128 descriptor for k-step ks (16 elements) of a 128-row tile.
+__device__ __forceinline__ uint64_t kdesc(uint32_t tile, int ks) {
+  return sdesc_sw128(tile + (ks >> 2) * kPanel + (ks & 3) * 32, 16, 1024);
+}
+// MN-major SW128 descriptor for k-step ks: K rows of 128 B, MN panels kPanel apart.
+__device__ __forceinline__ uint64_t mndesc(uint32_t tile, int ks) {
+  return sdesc_sw128(tile + ks * 2048, kPanel, 1024);
+}
+
+struct FwdParams {
+  const float* states;  // per (g, segment) exclusive-prefix records
+  float* gout;          // G*N
+  unsigned long long* flag;
+  int64_t N, G;
+  int64_t seg_len;      // rows per segment (multiple of kC)
+  int P;
+  int64_t row_offset;
+  float a, b;
+};
+
+// ================================================================ forward main
+template <bool kBF16>
+__global__ void __launch_bounds__(192, 1)
+    k_fwd_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+             FwdParams prm) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sQ = smem;                  // [2][32K]
+  uint8_t* sK = smem + 2 * kTile;      // [2][32K]
+  uint8_t* sV = smem + 4 * kTile;      // [2][32K]  V^T tile: rows j, cols t
+  uint8_t* sP = smem + 6 * kTile;      // P' (rows i, cols t) / O^T staging (rows j, cols i)
+  uint64_t* bars = (uint64_t*)(smem + 7 * kTile);
+  uint64_t* full = bars;               // [2]
+  uint64_t* empty = bars + 2;          // [2]
+  uint64_t* t1_full = bars + 4;
+  uint64_t* t1_empty = bars + 5;
+  uint64_t* sb_ready = bars + 6;
+  uint64_t* st_full = bars + 7;
+  uint64_t* p_ready = bars + 8;
+  uint64_t* o_full = bars + 9;
+  uint64_t* ot_empty = bars + 10;
+  uint32_t* tslot = (uint32_t*)(bars + 12);
+  float* ginv_s = (float*)(bars + 16);  // [128]
+  float* zq = ginv_s + kC;              // [128]
+
+  const int p = blockIdx.x;
+  const int64_t grp = blockIdx.y;
+  const int64_t s0 = (int64_t)p * prm.seg_len;
+  const int64_t s1 = lmin(prm.N, s0 + prm.seg_len);
+  const int nc = (int)((s1 - s0) / kC);
+  const uint32_t warp = warp_id();
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmO);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1 + 128);
+    }
+    mbar_init(t1_full, 1);
+    mbar_init(t1_empty, 128);
+    mbar_init(sb_ready, 128);
+    mbar_init(st_full, 1);
+    mbar_init(p_ready, 128);
+    mbar_init(o_full, 1);
+    mbar_init(ot_empty, 128);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      for (int c = 0; c < nc; ++c) {
+        const int s = c & 1;
+        if (c >= 2) mbar_wait(&empty[s], ((c >> 1) & 1) ^ 1);
+        const int64_t row0 = s0 + (int64_t)c * kC;
+        mbar_expect_tx(&full[s], 3 * kTile);
+        tma_load_3d(sQ + s * kTile, &tmQ, &full[s], 0, (int)(grp * prm.N + row0), 0);
+        tma_load_3d(sK + s * kTile, &tmK, &full[s], 0, (int)(grp * prm.N + row0), 0);
+        tma_load_3d(sV + s * kTile, &tmV, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t fmt = kBF16 ? 1 : 0;
+    const uint32_t id_kk = idesc_f16(128, 128, fmt, 0, 0);
+    const uint32_t id_kmn = idesc_f16(128, 128, fmt, 0, 1);
+    const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV), aP = smem_u32(sP);
+    for (int c = 0; c < nc; ++c) {
+      const int s = c & 1;
+      mbar_wait(&full[s], (c >> 1) & 1);
+      if (c >= 1) mbar_wait(t1_empty, (c - 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        for (int ks = 0; ks < 8; ++ks)  // T1 = Q K^T
+          mma_ss(tmem + kT1, kdesc(aQ + s * kTile, ks), kdesc(aK + s * kTile, ks), id_kk, ks > 0);
+        mma_commit(t1_full);
+      }
+      __syncwarp();
+      mbar_wait(sb_ready, c & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        for (int ks = 0; ks < 8; ++ks)  // S^T += V^T K   (B = K viewed (N=m, K=t): MN-major)
+          mma_ss(tmem + kST, kdesc(aV + s * kTile, ks), mndesc(aK + s * kTile, ks), id_kmn, 1);
+        mma_commit(st_full);
+      }
+      __syncwarp();
+      mbar_wait(p_ready, c & 1);
+      if (c >= 1) mbar_wait(ot_empty, (c - 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        for (int ks = 0; ks < 8; ++ks)  // O^T = V^T P'^T
+          mma_ss(tmem + kOT, kdesc(aV + s * kTile, ks), kdesc(aP, ks), id_kk, ks > 0);
+        for (int ks = 0; ks < 8; ++ks)  // O^T += bf16(b S^T) Q^T   (A from TMEM)
+          mma_ts(tmem + kOT, tmem + kSB + ks * 8, kdesc(aQ + s * kTile, ks), id_kk, 1);
+        mma_commit(o_full);
+        mma_commit(&empty[s]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 2..5)
+    const uint32_t qd = warp & 3;                 // TMEM lane quadrant of this warp
+    const int r = (int)(qd * 32 + lane_id());     // row owned: i for T1, j for O^T / S^T
+    const uint32_t lane_base = (qd * 32u) << 16;
+    const int et = (int)threadIdx.x - 64;         // 0..127
+    const float a = prm.a, b = prm.b;
+    const float* st = prm.states + (grp * prm.P + p) * state_floats(kD);
+    // carry-in: S^T row r = S[:, r], z, sigma
+    for (int m0 = 0; m0 < kD; m0 += 32) {
+      uint32_t v[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) v[u] = __float_as_uint(st[(m0 + u) * kD + r]);
+      tmem_st32(tmem + lane_base + kST + m0, v);
+    }
+    tmem_st_wait();
+    zq[r] = st[kD * kD + r];
+    float sigma_prev = st[kD * kD + kD + r];
+    tc_fence_before();
+    named_bar(1, 128);
+    tc_fence_after();
+
+    for (int c = 0; c < nc; ++c) {
+      const int s = c & 1;
+      const int64_t row0 = s0 + (int64_t)c * kC;
+      const uint8_t* q_t = sQ + s * kTile;
+      const uint8_t* k_t = sK + s * kTile;
+      const uint8_t* v_t = sV + s * kTile;
+      // ---- E2: S^T -> bf16(b S^T) in TMEM (A operand of the Q S term)
+      if (c >= 1) mbar_wait(st_full, (c - 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        uint32_t x0[32], x1[32], pk[32];
+        tmem_ld32(tmem + lane_base + kST + half * 64, x0);
+        tmem_ld32(tmem + lane_base + kST + half * 64 + 32, x1);
+        tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          pk[u] = pack2<kBF16>(b * __uint_as_float(x0[2 * u]), b * __uint_as_float(x0[2 * u + 1]));
+          pk[16 + u] = pack2<kBF16>(b * __uint_as_float(x1[2 * u]), b * __uint_as_float(x1[2 * u + 1]));
+        }
+        tmem_st32(tmem + lane_base + kSB + half * 32, pk);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(sb_ready);
+
+      // ---- E1: T1 -> P' (smem), g
+      mbar_wait(&full[s], (c >> 1) & 1);
+      mbar_wait(t1_full, c & 1);
+      tc_fence_after();
+      if (c >= 1) {
+        if (et == 0) tma_store_wait_read0();  // O^T staging of chunk c-1 has left sP
+        named_bar(1, 128);
+      }
+      float rowsum = 0.f;
+#pragma unroll 1
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t x[32];
+        tmem_ld32(tmem + lane_base + kT1 + cc * 32, x);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int t0 = cc * 32 + 2 * u;
+          const float p0 = t0 <= r ? a + b * __uint_as_float(x[2 * u]) : 0.f;
+          const float p1 = t0 + 1 <= r ? a + b * __uint_as_float(x[2 * u + 1]) : 0.f;
+          rowsum += p0 + p1;
+          pk[u] = pack2<kBF16>(p0, p1);
+        }
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          uint4 v4 = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
+          *(uint4*)(sP + sw128_off(r, cc * 32 + 8 * w, kC)) = v4;
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(t1_empty);
+      // q_i . z_prev (fp32) from the Q tile row i = r
+      float qz = 0.f;
+#pragma unroll 4
+      for (int m8 = 0; m8 < kD; m8 += 8) {
+        const uint4 v4 = *(const uint4*)(q_t + sw128_off(r, m8, kC));
+        const uint32_t w4[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float2 f = unpack2<kBF16>(w4[u]);
+          qz += f.x * zq[m8 + 2 * u] + f.y * zq[m8 + 2 * u + 1];
+        }
+      }
+      const float gi = rowsum + a * (float)(prm.row_offset + row0) + b * qz;
+      if (fabsf(gi) < kEpsF32) flag_degenerate(prm.flag, grp, prm.row_offset + row0 + r);
+      ginv_s[r] = 1.f / gi;
+      prm.gout[grp * prm.N + row0 + r] = gi;
+      // sigma_j += sum_t V^T[j][t]   (j = r)
+      float vs = 0.f;
+#pragma unroll 4
+      for (int t8 = 0; t8 < kC; t8 += 8) {
+        const uint4 v4 = *(const uint4*)(v_t + sw128_off(r, t8, kD));
+        const uint32_t w4[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float2 f = unpack2<kBF16>(w4[u]);
+          vs += f.x + f.y;
+        }
+      }
+      named_bar(1, 128);  // every thread is done reading zq
+      // z_m += sum_t K[t][m]   (m = r)
+      float ks_ = 0.f;
+#pragma unroll 8
+      for (int t = 0; t < kC; ++t) {
+        const uint16_t h = *(const uint16_t*)(k_t + sw128_off(t, r, kC));
+        ks_ += kBF16 ? __bfloat162float(__ushort_as_bfloat16(h)) : __half2float(__ushort_as_half(h));
+      }
+      zq[r] += ks_;
+      fence_proxy_async();  // P' generic stores -> visible to the tensor core
+      mbar_arrive(p_ready);
+      mbar_arrive(&empty[s]);
+
+      // ---- E3: O^T -> o = (O^T + a sigma) / g -> bf16 -> TMA store
+      mbar_wait(o_full, c & 1);
+      tc_fence_after();
+      const float asig = a * sigma_prev;
+#pragma unroll 1
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t x[32];
+        tmem_ld32(tmem + lane_base + kOT + cc * 32, x);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int i0 = cc * 32 + 2 * u;
+          pk[u] = pack2<kBF16>((__uint_as_float(x[2 * u]) + asig) * ginv_s[i0],
+                               (__uint_as_float(x[2 * u + 1]) + asig) * ginv_s[i0 + 1]);
+        }
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          uint4 v4 = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
+          *(uint4*)(sP + sw128_off(r, cc * 32 + 8 * w, kD)) = v4;
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(ot_empty);
+      sigma_prev += vs;
+      fence_proxy_async();
+      named_bar(1, 128);
+      if (et == 0) {
+        tma_store_3d(&tmO, sP, 0, (int)(grp * kD), (int)(row0 / 64));
+        tma_store_commit();
+      }
+    }
+    if (et == 0) tma_store_wait0();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// ================================================================ segment aggregates
+// Per (g, segment): S = sum_t k_t^T v_t (stored X[m][j]), z = sum k, sigma = sum v,
+// count; the record layout of la_simt.cu's k_seg_sums (internal.h).
+template <bool kBF16>
+__global__ void __launch_bounds__(192, 1)
+    k_fwd_agg_tc(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                 float* states, int64_t N, int64_t seg_len, int P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sK = smem;                  // [2][32K]
+  uint8_t* sV = smem + 2 * kTile;      // [2][32K]
+  uint64_t* bars = (uint64_t*)(smem + 4 * kTile);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + 2;
+  uint64_t* done = bars + 4;
+  uint32_t* tslot = (uint32_t*)(bars + 8);
+  const int p = blockIdx.x;
+  const int64_t grp = blockIdx.y;
+  const int64_t s0 = (int64_t)p * seg_len;
+  const int64_t s1 = lmin(N, s0 + seg_len);
+  const int nc = (int)((s1 - s0) / kC);
+  const uint32_t warp = warp_id();
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1 + 128);
+    }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<128>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int c = 0; c < nc; ++c) {
+        const int s = c & 1;
+        if (c >= 2) mbar_wait(&empty[s], ((c >> 1) & 1) ^ 1);
+        const int64_t row0 = s0 + (int64_t)c * kC;
+        mbar_expect_tx(&full[s], 2 * kTile);
+        tma_load_3d(sK + s * kTile, &tmK, &full[s], 0, (int)(grp * N + row0), 0);
+        tma_load_3d(sV + s * kTile, &tmV, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t id_kmn = idesc_f16(128, 128, kBF16 ? 1 : 0, 0, 1);
+    const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
+    for (int c = 0; c < nc; ++c) {
+      const int s = c & 1;
+      mbar_wait(&full[s], (c >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        for (int ks = 0; ks < 8; ++ks)
+          mma_ss(tmem, kdesc(aV + s * kTile, ks), mndesc(aK + s * kTile, ks), id_kmn,
+                 (c > 0 || ks > 0) ? 1u : 0u);
+        mma_commit(&empty[s]);
+        if (c == nc - 1) mma_commit(done);
+      }
+      __syncwarp();
+    }
+  } else {
+    const uint32_t qd = warp & 3;
+    const int r = (int)(qd * 32 + lane_id());
+    float zs = 0.f, vs = 0.f;
+    for (int c = 0; c < nc; ++c) {
+      const int s = c & 1;
+      mbar_wait(&full[s], (c >> 1) & 1);
+      const uint8_t* k_t = sK + s * kTile;
+      const uint8_t* v_t = sV + s * kTile;
+#pragma unroll 4
+      for (int t8 = 0; t8 < kC; t8 += 8) {
+        const uint4 v4 = *(const uint4*)(v_t + sw128_off(r, t8, kD));
+        const uint32_t w4[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float2 f = unpack2<kBF16>(w4[u]);
+          vs += f.x + f.y;
+        }
+      }
+#pragma unroll 8
+      for (int t = 0; t < kC; ++t) {
+        const uint16_t h = *(const uint16_t*)(k_t + sw128_off(t, r, kC));
+        zs += kBF16 ? __bfloat162float(__ushort_as_bfloat16(h)) : __half2float(__ushort_as_half(h));
+      }
+      mbar_arrive(&empty[s]);
+    }
+    float* st = states + (grp * P + p) * state_floats(kD);
+    if (nc > 0) {
+      mbar_wait(done, 0);
+      tc_fence_after();
+      const uint32_t lane_base = (qd * 32u) << 16;
+      for (int m0 = 0; m0 < kD; m0 += 32) {
+        uint32_t x[32];
+        tmem_ld32(tmem + lane_base + m0, x);
+        tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 32; ++u) st[(m0 + u) * kD + r] = __uint_as_float(x[u]);  // X[m][j=r]
+      }
+    } else {
+      for (int m = 0; m < kD; ++m) st[m * kD + r] = 0.f;
+    }
+    st[kD * kD + r] = zs;
+    st[kD * kD + kD + r] = vs;
+    if (r == 0) st[kD * kD + 2 * kD] = (float)(s1 - s0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<128>(tmem);
+}
+
+constexpr size_t kFwdSmem = 7 * kTile + 256 + 2 * kC * 4 + 1024;
+constexpr size_t kAggSmem = 4 * kTile + 128 + 1024;
+
+int tc_segments(int64_t G, int64_t N) {
+  const int64_t chunks = N / kC;
+  // aim for >= 3 waves of 148 CTAs, segments of >= 8 chunks
+  int64_t p = (3 * 148 + G - 1) / G;
+  p = lmin(p, lmax(1, chunks / 8));
+  return (int)lmax(1, p);
+}
+
+__global__ void k_scan_fwd(float* states, int P, int64_t SZ, const float* carry) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t grp = blockIdx.y;
+  if (e >= SZ) return;
+  float* base = states + grp * P * SZ + e;
+  float run = carry ? carry[grp * SZ + e] : 0.f;
+  for (int q = 0; q < P; ++q) {
+    const float t = base[q * SZ];
+    base[q * SZ] = run;
+    run += t;
+  }
+}
+
+}  // namespace
+
+bool tc_forward_supported(const Launch& L, const Tensors& t) {
+  return (L.dtype == LA_BF16 || L.dtype == LA_F16) && L.D == kD && L.causal && L.fault == LA_FAULT_NONE &&
+         L.N % kC == 0 && t.lq == LA_SEQUENCE_MAJOR && t.lk == LA_SEQUENCE_MAJOR &&
+         t.lv == LA_FEATURE_MAJOR && L.G * L.N < (1ll << 31) && L.G * kD < (1ll << 31);
+}
+bool tc_backward_supported(const Launch&, const Tensors&) { return false; }
+
+size_t tc_forward_ws_floats(int64_t G, int64_t N, int64_t D) {
+  if (D != kD || N % kC) return 0;
+  return (size_t)(G * tc_segments(G, N) * state_floats(kD));
+}
+size_t tc_backward_ws_floats(int64_t, int64_t, int64_t) { return 0; }
+
+cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws) {
+  const bool bf = L.dtype == LA_BF16;
+  const int64_t G = L.G, N = L.N;
+  const int P = tc_segments(G, N);
+  const int64_t chunks = N / kC;
+  const int64_t seg = ((chunks + P - 1) / P) * kC;
+  const int64_t SZ = state_floats(kD);
+  float* states = ws.base;
+  CUtensorMap mQ, mK, mV, mO;
+  if (!make_map(&mQ, t.q, bf, (uint64_t)(G * N), kD) || !make_map(&mK, t.k, bf, (uint64_t)(G * N), kD) ||
+      !make_map(&mV, t.v, bf, (uint64_t)(G * kD), (uint64_t)N) ||
+      !make_map(&mO, out, bf, (uint64_t)(G * kD), (uint64_t)N))
+    return cudaErrorInvalidValue;
+  auto agg = bf ? k_fwd_agg_tc<true> : k_fwd_agg_tc<false>;
+  auto main_k = bf ? k_fwd_tc<true> : k_fwd_tc<false>;
+  cudaFuncSetAttribute(agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggSmem);
+  cudaFuncSetAttribute(main_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem);
+  {
+    ProfScope ps("la_fwd_agg", L.stream);
+    agg<<<dim3(P, G), 192, kAggSmem, L.stream>>>(mK, mV, states, N, seg, P);
+  }
+  {
+    ProfScope ps("la_fwd_scan", L.stream);
+    k_scan_fwd<<<dim3((unsigned)((SZ + 255) / 256), (unsigned)G), 256, 0, L.stream>>>(states, P, SZ,
+                                                                                    L.carry_prefix);
+  }
+  FwdParams prm{states, g, ws.flag, N, G, seg, P, L.row_offset, L.a, L.b};
+  {
+    ProfScope ps("la_fwd_causal", L.stream);
+    main_k<<<dim3(P, G), 192, kFwdSmem, L.stream>>>(mQ, mK, mV, mO, prm);
+  }
+  note_launch(3);
+  return cudaGetLastError();
+}
+
 cudaError_t tc_backward(const Launch&, const Tensors&, void*, void*, void*, Workspace) {
   return cudaErrorNotSupported;
 }
+
 }  // namespace lab

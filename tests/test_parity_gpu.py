@@ -221,3 +221,14 @@ def test_backward_linear_in_cotangent(cuda):
     rs = run_dev(q, k, v, w1 + w2, "f32", cuda)
     for key in ("dq", "dk", "dv"):
         assert rel_err(r1[key] + r2[key], rs[key]) <= 1e-5, key
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+@pytest.mark.parametrize("N", [128, 4096])
+def test_tcgen05_forward_parity(cuda, dtype, N):
+    # the sm_100a chunked forward (forced), multi-segment carries at N=4096
+    q, k, v, _ = fast_inputs(3, N, 128, seed=N + len(dtype))
+    res = run_dev(q, k, v, None, dtype, cuda, impl="tcgen05")
+    ref = oracle_all(res, True)
+    assert max_abs(res["out"], ref["out"]) <= BF16_ABS
+    assert rel_err(res["g"], ref["g"]) <= 1e-3
