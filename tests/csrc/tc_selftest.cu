@@ -24,6 +24,57 @@ __global__ void __launch_bounds__(128) k_selftest(const __nv_bfloat16* A, const 
   const int tid = threadIdx.x;
   const int M = 128, N = 128, K = 128;
   const bool a_mn = mode == 1, b_mn = mode == 2, a_tmem = mode == 3, use_tma = mode == 4;
+  if (mode >= 5) {
+    // M = N = 64, K = 128: A rows m < 64, B rows n < 64
+    const bool amn = mode == 6;
+    if (warp_id() == 0) tmem_alloc<512>(tslot);
+    if (tid == 0) {
+      mbar_init(&bar[0], 1);
+      fence_barrier_init();
+    }
+    for (int e = tid; e < 64 * K; e += 128) {
+      const int m = e / K, k = e % K;
+      const uint32_t offa = amn ? sw128_off(k, m, K) : sw128_off(m, k, 64);
+      *(__nv_bfloat16*)(sA + offa) = A[e];
+      *(__nv_bfloat16*)(sB + sw128_off(m, k, 64)) = B[e];
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tb = *tslot;
+    const uint32_t dlane = mode == 5 ? (16u << 16) : 0u;
+    if (warp_id() == 1) {
+      if (elect_one()) {
+        const uint32_t id = idesc_f16(64, 64, 1, amn ? 1 : 0, 0, mode == 6 ? 1 : 0);
+        for (int s = 0; s < K / 16; ++s) {
+          const uint64_t da = amn ? sdesc_sw128(smem_u32(sA) + s * 2048, K * 128, 1024)
+                                  : sdesc_sw128(smem_u32(sA) + (s / 4) * 64 * 128 + (s % 4) * 32, 16, 1024);
+          const uint64_t db = sdesc_sw128(smem_u32(sB) + (s / 4) * 64 * 128 + (s % 4) * 32, 16, 1024);
+          mma_ss(tb + dlane, da, db, id, s > 0);
+        }
+        mma_commit(&bar[0]);
+      }
+      __syncwarp();
+    }
+    mbar_wait(&bar[0], 0);
+    tc_fence_after();
+    // row m of the M=64 accumulator lives in lane (m % 16) + 32 * (m / 16) (+16 for the upper half)
+    const uint32_t qd = warp_id() % 4, l = lane_id();
+    uint32_t r[32];
+    for (int c0 = 0; c0 < 64; c0 += 32) {
+      tmem_ld32(tb + ((qd * 32u) << 16) + c0, r);
+      tmem_ld_wait();
+      const bool mine = mode == 5 ? l >= 16 : l < 16;
+      const int row = (int)(qd * 16 + (l & 15));
+      if (mine)
+        for (int c = 0; c < 32; ++c) D[row * 128 + c0 + c] = __uint_as_float(r[c]);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp_id() == 0) tmem_dealloc<512>(tb);
+    return;
+  }
 
   if (warp_id() == 0) tmem_alloc<512>(tslot);
   if (tid == 0) {
