@@ -13,13 +13,10 @@
 //   the TMEM<->register epilogue. Q/K/V tiles arrive by TMA (128B swizzle) in a
 //   2-stage ring. Segment carries come from an aggregate pass (S, z, sigma per
 //   segment via the same tcgen05 state MMA) and an exclusive scan.
-#include <cudaTypedefs.h>
-
-#include <mutex>
-
 #include "common.cuh"
 #include "internal.h"
 #include "sm100.cuh"
+#include "tma_host.h"
 
 namespace lab {
 
@@ -35,31 +32,9 @@ constexpr int kPanel = 128 * 128;   // bytes per 64-column panel of 128 rows
 // TMEM columns (forward main)
 constexpr uint32_t kT1 = 0, kOT = 128, kST = 256, kSB = 384;
 
-// ---------------------------------------------------------------- host TMA maps
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
-    fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
-  });
-  return fn;
-}
-
-// A (rows x 128) 16-bit tile of a row-major [R][inner] matrix, as two 64-column
-// SW128 panels: dims {64, R, inner/64}, box {64, 128, 2}.
+// A (rows x 128) 16-bit tile of a row-major [R][inner] matrix as two SW128 panels.
 bool make_map(CUtensorMap* m, const void* base, bool bf16, uint64_t rows, uint64_t inner) {
-  cuuint64_t dims[3] = {64, rows, inner / 64};
-  cuuint64_t strides[2] = {inner * 2, 128};
-  cuuint32_t box[3] = {64, 128, 2};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = encode_fn()(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                           3, const_cast<void*>(base), dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  return make_tma_map(m, base, bf16, rows, inner, 128, 2);
 }
 
 // K-major SW128 descriptor for k-step ks (16 elements) of a 128-row tile.
@@ -494,13 +469,11 @@ bool tc_forward_supported(const Launch& L, const Tensors& t) {
          L.N % kC == 0 && t.lq == LA_SEQUENCE_MAJOR && t.lk == LA_SEQUENCE_MAJOR &&
          t.lv == LA_FEATURE_MAJOR && L.G * L.N < (1ll << 31) && L.G * kD < (1ll << 31);
 }
-bool tc_backward_supported(const Launch&, const Tensors&) { return false; }
 
 size_t tc_forward_ws_floats(int64_t G, int64_t N, int64_t D) {
   if (D != kD || N % kC) return 0;
   return (size_t)(G * tc_segments(G, N) * state_floats(kD));
 }
-size_t tc_backward_ws_floats(int64_t, int64_t, int64_t) { return 0; }
 
 cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws) {
   const bool bf = L.dtype == LA_BF16;
@@ -537,8 +510,5 @@ cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, W
   return cudaGetLastError();
 }
 
-cudaError_t tc_backward(const Launch&, const Tensors&, void*, void*, void*, Workspace) {
-  return cudaErrorNotSupported;
-}
 
 }  // namespace lab

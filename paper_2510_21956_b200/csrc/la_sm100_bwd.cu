@@ -1,0 +1,714 @@
+// sm_100a tensor-core backward: chunked causal linear attention, f(x) = a + b*x.
+//
+// Replaces backward_kernels.hpp run_backward<T> (causal, D = 128): its four
+// barrier-separated CPU sweeps (dQ prefix, dK alpha/beta suffix, dV suffix)
+// become ONE reverse sweep per (group, segment) over chunks of C = 64 rows.
+// With w_hat = omega / g and s_i = o_i . w_hat_i (backward_kernels.hpp:33-38):
+//   dPt = W_hat V^T, T1 = Q K^T                          (M=64, lanes i)
+//   dS  = b tril(dPt - s 1^T),  P = tril(a + b T1)       -> bf16 smem
+//   dQ  = dS K + W_hat (b S_prev)^T - b s z_prev^T        (M=64, two lane halves)
+//   dK^T = Q^T dS^T + (b R_next) V^T - b u_next           (M=128, lanes m)
+//   dV^T = W_hat^T P + (b R_next)^T K^T + a c_next        (M=128, lanes j)
+//   R += Q^T W_hat (suffix state, lanes m);  S -= K^T V (prefix state by
+//   negated MMA from the segment-end prefix, lanes m); u, z, c on CUDA cores.
+// The reference's beta^K state collapses to the D-vector u and beta^V aliases
+// alpha^K = b R. TMEM holds exactly 512 columns:
+//   [0,64) dPt (lanes 0-15,32-47,..) + T1 (other half), [64,128) dQ halves,
+//   [128,192) dK^T, [192,256) dV^T, [256,384) R, [384,512) S.
+// Segment carries: an aggregate pass (R, u, c and S, z per segment) + scan.
+#include "common.cuh"
+#include "internal.h"
+#include "sm100.cuh"
+#include "tma_host.h"
+
+namespace lab {
+
+using namespace sm100;
+
+namespace {
+
+constexpr int kCB = 64;   // chunk rows
+constexpr int kD = 128;   // head dim
+constexpr int kT64 = 16384;  // a 64x128 or 128x64 16-bit tile
+constexpr int kStage = 4 * kT64;  // Q, K, V^T, Omega^T
+constexpr uint32_t kDP = 0, kDQ = 64, kDK = 128, kDV = 192, kR = 256, kS = 384;
+constexpr uint32_t kHalf = 16u << 16;  // TMEM lane offset of the upper M=64 half
+
+// descriptors ---------------------------------------------------------------
+// K-major tile with `rows` rows and 64-column panels `rows*128` bytes apart.
+__device__ __forceinline__ uint64_t kd(uint32_t tile, int ks, uint32_t rows) {
+  return sdesc_sw128(tile + (ks >> 2) * rows * 128 + (ks & 3) * 32, 16, 1024);
+}
+// MN-major tile: K rows of 128 B (16 per k-step), MN panels `panel` bytes apart.
+__device__ __forceinline__ uint64_t mn(uint32_t tile, int ks, uint32_t panel) {
+  return sdesc_sw128(tile + ks * 2048, panel, 1024);
+}
+
+template <bool kBF16>
+__device__ __forceinline__ float h2f(uint16_t h) {
+  return kBF16 ? __bfloat162float(__ushort_as_bfloat16(h)) : __half2float(__ushort_as_half(h));
+}
+
+struct BwdParams {
+  const void* o;         // O^T  [G][D][N]
+  const float* g;        // [G][N]
+  void* dq;              // [G][N][D]
+  void* dk;              // [G][D][N]
+  void* dv;              // [G][D][N]
+  float* stS;            // per-segment S records (agg: out; main: inclusive prefix)
+  float* stR;            // per-segment R records (agg: out; main: exclusive suffix)
+  int64_t N;
+  int64_t seg_len;
+  int P;
+  float a, b;
+};
+
+// Epilogue step E0: W_hat = omega / g in place (bf16) and s_i = sum_j o_ij w_hat_ij.
+// 128 threads: lane = jg + 16 * (ig & 1), warp w -> ig = 2 w + lane / 16, each thread
+// owns rows j in [8 jg, 8 jg + 8) and columns i in [8 ig, 8 ig + 8) of the 128 x 64 tile.
+template <bool kBF16>
+__device__ __forceinline__ void what_pass(uint8_t* w_t, const uint4 (&o8)[8], const float4 (&g8)[2],
+                                          float* s_s, int et) {
+  const int lane = et & 31, w = et >> 5;
+  const int jg = lane & 15, ig = 2 * w + (lane >> 4);
+  float ginv[8] = {1.f / g8[0].x, 1.f / g8[0].y, 1.f / g8[0].z, 1.f / g8[0].w,
+                   1.f / g8[1].x, 1.f / g8[1].y, 1.f / g8[1].z, 1.f / g8[1].w};
+  float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int rr = 0; rr < 8; ++rr) {
+    const int j = 8 * jg + rr;
+    uint4* p = (uint4*)(w_t + sw128_off(j, 8 * ig, 128));
+    const uint4 wv = *p;
+    const uint32_t wa[4] = {wv.x, wv.y, wv.z, wv.w};
+    const uint32_t oa[4] = {o8[rr].x, o8[rr].y, o8[rr].z, o8[rr].w};
+    uint32_t res[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float2 wf = unpack2<kBF16>(wa[u]);
+      const float2 of = unpack2<kBF16>(oa[u]);
+      const float w0 = wf.x * ginv[2 * u], w1 = wf.y * ginv[2 * u + 1];
+      sp[2 * u] += of.x * w0;
+      sp[2 * u + 1] += of.y * w1;
+      res[u] = pack2<kBF16>(w0, w1);
+    }
+    *p = make_uint4(res[0], res[1], res[2], res[3]);
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+#pragma unroll
+    for (int off = 1; off < 16; off <<= 1) sp[u] += __shfl_xor_sync(0xffffffffu, sp[u], off);
+  }
+  if (jg == 0) {
+    *(float4*)(s_s + 8 * ig) = make_float4(sp[0], sp[1], sp[2], sp[3]);
+    *(float4*)(s_s + 8 * ig + 4) = make_float4(sp[4], sp[5], sp[6], sp[7]);
+  }
+}
+
+// Prefetch of this thread's O^T slice (8 rows j x 8 columns i) and g for a chunk.
+template <bool kBF16>
+__device__ __forceinline__ void what_prefetch(const BwdParams& prm, int64_t grp, int64_t row0, int et,
+                                              uint4 (&o8)[8], float4 (&g8)[2]) {
+  const int lane = et & 31, w = et >> 5;
+  const int jg = lane & 15, ig = 2 * w + (lane >> 4);
+  const uint16_t* o = (const uint16_t*)prm.o;
+#pragma unroll
+  for (int rr = 0; rr < 8; ++rr)
+    o8[rr] = __ldg((const uint4*)(o + (grp * kD + 8 * jg + rr) * prm.N + row0 + 8 * ig));
+  const float* gp = prm.g + grp * prm.N + row0 + 8 * ig;
+  g8[0] = __ldg((const float4*)gp);
+  g8[1] = __ldg((const float4*)(gp + 4));
+}
+
+// ================================================================ aggregates
+// Per (g, segment): S = sum k^T v, z = sum k (stS record); R = sum q^T w_hat,
+// u = sum s q, c = sum w_hat (stR record). Record layout of internal.h.
+template <bool kBF16>
+__global__ void __launch_bounds__(192, 1)
+    k_bwd_agg_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmW,
+                 BwdParams prm) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = (uint64_t*)(smem + 2 * kStage);
+  uint64_t* full = bars;       // [2]
+  uint64_t* empty = bars + 2;  // [2]
+  uint64_t* w_ready = bars + 4;
+  uint64_t* done = bars + 5;
+  uint32_t* tslot = (uint32_t*)(bars + 8);
+  float* s_s = (float*)(bars + 16);  // [64]
+
+  const int p = blockIdx.x;
+  const int64_t grp = blockIdx.y;
+  const int64_t s0 = (int64_t)p * prm.seg_len;
+  const int64_t s1 = lmin(prm.N, s0 + prm.seg_len);
+  const int nc = (int)((s1 - s0) / kCB);
+  const uint32_t warp = warp_id();
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmW);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1 + 128);
+    }
+    mbar_init(w_ready, 128);
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<256>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;  // [0,128) R, [128,256) S
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int c = 0; c < nc; ++c) {
+        const int s = c & 1;
+        if (c >= 2) mbar_wait(&empty[s], ((c >> 1) & 1) ^ 1);
+        const int64_t row0 = s0 + (int64_t)c * kCB;
+        uint8_t* st = smem + s * kStage;
+        mbar_expect_tx(&full[s], kStage);
+        tma_load_3d(st, &tmQ, &full[s], 0, (int)(grp * prm.N + row0), 0);
+        tma_load_3d(st + kT64, &tmK, &full[s], 0, (int)(grp * prm.N + row0), 0);
+        tma_load_3d(st + 2 * kT64, &tmV, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
+        tma_load_3d(st + 3 * kT64, &tmW, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t f = kBF16 ? 1 : 0;
+    const uint32_t id_R = idesc_f16(128, 128, f, 1, 0);  // A = Q^T (MN), B = W_hat (K-major rows j)
+    const uint32_t id_S = idesc_f16(128, 128, f, 1, 0);  // A = K^T (MN), B = V (K-major rows j)
+    for (int c = 0; c < nc; ++c) {
+      const int s = c & 1;
+      const uint32_t st = smem_u32(smem + s * kStage);
+      mbar_wait(&full[s], (c >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        for (int ks = 0; ks < 4; ++ks)
+          mma_ss(tmem + 128, mn(st + kT64, ks, 8192), kd(st + 2 * kT64, ks, 128), id_S,
+                 (c > 0 || ks > 0) ? 1u : 0u);
+      }
+      __syncwarp();
+      mbar_wait(w_ready, c & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        for (int ks = 0; ks < 4; ++ks)
+          mma_ss(tmem, mn(st, ks, 8192), kd(st + 3 * kT64, ks, 128), id_R, (c > 0 || ks > 0) ? 1u : 0u);
+        mma_commit(&empty[s]);
+        if (c == nc - 1) mma_commit(done);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int et = (int)threadIdx.x - 64;
+    const uint32_t qd = warp & 3;
+    const int r = (int)(qd * 32 + lane_id());
+    float u = 0.f, z = 0.f, cc = 0.f;
+    uint4 o8[8];
+    float4 g8[2];
+    if (nc > 0) what_prefetch<kBF16>(prm, grp, s0, et, o8, g8);
+    for (int c = 0; c < nc; ++c) {
+      const int s = c & 1;
+      uint8_t* st = smem + s * kStage;
+      named_bar(1, 128);  // previous chunk's s_s readers are done
+      mbar_wait(&full[s], (c >> 1) & 1);
+      what_pass<kBF16>(st + 3 * kT64, o8, g8, s_s, et);
+      if (c + 1 < nc) what_prefetch<kBF16>(prm, grp, s0 + (int64_t)(c + 1) * kCB, et, o8, g8);
+      fence_proxy_async();
+      mbar_arrive(w_ready);
+      named_bar(1, 128);  // s_s and W_hat complete
+      // u_m += sum_i q_im s_i ; z_m += sum_t k_tm   (m = r) ; c_j += sum_i w_hat_ji (j = r)
+#pragma unroll 8
+      for (int i = 0; i < kCB; ++i) {
+        u += h2f<kBF16>(*(const uint16_t*)(st + sw128_off(i, r, kCB))) * s_s[i];
+        z += h2f<kBF16>(*(const uint16_t*)(st + kT64 + sw128_off(i, r, kCB)));
+      }
+#pragma unroll
+      for (int i8 = 0; i8 < kCB; i8 += 8) {
+        const uint4 v4 = *(const uint4*)(st + 3 * kT64 + sw128_off(r, i8, 128));
+        const uint32_t w4[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 f2 = unpack2<kBF16>(w4[q]);
+          cc += f2.x + f2.y;
+        }
+      }
+      mbar_arrive(&empty[s]);
+    }
+    float* rS = prm.stS + (grp * prm.P + p) * state_floats(kD);
+    float* rR = prm.stR + (grp * prm.P + p) * state_floats(kD);
+    const uint32_t lb = (qd * 32u) << 16;
+    if (nc > 0) {
+      mbar_wait(done, 0);
+      tc_fence_after();
+    }
+    for (int j0 = 0; j0 < kD; j0 += 32) {
+      uint32_t xr[32], xs[32];
+      if (nc > 0) {
+        tmem_ld32(tmem + lb + j0, xr);
+        tmem_ld32(tmem + lb + 128 + j0, xs);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) xr[q] = xs[q] = 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < 32; q += 4) {
+        *(float4*)(rR + r * kD + j0 + q) = make_float4(__uint_as_float(xr[q]), __uint_as_float(xr[q + 1]),
+                                                      __uint_as_float(xr[q + 2]), __uint_as_float(xr[q + 3]));
+        *(float4*)(rS + r * kD + j0 + q) = make_float4(__uint_as_float(xs[q]), __uint_as_float(xs[q + 1]),
+                                                      __uint_as_float(xs[q + 2]), __uint_as_float(xs[q + 3]));
+      }
+    }
+    rS[kD * kD + r] = z;
+    rR[kD * kD + r] = u;
+    rR[kD * kD + kD + r] = cc;
+    if (r == 0) {
+      rS[kD * kD + 2 * kD] = (float)(s1 - s0);
+      rR[kD * kD + 2 * kD] = (float)(s1 - s0);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<256>(tmem);
+}
+
+// Scan: S records -> inclusive prefix (+carry), R records -> exclusive suffix (+carry).
+__global__ void k_scan_bwd(float* stS, float* stR, int P, int64_t SZ, const float* carry_pre,
+                           const float* carry_suf) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t grp = blockIdx.y;
+  if (e >= SZ) return;
+  float* bs = stS + grp * P * SZ + e;
+  float* br = stR + grp * P * SZ + e;
+  float run = carry_pre ? carry_pre[grp * SZ + e] : 0.f;
+  for (int q = 0; q < P; ++q) {
+    run += bs[q * SZ];
+    bs[q * SZ] = run;
+  }
+  run = carry_suf ? carry_suf[grp * SZ + e] : 0.f;
+  for (int q = P - 1; q >= 0; --q) {
+    const float t = br[q * SZ];
+    br[q * SZ] = run;
+    run += t;
+  }
+}
+
+// ================================================================ main reverse sweep
+template <bool kBF16>
+__global__ void __launch_bounds__(192, 1)
+    k_bwd_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmW,
+             BwdParams prm) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sP = smem + 2 * kStage;         // P  [64 rows i][64 t]     8 KB
+  uint8_t* sdS = sP + 8192;                // dS [64 rows i][64 t]     8 KB
+  uint8_t* sR = sdS + 8192;                // b R  [128 rows m][128 j] 32 KB
+  uint8_t* sS = sR + 32768;                // b S  [128 rows m][128 j] 32 KB
+  uint64_t* bars = (uint64_t*)(sS + 32768);
+  uint64_t* full = bars;        // [2]
+  uint64_t* empty = bars + 2;   // [2]
+  uint64_t* w_ready = bars + 4;
+  uint64_t* s_full = bars + 5;
+  uint64_t* dpt_full = bars + 6;
+  uint64_t* dpt_empty = bars + 7;
+  uint64_t* sS_ready = bars + 8;
+  uint64_t* ps_ready = bars + 9;
+  uint64_t* sR_ready = bars + 10;
+  uint64_t* gr_full = bars + 11;
+  uint64_t* gr_empty = bars + 12;
+  uint64_t* r_full = bars + 13;
+  uint32_t* tslot = (uint32_t*)(bars + 16);
+  float* s_s = (float*)(bars + 20);   // [64]
+  float* zq = s_s + kCB;              // [128]
+
+  const int p = blockIdx.x;
+  const int64_t grp = blockIdx.y;
+  const int64_t s0 = (int64_t)p * prm.seg_len;
+  const int64_t s1 = lmin(prm.N, s0 + prm.seg_len);
+  const int nc = (int)((s1 - s0) / kCB);
+  const uint32_t warp = warp_id();
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmW);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1 + 128);
+    }
+    mbar_init(w_ready, 128);
+    mbar_init(s_full, 1);
+    mbar_init(dpt_full, 1);
+    mbar_init(dpt_empty, 128);
+    mbar_init(sS_ready, 128);
+    mbar_init(ps_ready, 128);
+    mbar_init(sR_ready, 128);
+    mbar_init(gr_full, 1);
+    mbar_init(gr_empty, 128);
+    mbar_init(r_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (reverse)
+    if (elect_one()) {
+      for (int n = 0; n < nc; ++n) {
+        const int s = n & 1;
+        if (n >= 2) mbar_wait(&empty[s], ((n >> 1) & 1) ^ 1);
+        const int64_t row0 = s0 + (int64_t)(nc - 1 - n) * kCB;
+        uint8_t* st = smem + s * kStage;
+        mbar_expect_tx(&full[s], kStage);
+        tma_load_3d(st, &tmQ, &full[s], 0, (int)(grp * prm.N + row0), 0);
+        tma_load_3d(st + kT64, &tmK, &full[s], 0, (int)(grp * prm.N + row0), 0);
+        tma_load_3d(st + 2 * kT64, &tmV, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
+        tma_load_3d(st + 3 * kT64, &tmW, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t f = kBF16 ? 1 : 0;
+    const uint32_t id_T1 = idesc_f16(64, 64, f, 0, 0);
+    const uint32_t id_dPt = idesc_f16(64, 64, f, 1, 1);
+    const uint32_t id_Sneg = idesc_f16(128, 128, f, 1, 0, 1);
+    const uint32_t id_dQ1 = idesc_f16(64, 64, f, 0, 1);
+    const uint32_t id_dQ2 = idesc_f16(64, 64, f, 1, 0);
+    const uint32_t id_dK1 = idesc_f16(128, 64, f, 1, 1);
+    const uint32_t id_dK2 = idesc_f16(128, 64, f, 0, 1);
+    const uint32_t id_dV1 = idesc_f16(128, 64, f, 0, 1);
+    const uint32_t id_dV2 = idesc_f16(128, 64, f, 1, 0);
+    const uint32_t id_R = idesc_f16(128, 128, f, 1, 0);
+    const uint32_t aP = smem_u32(sP), adS = smem_u32(sdS), aR = smem_u32(sR), aS = smem_u32(sS);
+    for (int n = 0; n < nc; ++n) {
+      const int s = n & 1;
+      const uint32_t aQ = smem_u32(smem + s * kStage), aK = aQ + kT64, aV = aQ + 2 * kT64,
+                     aW = aQ + 3 * kT64;
+      mbar_wait(&full[s], (n >> 1) & 1);
+      if (n >= 1) mbar_wait(dpt_empty, (n - 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        for (int ks = 0; ks < 8; ++ks)  // T1 = Q K^T -> upper lane half
+          mma_ss(tmem + kDP + kHalf, kd(aQ, ks, 64), kd(aK, ks, 64), id_T1, ks > 0);
+        for (int ks = 0; ks < 4; ++ks)  // S -= K^T V
+          mma_ss(tmem + kS, mn(aK, ks, 8192), kd(aV, ks, 128), id_Sneg, 1);
+        mma_commit(s_full);
+      }
+      __syncwarp();
+      mbar_wait(w_ready, n & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        for (int ks = 0; ks < 8; ++ks)  // dPt = W_hat V^T -> lower lane half
+          mma_ss(tmem + kDP, mn(aW, ks, 8192), mn(aV, ks, 8192), id_dPt, ks > 0);
+        mma_commit(dpt_full);
+      }
+      __syncwarp();
+      mbar_wait(sS_ready, n & 1);
+      mbar_wait(ps_ready, n & 1);
+      if (n >= 1) mbar_wait(gr_empty, (n - 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        for (int h = 0; h < 2; ++h) {  // dQ[:, 64h:64h+64]
+          const uint32_t d = tmem + kDQ + (h ? kHalf : 0u);
+          for (int ks = 0; ks < 4; ++ks)  // dS K
+            mma_ss(d, kd(adS, ks, 64), mn(aK + h * 8192, ks, 8192), id_dQ1, ks > 0);
+          for (int ks = 0; ks < 8; ++ks)  // W_hat (b S)^T
+            mma_ss(d, mn(aW, ks, 8192), kd(aS + h * 8192, ks, 128), id_dQ2, 1);
+        }
+      }
+      __syncwarp();
+      mbar_wait(sR_ready, n & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        for (int ks = 0; ks < 4; ++ks)  // dK^T = Q^T dS^T
+          mma_ss(tmem + kDK, mn(aQ, ks, 8192), mn(adS, ks, 8192), id_dK1, ks > 0);
+        for (int ks = 0; ks < 8; ++ks)  //      + (b R) V^T
+          mma_ss(tmem + kDK, kd(aR, ks, 128), mn(aV, ks, 8192), id_dK2, 1);
+        for (int ks = 0; ks < 4; ++ks)  // dV^T = W_hat^T P
+          mma_ss(tmem + kDV, kd(aW, ks, 128), mn(aP, ks, 8192), id_dV1, ks > 0);
+        for (int ks = 0; ks < 8; ++ks)  //      + (b R)^T K^T
+          mma_ss(tmem + kDV, mn(aR, ks, 16384), kd(aK, ks, 64), id_dV2, 1);
+        mma_commit(gr_full);
+        for (int ks = 0; ks < 4; ++ks)  // R += Q^T W_hat
+          mma_ss(tmem + kR, mn(aQ, ks, 8192), kd(aW, ks, 128), id_R, 1);
+        mma_commit(r_full);
+        mma_commit(&empty[s]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 2..5)
+    const uint32_t qd = warp & 3;
+    const int l = (int)lane_id();
+    const int r = (int)(qd * 32) + l;            // full-lane row: m (R, S, dK) or j (dV)
+    const int ih = (int)(qd * 16) + (l & 15);    // half-lane row i of M=64 accumulators
+    const bool upper = l >= 16;                  // lanes 16..31 of a quadrant: upper half
+    const uint32_t lb = (qd * 32u) << 16;
+    const int et = (int)threadIdx.x - 64;
+    const float a = prm.a, b = prm.b;
+    const float* recS = prm.stS + (grp * prm.P + p) * state_floats(kD);  // inclusive prefix at s1
+    const float* recR = prm.stR + (grp * prm.P + p) * state_floats(kD);  // exclusive suffix after s1
+    // carries: R_next and S_end into TMEM (lanes m), u, c, z
+    for (int j0 = 0; j0 < kD; j0 += 32) {
+      uint32_t xr[32], xs[32];
+#pragma unroll
+      for (int q = 0; q < 32; q += 4) {
+        const float4 fr = *(const float4*)(recR + r * kD + j0 + q);
+        const float4 fs = *(const float4*)(recS + r * kD + j0 + q);
+        xr[q] = __float_as_uint(fr.x); xr[q + 1] = __float_as_uint(fr.y);
+        xr[q + 2] = __float_as_uint(fr.z); xr[q + 3] = __float_as_uint(fr.w);
+        xs[q] = __float_as_uint(fs.x); xs[q + 1] = __float_as_uint(fs.y);
+        xs[q + 2] = __float_as_uint(fs.z); xs[q + 3] = __float_as_uint(fs.w);
+      }
+      tmem_st32(tmem + lb + kR + j0, xr);
+      tmem_st32(tmem + lb + kS + j0, xs);
+    }
+    tmem_st_wait();
+    float u = recR[kD * kD + r];        // u_next (m = r)
+    float cj = recR[kD * kD + kD + r];  // c_next (j = r)
+    zq[r] = recS[kD * kD + r];          // z at the segment end
+    tc_fence_before();
+    named_bar(1, 128);
+    tc_fence_after();
+
+    uint4 o8[8];
+    float4 g8[2];
+    if (nc > 0) what_prefetch<kBF16>(prm, grp, s0 + (int64_t)(nc - 1) * kCB, et, o8, g8);
+    for (int n = 0; n < nc; ++n) {
+      const int s = n & 1;
+      const int64_t row0 = s0 + (int64_t)(nc - 1 - n) * kCB;
+      uint8_t* st = smem + s * kStage;
+      const uint8_t* q_t = st;
+      const uint8_t* k_t = st + kT64;
+      uint8_t* w_t = st + 3 * kT64;
+      // ---- E0: W_hat, s
+      named_bar(1, 128);
+      mbar_wait(&full[s], (n >> 1) & 1);
+      what_pass<kBF16>(w_t, o8, g8, s_s, et);
+      if (n + 1 < nc) what_prefetch<kBF16>(prm, grp, row0 - kCB, et, o8, g8);
+      fence_proxy_async();
+      mbar_arrive(w_ready);
+      named_bar(1, 128);  // s_s complete before any thread reads it
+      // ---- E_R: b R_next -> sR
+      if (n >= 1) mbar_wait(r_full, (n - 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int j0 = 0; j0 < kD; j0 += 32) {
+        uint32_t x[32];
+        tmem_ld32(tmem + lb + kR + j0, x);
+        tmem_ld_wait();
+#pragma unroll
+        for (int w8 = 0; w8 < 4; ++w8) {
+          uint4 v;
+          v.x = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 0]), b * __uint_as_float(x[8 * w8 + 1]));
+          v.y = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 2]), b * __uint_as_float(x[8 * w8 + 3]));
+          v.z = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 4]), b * __uint_as_float(x[8 * w8 + 5]));
+          v.w = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 6]), b * __uint_as_float(x[8 * w8 + 7]));
+          *(uint4*)(sR + sw128_off(r, j0 + 8 * w8, 128)) = v;
+        }
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(sR_ready);
+      // ---- E_S: b S_prev -> sS ; z_prev
+      mbar_wait(s_full, n & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int j0 = 0; j0 < kD; j0 += 32) {
+        uint32_t x[32];
+        tmem_ld32(tmem + lb + kS + j0, x);
+        tmem_ld_wait();
+#pragma unroll
+        for (int w8 = 0; w8 < 4; ++w8) {
+          uint4 v;
+          v.x = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 0]), b * __uint_as_float(x[8 * w8 + 1]));
+          v.y = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 2]), b * __uint_as_float(x[8 * w8 + 3]));
+          v.z = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 4]), b * __uint_as_float(x[8 * w8 + 5]));
+          v.w = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 6]), b * __uint_as_float(x[8 * w8 + 7]));
+          *(uint4*)(sS + sw128_off(r, j0 + 8 * w8, 128)) = v;
+        }
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(sS_ready);
+      {
+        float ks_ = 0.f;  // z_m -= sum_t k_tm over this chunk (m = r)
+#pragma unroll 8
+        for (int t = 0; t < kCB; ++t) ks_ += h2f<kBF16>(*(const uint16_t*)(k_t + sw128_off(t, r, kCB)));
+        zq[r] -= ks_;
+      }
+      // ---- E1: dPt -> dS (lower half lanes), T1 -> P (upper half lanes)
+      mbar_wait(dpt_full, n & 1);
+      tc_fence_after();
+      {
+        const float si = s_s[ih];
+        uint8_t* dst = upper ? sP : sdS;
+#pragma unroll 1
+        for (int t0 = 0; t0 < kCB; t0 += 32) {
+          uint32_t x[32];
+          tmem_ld32(tmem + lb + kDP + t0, x);
+          tmem_ld_wait();
+#pragma unroll
+          for (int w8 = 0; w8 < 4; ++w8) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int t = t0 + 8 * w8 + 2 * q;
+              const float x0 = __uint_as_float(x[8 * w8 + 2 * q]), x1 = __uint_as_float(x[8 * w8 + 2 * q + 1]);
+              float v0, v1;
+              if (upper) {
+                v0 = t <= ih ? a + b * x0 : 0.f;
+                v1 = t + 1 <= ih ? a + b * x1 : 0.f;
+              } else {
+                v0 = t <= ih ? b * (x0 - si) : 0.f;
+                v1 = t + 1 <= ih ? b * (x1 - si) : 0.f;
+              }
+              pk[q] = pack2<kBF16>(v0, v1);
+            }
+            *(uint4*)(dst + sw128_off(ih, t0 + 8 * w8, kCB)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+        }
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(dpt_empty);
+      mbar_arrive(ps_ready);
+      named_bar(1, 128);  // zq updated by every thread
+      // ---- E_out: dQ (half lanes), dK^T (lanes m), dV^T (lanes j)
+      mbar_wait(gr_full, n & 1);
+      tc_fence_after();
+      {
+        const float si = s_s[ih];
+        const int m0 = upper ? 64 : 0;
+        uint16_t* dq = (uint16_t*)prm.dq + (grp * prm.N + row0 + ih) * kD + m0;
+#pragma unroll 1
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          uint32_t x[32];
+          tmem_ld32(tmem + lb + kDQ + c0, x);
+          tmem_ld_wait();
+          uint32_t pk[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int m = m0 + c0 + 2 * q;
+            pk[q] = pack2<kBF16>(__uint_as_float(x[2 * q]) - si * b * zq[m],
+                                 __uint_as_float(x[2 * q + 1]) - si * b * zq[m + 1]);
+          }
+#pragma unroll
+          for (int w4 = 0; w4 < 4; ++w4)
+            *(uint4*)(dq + c0 + 8 * w4) = make_uint4(pk[4 * w4], pk[4 * w4 + 1], pk[4 * w4 + 2], pk[4 * w4 + 3]);
+        }
+      }
+      {
+        uint16_t* dk = (uint16_t*)prm.dk + (grp * kD + r) * prm.N + row0;
+        uint16_t* dv = (uint16_t*)prm.dv + (grp * kD + r) * prm.N + row0;
+        const float bu = b * u, ac = a * cj;
+#pragma unroll 1
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          uint32_t xk[32], xv[32];
+          tmem_ld32(tmem + lb + kDK + c0, xk);
+          tmem_ld32(tmem + lb + kDV + c0, xv);
+          tmem_ld_wait();
+          uint32_t pkk[16], pkv[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            pkk[q] = pack2<kBF16>(__uint_as_float(xk[2 * q]) - bu, __uint_as_float(xk[2 * q + 1]) - bu);
+            pkv[q] = pack2<kBF16>(__uint_as_float(xv[2 * q]) + ac, __uint_as_float(xv[2 * q + 1]) + ac);
+          }
+#pragma unroll
+          for (int w4 = 0; w4 < 4; ++w4) {
+            *(uint4*)(dk + c0 + 8 * w4) = make_uint4(pkk[4 * w4], pkk[4 * w4 + 1], pkk[4 * w4 + 2], pkk[4 * w4 + 3]);
+            *(uint4*)(dv + c0 + 8 * w4) = make_uint4(pkv[4 * w4], pkv[4 * w4 + 1], pkv[4 * w4 + 2], pkv[4 * w4 + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(gr_empty);
+      // ---- suffix vectors: u_m += sum_i q_im s_i ; c_j += sum_i w_hat_ji
+#pragma unroll 8
+      for (int i = 0; i < kCB; ++i) u += h2f<kBF16>(*(const uint16_t*)(q_t + sw128_off(i, r, kCB))) * s_s[i];
+#pragma unroll
+      for (int i8 = 0; i8 < kCB; i8 += 8) {
+        const uint4 v4 = *(const uint4*)(w_t + sw128_off(r, i8, 128));
+        const uint32_t w4[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 f2 = unpack2<kBF16>(w4[q]);
+          cj += f2.x + f2.y;
+        }
+      }
+      mbar_arrive(&empty[s]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+constexpr size_t kAggSmemB = 2 * kStage + 512 + 1024;
+constexpr size_t kMainSmemB = 2 * kStage + 2 * 8192 + 2 * 32768 + 160 + (kCB + kD) * 4 + 1024;
+
+int tcb_segments(int64_t G, int64_t N) {
+  const int64_t chunks = N / kCB;
+  int64_t p = (3 * 148 + G - 1) / G;
+  p = lmin(p, lmax(1, chunks / 16));
+  return (int)lmax(1, p);
+}
+
+}  // namespace
+
+bool tc_backward_supported(const Launch& L, const Tensors& t) {
+  return (L.dtype == LA_BF16 || L.dtype == LA_F16) && L.D == kD && L.causal && L.fault == LA_FAULT_NONE &&
+         L.N % kCB == 0 && t.lq == LA_SEQUENCE_MAJOR && t.lk == LA_SEQUENCE_MAJOR &&
+         t.lv == LA_FEATURE_MAJOR && t.lw == LA_FEATURE_MAJOR && t.lo == LA_FEATURE_MAJOR &&
+         L.G * L.N < (1ll << 31) && L.G * kD < (1ll << 31);
+}
+
+size_t tc_backward_ws_floats(int64_t G, int64_t N, int64_t D) {
+  if (D != kD || N % kCB) return 0;
+  return (size_t)(2 * G * tcb_segments(G, N) * state_floats(kD));
+}
+
+cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv, Workspace ws) {
+  const bool bf = L.dtype == LA_BF16;
+  const int64_t G = L.G, N = L.N;
+  const int P = tcb_segments(G, N);
+  const int64_t chunks = N / kCB;
+  const int64_t seg = ((chunks + P - 1) / P) * kCB;
+  const int64_t SZ = state_floats(kD);
+  float* stS = ws.base;
+  float* stR = stS + G * P * SZ;
+  CUtensorMap mQ, mK, mV, mW;
+  if (!make_tma_map(&mQ, t.q, bf, (uint64_t)(G * N), kD, 64, 2) ||
+      !make_tma_map(&mK, t.k, bf, (uint64_t)(G * N), kD, 64, 2) ||
+      !make_tma_map(&mV, t.v, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1) ||
+      !make_tma_map(&mW, t.w, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1))
+    return cudaErrorInvalidValue;
+  BwdParams prm{t.o, t.g, dq, dk, dv, stS, stR, N, seg, P, L.a, L.b};
+  auto agg = bf ? k_bwd_agg_tc<true> : k_bwd_agg_tc<false>;
+  auto main_k = bf ? k_bwd_tc<true> : k_bwd_tc<false>;
+  cudaFuncSetAttribute(agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggSmemB);
+  cudaFuncSetAttribute(main_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmemB);
+  {
+    ProfScope ps("la_bwd_agg", L.stream);
+    agg<<<dim3(P, G), 192, kAggSmemB, L.stream>>>(mQ, mK, mV, mW, prm);
+  }
+  {
+    ProfScope ps("la_bwd_scan", L.stream);
+    k_scan_bwd<<<dim3((unsigned)((SZ + 255) / 256), (unsigned)G), 256, 0, L.stream>>>(
+        stS, stR, P, SZ, L.carry_prefix, L.carry_suffix);
+  }
+  {
+    ProfScope ps("la_bwd_causal", L.stream);
+    main_k<<<dim3(P, G), 192, kMainSmemB, L.stream>>>(mQ, mK, mV, mW, prm);
+  }
+  note_launch(3);
+  return cudaGetLastError();
+}
+
+}  // namespace lab
