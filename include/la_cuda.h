@@ -107,7 +107,7 @@ const char* la_version(void);
 const char* la_status_name(la_status s);
 size_t la_forward_workspace_bytes(const la_problem* p);
 size_t la_backward_workspace_bytes(const la_problem* p);
-size_t la_shard_state_floats(const la_problem* p); /* G * (D*D + 2*D + 1) */
+size_t la_shard_state_floats(const la_problem* p); /* G * (D*D + 2*D + 1, padded to 4) */
 la_status la_validate_plan(const la_block_plan* plan, int64_t groups, int64_t dim,
                            la_error_info* err);
 la_status la_default_plan(int64_t groups, int64_t dim, int32_t workers, la_block_plan* out);

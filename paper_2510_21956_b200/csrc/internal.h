@@ -15,7 +15,7 @@ namespace lab {
 #ifdef __CUDACC__
 __host__ __device__
 #endif
-inline int64_t state_floats(int64_t d) { return d * d + 2 * d + 1; }
+inline int64_t state_floats(int64_t d) { return (d * d + 2 * d + 1 + 3) & ~(int64_t)3; }  // 16-byte records
 
 struct Tensors {
   const void* q; int lq;
