@@ -16,6 +16,8 @@
 //   [0,64) dPt (lanes 0-15,32-47,..) + T1 (other half), [64,128) dQ halves,
 //   [128,192) dK^T, [192,256) dV^T, [256,384) R, [384,512) S.
 // Segment carries: an aggregate pass (R, u, c and S, z per segment) + scan.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 #include "sm100.cuh"
@@ -61,6 +63,7 @@ struct BwdParams {
   int64_t seg_len;
   int P;
   float a, b;
+  int dbg;  // debug bitmask (LA_BWD_DEBUG): 1 skip dS K, 2 skip W_hat S^T
 };
 
 // Epilogue step E0: W_hat = omega / g in place (bf16) and s_i = sum_j o_ij w_hat_ij.
@@ -356,6 +359,39 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  // Carries (R_next, S_end, u, c, z) are written into TMEM by the epilogue warps
+  // before any role starts: the first S -= K^T V must see S_end.
+  float u = 0.f, cj = 0.f;
+  if (warp >= 2) {
+    const uint32_t qd = warp & 3;
+    const int r = (int)(qd * 32 + lane_id());
+    const uint32_t lb = (qd * 32u) << 16;
+    const float* recS = prm.stS + (grp * prm.P + p) * state_floats(kD);  // inclusive prefix at s1
+    const float* recR = prm.stR + (grp * prm.P + p) * state_floats(kD);  // exclusive suffix after s1
+    // carries: R_next and S_end into TMEM (lanes m), u, c, z
+    for (int j0 = 0; j0 < kD; j0 += 32) {
+      uint32_t xr[32], xs[32];
+#pragma unroll
+      for (int q = 0; q < 32; q += 4) {
+        const float4 fr = *(const float4*)(recR + r * kD + j0 + q);
+        const float4 fs = *(const float4*)(recS + r * kD + j0 + q);
+        xr[q] = __float_as_uint(fr.x); xr[q + 1] = __float_as_uint(fr.y);
+        xr[q + 2] = __float_as_uint(fr.z); xr[q + 3] = __float_as_uint(fr.w);
+        xs[q] = __float_as_uint(fs.x); xs[q + 1] = __float_as_uint(fs.y);
+        xs[q + 2] = __float_as_uint(fs.z); xs[q + 3] = __float_as_uint(fs.w);
+      }
+      tmem_st32(tmem + lb + kR + j0, xr);
+      tmem_st32(tmem + lb + kS + j0, xs);
+    }
+    tmem_st_wait();
+    u = recR[kD * kD + r];        // u_next (m = r)
+    cj = recR[kD * kD + kD + r];  // c_next (j = r)
+    zq[r] = recS[kD * kD + r];          // z at the segment end
+
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (reverse)
@@ -397,7 +433,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int ks = 0; ks < 8; ++ks)  // T1 = Q K^T -> upper lane half
           mma_ss(tmem + kDP + kHalf, kd(aQ, ks, 64), kd(aK, ks, 64), id_T1, ks > 0);
         for (int ks = 0; ks < 4; ++ks)  // S -= K^T V
-          mma_ss(tmem + kS, mn(aK, ks, 8192), kd(aV, ks, 128), id_Sneg, 1);
+          if (!(prm.dbg & 4)) mma_ss(tmem + kS, mn(aK, ks, 8192), kd(aV, ks, 128), id_Sneg, 1);
         mma_commit(s_full);
       }
       __syncwarp();
@@ -417,9 +453,9 @@ __global__ void __launch_bounds__(192, 1)
         for (int h = 0; h < 2; ++h) {  // dQ[:, 64h:64h+64]
           const uint32_t d = tmem + kDQ + (h ? kHalf : 0u);
           for (int ks = 0; ks < 4; ++ks)  // dS K
-            mma_ss(d, kd(adS, ks, 64), mn(aK + h * 8192, ks, 8192), id_dQ1, ks > 0);
+            if (!(prm.dbg & 1)) mma_ss(d, kd(adS, ks, 64), mn(aK + h * 8192, ks, 8192), id_dQ1, ks > 0);
           for (int ks = 0; ks < 8; ++ks)  // W_hat (b S)^T
-            mma_ss(d, mn(aW, ks, 8192), kd(aS + h * 8192, ks, 128), id_dQ2, 1);
+            if (!(prm.dbg & 2)) mma_ss(d, mn(aW, ks, 8192), kd(aS + h * 8192, ks, 128), id_dQ2, (prm.dbg & 1) ? ks > 0 : 1);
         }
       }
       __syncwarp();
@@ -452,31 +488,6 @@ __global__ void __launch_bounds__(192, 1)
     const uint32_t lb = (qd * 32u) << 16;
     const int et = (int)threadIdx.x - 64;
     const float a = prm.a, b = prm.b;
-    const float* recS = prm.stS + (grp * prm.P + p) * state_floats(kD);  // inclusive prefix at s1
-    const float* recR = prm.stR + (grp * prm.P + p) * state_floats(kD);  // exclusive suffix after s1
-    // carries: R_next and S_end into TMEM (lanes m), u, c, z
-    for (int j0 = 0; j0 < kD; j0 += 32) {
-      uint32_t xr[32], xs[32];
-#pragma unroll
-      for (int q = 0; q < 32; q += 4) {
-        const float4 fr = *(const float4*)(recR + r * kD + j0 + q);
-        const float4 fs = *(const float4*)(recS + r * kD + j0 + q);
-        xr[q] = __float_as_uint(fr.x); xr[q + 1] = __float_as_uint(fr.y);
-        xr[q + 2] = __float_as_uint(fr.z); xr[q + 3] = __float_as_uint(fr.w);
-        xs[q] = __float_as_uint(fs.x); xs[q + 1] = __float_as_uint(fs.y);
-        xs[q + 2] = __float_as_uint(fs.z); xs[q + 3] = __float_as_uint(fs.w);
-      }
-      tmem_st32(tmem + lb + kR + j0, xr);
-      tmem_st32(tmem + lb + kS + j0, xs);
-    }
-    tmem_st_wait();
-    float u = recR[kD * kD + r];        // u_next (m = r)
-    float cj = recR[kD * kD + kD + r];  // c_next (j = r)
-    zq[r] = recS[kD * kD + r];          // z at the segment end
-    tc_fence_before();
-    named_bar(1, 128);
-    tc_fence_after();
-
     uint4 o8[8];
     float4 g8[2];
     if (nc > 0) what_prefetch<kBF16>(prm, grp, s0 + (int64_t)(nc - 1) * kCB, et, o8, g8);
@@ -689,7 +700,8 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
       !make_tma_map(&mV, t.v, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1) ||
       !make_tma_map(&mW, t.w, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1))
     return cudaErrorInvalidValue;
-  BwdParams prm{t.o, t.g, dq, dk, dv, stS, stR, N, seg, P, L.a, L.b};
+  const char* dbg = getenv("LA_BWD_DEBUG");
+  BwdParams prm{t.o, t.g, dq, dk, dv, stS, stR, N, seg, P, L.a, L.b, dbg ? atoi(dbg) : 0};
   auto agg = bf ? k_bwd_agg_tc<true> : k_bwd_agg_tc<false>;
   auto main_k = bf ? k_bwd_tc<true> : k_bwd_tc<false>;
   cudaFuncSetAttribute(agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggSmemB);

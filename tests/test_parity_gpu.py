@@ -23,7 +23,7 @@ def dev(x, dtype, layout, cuda):
 
 
 def run_dev(q, k, v, w, dtype, cuda, causal=True, a=1.0, b=1.0, impl="auto", fault=la.Fault.None_,
-            lq=SM, lk=SM, lv=FM, lw=FM):
+            lq=SM, lk=SM, lv=FM, lw=FM, impl_bwd=None):
     qt, qr = dev(q, dtype, lq, cuda)
     kt, kr = dev(k, dtype, lk, cuda)
     vt, vr = dev(v, dtype, lv, cuda)
@@ -35,7 +35,7 @@ def run_dev(q, k, v, w, dtype, cuda, causal=True, a=1.0, b=1.0, impl="auto", fau
            "rounded": (qr, kr, vr)}
     if w is not None:
         wt, wr = dev(w, dtype, lw, cuda)
-        gr = bwd(art, wt, c, None, fault, impl=impl)
+        gr = bwd(art, wt, c, None, fault, impl=impl_bwd or impl)
         res.update(dq=gr.dq.logical(), dk=gr.dk.logical(), dv=gr.dv.logical(), w=wr)
     return res
 
