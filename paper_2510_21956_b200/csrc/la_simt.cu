@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(512) k_fwd_rows(const T* q, Strides sq, const 
   const int64_t j0 = (int64_t)blockIdx.z * rb;
   const bool jok = act && j0 + jl < D;
   const int64_t j = jok ? j0 + jl : 0;
-  const int64_t SZ = D * D + 2 * D + 1;
+  const int64_t SZ = state_floats(D);
   const float* st = states + (grp * P + p) * SZ;
   const T* qg = q + grp * N * D;
   const T* kg = k + grp * N * D;
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(512) k_bwd_rows(const T* q, Strides sq, const 
   const int64_t r0b = (int64_t)blockIdx.z * rb;
   const bool rok = act && r0b + rl < D;
   const int r = rok ? (int)(r0b + rl) : 0;
-  const int64_t SZ = D * D + 2 * D + 1;
+  const int64_t SZ = state_floats(D);
   const float* st = states + (grp * P + p) * SZ;
   const int64_t off = grp * N * D;
 
