@@ -13,6 +13,8 @@
 //   the TMEM<->register epilogue. Q/K/V tiles arrive by TMA (128B swizzle) in a
 //   2-stage ring. Segment carries come from an aggregate pass (S, z, sigma per
 //   segment via the same tcgen05 state MMA) and an exclusive scan.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 #include "sm100.cuh"
@@ -47,7 +49,7 @@ __device__ __forceinline__ uint64_t mndesc(uint32_t tile, int ks) {
 }
 
 struct FwdParams {
-  const float* states;  // per (g, segment) exclusive-prefix records
+  const float* states;  // per (g, segment) exclusive-prefix records, or null (no carry)
   float* gout;          // G*N
   unsigned long long* flag;
   int64_t N, G;
@@ -55,20 +57,25 @@ struct FwdParams {
   int P;
   int64_t row_offset;
   float a, b;
+  float* st_out;        // per-group final (S, z, sigma, rows) for the backward, or null
 };
 
 // ================================================================ forward main
+// Warp roles (320 threads): 0 TMA producer; 1 MMA issuer + TMEM owner;
+// 2-5 "WG-A" (S^T -> bf16 operand, T1 -> P', g, z); 6-9 "WG-B" (O^T -> o ->
+// TMA store through the chunk's Q slot, sigma). The two warpgroups overlap:
+// WG-A prepares chunk c+1 while WG-B drains chunk c.
 template <bool kBF16>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     k_fwd_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
              const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
              FwdParams prm) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sQ = smem;                  // [2][32K]
+  uint8_t* sQ = smem;                  // [2][32K]  (also the O^T staging of its chunk)
   uint8_t* sK = smem + 2 * kTile;      // [2][32K]
   uint8_t* sV = smem + 4 * kTile;      // [2][32K]  V^T tile: rows j, cols t
-  uint8_t* sP = smem + 6 * kTile;      // P' (rows i, cols t) / O^T staging (rows j, cols i)
+  uint8_t* sP = smem + 6 * kTile;      // P' (rows i, cols t)
   uint64_t* bars = (uint64_t*)(smem + 7 * kTile);
   uint64_t* full = bars;               // [2]
   uint64_t* empty = bars + 2;          // [2]
@@ -80,8 +87,8 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* o_full = bars + 9;
   uint64_t* ot_empty = bars + 10;
   uint32_t* tslot = (uint32_t*)(bars + 12);
-  float* ginv_s = (float*)(bars + 16);  // [128]
-  float* zq = ginv_s + kC;              // [128]
+  float* ginv_s = (float*)(bars + 16);  // [2][128]
+  float* zq = ginv_s + 2 * kC;          // [128]
 
   const int p = blockIdx.x;
   const int64_t grp = blockIdx.y;
@@ -97,7 +104,7 @@ __global__ void __launch_bounds__(192, 1)
     tma_prefetch(&tmO);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1 + 128);
+      mbar_init(&empty[s], 1 + 128 + 1);
     }
     mbar_init(t1_full, 1);
     mbar_init(t1_empty, 128);
@@ -113,6 +120,7 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  const float* st_in = prm.states ? prm.states + (grp * prm.P + p) * state_floats(kD) : nullptr;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -165,24 +173,21 @@ __global__ void __launch_bounds__(192, 1)
       }
       __syncwarp();
     }
-  } else {
-    // ------------------------------------------------------------ epilogue (warps 2..5)
-    const uint32_t qd = warp & 3;                 // TMEM lane quadrant of this warp
-    const int r = (int)(qd * 32 + lane_id());     // row owned: i for T1, j for O^T / S^T
+  } else if (warp < 6) {
+    // ------------------------------------------------------------ WG-A (warps 2..5)
+    const uint32_t qd = warp & 3;
+    const int r = (int)(qd * 32 + lane_id());
     const uint32_t lane_base = (qd * 32u) << 16;
-    const int et = (int)threadIdx.x - 64;         // 0..127
     const float a = prm.a, b = prm.b;
-    const float* st = prm.states + (grp * prm.P + p) * state_floats(kD);
-    // carry-in: S^T row r = S[:, r], z, sigma
+    // carry-in: S^T row r = S[:, r] and z (zero without a carry)
     for (int m0 = 0; m0 < kD; m0 += 32) {
       uint32_t v[32];
 #pragma unroll
-      for (int u = 0; u < 32; ++u) v[u] = __float_as_uint(st[(m0 + u) * kD + r]);
+      for (int u = 0; u < 32; ++u) v[u] = st_in ? __float_as_uint(st_in[(m0 + u) * kD + r]) : 0u;
       tmem_st32(tmem + lane_base + kST + m0, v);
     }
     tmem_st_wait();
-    zq[r] = st[kD * kD + r];
-    float sigma_prev = st[kD * kD + kD + r];
+    zq[r] = st_in ? st_in[kD * kD + r] : 0.f;
     tc_fence_before();
     named_bar(1, 128);
     tc_fence_after();
@@ -192,7 +197,6 @@ __global__ void __launch_bounds__(192, 1)
       const int64_t row0 = s0 + (int64_t)c * kC;
       const uint8_t* q_t = sQ + s * kTile;
       const uint8_t* k_t = sK + s * kTile;
-      const uint8_t* v_t = sV + s * kTile;
       // ---- E2: S^T -> bf16(b S^T) in TMEM (A operand of the Q S term)
       if (c >= 1) mbar_wait(st_full, (c - 1) & 1);
       tc_fence_after();
@@ -217,10 +221,6 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&full[s], (c >> 1) & 1);
       mbar_wait(t1_full, c & 1);
       tc_fence_after();
-      if (c >= 1) {
-        if (et == 0) tma_store_wait_read0();  // O^T staging of chunk c-1 has left sP
-        named_bar(1, 128);
-      }
       float rowsum = 0.f;
 #pragma unroll 1
       for (int cc = 0; cc < 4; ++cc) {
@@ -258,9 +258,76 @@ __global__ void __launch_bounds__(192, 1)
       }
       const float gi = rowsum + a * (float)(prm.row_offset + row0) + b * qz;
       if (fabsf(gi) < kEpsF32) flag_degenerate(prm.flag, grp, prm.row_offset + row0 + r);
-      ginv_s[r] = 1.f / gi;
+      ginv_s[s * kC + r] = 1.f / gi;
       prm.gout[grp * prm.N + row0 + r] = gi;
-      // sigma_j += sum_t V^T[j][t]   (j = r)
+      named_bar(1, 128);  // every WG-A thread is done reading zq
+      // z_m += sum_t K[t][m]   (m = r): 16 x 16B column reads, 8 m per load
+      {
+        float ks_ = 0.f;
+#pragma unroll 8
+        for (int t = 0; t < kC; ++t) {
+          const uint16_t h = *(const uint16_t*)(k_t + sw128_off(t, r, kC));
+          ks_ += kBF16 ? __bfloat162float(__ushort_as_bfloat16(h)) : __half2float(__ushort_as_half(h));
+        }
+        zq[r] += ks_;
+      }
+      fence_proxy_async();  // P' generic stores -> visible to the tensor core
+      mbar_arrive(p_ready);
+      mbar_arrive(&empty[s]);
+    }
+    if (prm.st_out && nc > 0) {  // final state for the backward (S, z)
+      mbar_wait(st_full, (nc - 1) & 1);
+      tc_fence_after();
+      float* so = prm.st_out + grp * state_floats(kD);
+      for (int m0 = 0; m0 < kD; m0 += 32) {
+        uint32_t x[32];
+        tmem_ld32(tmem + lane_base + kST + m0, x);
+        tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 32; ++u) so[(m0 + u) * kD + r] = __uint_as_float(x[u]);
+      }
+      so[kD * kD + r] = zq[r];
+      if (r == 0) so[kD * kD + 2 * kD] = (float)(prm.row_offset + s1);
+    }
+  } else {
+    // ------------------------------------------------------------ WG-B (warps 6..9)
+    const uint32_t qd = warp & 3;
+    const int r = (int)(qd * 32 + lane_id());     // j of O^T
+    const uint32_t lane_base = (qd * 32u) << 16;
+    const int eb = (int)threadIdx.x - 192;        // 0..127
+    const float a = prm.a;
+    float sigma = st_in ? st_in[kD * kD + kD + r] : 0.f;
+    for (int c = 0; c < nc; ++c) {
+      const int s = c & 1;
+      const int64_t row0 = s0 + (int64_t)c * kC;
+      uint8_t* stage_o = sQ + s * kTile;          // Q(c) is dead once O^T(c) is complete
+      const uint8_t* v_t = sV + s * kTile;
+      mbar_wait(o_full, c & 1);
+      mbar_wait(p_ready, c & 1);                  // WG-A finished reading Q(c); ginv(c) ready
+      tc_fence_after();
+      const float asig = a * sigma;
+      const float* gv = ginv_s + s * kC;
+#pragma unroll 1
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t x[32];
+        tmem_ld32(tmem + lane_base + kOT + cc * 32, x);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int i0 = cc * 32 + 2 * u;
+          pk[u] = pack2<kBF16>((__uint_as_float(x[2 * u]) + asig) * gv[i0],
+                               (__uint_as_float(x[2 * u + 1]) + asig) * gv[i0 + 1]);
+        }
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          uint4 v4 = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
+          *(uint4*)(stage_o + sw128_off(r, cc * 32 + 8 * w, kD)) = v4;
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(ot_empty);
+      // sigma_j += sum_t V^T[j][t]   (j = r), for the next chunk
       float vs = 0.f;
 #pragma unroll 4
       for (int t8 = 0; t8 < kC; t8 += 8) {
@@ -272,52 +339,18 @@ __global__ void __launch_bounds__(192, 1)
           vs += f.x + f.y;
         }
       }
-      named_bar(1, 128);  // every thread is done reading zq
-      // z_m += sum_t K[t][m]   (m = r)
-      float ks_ = 0.f;
-#pragma unroll 8
-      for (int t = 0; t < kC; ++t) {
-        const uint16_t h = *(const uint16_t*)(k_t + sw128_off(t, r, kC));
-        ks_ += kBF16 ? __bfloat162float(__ushort_as_bfloat16(h)) : __half2float(__ushort_as_half(h));
-      }
-      zq[r] += ks_;
-      fence_proxy_async();  // P' generic stores -> visible to the tensor core
-      mbar_arrive(p_ready);
-      mbar_arrive(&empty[s]);
-
-      // ---- E3: O^T -> o = (O^T + a sigma) / g -> bf16 -> TMA store
-      mbar_wait(o_full, c & 1);
-      tc_fence_after();
-      const float asig = a * sigma_prev;
-#pragma unroll 1
-      for (int cc = 0; cc < 4; ++cc) {
-        uint32_t x[32];
-        tmem_ld32(tmem + lane_base + kOT + cc * 32, x);
-        tmem_ld_wait();
-        uint32_t pk[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int i0 = cc * 32 + 2 * u;
-          pk[u] = pack2<kBF16>((__uint_as_float(x[2 * u]) + asig) * ginv_s[i0],
-                               (__uint_as_float(x[2 * u + 1]) + asig) * ginv_s[i0 + 1]);
-        }
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          uint4 v4 = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
-          *(uint4*)(sP + sw128_off(r, cc * 32 + 8 * w, kD)) = v4;
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(ot_empty);
-      sigma_prev += vs;
+      sigma += vs;
       fence_proxy_async();
-      named_bar(1, 128);
-      if (et == 0) {
-        tma_store_3d(&tmO, sP, 0, (int)(grp * kD), (int)(row0 / 64));
+      named_bar(2, 128);
+      if (eb == 0) {
+        tma_store_3d(&tmO, stage_o, 0, (int)(grp * kD), (int)(row0 / 64));
         tma_store_commit();
+        tma_store_wait_read0();   // staging (Q slot) read out -> the stage may be refilled
+        mbar_arrive(&empty[s]);
       }
     }
-    if (et == 0) tma_store_wait0();
+    if (eb == 0) tma_store_wait0();
+    if (prm.st_out && nc > 0) prm.st_out[grp * state_floats(kD) + kD * kD + kD + r] = sigma;
   }
   tc_fence_before();
   __syncthreads();
@@ -438,7 +471,7 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc<128>(tmem);
 }
 
-constexpr size_t kFwdSmem = 7 * kTile + 256 + 2 * kC * 4 + 1024;
+constexpr size_t kFwdSmem = 7 * kTile + 256 + 3 * kC * 4 + 1024;
 constexpr size_t kAggSmem = 4 * kTile + 128 + 1024;
 
 int tc_segments(int64_t G, int64_t N) {
@@ -470,28 +503,46 @@ bool tc_forward_supported(const Launch& L, const Tensors& t) {
          t.lv == LA_FEATURE_MAJOR && L.G * L.N < (1ll << 31) && L.G * kD < (1ll << 31);
 }
 
+// One CTA per group walks the whole sequence (no carries, no aggregate pass)
+// when there are enough groups to keep HBM busy; otherwise the sequence is cut
+// into segments whose exclusive-prefix carries come from k_fwd_agg_tc + scan.
+static bool per_group_mode(int64_t G) {
+  const char* e = getenv("LA_FWD_SEGMENTS");
+  if (e) return atoi(e) <= 1;
+  return G >= 48;
+}
+
 size_t tc_forward_ws_floats(int64_t G, int64_t N, int64_t D) {
   if (D != kD || N % kC) return 0;
-  return (size_t)(G * tc_segments(G, N) * state_floats(kD));
+  const int64_t seg = per_group_mode(G) ? 0 : G * tc_segments(G, N) * state_floats(kD);
+  return (size_t)(seg + G * state_floats(kD));  // + per-group final state
 }
 
 cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws) {
   const bool bf = L.dtype == LA_BF16;
   const int64_t G = L.G, N = L.N;
-  const int P = tc_segments(G, N);
-  const int64_t chunks = N / kC;
-  const int64_t seg = ((chunks + P - 1) / P) * kC;
   const int64_t SZ = state_floats(kD);
-  float* states = ws.base;
   CUtensorMap mQ, mK, mV, mO;
   if (!make_map(&mQ, t.q, bf, (uint64_t)(G * N), kD) || !make_map(&mK, t.k, bf, (uint64_t)(G * N), kD) ||
       !make_map(&mV, t.v, bf, (uint64_t)(G * kD), (uint64_t)N) ||
       !make_map(&mO, out, bf, (uint64_t)(G * kD), (uint64_t)N))
     return cudaErrorInvalidValue;
-  auto agg = bf ? k_fwd_agg_tc<true> : k_fwd_agg_tc<false>;
   auto main_k = bf ? k_fwd_tc<true> : k_fwd_tc<false>;
-  cudaFuncSetAttribute(agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggSmem);
   cudaFuncSetAttribute(main_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem);
+  float* final_state = ws.base;  // G * SZ: (S, z, sigma, rows) after the last row of each group
+  if (per_group_mode(G)) {
+    FwdParams prm{L.carry_prefix, g, ws.flag, N, G, N, 1, L.row_offset, L.a, L.b, final_state};
+    ProfScope ps("la_fwd_causal", L.stream);
+    main_k<<<dim3(1, G), 320, kFwdSmem, L.stream>>>(mQ, mK, mV, mO, prm);
+    note_launch(1);
+    return cudaGetLastError();
+  }
+  const int P = tc_segments(G, N);
+  const int64_t chunks = N / kC;
+  const int64_t seg = ((chunks + P - 1) / P) * kC;
+  float* states = ws.base + G * SZ;
+  auto agg = bf ? k_fwd_agg_tc<true> : k_fwd_agg_tc<false>;
+  cudaFuncSetAttribute(agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggSmem);
   {
     ProfScope ps("la_fwd_agg", L.stream);
     agg<<<dim3(P, G), 192, kAggSmem, L.stream>>>(mK, mV, states, N, seg, P);
@@ -501,14 +552,13 @@ cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, W
     k_scan_fwd<<<dim3((unsigned)((SZ + 255) / 256), (unsigned)G), 256, 0, L.stream>>>(states, P, SZ,
                                                                                     L.carry_prefix);
   }
-  FwdParams prm{states, g, ws.flag, N, G, seg, P, L.row_offset, L.a, L.b};
+  FwdParams prm{states, g, ws.flag, N, G, seg, P, L.row_offset, L.a, L.b, nullptr};
   {
     ProfScope ps("la_fwd_causal", L.stream);
-    main_k<<<dim3(P, G), 192, kFwdSmem, L.stream>>>(mQ, mK, mV, mO, prm);
+    main_k<<<dim3(P, G), 320, kFwdSmem, L.stream>>>(mQ, mK, mV, mO, prm);
   }
   note_launch(3);
   return cudaGetLastError();
 }
-
 
 }  // namespace lab
