@@ -32,7 +32,7 @@ constexpr int kTile = kC * kD * 2;  // 32 KB: one 128x128 16-bit tile (2 SW128 p
 constexpr int kPanel = 128 * 128;   // bytes per 64-column panel of 128 rows
 
 // TMEM columns (forward main)
-constexpr uint32_t kT1 = 0, kOT = 128, kST = 256, kSB = 384;
+constexpr uint32_t kT1 = 0, kOT = 128, kST = 256, kSB = 384;  // kSB: 2 x 64 columns
 
 // A (rows x 128) 16-bit tile of a row-major [R][inner] matrix as two SW128 panels.
 bool make_map(CUtensorMap* m, const void* base, bool bf16, uint64_t rows, uint64_t inner) {
@@ -86,7 +86,8 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* p_ready = bars + 8;
   uint64_t* o_full = bars + 9;
   uint64_t* ot_empty = bars + 10;
-  uint32_t* tslot = (uint32_t*)(bars + 12);
+  uint64_t* a2b = bars + 11;            // [2] WG-A -> WG-B per stage: Q(c) read, ginv(c) ready
+  uint32_t* tslot = (uint32_t*)(bars + 14);
   float* ginv_s = (float*)(bars + 16);  // [2][128]
   float* zq = ginv_s + 2 * kC;          // [128]
 
@@ -113,6 +114,8 @@ __global__ void __launch_bounds__(320, 1)
     mbar_init(p_ready, 128);
     mbar_init(o_full, 1);
     mbar_init(ot_empty, 128);
+    mbar_init(&a2b[0], 128);
+    mbar_init(&a2b[1], 128);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
@@ -137,21 +140,24 @@ __global__ void __launch_bounds__(320, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
+    // Order per chunk: M3(c) S^T update, M1(c+1) next T1, M2(c) O^T. T1 of chunk
+    // c+1 is ready while WG-B drains c; the tensor pipe stays busy.
     constexpr uint32_t fmt = kBF16 ? 1 : 0;
     const uint32_t id_kk = idesc_f16(128, 128, fmt, 0, 0);
     const uint32_t id_kmn = idesc_f16(128, 128, fmt, 0, 1);
     const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV), aP = smem_u32(sP);
-    for (int c = 0; c < nc; ++c) {
-      const int s = c & 1;
-      mbar_wait(&full[s], (c >> 1) & 1);
-      if (c >= 1) mbar_wait(t1_empty, (c - 1) & 1);
+    if (nc > 0) {
+      mbar_wait(&full[0], 0);
       tc_fence_after();
       if (elect_one()) {
-        for (int ks = 0; ks < 8; ++ks)  // T1 = Q K^T
-          mma_ss(tmem + kT1, kdesc(aQ + s * kTile, ks), kdesc(aK + s * kTile, ks), id_kk, ks > 0);
+        for (int ks = 0; ks < 8; ++ks)  // T1(0) = Q K^T
+          mma_ss(tmem + kT1, kdesc(aQ, ks), kdesc(aK, ks), id_kk, ks > 0);
         mma_commit(t1_full);
       }
       __syncwarp();
+    }
+    for (int c = 0; c < nc; ++c) {
+      const int s = c & 1, s1n = s ^ 1;
       mbar_wait(sb_ready, c & 1);
       tc_fence_after();
       if (elect_one()) {
@@ -160,6 +166,17 @@ __global__ void __launch_bounds__(320, 1)
         mma_commit(st_full);
       }
       __syncwarp();
+      if (c + 1 < nc) {
+        mbar_wait(&full[s1n], ((c + 1) >> 1) & 1);
+        mbar_wait(t1_empty, c & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          for (int ks = 0; ks < 8; ++ks)  // T1(c+1) = Q K^T
+            mma_ss(tmem + kT1, kdesc(aQ + s1n * kTile, ks), kdesc(aK + s1n * kTile, ks), id_kk, ks > 0);
+          mma_commit(t1_full);
+        }
+        __syncwarp();
+      }
       mbar_wait(p_ready, c & 1);
       if (c >= 1) mbar_wait(ot_empty, (c - 1) & 1);
       tc_fence_after();
@@ -167,7 +184,7 @@ __global__ void __launch_bounds__(320, 1)
         for (int ks = 0; ks < 8; ++ks)  // O^T = V^T P'^T
           mma_ss(tmem + kOT, kdesc(aV + s * kTile, ks), kdesc(aP, ks), id_kk, ks > 0);
         for (int ks = 0; ks < 8; ++ks)  // O^T += bf16(b S^T) Q^T   (A from TMEM)
-          mma_ts(tmem + kOT, tmem + kSB + ks * 8, kdesc(aQ + s * kTile, ks), id_kk, 1);
+          mma_ts(tmem + kOT, tmem + kSB + s * 64 + ks * 8, kdesc(aQ + s * kTile, ks), id_kk, 1);
         mma_commit(o_full);
         mma_commit(&empty[s]);
       }
@@ -192,12 +209,13 @@ __global__ void __launch_bounds__(320, 1)
     named_bar(1, 128);
     tc_fence_after();
 
+    const int et = (int)threadIdx.x - 64;  // 0..127
     for (int c = 0; c < nc; ++c) {
       const int s = c & 1;
       const int64_t row0 = s0 + (int64_t)c * kC;
       const uint8_t* q_t = sQ + s * kTile;
       const uint8_t* k_t = sK + s * kTile;
-      // ---- E2: S^T -> bf16(b S^T) in TMEM (A operand of the Q S term)
+      // ---- E2: S^T -> bf16(b S^T) in TMEM buffer s (A operand of the Q S term)
       if (c >= 1) mbar_wait(st_full, (c - 1) & 1);
       tc_fence_after();
 #pragma unroll 1
@@ -211,35 +229,30 @@ __global__ void __launch_bounds__(320, 1)
           pk[u] = pack2<kBF16>(b * __uint_as_float(x0[2 * u]), b * __uint_as_float(x0[2 * u + 1]));
           pk[16 + u] = pack2<kBF16>(b * __uint_as_float(x1[2 * u]), b * __uint_as_float(x1[2 * u + 1]));
         }
-        tmem_st32(tmem + lane_base + kSB + half * 32, pk);
+        tmem_st32(tmem + lane_base + kSB + s * 64 + half * 32, pk);
       }
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(sb_ready);
 
-      // ---- E1: T1 -> P' (smem), g
+      // ---- E1: T1 -> P' (registers), g
       mbar_wait(&full[s], (c >> 1) & 1);
       mbar_wait(t1_full, c & 1);
       tc_fence_after();
       float rowsum = 0.f;
-#pragma unroll 1
+      uint32_t pk[64];
+#pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
         uint32_t x[32];
         tmem_ld32(tmem + lane_base + kT1 + cc * 32, x);
         tmem_ld_wait();
-        uint32_t pk[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
           const int t0 = cc * 32 + 2 * u;
           const float p0 = t0 <= r ? a + b * __uint_as_float(x[2 * u]) : 0.f;
           const float p1 = t0 + 1 <= r ? a + b * __uint_as_float(x[2 * u + 1]) : 0.f;
           rowsum += p0 + p1;
-          pk[u] = pack2<kBF16>(p0, p1);
-        }
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          uint4 v4 = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
-          *(uint4*)(sP + sw128_off(r, cc * 32 + 8 * w, kC)) = v4;
+          pk[cc * 16 + u] = pack2<kBF16>(p0, p1);
         }
       }
       tc_fence_before();
@@ -249,31 +262,50 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll 4
       for (int m8 = 0; m8 < kD; m8 += 8) {
         const uint4 v4 = *(const uint4*)(q_t + sw128_off(r, m8, kC));
-        const uint32_t w4[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float2 f = unpack2<kBF16>(w4[u]);
-          qz += f.x * zq[m8 + 2 * u] + f.y * zq[m8 + 2 * u + 1];
-        }
+        const float4 za = *(const float4*)(zq + m8), zb = *(const float4*)(zq + m8 + 4);
+        const float2 f0 = unpack2<kBF16>(v4.x), f1 = unpack2<kBF16>(v4.y);
+        const float2 f2 = unpack2<kBF16>(v4.z), f3 = unpack2<kBF16>(v4.w);
+        qz += f0.x * za.x + f0.y * za.y + f1.x * za.z + f1.y * za.w + f2.x * zb.x + f2.y * zb.y +
+              f3.x * zb.z + f3.y * zb.w;
       }
       const float gi = rowsum + a * (float)(prm.row_offset + row0) + b * qz;
       if (fabsf(gi) < kEpsF32) flag_degenerate(prm.flag, grp, prm.row_offset + row0 + r);
       ginv_s[s * kC + r] = 1.f / gi;
       prm.gout[grp * prm.N + row0 + r] = gi;
       named_bar(1, 128);  // every WG-A thread is done reading zq
-      // z_m += sum_t K[t][m]   (m = r): 16 x 16B column reads, 8 m per load
+      mbar_arrive(&a2b[s]);  // Q(c) fully read, ginv(c) written
+      // z_m += sum_t K[t][m]: thread (mg, tg) sums rows [16 tg, 16 tg + 16) of columns [8 mg, 8 mg + 8)
       {
-        float ks_ = 0.f;
-#pragma unroll 8
-        for (int t = 0; t < kC; ++t) {
-          const uint16_t h = *(const uint16_t*)(k_t + sw128_off(t, r, kC));
-          ks_ += kBF16 ? __bfloat162float(__ushort_as_bfloat16(h)) : __half2float(__ushort_as_half(h));
+        const int mg = et >> 3, tg = et & 7;
+        float zs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+        for (int t = 16 * tg; t < 16 * tg + 16; ++t) {
+          const uint4 v4 = *(const uint4*)(k_t + sw128_off(t, 8 * mg, kC));
+          const float2 f0 = unpack2<kBF16>(v4.x), f1 = unpack2<kBF16>(v4.y);
+          const float2 f2 = unpack2<kBF16>(v4.z), f3 = unpack2<kBF16>(v4.w);
+          zs[0] += f0.x; zs[1] += f0.y; zs[2] += f1.x; zs[3] += f1.y;
+          zs[4] += f2.x; zs[5] += f2.y; zs[6] += f3.x; zs[7] += f3.y;
         }
-        zq[r] += ks_;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          zs[u] += __shfl_xor_sync(0xffffffffu, zs[u], 1);
+          zs[u] += __shfl_xor_sync(0xffffffffu, zs[u], 2);
+          zs[u] += __shfl_xor_sync(0xffffffffu, zs[u], 4);
+        }
+        if (tg == 0) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) zq[8 * mg + u] += zs[u];
+        }
       }
+      mbar_arrive(&empty[s]);  // WG-A is done with Q(c), K(c)
+      // P'(c) -> smem once M2(c-1) has drained the buffer
+      if (c >= 1) mbar_wait(o_full, (c - 1) & 1);
+#pragma unroll
+      for (int w = 0; w < 16; ++w)
+        *(uint4*)(sP + sw128_off(r, 8 * w, kC)) = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
       fence_proxy_async();  // P' generic stores -> visible to the tensor core
+      named_bar(1, 128);    // zq updates visible before the next chunk's dot
       mbar_arrive(p_ready);
-      mbar_arrive(&empty[s]);
     }
     if (prm.st_out && nc > 0) {  // final state for the backward (S, z)
       mbar_wait(st_full, (nc - 1) & 1);
@@ -303,7 +335,7 @@ __global__ void __launch_bounds__(320, 1)
       uint8_t* stage_o = sQ + s * kTile;          // Q(c) is dead once O^T(c) is complete
       const uint8_t* v_t = sV + s * kTile;
       mbar_wait(o_full, c & 1);
-      mbar_wait(p_ready, c & 1);                  // WG-A finished reading Q(c); ginv(c) ready
+      mbar_wait(&a2b[s], (c >> 1) & 1);           // WG-A finished reading Q(c); ginv(c) ready
       tc_fence_after();
       const float asig = a * sigma;
       const float* gv = ginv_s + s * kC;
