@@ -24,6 +24,13 @@ namespace lab {
 
 using namespace sm100;
 
+// Pipeline tracing (diagnostics): CTA (0,0) records clock64 stamps per role,
+// chunk and event; read back with la_internal_trace_read (not part of the ABI).
+__device__ unsigned long long g_trace[4][64][8];
+__device__ __forceinline__ void trace(int role, int c, int ev) {
+  if (blockIdx.x == 0 && blockIdx.y == 0 && c < 64) g_trace[role][c][ev] = clock64();
+}
+
 namespace {
 
 constexpr int kC = 128;          // chunk rows
@@ -130,7 +137,9 @@ __global__ void __launch_bounds__(320, 1)
     if (elect_one()) {
       for (int c = 0; c < nc; ++c) {
         const int s = c & 1;
+        trace(3, c, 0);
         if (c >= 2) mbar_wait(&empty[s], ((c >> 1) & 1) ^ 1);
+        trace(3, c, 1);
         const int64_t row0 = s0 + (int64_t)c * kC;
         mbar_expect_tx(&full[s], 3 * kTile);
         tma_load_3d(sQ + s * kTile, &tmQ, &full[s], 0, (int)(grp * prm.N + row0), 0);
@@ -158,7 +167,9 @@ __global__ void __launch_bounds__(320, 1)
     }
     for (int c = 0; c < nc; ++c) {
       const int s = c & 1, s1n = s ^ 1;
+      if (lane_id() == 0) trace(0, c, 0);
       mbar_wait(sb_ready, c & 1);
+      if (lane_id() == 0) trace(0, c, 1);
       tc_fence_after();
       if (elect_one()) {
         for (int ks = 0; ks < 8; ++ks)  // S^T += V^T K   (B = K viewed (N=m, K=t): MN-major)
@@ -168,7 +179,9 @@ __global__ void __launch_bounds__(320, 1)
       __syncwarp();
       if (c + 1 < nc) {
         mbar_wait(&full[s1n], ((c + 1) >> 1) & 1);
+        if (lane_id() == 0) trace(0, c, 2);
         mbar_wait(t1_empty, c & 1);
+        if (lane_id() == 0) trace(0, c, 3);
         tc_fence_after();
         if (elect_one()) {
           for (int ks = 0; ks < 8; ++ks)  // T1(c+1) = Q K^T
@@ -178,7 +191,9 @@ __global__ void __launch_bounds__(320, 1)
         __syncwarp();
       }
       mbar_wait(p_ready, c & 1);
+      if (lane_id() == 0) trace(0, c, 4);
       if (c >= 1) mbar_wait(ot_empty, (c - 1) & 1);
+      if (lane_id() == 0) trace(0, c, 5);
       tc_fence_after();
       if (elect_one()) {
         for (int ks = 0; ks < 8; ++ks)  // O^T = V^T P'^T
@@ -216,7 +231,9 @@ __global__ void __launch_bounds__(320, 1)
       const uint8_t* q_t = sQ + s * kTile;
       const uint8_t* k_t = sK + s * kTile;
       // ---- E2: S^T -> bf16(b S^T) in TMEM buffer s (A operand of the Q S term)
+      if (et == 0) trace(1, c, 0);
       if (c >= 1) mbar_wait(st_full, (c - 1) & 1);
+      if (et == 0) trace(1, c, 1);
       tc_fence_after();
 #pragma unroll 1
       for (int half = 0; half < 2; ++half) {
@@ -234,10 +251,12 @@ __global__ void __launch_bounds__(320, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(sb_ready);
+      if (et == 0) trace(1, c, 2);
 
       // ---- E1: T1 -> P' (registers), g
       mbar_wait(&full[s], (c >> 1) & 1);
       mbar_wait(t1_full, c & 1);
+      if (et == 0) trace(1, c, 3);
       tc_fence_after();
       float rowsum = 0.f;
       uint32_t pk[64];
@@ -298,14 +317,17 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
       mbar_arrive(&empty[s]);  // WG-A is done with Q(c), K(c)
+      if (et == 0) trace(1, c, 4);
       // P'(c) -> smem once M2(c-1) has drained the buffer
       if (c >= 1) mbar_wait(o_full, (c - 1) & 1);
+      if (et == 0) trace(1, c, 5);
 #pragma unroll
       for (int w = 0; w < 16; ++w)
         *(uint4*)(sP + sw128_off(r, 8 * w, kC)) = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
       fence_proxy_async();  // P' generic stores -> visible to the tensor core
       named_bar(1, 128);    // zq updates visible before the next chunk's dot
       mbar_arrive(p_ready);
+      if (et == 0) trace(1, c, 6);
     }
     if (prm.st_out && nc > 0) {  // final state for the backward (S, z)
       mbar_wait(st_full, (nc - 1) & 1);
@@ -334,8 +356,11 @@ __global__ void __launch_bounds__(320, 1)
       const int64_t row0 = s0 + (int64_t)c * kC;
       uint8_t* stage_o = sQ + s * kTile;          // Q(c) is dead once O^T(c) is complete
       const uint8_t* v_t = sV + s * kTile;
+      if (eb == 0) trace(2, c, 0);
       mbar_wait(o_full, c & 1);
+      if (eb == 0) trace(2, c, 1);
       mbar_wait(&a2b[s], (c >> 1) & 1);           // WG-A finished reading Q(c); ginv(c) ready
+      if (eb == 0) trace(2, c, 2);
       tc_fence_after();
       const float asig = a * sigma;
       const float* gv = ginv_s + s * kC;
@@ -359,6 +384,7 @@ __global__ void __launch_bounds__(320, 1)
       }
       tc_fence_before();
       mbar_arrive(ot_empty);
+      if (eb == 0) trace(2, c, 3);
       // sigma_j += sum_t V^T[j][t]   (j = r), for the next chunk
       float vs = 0.f;
 #pragma unroll 4
@@ -377,7 +403,9 @@ __global__ void __launch_bounds__(320, 1)
       if (eb == 0) {
         tma_store_3d(&tmO, stage_o, 0, (int)(grp * kD), (int)(row0 / 64));
         tma_store_commit();
+        trace(2, c, 4);
         tma_store_wait_read0();   // staging (Q slot) read out -> the stage may be refilled
+        trace(2, c, 5);
         mbar_arrive(&empty[s]);
       }
     }
@@ -594,3 +622,7 @@ cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, W
 }
 
 }  // namespace lab
+
+extern "C" int la_internal_trace_read(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, lab::g_trace, sizeof(lab::g_trace));
+}
