@@ -27,6 +27,11 @@ namespace lab {
 
 using namespace sm100;
 
+__device__ unsigned long long g_trace_b[4][64][10];
+__device__ __forceinline__ void traceb(int role, int n, int ev) {
+  if (blockIdx.x == 0 && blockIdx.y == 0 && n < 64) g_trace_b[role][n][ev] = clock64();
+}
+
 namespace {
 
 constexpr int kCB = 64;   // chunk rows
@@ -426,8 +431,11 @@ __global__ void __launch_bounds__(192, 1)
       const int s = n & 1;
       const uint32_t aQ = smem_u32(smem + s * kStage), aK = aQ + kT64, aV = aQ + 2 * kT64,
                      aW = aQ + 3 * kT64;
+      if (lane_id() == 0) traceb(0, n, 0);
       mbar_wait(&full[s], (n >> 1) & 1);
+      if (lane_id() == 0) traceb(0, n, 1);
       if (n >= 1) mbar_wait(dpt_empty, (n - 1) & 1);
+      if (lane_id() == 0) traceb(0, n, 2);
       tc_fence_after();
       if (elect_one()) {
         for (int ks = 0; ks < 8; ++ks)  // T1 = Q K^T -> upper lane half
@@ -438,6 +446,7 @@ __global__ void __launch_bounds__(192, 1)
       }
       __syncwarp();
       mbar_wait(w_ready, n & 1);
+      if (lane_id() == 0) traceb(0, n, 3);
       tc_fence_after();
       if (elect_one()) {
         for (int ks = 0; ks < 8; ++ks)  // dPt = W_hat V^T -> lower lane half
@@ -446,8 +455,11 @@ __global__ void __launch_bounds__(192, 1)
       }
       __syncwarp();
       mbar_wait(sS_ready, n & 1);
+      if (lane_id() == 0) traceb(0, n, 4);
       mbar_wait(ps_ready, n & 1);
+      if (lane_id() == 0) traceb(0, n, 5);
       if (n >= 1) mbar_wait(gr_empty, (n - 1) & 1);
+      if (lane_id() == 0) traceb(0, n, 6);
       tc_fence_after();
       if (elect_one()) {
         for (int h = 0; h < 2; ++h) {  // dQ[:, 64h:64h+64]
@@ -460,6 +472,7 @@ __global__ void __launch_bounds__(192, 1)
       }
       __syncwarp();
       mbar_wait(sR_ready, n & 1);
+      if (lane_id() == 0) traceb(0, n, 7);
       tc_fence_after();
       if (elect_one()) {
         for (int ks = 0; ks < 4; ++ks)  // dK^T = Q^T dS^T
@@ -499,15 +512,19 @@ __global__ void __launch_bounds__(192, 1)
       const uint8_t* k_t = st + kT64;
       uint8_t* w_t = st + 3 * kT64;
       // ---- E0: W_hat, s
+      if (et == 0) traceb(1, n, 0);
       named_bar(1, 128);
       mbar_wait(&full[s], (n >> 1) & 1);
+      if (et == 0) traceb(1, n, 1);
       what_pass<kBF16>(w_t, o8, g8, s_s, et);
       if (n + 1 < nc) what_prefetch<kBF16>(prm, grp, row0 - kCB, et, o8, g8);
       fence_proxy_async();
       mbar_arrive(w_ready);
       named_bar(1, 128);  // s_s complete before any thread reads it
       // ---- E_R: b R_next -> sR
+      if (et == 0) traceb(1, n, 2);
       if (n >= 1) mbar_wait(r_full, (n - 1) & 1);
+      if (et == 0) traceb(1, n, 3);
       tc_fence_after();
 #pragma unroll 1
       for (int j0 = 0; j0 < kD; j0 += 32) {
@@ -528,6 +545,7 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_before();
       mbar_arrive(sR_ready);
       // ---- E_S: b S_prev -> sS ; z_prev
+      if (et == 0) traceb(1, n, 4);
       mbar_wait(s_full, n & 1);
       tc_fence_after();
 #pragma unroll 1
@@ -555,7 +573,9 @@ __global__ void __launch_bounds__(192, 1)
         zq[r] -= ks_;
       }
       // ---- E1: dPt -> dS (lower half lanes), T1 -> P (upper half lanes)
+      if (et == 0) traceb(1, n, 5);
       mbar_wait(dpt_full, n & 1);
+      if (et == 0) traceb(1, n, 6);
       tc_fence_after();
       {
         const float si = s_s[ih];
@@ -592,7 +612,9 @@ __global__ void __launch_bounds__(192, 1)
       mbar_arrive(ps_ready);
       named_bar(1, 128);  // zq updated by every thread
       // ---- E_out: dQ (half lanes), dK^T (lanes m), dV^T (lanes j)
+      if (et == 0) traceb(1, n, 7);
       mbar_wait(gr_full, n & 1);
+      if (et == 0) traceb(1, n, 8);
       tc_fence_after();
       {
         const float si = s_s[ih];
@@ -653,6 +675,7 @@ __global__ void __launch_bounds__(192, 1)
           cj += f2.x + f2.y;
         }
       }
+      if (et == 0) traceb(1, n, 9);
       mbar_arrive(&empty[s]);
     }
   }
@@ -724,3 +747,7 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
 }
 
 }  // namespace lab
+
+extern "C" int la_internal_trace_read_bwd(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, lab::g_trace_b, sizeof(lab::g_trace_b));
+}
