@@ -22,4 +22,4 @@ for role in range(4):
     print(names[role])
     for c in range(10, 16):
         print(c, (t[role, c] - t0).tolist())
-print("per-chunk period (MMA start):", np.diff(t[0, 5:40, 0]).mean())
+print("per-chunk period (MMA start):", np.diff(t[0, 5:60, 0]).mean())
