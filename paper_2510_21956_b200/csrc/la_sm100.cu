@@ -296,6 +296,7 @@ __global__ void __launch_bounds__(320, 1)
       }
       tc_fence_before();
       mbar_arrive(t1_empty);
+      if (et == 0) trace(1, c, 7);
       float qz = 0.f;
       if (!lower) {
 #pragma unroll 4
@@ -315,7 +316,9 @@ __global__ void __launch_bounds__(320, 1)
         ginv_s[(c & 3) * kCF + ih] = 1.f / gi;
         prm.gout[grp * prm.N + row0 + ih] = gi;
       }
+      if (et == 0) trace(2, c, 6);
       named_bar(1, 128);  // zq reads done, ginv(c) written
+      if (et == 0) trace(2, c, 7);
       mbar_arrive(&a2b[c & 3]);
       {  // z_m += sum_t K[t][m]: thread (mg, tg) sums rows [8 tg, 8 tg + 8) of columns [8 mg, 8 mg + 8)
         const int mg = et >> 3, tg = et & 7;

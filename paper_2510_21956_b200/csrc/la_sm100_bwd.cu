@@ -51,6 +51,28 @@ __device__ __forceinline__ uint64_t mn(uint32_t tile, int ks, uint32_t panel) {
   return sdesc_sw128(tile + ks * 2048, panel, 1024);
 }
 
+// Per-warp transpose of 32 row segments (128 B each) through a 4 KB smem scratch
+// (XOR-swizzled 16 B chunks), then coalesced 128 B-row global stores: lane L holds
+// segment L in v[8]; dst(seg) gives the segment's global address.
+template <typename DstFn>
+__device__ __forceinline__ void warp_store_rows(uint8_t* scratch_lo, uint8_t* scratch_hi,
+                                                const uint4 (&v)[8], DstFn dst) {
+  const int lane = (int)lane_id();
+  auto slot = [&](int seg, int ch) -> uint4* {
+    uint8_t* base = seg < 16 ? scratch_lo : scratch_hi;
+    return (uint4*)(base + (seg & 15) * 128 + ((ch ^ (seg & 7)) << 4));
+  };
+#pragma unroll
+  for (int ch = 0; ch < 8; ++ch) *slot(lane, ch) = v[ch];
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int seg = 4 * k + (lane >> 3), ch = lane & 7;
+    *(uint4*)((uint8_t*)dst(seg) + ch * 16) = *slot(seg, ch);
+  }
+  __syncwarp();
+}
+
 template <bool kBF16>
 __device__ __forceinline__ float h2f(uint16_t h) {
   return kBF16 ? __bfloat162float(__ushort_as_bfloat16(h)) : __half2float(__ushort_as_half(h));
@@ -73,7 +95,8 @@ struct BwdParams {
 
 // Epilogue step E0: W_hat = omega / g in place (bf16) and s_i = sum_j o_ij w_hat_ij.
 // 128 threads: lane = jg + 16 * (ig & 1), warp w -> ig = 2 w + lane / 16, each thread
-// owns rows j in [8 jg, 8 jg + 8) and columns i in [8 ig, 8 ig + 8) of the 128 x 64 tile.
+// owns rows j = 16 rr + jg (rr < 8) and columns i in [8 ig, 8 ig + 8) of the 128 x 64
+// tile; the 8 lanes of a quarter-warp touch 8 distinct swizzle rows (no bank conflicts).
 template <bool kBF16>
 __device__ __forceinline__ void what_pass(uint8_t* w_t, const uint4 (&o8)[8], const float4 (&g8)[2],
                                           float* s_s, int et) {
@@ -84,7 +107,7 @@ __device__ __forceinline__ void what_pass(uint8_t* w_t, const uint4 (&o8)[8], co
   float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int rr = 0; rr < 8; ++rr) {
-    const int j = 8 * jg + rr;
+    const int j = 16 * rr + jg;
     uint4* p = (uint4*)(w_t + sw128_off(j, 8 * ig, 128));
     const uint4 wv = *p;
     const uint32_t wa[4] = {wv.x, wv.y, wv.z, wv.w};
@@ -121,7 +144,7 @@ __device__ __forceinline__ void what_prefetch(const BwdParams& prm, int64_t grp,
   const uint16_t* o = (const uint16_t*)prm.o;
 #pragma unroll
   for (int rr = 0; rr < 8; ++rr)
-    o8[rr] = __ldg((const uint4*)(o + (grp * kD + 8 * jg + rr) * prm.N + row0 + 8 * ig));
+    o8[rr] = __ldg((const uint4*)(o + (grp * kD + 16 * rr + jg) * prm.N + row0 + 8 * ig));
   const float* gp = prm.g + grp * prm.N + row0 + 8 * ig;
   g8[0] = __ldg((const float4*)gp);
   g8[1] = __ldg((const float4*)(gp + 4));
@@ -617,48 +640,57 @@ __global__ void __launch_bounds__(192, 1)
       if (et == 0) traceb(1, n, 8);
       tc_fence_after();
       {
+        // this warp's scratch: its own 16 P rows and 16 dS rows (dead after gr_full)
+        uint8_t* scr_lo = sP + qd * 2048;
+        uint8_t* scr_hi = sdS + qd * 2048;
         const float si = s_s[ih];
         const int m0 = upper ? 64 : 0;
-        uint16_t* dq = (uint16_t*)prm.dq + (grp * prm.N + row0 + ih) * kD + m0;
-#pragma unroll 1
+        uint4 v[8];
+#pragma unroll
         for (int c0 = 0; c0 < 64; c0 += 32) {
           uint32_t x[32];
           tmem_ld32(tmem + lb + kDQ + c0, x);
           tmem_ld_wait();
-          uint32_t pk[16];
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int m = m0 + c0 + 2 * q;
-            pk[q] = pack2<kBF16>(__uint_as_float(x[2 * q]) - si * b * zq[m],
-                                 __uint_as_float(x[2 * q + 1]) - si * b * zq[m + 1]);
+          for (int w4 = 0; w4 < 4; ++w4) {
+            uint32_t q4[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int m = m0 + c0 + 8 * w4 + 2 * q;
+              q4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) - si * b * zq[m],
+                                   __uint_as_float(x[8 * w4 + 2 * q + 1]) - si * b * zq[m + 1]);
+            }
+            v[c0 / 8 + w4] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
           }
-#pragma unroll
-          for (int w4 = 0; w4 < 4; ++w4)
-            *(uint4*)(dq + c0 + 8 * w4) = make_uint4(pk[4 * w4], pk[4 * w4 + 1], pk[4 * w4 + 2], pk[4 * w4 + 3]);
         }
-      }
-      {
-        uint16_t* dk = (uint16_t*)prm.dk + (grp * kD + r) * prm.N + row0;
-        uint16_t* dv = (uint16_t*)prm.dv + (grp * kD + r) * prm.N + row0;
+        // segment L: dQ row 16 qd + (L & 15), columns [64 (L >> 4), +64)
+        uint16_t* dqb = (uint16_t*)prm.dq + (grp * prm.N + row0 + qd * 16) * kD;
+        warp_store_rows(scr_lo, scr_hi, v, [&](int seg) { return dqb + (seg & 15) * kD + (seg >> 4) * 64; });
         const float bu = b * u, ac = a * cj;
-#pragma unroll 1
+        uint4 vk[8], vv[8];
+#pragma unroll
         for (int c0 = 0; c0 < 64; c0 += 32) {
           uint32_t xk[32], xv[32];
           tmem_ld32(tmem + lb + kDK + c0, xk);
           tmem_ld32(tmem + lb + kDV + c0, xv);
           tmem_ld_wait();
-          uint32_t pkk[16], pkv[16];
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            pkk[q] = pack2<kBF16>(__uint_as_float(xk[2 * q]) - bu, __uint_as_float(xk[2 * q + 1]) - bu);
-            pkv[q] = pack2<kBF16>(__uint_as_float(xv[2 * q]) + ac, __uint_as_float(xv[2 * q + 1]) + ac);
-          }
 #pragma unroll
           for (int w4 = 0; w4 < 4; ++w4) {
-            *(uint4*)(dk + c0 + 8 * w4) = make_uint4(pkk[4 * w4], pkk[4 * w4 + 1], pkk[4 * w4 + 2], pkk[4 * w4 + 3]);
-            *(uint4*)(dv + c0 + 8 * w4) = make_uint4(pkv[4 * w4], pkv[4 * w4 + 1], pkv[4 * w4 + 2], pkv[4 * w4 + 3]);
+            uint32_t k4[4], v4[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              k4[q] = pack2<kBF16>(__uint_as_float(xk[8 * w4 + 2 * q]) - bu, __uint_as_float(xk[8 * w4 + 2 * q + 1]) - bu);
+              v4[q] = pack2<kBF16>(__uint_as_float(xv[8 * w4 + 2 * q]) + ac, __uint_as_float(xv[8 * w4 + 2 * q + 1]) + ac);
+            }
+            vk[c0 / 8 + w4] = make_uint4(k4[0], k4[1], k4[2], k4[3]);
+            vv[c0 / 8 + w4] = make_uint4(v4[0], v4[1], v4[2], v4[3]);
           }
         }
+        // segment L: row 32 qd + L of dK^T / dV^T, columns [row0, row0 + 64)
+        uint16_t* dkb = (uint16_t*)prm.dk + (grp * kD + qd * 32) * prm.N + row0;
+        uint16_t* dvb = (uint16_t*)prm.dv + (grp * kD + qd * 32) * prm.N + row0;
+        warp_store_rows(scr_lo, scr_hi, vk, [&](int seg) { return dkb + seg * prm.N; });
+        warp_store_rows(scr_lo, scr_hi, vv, [&](int seg) { return dvb + seg * prm.N; });
       }
       tc_fence_before();
       mbar_arrive(gr_empty);

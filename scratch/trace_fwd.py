@@ -23,3 +23,5 @@ for role in range(4):
     for c in range(10, 16):
         print(c, (t[role, c] - t0).tolist())
 print("per-chunk period (MMA start):", np.diff(t[0, 5:60, 0]).mean())
+print("WGA fine: t1_full, after T1 loads, after dot+g, after named_bar, after z(empty)")
+for c in range(10, 16): print(c, (t[1, c, [3, 7]] - t0).tolist(), (t[2, c, [6, 7]] - t0).tolist(), (t[1, c, 4] - t0))
