@@ -39,7 +39,7 @@ constexpr int kTile = kC * kD * 2;  // 32 KB: one 128x128 16-bit tile (2 SW128 p
 constexpr int kPanel = 128 * 128;   // bytes per 64-column panel of 128 rows
 
 // TMEM columns (forward main)
-constexpr uint32_t kT1 = 0, kOT = 128, kST = 256, kSB = 384;  // kSB: 2 x 64 columns
+
 
 // A (rows x 128) 16-bit tile of a row-major [R][inner] matrix as two SW128 panels.
 bool make_map(CUtensorMap* m, const void* base, bool bf16, uint64_t rows, uint64_t inner) {
@@ -598,7 +598,10 @@ bool tc_forward_supported(const Launch& L, const Tensors& t) {
 static bool per_group_mode(int64_t G) {
   const char* e = getenv("LA_FWD_SEGMENTS");
   if (e) return atoi(e) <= 1;
-  return G >= 48;
+  // A single CTA per group only pays off once every SM has a group: the chunked
+  // kernel is bounded per SM by shared-memory bandwidth (TMA writes + SS-MMA operand
+  // reads), so using all 148 SMs via segments beats skipping the aggregate pass.
+  return G >= 148;
 }
 
 size_t tc_forward_ws_floats(int64_t G, int64_t N, int64_t D) {
