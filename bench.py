@@ -219,17 +219,22 @@ def run_our_arm(args):
     dv = torch.empty((G, D, N), device=dev, dtype=torch.bfloat16)
     wsf = torch.empty(L.la_forward_workspace_bytes(C.byref(p)), device=dev, dtype=torch.uint8)
     wsb = torch.empty(L.la_backward_workspace_bytes(C.byref(p)), device=dev, dtype=torch.uint8)
+    # per-(group, segment) prefix states saved by the forward for the backward
+    # (the analogue of keeping (out, g) in ForwardArtifacts)
+    saved = torch.empty(L.la_saved_state_bytes(C.byref(p)), device=dev, dtype=torch.uint8)
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
     FMj, SMj = 0, 1
 
     def step():
-        st = L.la_forward(C.byref(p), q.data_ptr(), SMj, k.data_ptr(), SMj, v.data_ptr(), FMj,
-                          out.data_ptr(), g.data_ptr(), wsf.data_ptr(), wsf.numel(), sp, None)
+        st = L.la_forward_save(C.byref(p), q.data_ptr(), SMj, k.data_ptr(), SMj, v.data_ptr(), FMj,
+                               out.data_ptr(), g.data_ptr(), saved.data_ptr(), saved.numel(), wsf.data_ptr(),
+                               wsf.numel(), sp, None)
         assert st == 0, _abi.STATUS_NAMES[st]
-        st = L.la_backward(C.byref(p), q.data_ptr(), SMj, k.data_ptr(), SMj, v.data_ptr(), FMj,
-                           out.data_ptr(), w.data_ptr(), FMj, g.data_ptr(), dq.data_ptr(), dk.data_ptr(),
-                           dv.data_ptr(), wsb.data_ptr(), wsb.numel(), sp, None)
+        st = L.la_backward_saved(C.byref(p), q.data_ptr(), SMj, k.data_ptr(), SMj, v.data_ptr(), FMj,
+                                 out.data_ptr(), w.data_ptr(), FMj, g.data_ptr(), saved.data_ptr(), saved.numel(),
+                                 dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), wsb.data_ptr(), wsb.numel(), sp,
+                                 None)
         assert st == 0, _abi.STATUS_NAMES[st]
 
     for _ in range(args.warmup):

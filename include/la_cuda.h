@@ -133,6 +133,21 @@ la_status la_backward(const la_problem* p, const void* q, la_layout lq, const vo
                       void* dv /* FeatureMajor */, void* workspace, size_t ws_bytes,
                       void* stream, la_error_info* err);
 
+/* Forward that also saves, per (group, segment), the prefix state at the
+ * segment's last row (la_saved_state_bytes(p) bytes, device memory). Handing it
+ * to la_backward_saved spares the backward from re-reading K and V for its
+ * prefix states, the way ForwardArtifacts carries (out, g) (forward.hpp:35-41). */
+size_t la_saved_state_bytes(const la_problem* p);
+la_status la_forward_save(const la_problem* p, const void* q, la_layout lq, const void* k,
+                          la_layout lk, const void* v, la_layout lv, void* out, float* g,
+                          void* saved, size_t saved_bytes, void* workspace, size_t ws_bytes,
+                          void* stream, la_error_info* err);
+la_status la_backward_saved(const la_problem* p, const void* q, la_layout lq, const void* k,
+                            la_layout lk, const void* v, la_layout lv, const void* o,
+                            const void* omega, la_layout lw, const float* g, const void* saved,
+                            size_t saved_bytes, void* dq, void* dk, void* dv, void* workspace,
+                            size_t ws_bytes, void* stream, la_error_info* err);
+
 /* Sequence-sharded variants: same as above on one shard, with carries. */
 la_status la_forward_sharded(const la_problem* p, const la_shard* shard, const void* q,
                              la_layout lq, const void* k, la_layout lk, const void* v,

@@ -26,6 +26,7 @@ EXPORTS = [
     "la_backward", "la_forward_sharded", "la_backward_sharded", "la_forward_shard_state",
     "la_backward_shard_state", "la_combine_shard_states", "la_query_status", "la_host_forward",
     "la_host_backward", "la_host_release", "la_profile_enable", "la_profile_read",
+    "la_saved_state_bytes", "la_forward_save", "la_backward_saved",
 ]
 
 
@@ -87,6 +88,11 @@ def lib():
         L.la_backward_shard_state.argtypes = [P, vp, C.c_int, vp, vp, C.c_int, vp, vp, vp]
         L.la_combine_shard_states.argtypes = [P, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp]
         L.la_query_status.argtypes = [vp, vp, E]
+        L.la_saved_state_bytes.restype = sz
+        L.la_saved_state_bytes.argtypes = [P]
+        L.la_forward_save.argtypes = [P, vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, vp, sz, vp, sz, vp, E]
+        L.la_backward_saved.argtypes = [P, vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, C.c_int, vp, vp, sz,
+                                        vp, vp, vp, vp, sz, vp, E]
         L.la_host_forward.argtypes = [P, vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, E]
         L.la_host_backward.argtypes = [P, vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, C.c_int, vp,
                                        vp, vp, vp, E]

@@ -219,6 +219,7 @@ class ForwardArtifacts:
     q: HeadTensor = None
     k: HeadTensor = None
     v: HeadTensor = None
+    saved: object = None  # device path: per-segment prefix states (la_forward_save)
 
 
 @dataclass
@@ -299,9 +300,11 @@ def _run_forward(q, k, v, c, plan, causal, fault, dtype, impl):
         out = torch.empty(G * N * D, dtype=q.data.dtype, device=dev)
         g = torch.empty(G * N, dtype=torch.float32, device=dev)
         ws = torch.empty(L.la_forward_workspace_bytes(C.byref(p)), dtype=torch.uint8, device=dev)
-        st = L.la_forward(C.byref(p), q.data.data_ptr(), int(q.layout()), k.data.data_ptr(),
-                          int(k.layout()), v.data.data_ptr(), int(v.layout()), out.data_ptr(),
-                          g.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(), C.byref(err))
+        saved = torch.empty(L.la_saved_state_bytes(C.byref(p)), dtype=torch.uint8, device=dev)
+        st = L.la_forward_save(C.byref(p), q.data.data_ptr(), int(q.layout()), k.data.data_ptr(),
+                               int(k.layout()), v.data.data_ptr(), int(v.layout()), out.data_ptr(),
+                               g.data_ptr(), saved.data_ptr(), saved.numel(), ws.data_ptr(), ws.numel(),
+                               _stream_ptr(), C.byref(err))
         _raise(st, err)
     else:
         dtype = dtype or "f32"
@@ -317,6 +320,7 @@ def _run_forward(q, k, v, c, plan, causal, fault, dtype, impl):
     art.out = HeadTensor(G, N, D, Layout.FeatureMajor, out)
     art.g = g
     art.q, art.k, art.v = q, k, v
+    art.saved = saved if _is_torch(q.data) else None
     return art
 
 
@@ -363,11 +367,18 @@ def _run_backward(art, omega, c, plan, causal, fault, dtype, impl):
         dq, dk, dv = (torch.empty(G * N * D, dtype=q.data.dtype, device=dev) for _ in range(3))
         ws = torch.empty(L.la_backward_workspace_bytes(C.byref(p)), dtype=torch.uint8, device=dev)
         g = art.g if _is_torch(art.g) else torch.as_tensor(np.asarray(art.g, np.float32), device=dev)
-        st = L.la_backward(C.byref(p), q.data.data_ptr(), int(q.layout()), k.data.data_ptr(),
-                           int(k.layout()), v.data.data_ptr(), int(v.layout()), o.data.data_ptr(),
-                           omega.data.data_ptr(), int(omega.layout()), g.data_ptr(), dq.data_ptr(),
-                           dk.data_ptr(), dv.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(),
-                           C.byref(err))
+        if art.saved is not None and causal:
+            st = L.la_backward_saved(C.byref(p), q.data.data_ptr(), int(q.layout()), k.data.data_ptr(),
+                                     int(k.layout()), v.data.data_ptr(), int(v.layout()), o.data.data_ptr(),
+                                     omega.data.data_ptr(), int(omega.layout()), g.data_ptr(),
+                                     art.saved.data_ptr(), art.saved.numel(), dq.data_ptr(), dk.data_ptr(),
+                                     dv.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(), C.byref(err))
+        else:
+            st = L.la_backward(C.byref(p), q.data.data_ptr(), int(q.layout()), k.data.data_ptr(),
+                               int(k.layout()), v.data.data_ptr(), int(v.layout()), o.data.data_ptr(),
+                               omega.data.data_ptr(), int(omega.layout()), g.data_ptr(), dq.data_ptr(),
+                               dk.data_ptr(), dv.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(),
+                               C.byref(err))
         _raise(st, err)
     else:
         dtype = dtype or "f32"

@@ -17,6 +17,30 @@ __host__ __device__
 #endif
 inline int64_t state_floats(int64_t d) { return (d * d + 2 * d + 1 + 3) & ~(int64_t)3; }  // 16-byte records
 
+// Sequence segmentation shared by the tensor-core forward and backward so a
+// forward's saved per-segment states line up with the backward's segments.
+// Segments are whole multiples of 128 rows. The count minimises a simple model
+// of the makespan: waves(P) x (chunks per segment + fixed per-CTA overhead) plus
+// the aggregate pre-pass that P > 1 needs.
+inline int choose_segments(int64_t G, int64_t N, int num_sms = 148) {
+  const int64_t c128 = N / 128;
+  if (c128 <= 1) return 1;
+  double best = 1e300;
+  int bestP = 1;
+  for (int64_t P = 1; P <= c128 && P <= 64; ++P) {
+    const int64_t seg = (c128 + P - 1) / P;  // 128-row chunks per segment
+    if (seg * (P - 1) >= c128) continue;     // no empty trailing segment
+    const double waves = (double)((G * P + num_sms - 1) / num_sms);
+    double t = waves * (2.0 * seg + 3.0);    // in 64-row chunk times
+    if (P > 1) t += 0.45 * waves * 2.0 * seg;  // aggregate pre-pass
+    if (t < best * 0.995) {
+      best = t;
+      bestP = (int)P;
+    }
+  }
+  return bestP;
+}
+
 struct Tensors {
   const void* q; int lq;
   const void* k; int lk;
@@ -36,8 +60,16 @@ struct Launch {
   int64_t n_total;           // non-causal normaliser length (a * N_total)
   const float* carry_prefix; // G * state_floats(D) or null
   const float* carry_suffix; // G * state_floats(D) or null
+  float* saved_out;          // forward: per-(group, segment) end states (la_forward_save) or null
+  const float* saved_in;     // backward: the same, from the paired forward, or null
   cudaStream_t stream;
 };
+
+// Saved-state buffer (la_forward_save -> la_backward_saved): a 16-float header
+// {magic, G, N, D, P, seg_rows} then G * P state records (inclusive prefix at
+// each segment's last row: S, z, sigma, rows).
+constexpr float kSavedMagic = 1279348566.0f;  // 'LASV'
+constexpr int kSavedHeader = 16;
 
 // Workspace carving shared by every path.
 struct Workspace {
@@ -65,6 +97,8 @@ bool tc_forward_supported(const Launch& L, const Tensors& t);
 bool tc_backward_supported(const Launch& L, const Tensors& t);
 size_t tc_forward_ws_floats(int64_t G, int64_t N, int64_t D);
 size_t tc_backward_ws_floats(int64_t G, int64_t N, int64_t D);
+size_t tc_saved_floats(int64_t G, int64_t N, int64_t D);
+int tc_segments(int64_t G, int64_t N);
 cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws);
 cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv,
                         Workspace ws);

@@ -108,6 +108,8 @@ Launch make_launch(const la_problem* p, const la_shard* sh, void* stream) {
   L.n_total = p->seq_len;
   L.carry_prefix = sh ? sh->carry_in : nullptr;
   L.carry_suffix = sh ? sh->carry_suffix : nullptr;
+  L.saved_out = nullptr;
+  L.saved_in = nullptr;
   L.stream = (cudaStream_t)stream;
   return L;
 }
@@ -149,7 +151,8 @@ size_t bwd_floats(const la_problem* p) {
 
 la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, la_layout lq,
                        const void* k, la_layout lk, const void* v, la_layout lv, void* out,
-                       float* g, void* ws, size_t ws_bytes, void* stream, la_error_info* err) {
+                       float* g, void* ws, size_t ws_bytes, void* stream, la_error_info* err,
+                       void* saved = nullptr, size_t saved_bytes = 0) {
   la_status s = check_problem(p, err);
   if (s != LA_OK) return s;
   if (!q || !k || !v || !out || !g)
@@ -163,9 +166,20 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
   Launch L = make_launch(p, sh, stream);
   Tensors t{q, lq, k, lk, v, lv, nullptr, 0, nullptr, 0, nullptr};
   Workspace w = carve(ws, ws_bytes);
+  if (saved && saved_bytes < la_saved_state_bytes(p))
+    return fail(err, LA_ERR_WORKSPACE, "saved-state buffer smaller than la_saved_state_bytes");
   cudaMemsetAsync(w.flag, 0xFF, sizeof(unsigned long long), L.stream);
   cudaError_t e;
-  if (use_tc(p, tc_forward_supported(L, t)))
+  const bool tc = use_tc(p, tc_forward_supported(L, t));
+  if (saved) {
+    if (tc) {
+      L.saved_out = (float*)saved;
+    } else {  // header only: the backward recomputes its prefix states
+      const float hdr[kSavedHeader] = {kSavedMagic, (float)p->groups, (float)p->seq_len, (float)p->dim, 0.f};
+      cudaMemcpyAsync(saved, hdr, sizeof(hdr), cudaMemcpyHostToDevice, L.stream);
+    }
+  }
+  if (tc)
     e = tc_forward(L, t, out, g, w);
   else if (p->impl == LA_IMPL_TCGEN05)
     return fail(err, LA_ERR_UNSUPPORTED, "tcgen05 path needs bf16/fp16, D=128, canonical layouts");
@@ -178,7 +192,8 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
 la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, la_layout lq,
                         const void* k, la_layout lk, const void* v, la_layout lv, const void* o,
                         const void* omega, la_layout lw, const float* g, void* dq, void* dk,
-                        void* dv, void* ws, size_t ws_bytes, void* stream, la_error_info* err) {
+                        void* dv, void* ws, size_t ws_bytes, void* stream, la_error_info* err,
+                        const void* saved = nullptr, size_t saved_bytes = 0) {
   // check_backward_inputs (backward.cpp:13-28)
   if (p && (!o || !q || !k || !v))
     return fail(err, LA_ERR_MISSING_FORWARD_STATE,
@@ -198,9 +213,25 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
   Launch L = make_launch(p, sh, stream);
   Tensors t{q, lq, k, lk, v, lv, o, LA_FEATURE_MAJOR, omega, lw, g};
   Workspace w = carve(ws, ws_bytes);
+  const bool tc = use_tc(p, tc_backward_supported(L, t));
+  if (saved && tc) {
+    // validate the saved-state header written by la_forward_save
+    float hdr[kSavedHeader];
+    if (saved_bytes < sizeof(hdr) ||
+        cudaMemcpyAsync(hdr, saved, sizeof(hdr), cudaMemcpyDeviceToHost, L.stream) != cudaSuccess ||
+        cudaStreamSynchronize(L.stream) != cudaSuccess)
+      return fail(err, LA_ERR_MISSING_FORWARD_STATE, "cannot read the saved forward state");
+    const int P = tc_segments(p->groups, p->seq_len);
+    const int64_t seg = ((p->seq_len / 128 + P - 1) / P) * 128;
+    if (hdr[0] != kSavedMagic || hdr[1] != (float)p->groups || hdr[2] != (float)p->seq_len ||
+        hdr[3] != (float)p->dim)
+      return fail(err, LA_ERR_MISSING_FORWARD_STATE, "saved forward state does not match the problem");
+    if (hdr[4] == (float)P && hdr[5] == (float)seg && saved_bytes >= la_saved_state_bytes(p))
+      L.saved_in = (const float*)saved;  // else: produced by another path; recompute
+  }
   cudaMemsetAsync(w.flag, 0xFF, sizeof(unsigned long long), L.stream);
   cudaError_t e;
-  if (use_tc(p, tc_backward_supported(L, t)))
+  if (tc)
     e = tc_backward(L, t, dq, dk, dv, w);
   else if (p->impl == LA_IMPL_TCGEN05)
     return fail(err, LA_ERR_UNSUPPORTED, "tcgen05 path needs bf16/fp16, D=128, canonical layouts");
@@ -297,6 +328,29 @@ int32_t la_profile_read(char* json, size_t cap) {
 
 size_t la_shard_state_floats(const la_problem* p) {
   return p ? (size_t)(p->groups * state_floats(p->dim)) : 0;
+}
+
+size_t la_saved_state_bytes(const la_problem* p) {
+  if (!p || p->groups <= 0 || p->seq_len <= 0 || p->dim <= 0) return kSavedHeader * sizeof(float);
+  return tc_saved_floats(p->groups, p->seq_len, p->dim) * sizeof(float);
+}
+
+la_status la_forward_save(const la_problem* p, const void* q, la_layout lq, const void* k,
+                          la_layout lk, const void* v, la_layout lv, void* out, float* g,
+                          void* saved, size_t saved_bytes, void* workspace, size_t ws_bytes,
+                          void* stream, la_error_info* err) {
+  if (!saved) return fail(err, LA_ERR_INVALID_ARGUMENT, "null saved-state buffer");
+  return forward_impl(p, nullptr, q, lq, k, lk, v, lv, out, g, workspace, ws_bytes, stream, err, saved,
+                      saved_bytes);
+}
+
+la_status la_backward_saved(const la_problem* p, const void* q, la_layout lq, const void* k,
+                            la_layout lk, const void* v, la_layout lv, const void* o,
+                            const void* omega, la_layout lw, const float* g, const void* saved,
+                            size_t saved_bytes, void* dq, void* dk, void* dv, void* workspace,
+                            size_t ws_bytes, void* stream, la_error_info* err) {
+  return backward_impl(p, nullptr, q, lq, k, lk, v, lv, o, omega, lw, g, dq, dk, dv, workspace, ws_bytes,
+                       stream, err, saved, saved_bytes);
 }
 
 size_t la_forward_workspace_bytes(const la_problem* p) {

@@ -64,7 +64,7 @@ struct FwdParams {
   int P;
   int64_t row_offset;
   float a, b;
-  float* st_out;        // per-group final (S, z, sigma, rows) for the backward, or null
+  float* st_out;        // per-(group, segment) end state (S, z, sigma, rows) for the backward, or null
 };
 
 // ================================================================ forward main
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(320, 1)
     if (prm.st_out && nc > 0) {  // final state for the backward (S, z)
       mbar_wait(st_full, (nc - 1) & 1);
       tc_fence_after();
-      float* so = prm.st_out + grp * state_floats(kD);
+      float* so = prm.st_out + (grp * prm.P + p) * state_floats(kD);
       for (int m0 = 0; m0 < kD; m0 += 32) {
         uint32_t x[32];
         tmem_ld32(tmem + lane_base + kF_ST + m0, x);
@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
     if (eb == 0) tma_store_wait0();
-    if (prm.st_out && nc > 0) prm.st_out[grp * state_floats(kD) + kD * kD + kD + r] = sigma;
+    if (prm.st_out && nc > 0) prm.st_out[(grp * prm.P + p) * state_floats(kD) + kD * kD + kD + r] = sigma;
   }
   tc_fence_before();
   __syncthreads();
@@ -559,14 +559,6 @@ __global__ void __launch_bounds__(192, 1)
 constexpr size_t kFwdSmem = kFStages * kFStage + 2 * 8192 + 2 * kFT + 256 + (4 * kCF + kD) * 4 + 1024;
 constexpr size_t kAggSmem = 4 * kTile + 128 + 1024;
 
-int tc_segments(int64_t G, int64_t N) {
-  const int64_t chunks = N / kC;
-  // aim for >= 3 waves of 148 CTAs, segments of >= 8 chunks
-  int64_t p = (3 * 148 + G - 1) / G;
-  p = lmin(p, lmax(1, chunks / 8));
-  return (int)lmax(1, p);
-}
-
 __global__ void k_scan_fwd(float* states, int P, int64_t SZ, const float* carry) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t grp = blockIdx.y;
@@ -582,81 +574,76 @@ __global__ void k_scan_fwd(float* states, int P, int64_t SZ, const float* carry)
 
 }  // namespace
 
-static bool per_group_mode(int64_t G);
+int tc_segments(int64_t G, int64_t N) {
+  const char* e = getenv("LA_SEGMENTS");
+  if (e) return (int)lmax(1, atoi(e));
+  return choose_segments(G, N);
+}
 
 bool tc_forward_supported(const Launch& L, const Tensors& t) {
-  // segmented mode keeps 128-row segment boundaries (k_fwd_agg_tc tiles)
-  const int64_t align = per_group_mode(L.G) ? kCF : kC;
   return (L.dtype == LA_BF16 || L.dtype == LA_F16) && L.D == kD && L.causal && L.fault == LA_FAULT_NONE &&
-         L.N % align == 0 && t.lq == LA_SEQUENCE_MAJOR && t.lk == LA_SEQUENCE_MAJOR &&
+         L.N % kC == 0 && t.lq == LA_SEQUENCE_MAJOR && t.lk == LA_SEQUENCE_MAJOR &&
          t.lv == LA_FEATURE_MAJOR && L.G * L.N < (1ll << 31) && L.G * kD < (1ll << 31);
 }
 
-// One CTA per group walks the whole sequence (no carries, no aggregate pass)
-// when there are enough groups to keep HBM busy; otherwise the sequence is cut
-// into segments whose exclusive-prefix carries come from k_fwd_agg_tc + scan.
-static bool per_group_mode(int64_t G) {
-  const char* e = getenv("LA_FWD_SEGMENTS");
-  if (e) return atoi(e) <= 1;
-  // A single CTA per group only pays off once every SM has a group: the chunked
-  // kernel is bounded per SM by shared-memory bandwidth (TMA writes + SS-MMA operand
-  // reads), so using all 148 SMs via segments beats skipping the aggregate pass.
-  return G >= 148;
-}
-
 size_t tc_forward_ws_floats(int64_t G, int64_t N, int64_t D) {
-  if (D != kD || N % kCF) return 0;
-  const int64_t seg = per_group_mode(G) ? 0 : G * tc_segments(G, N) * state_floats(kD);
-  return (size_t)(seg + G * state_floats(kD));  // + per-group final state
+  if (D != kD || N % kC) return 0;
+  const int P = tc_segments(G, N);
+  return P > 1 ? (size_t)(G * P * state_floats(kD)) : 0;
 }
 
+size_t tc_saved_floats(int64_t G, int64_t N, int64_t D) {
+  if (D != kD || N % kC) return kSavedHeader;
+  return (size_t)(kSavedHeader + G * tc_segments(G, N) * state_floats(kD));
+}
+
+// One CTA per (group, segment). P = 1 walks whole sequences (no carries, no
+// aggregate pass); P > 1 takes exclusive-prefix carries from k_fwd_agg_tc + scan.
 cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws) {
   const bool bf = L.dtype == LA_BF16;
   const int64_t G = L.G, N = L.N;
   const int64_t SZ = state_floats(kD);
-  CUtensorMap mQ, mK, mV, mO;
-  if (!make_map(&mQ, t.q, bf, (uint64_t)(G * N), kD) || !make_map(&mK, t.k, bf, (uint64_t)(G * N), kD) ||
-      !make_map(&mV, t.v, bf, (uint64_t)(G * kD), (uint64_t)N) ||
-      !make_map(&mO, out, bf, (uint64_t)(G * kD), (uint64_t)N))
-    return cudaErrorInvalidValue;
-  // the main kernel works on 64-row chunks: Q/K boxes of 64 rows, V^T/O^T boxes of 64 columns
-  CUtensorMap mQ64, mK64, mV64, mO64;
-  if (!make_tma_map(&mQ64, t.q, bf, (uint64_t)(G * N), kD, 64, 2) ||
+  const int P = tc_segments(G, N);
+  const int64_t chunks = N / kC;
+  const int64_t seg = ((chunks + P - 1) / P) * kC;
+  CUtensorMap mK, mV, mQ64, mK64, mV64, mO64;
+  if (!make_map(&mK, t.k, bf, (uint64_t)(G * N), kD) || !make_map(&mV, t.v, bf, (uint64_t)(G * kD), (uint64_t)N) ||
+      !make_tma_map(&mQ64, t.q, bf, (uint64_t)(G * N), kD, 64, 2) ||
       !make_tma_map(&mK64, t.k, bf, (uint64_t)(G * N), kD, 64, 2) ||
       !make_tma_map(&mV64, t.v, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1) ||
       !make_tma_map(&mO64, out, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1))
     return cudaErrorInvalidValue;
   auto main_k = bf ? k_fwd_tc<true> : k_fwd_tc<false>;
   cudaFuncSetAttribute(main_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem);
-  float* final_state = ws.base;  // G * SZ: (S, z, sigma, rows) after the last row of each group
-  if (per_group_mode(G)) {
-    FwdParams prm{L.carry_prefix, g, ws.flag, N, G, N, 1, L.row_offset, L.a, L.b, final_state};
-    ProfScope ps("la_fwd_causal", L.stream);
-    main_k<<<dim3(1, G), 320, kFwdSmem, L.stream>>>(mQ64, mK64, mV64, mO64, prm);
-    note_launch(1);
-    return cudaGetLastError();
+  float* saved = L.saved_out ? L.saved_out + kSavedHeader : nullptr;
+  const float* states = L.carry_prefix;
+  int launches = 1;
+  if (P > 1) {
+    float* st = ws.base;
+    auto agg = bf ? k_fwd_agg_tc<true> : k_fwd_agg_tc<false>;
+    cudaFuncSetAttribute(agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggSmem);
+    {
+      ProfScope ps("la_fwd_agg", L.stream);
+      agg<<<dim3(P, G), 192, kAggSmem, L.stream>>>(mK, mV, st, N, seg, P);
+    }
+    {
+      ProfScope ps("la_fwd_scan", L.stream);
+      k_scan_fwd<<<dim3((unsigned)((SZ + 255) / 256), (unsigned)G), 256, 0, L.stream>>>(st, P, SZ,
+                                                                                      L.carry_prefix);
+    }
+    states = st;
+    launches += 2;
   }
-  const int P = tc_segments(G, N);
-  const int64_t chunks = N / kC;
-  const int64_t seg = ((chunks + P - 1) / P) * kC;
-  float* states = ws.base + G * SZ;
-  auto agg = bf ? k_fwd_agg_tc<true> : k_fwd_agg_tc<false>;
-  cudaFuncSetAttribute(agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggSmem);
-  {
-    ProfScope ps("la_fwd_agg", L.stream);
-    agg<<<dim3(P, G), 192, kAggSmem, L.stream>>>(mK, mV, states, N, seg, P);
+  if (L.saved_out) {
+    const float hdr[kSavedHeader] = {kSavedMagic, (float)G, (float)N, (float)kD, (float)P, (float)seg};
+    cudaMemcpyAsync(L.saved_out, hdr, sizeof(hdr), cudaMemcpyHostToDevice, L.stream);
   }
-  {
-    ProfScope ps("la_fwd_scan", L.stream);
-    k_scan_fwd<<<dim3((unsigned)((SZ + 255) / 256), (unsigned)G), 256, 0, L.stream>>>(states, P, SZ,
-                                                                                    L.carry_prefix);
-  }
-  FwdParams prm{states, g, ws.flag, N, G, seg, P, L.row_offset, L.a, L.b, nullptr};
+  FwdParams prm{states, g, ws.flag, N, G, seg, P, L.row_offset, L.a, L.b, saved};
   {
     ProfScope ps("la_fwd_causal", L.stream);
     main_k<<<dim3(P, G), 320, kFwdSmem, L.stream>>>(mQ64, mK64, mV64, mO64, prm);
   }
-  note_launch(3);
+  note_launch(launches);
   return cudaGetLastError();
 }
 

@@ -90,7 +90,8 @@ struct BwdParams {
   int64_t seg_len;
   int P;
   float a, b;
-  int dbg;  // debug bitmask (LA_BWD_DEBUG): 1 skip dS K, 2 skip W_hat S^T
+  int dbg;     // debug bitmask (LA_BWD_DEBUG): 1 skip dS K, 2 skip W_hat S^T
+  int skipS;   // aggregate pass: S records come from the forward (la_backward_saved)
 };
 
 // Epilogue step E0: W_hat = omega / g in place (bf16) and s_i = sum_j o_ij w_hat_ij.
@@ -199,10 +200,12 @@ __global__ void __launch_bounds__(192, 1)
         if (c >= 2) mbar_wait(&empty[s], ((c >> 1) & 1) ^ 1);
         const int64_t row0 = s0 + (int64_t)c * kCB;
         uint8_t* st = smem + s * kStage;
-        mbar_expect_tx(&full[s], kStage);
+        mbar_expect_tx(&full[s], prm.skipS ? 2 * kT64 : kStage);
         tma_load_3d(st, &tmQ, &full[s], 0, (int)(grp * prm.N + row0), 0);
-        tma_load_3d(st + kT64, &tmK, &full[s], 0, (int)(grp * prm.N + row0), 0);
-        tma_load_3d(st + 2 * kT64, &tmV, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
+        if (!prm.skipS) {
+          tma_load_3d(st + kT64, &tmK, &full[s], 0, (int)(grp * prm.N + row0), 0);
+          tma_load_3d(st + 2 * kT64, &tmV, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
+        }
         tma_load_3d(st + 3 * kT64, &tmW, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
       }
     }
@@ -215,7 +218,7 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t st = smem_u32(smem + s * kStage);
       mbar_wait(&full[s], (c >> 1) & 1);
       tc_fence_after();
-      if (elect_one()) {
+      if (!prm.skipS && elect_one()) {
         for (int ks = 0; ks < 4; ++ks)
           mma_ss(tmem + 128, mn(st + kT64, ks, 8192), kd(st + 2 * kT64, ks, 128), id_S,
                  (c > 0 || ks > 0) ? 1u : 0u);
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll 8
       for (int i = 0; i < kCB; ++i) {
         u += h2f<kBF16>(*(const uint16_t*)(st + sw128_off(i, r, kCB))) * s_s[i];
-        z += h2f<kBF16>(*(const uint16_t*)(st + kT64 + sw128_off(i, r, kCB)));
+        if (!prm.skipS) z += h2f<kBF16>(*(const uint16_t*)(st + kT64 + sw128_off(i, r, kCB)));
       }
 #pragma unroll
       for (int i8 = 0; i8 < kCB; i8 += 8) {
@@ -288,15 +291,16 @@ __global__ void __launch_bounds__(192, 1)
       for (int q = 0; q < 32; q += 4) {
         *(float4*)(rR + r * kD + j0 + q) = make_float4(__uint_as_float(xr[q]), __uint_as_float(xr[q + 1]),
                                                       __uint_as_float(xr[q + 2]), __uint_as_float(xr[q + 3]));
-        *(float4*)(rS + r * kD + j0 + q) = make_float4(__uint_as_float(xs[q]), __uint_as_float(xs[q + 1]),
-                                                      __uint_as_float(xs[q + 2]), __uint_as_float(xs[q + 3]));
+        if (!prm.skipS)
+          *(float4*)(rS + r * kD + j0 + q) = make_float4(__uint_as_float(xs[q]), __uint_as_float(xs[q + 1]),
+                                                        __uint_as_float(xs[q + 2]), __uint_as_float(xs[q + 3]));
       }
     }
-    rS[kD * kD + r] = z;
+    if (!prm.skipS) rS[kD * kD + r] = z;
     rR[kD * kD + r] = u;
     rR[kD * kD + kD + r] = cc;
     if (r == 0) {
-      rS[kD * kD + 2 * kD] = (float)(s1 - s0);
+      if (!prm.skipS) rS[kD * kD + 2 * kD] = (float)(s1 - s0);
       rR[kD * kD + 2 * kD] = (float)(s1 - s0);
     }
   }
@@ -311,12 +315,15 @@ __global__ void k_scan_bwd(float* stS, float* stR, int P, int64_t SZ, const floa
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t grp = blockIdx.y;
   if (e >= SZ) return;
-  float* bs = stS + grp * P * SZ + e;
   float* br = stR + grp * P * SZ + e;
-  float run = carry_pre ? carry_pre[grp * SZ + e] : 0.f;
-  for (int q = 0; q < P; ++q) {
-    run += bs[q * SZ];
-    bs[q * SZ] = run;
+  float run;
+  if (stS) {  // null when the forward's saved (already inclusive) S records are used
+    float* bs = stS + grp * P * SZ + e;
+    run = carry_pre ? carry_pre[grp * SZ + e] : 0.f;
+    for (int q = 0; q < P; ++q) {
+      run += bs[q * SZ];
+      bs[q * SZ] = run;
+    }
   }
   run = carry_suf ? carry_suf[grp * SZ + e] : 0.f;
   for (int q = P - 1; q >= 0; --q) {
@@ -719,24 +726,19 @@ __global__ void __launch_bounds__(192, 1)
 constexpr size_t kAggSmemB = 2 * kStage + 512 + 1024;
 constexpr size_t kMainSmemB = 2 * kStage + 2 * 8192 + 2 * 32768 + 160 + (kCB + kD) * 4 + 1024;
 
-int tcb_segments(int64_t G, int64_t N) {
-  const int64_t chunks = N / kCB;
-  int64_t p = (3 * 148 + G - 1) / G;
-  p = lmin(p, lmax(1, chunks / 16));
-  return (int)lmax(1, p);
-}
+int tcb_segments(int64_t G, int64_t N) { return tc_segments(G, N); }
 
 }  // namespace
 
 bool tc_backward_supported(const Launch& L, const Tensors& t) {
   return (L.dtype == LA_BF16 || L.dtype == LA_F16) && L.D == kD && L.causal && L.fault == LA_FAULT_NONE &&
-         L.N % kCB == 0 && t.lq == LA_SEQUENCE_MAJOR && t.lk == LA_SEQUENCE_MAJOR &&
+         L.N % 128 == 0 && t.lq == LA_SEQUENCE_MAJOR && t.lk == LA_SEQUENCE_MAJOR &&
          t.lv == LA_FEATURE_MAJOR && t.lw == LA_FEATURE_MAJOR && t.lo == LA_FEATURE_MAJOR &&
          L.G * L.N < (1ll << 31) && L.G * kD < (1ll << 31);
 }
 
 size_t tc_backward_ws_floats(int64_t G, int64_t N, int64_t D) {
-  if (D != kD || N % kCB) return 0;
+  if (D != kD || N % 128) return 0;
   return (size_t)(2 * G * tcb_segments(G, N) * state_floats(kD));
 }
 
@@ -744,9 +746,13 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
   const bool bf = L.dtype == LA_BF16;
   const int64_t G = L.G, N = L.N;
   const int P = tcb_segments(G, N);
-  const int64_t chunks = N / kCB;
-  const int64_t seg = ((chunks + P - 1) / P) * kCB;
+  const int64_t c128 = N / 128;
+  const int64_t seg = ((c128 + P - 1) / P) * 128;
   const int64_t SZ = state_floats(kD);
+  // S records: the paired forward's saved end states when they match this
+  // segmentation (no K/V re-read), else computed by the aggregate pass.
+  const float* sv = L.saved_in;
+  const bool use_saved = sv != nullptr;  // validated by the ABI layer
   float* stS = ws.base;
   float* stR = stS + G * P * SZ;
   CUtensorMap mQ, mK, mV, mW;
@@ -756,7 +762,8 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
       !make_tma_map(&mW, t.w, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1))
     return cudaErrorInvalidValue;
   const char* dbg = getenv("LA_BWD_DEBUG");
-  BwdParams prm{t.o, t.g, dq, dk, dv, stS, stR, N, seg, P, L.a, L.b, dbg ? atoi(dbg) : 0};
+  BwdParams prm{t.o, t.g, dq, dk, dv, use_saved ? const_cast<float*>(sv + kSavedHeader) : stS, stR, N, seg, P,
+                L.a, L.b, dbg ? atoi(dbg) : 0, use_saved ? 1 : 0};
   auto agg = bf ? k_bwd_agg_tc<true> : k_bwd_agg_tc<false>;
   auto main_k = bf ? k_bwd_tc<true> : k_bwd_tc<false>;
   cudaFuncSetAttribute(agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggSmemB);
@@ -768,7 +775,7 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
   {
     ProfScope ps("la_bwd_scan", L.stream);
     k_scan_bwd<<<dim3((unsigned)((SZ + 255) / 256), (unsigned)G), 256, 0, L.stream>>>(
-        stS, stR, P, SZ, L.carry_prefix, L.carry_suffix);
+        use_saved ? nullptr : stS, stR, P, SZ, L.carry_prefix, L.carry_suffix);
   }
   {
     ProfScope ps("la_bwd_causal", L.stream);
