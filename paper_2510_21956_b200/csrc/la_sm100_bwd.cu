@@ -334,8 +334,28 @@ __global__ void k_scan_bwd(float* stS, float* stR, int P, int64_t SZ, const floa
 }
 
 // ================================================================ main reverse sweep
+// Warp roles (320 threads): 0 TMA producer; 1 MMA issuer + TMEM owner;
+// 2-5 WG-A: W_hat/s, dS/P, dK^T/dV^T out, u/c; 6-9 WG-B: bR/bS operand copies,
+// z, dQ out. Each epilogue column sum uses 16-byte loads over a conflict-free
+// (rows-by-lane) mapping and a shuffle reduction.
+__device__ __forceinline__ void colsum8(const uint8_t* tile, int rows_tile, int c0, int r_begin, int nrows,
+                                        const float* wrow, float (&acc)[8], bool bf) {
+  // acc[u] += sum_{r in [r_begin, r_begin + nrows)} w[r] * tile[r][c0 + u]
+  for (int r = r_begin; r < r_begin + nrows; ++r) {
+    const uint4 v4 = *(const uint4*)(tile + sw128_off(r, c0, rows_tile));
+    const float w = wrow ? wrow[r] : 1.f;
+    const uint32_t x[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = bf ? unpack2<true>(x[q]) : unpack2<false>(x[q]);
+      acc[2 * q] += w * f.x;
+      acc[2 * q + 1] += w * f.y;
+    }
+  }
+}
+
 template <bool kBF16>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     k_bwd_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
              const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmW,
              BwdParams prm) {
@@ -358,9 +378,10 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* gr_full = bars + 11;
   uint64_t* gr_empty = bars + 12;
   uint64_t* r_full = bars + 13;
+  uint64_t* a2b = bars + 14;    // [2] per stage: WG-A wrote s of that chunk
   uint32_t* tslot = (uint32_t*)(bars + 16);
-  float* s_s = (float*)(bars + 20);   // [64]
-  float* zq = s_s + kCB;              // [128]
+  float* s_s = (float*)(bars + 20);   // [2][64]
+  float* zq = s_s + 2 * kCB;          // [128]
 
   const int p = blockIdx.x;
   const int64_t grp = blockIdx.y;
@@ -375,7 +396,7 @@ __global__ void __launch_bounds__(192, 1)
     tma_prefetch(&tmW);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1 + 128);
+      mbar_init(&empty[s], 1 + 256);
     }
     mbar_init(w_ready, 128);
     mbar_init(s_full, 1);
@@ -385,8 +406,10 @@ __global__ void __launch_bounds__(192, 1)
     mbar_init(ps_ready, 128);
     mbar_init(sR_ready, 128);
     mbar_init(gr_full, 1);
-    mbar_init(gr_empty, 128);
+    mbar_init(gr_empty, 256);
     mbar_init(r_full, 1);
+    mbar_init(&a2b[0], 128);
+    mbar_init(&a2b[1], 128);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
@@ -394,16 +417,14 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  // Carries (R_next, S_end, u, c, z) are written into TMEM by the epilogue warps
-  // before any role starts: the first S -= K^T V must see S_end.
-  float u = 0.f, cj = 0.f;
-  if (warp >= 2) {
+  // Carries (R_next, S_end, u, c, z) are written into TMEM by WG-B before any role
+  // starts: the first S -= K^T V must see S_end.
+  if (warp >= 6) {
     const uint32_t qd = warp & 3;
     const int r = (int)(qd * 32 + lane_id());
     const uint32_t lb = (qd * 32u) << 16;
     const float* recS = prm.stS + (grp * prm.P + p) * state_floats(kD);  // inclusive prefix at s1
     const float* recR = prm.stR + (grp * prm.P + p) * state_floats(kD);  // exclusive suffix after s1
-    // carries: R_next and S_end into TMEM (lanes m), u, c, z
     for (int j0 = 0; j0 < kD; j0 += 32) {
       uint32_t xr[32], xs[32];
 #pragma unroll
@@ -419,10 +440,7 @@ __global__ void __launch_bounds__(192, 1)
       tmem_st32(tmem + lb + kS + j0, xs);
     }
     tmem_st_wait();
-    u = recR[kD * kD + r];        // u_next (m = r)
-    cj = recR[kD * kD + kD + r];  // c_next (j = r)
-    zq[r] = recS[kD * kD + r];          // z at the segment end
-
+    zq[r] = recS[kD * kD + r];  // z at the segment end
   }
   tc_fence_before();
   __syncthreads();
@@ -471,7 +489,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int ks = 0; ks < 8; ++ks)  // T1 = Q K^T -> upper lane half
           mma_ss(tmem + kDP + kHalf, kd(aQ, ks, 64), kd(aK, ks, 64), id_T1, ks > 0);
         for (int ks = 0; ks < 4; ++ks)  // S -= K^T V
-          if (!(prm.dbg & 4)) mma_ss(tmem + kS, mn(aK, ks, 8192), kd(aV, ks, 128), id_Sneg, 1);
+          mma_ss(tmem + kS, mn(aK, ks, 8192), kd(aV, ks, 128), id_Sneg, 1);
         mma_commit(s_full);
       }
       __syncwarp();
@@ -495,9 +513,9 @@ __global__ void __launch_bounds__(192, 1)
         for (int h = 0; h < 2; ++h) {  // dQ[:, 64h:64h+64]
           const uint32_t d = tmem + kDQ + (h ? kHalf : 0u);
           for (int ks = 0; ks < 4; ++ks)  // dS K
-            if (!(prm.dbg & 1)) mma_ss(d, kd(adS, ks, 64), mn(aK + h * 8192, ks, 8192), id_dQ1, ks > 0);
+            mma_ss(d, kd(adS, ks, 64), mn(aK + h * 8192, ks, 8192), id_dQ1, ks > 0);
           for (int ks = 0; ks < 8; ++ks)  // W_hat (b S)^T
-            if (!(prm.dbg & 2)) mma_ss(d, mn(aW, ks, 8192), kd(aS + h * 8192, ks, 128), id_dQ2, (prm.dbg & 1) ? ks > 0 : 1);
+            mma_ss(d, mn(aW, ks, 8192), kd(aS + h * 8192, ks, 128), id_dQ2, 1);
         }
       }
       __syncwarp();
@@ -521,16 +539,19 @@ __global__ void __launch_bounds__(192, 1)
       }
       __syncwarp();
     }
-  } else {
-    // ------------------------------------------------------------ epilogue (warps 2..5)
+  } else if (warp < 6) {
+    // ------------------------------------------------------------ WG-A (warps 2..5)
     const uint32_t qd = warp & 3;
     const int l = (int)lane_id();
-    const int r = (int)(qd * 32) + l;            // full-lane row: m (R, S, dK) or j (dV)
+    const int r = (int)(qd * 32) + l;            // full-lane row: m (dK) or j (dV)
     const int ih = (int)(qd * 16) + (l & 15);    // half-lane row i of M=64 accumulators
     const bool upper = l >= 16;                  // lanes 16..31 of a quadrant: upper half
     const uint32_t lb = (qd * 32u) << 16;
     const int et = (int)threadIdx.x - 64;
     const float a = prm.a, b = prm.b;
+    const float* recR = prm.stR + (grp * prm.P + p) * state_floats(kD);
+    float u = recR[kD * kD + r];        // u_next (m = r)
+    float cj = recR[kD * kD + kD + r];  // c_next (j = r)
     uint4 o8[8];
     float4 g8[2];
     if (nc > 0) what_prefetch<kBF16>(prm, grp, s0 + (int64_t)(nc - 1) * kCB, et, o8, g8);
@@ -539,76 +560,25 @@ __global__ void __launch_bounds__(192, 1)
       const int64_t row0 = s0 + (int64_t)(nc - 1 - n) * kCB;
       uint8_t* st = smem + s * kStage;
       const uint8_t* q_t = st;
-      const uint8_t* k_t = st + kT64;
       uint8_t* w_t = st + 3 * kT64;
+      float* ss = s_s + s * kCB;
       // ---- E0: W_hat, s
       if (et == 0) traceb(1, n, 0);
-      named_bar(1, 128);
       mbar_wait(&full[s], (n >> 1) & 1);
       if (et == 0) traceb(1, n, 1);
-      what_pass<kBF16>(w_t, o8, g8, s_s, et);
+      what_pass<kBF16>(w_t, o8, g8, ss, et);
       if (n + 1 < nc) what_prefetch<kBF16>(prm, grp, row0 - kCB, et, o8, g8);
       fence_proxy_async();
+      named_bar(1, 128);  // s complete before any WG-A thread reads it
       mbar_arrive(w_ready);
-      named_bar(1, 128);  // s_s complete before any thread reads it
-      // ---- E_R: b R_next -> sR
+      mbar_arrive(&a2b[s]);
       if (et == 0) traceb(1, n, 2);
-      if (n >= 1) mbar_wait(r_full, (n - 1) & 1);
+      // ---- E1: dPt -> dS (lower half lanes), T1 -> P (upper half lanes)
+      mbar_wait(dpt_full, n & 1);
       if (et == 0) traceb(1, n, 3);
       tc_fence_after();
-#pragma unroll 1
-      for (int j0 = 0; j0 < kD; j0 += 32) {
-        uint32_t x[32];
-        tmem_ld32(tmem + lb + kR + j0, x);
-        tmem_ld_wait();
-#pragma unroll
-        for (int w8 = 0; w8 < 4; ++w8) {
-          uint4 v;
-          v.x = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 0]), b * __uint_as_float(x[8 * w8 + 1]));
-          v.y = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 2]), b * __uint_as_float(x[8 * w8 + 3]));
-          v.z = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 4]), b * __uint_as_float(x[8 * w8 + 5]));
-          v.w = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 6]), b * __uint_as_float(x[8 * w8 + 7]));
-          *(uint4*)(sR + sw128_off(r, j0 + 8 * w8, 128)) = v;
-        }
-      }
-      fence_proxy_async();
-      tc_fence_before();
-      mbar_arrive(sR_ready);
-      // ---- E_S: b S_prev -> sS ; z_prev
-      if (et == 0) traceb(1, n, 4);
-      mbar_wait(s_full, n & 1);
-      tc_fence_after();
-#pragma unroll 1
-      for (int j0 = 0; j0 < kD; j0 += 32) {
-        uint32_t x[32];
-        tmem_ld32(tmem + lb + kS + j0, x);
-        tmem_ld_wait();
-#pragma unroll
-        for (int w8 = 0; w8 < 4; ++w8) {
-          uint4 v;
-          v.x = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 0]), b * __uint_as_float(x[8 * w8 + 1]));
-          v.y = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 2]), b * __uint_as_float(x[8 * w8 + 3]));
-          v.z = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 4]), b * __uint_as_float(x[8 * w8 + 5]));
-          v.w = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 6]), b * __uint_as_float(x[8 * w8 + 7]));
-          *(uint4*)(sS + sw128_off(r, j0 + 8 * w8, 128)) = v;
-        }
-      }
-      fence_proxy_async();
-      tc_fence_before();
-      mbar_arrive(sS_ready);
       {
-        float ks_ = 0.f;  // z_m -= sum_t k_tm over this chunk (m = r)
-#pragma unroll 8
-        for (int t = 0; t < kCB; ++t) ks_ += h2f<kBF16>(*(const uint16_t*)(k_t + sw128_off(t, r, kCB)));
-        zq[r] -= ks_;
-      }
-      // ---- E1: dPt -> dS (lower half lanes), T1 -> P (upper half lanes)
-      if (et == 0) traceb(1, n, 5);
-      mbar_wait(dpt_full, n & 1);
-      if (et == 0) traceb(1, n, 6);
-      tc_fence_after();
-      {
-        const float si = s_s[ih];
+        const float si = ss[ih];
         uint8_t* dst = upper ? sP : sdS;
 #pragma unroll 1
         for (int t0 = 0; t0 < kCB; t0 += 32) {
@@ -640,39 +610,50 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_before();
       mbar_arrive(dpt_empty);
       mbar_arrive(ps_ready);
-      named_bar(1, 128);  // zq updated by every thread
-      // ---- E_out: dQ (half lanes), dK^T (lanes m), dV^T (lanes j)
+      if (et == 0) traceb(1, n, 4);
+      // ---- suffix-vector increments of this chunk (applied after its outputs):
+      //      du_m = sum_i q_im s_i ; dc_j = sum_i w_hat_ji
+      float du[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      {
+        const int mg = et >> 3, tg = et & 7;  // rows tg + 8k: conflict-free quarter-warps
+        for (int k8 = 0; k8 < kCB / 8; ++k8) {
+          const int i = tg + 8 * k8;
+          const uint4 v4 = *(const uint4*)(q_t + sw128_off(i, 8 * mg, kCB));
+          const float w = ss[i];
+          const uint32_t xx[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 f2 = unpack2<kBF16>(xx[q]);
+            du[2 * q] += w * f2.x;
+            du[2 * q + 1] += w * f2.y;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          du[q] += __shfl_xor_sync(0xffffffffu, du[q], 1);
+          du[q] += __shfl_xor_sync(0xffffffffu, du[q], 2);
+          du[q] += __shfl_xor_sync(0xffffffffu, du[q], 4);
+        }
+      }
+      float dc = 0.f;
+#pragma unroll
+      for (int i8 = 0; i8 < kCB; i8 += 8) {
+        const uint4 v4 = *(const uint4*)(w_t + sw128_off(r, i8, 128));
+        const uint32_t w4[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 f2 = unpack2<kBF16>(w4[q]);
+          dc += f2.x + f2.y;
+        }
+      }
+      // ---- E_out: dK^T (lanes m), dV^T (lanes j)
       if (et == 0) traceb(1, n, 7);
       mbar_wait(gr_full, n & 1);
       if (et == 0) traceb(1, n, 8);
       tc_fence_after();
       {
-        // this warp's scratch: its own 16 P rows and 16 dS rows (dead after gr_full)
-        uint8_t* scr_lo = sP + qd * 2048;
+        uint8_t* scr_lo = sP + qd * 2048;   // this warp's own P / dS rows are dead now
         uint8_t* scr_hi = sdS + qd * 2048;
-        const float si = s_s[ih];
-        const int m0 = upper ? 64 : 0;
-        uint4 v[8];
-#pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 32) {
-          uint32_t x[32];
-          tmem_ld32(tmem + lb + kDQ + c0, x);
-          tmem_ld_wait();
-#pragma unroll
-          for (int w4 = 0; w4 < 4; ++w4) {
-            uint32_t q4[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int m = m0 + c0 + 8 * w4 + 2 * q;
-              q4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) - si * b * zq[m],
-                                   __uint_as_float(x[8 * w4 + 2 * q + 1]) - si * b * zq[m + 1]);
-            }
-            v[c0 / 8 + w4] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
-          }
-        }
-        // segment L: dQ row 16 qd + (L & 15), columns [64 (L >> 4), +64)
-        uint16_t* dqb = (uint16_t*)prm.dq + (grp * prm.N + row0 + qd * 16) * kD;
-        warp_store_rows(scr_lo, scr_hi, v, [&](int seg) { return dqb + (seg & 15) * kD + (seg >> 4) * 64; });
         const float bu = b * u, ac = a * cj;
         uint4 vk[8], vv[8];
 #pragma unroll
@@ -693,28 +674,153 @@ __global__ void __launch_bounds__(192, 1)
             vv[c0 / 8 + w4] = make_uint4(v4[0], v4[1], v4[2], v4[3]);
           }
         }
-        // segment L: row 32 qd + L of dK^T / dV^T, columns [row0, row0 + 64)
+        tc_fence_before();
+        mbar_arrive(gr_empty);
         uint16_t* dkb = (uint16_t*)prm.dk + (grp * kD + qd * 32) * prm.N + row0;
         uint16_t* dvb = (uint16_t*)prm.dv + (grp * kD + qd * 32) * prm.N + row0;
         warp_store_rows(scr_lo, scr_hi, vk, [&](int seg) { return dkb + seg * prm.N; });
         warp_store_rows(scr_lo, scr_hi, vv, [&](int seg) { return dvb + seg * prm.N; });
       }
-      tc_fence_before();
-      mbar_arrive(gr_empty);
-      // ---- suffix vectors: u_m += sum_i q_im s_i ; c_j += sum_i w_hat_ji
-#pragma unroll 8
-      for (int i = 0; i < kCB; ++i) u += h2f<kBF16>(*(const uint16_t*)(q_t + sw128_off(i, r, kCB))) * s_s[i];
+      // apply this chunk's suffix increments: lane group leader (tg == 0) owns m = 8 mg .. 8 mg + 7
+      {
+        float* du_s = zq + kD;  // [128] scratch after z (WG-A only)
+        if ((et & 7) == 0) {
+          const int mg = et >> 3;
+          *(float4*)(du_s + 8 * mg) = make_float4(du[0], du[1], du[2], du[3]);
+          *(float4*)(du_s + 8 * mg + 4) = make_float4(du[4], du[5], du[6], du[7]);
+        }
+        named_bar(1, 128);
+        u += du_s[r];
+        named_bar(1, 128);
+      }
+      cj += dc;
+      if (et == 0) traceb(1, n, 9);
+      mbar_arrive(&empty[s]);
+    }
+  } else {
+    // ------------------------------------------------------------ WG-B (warps 6..9)
+    const uint32_t qd = warp & 3;
+    const int l = (int)lane_id();
+    const int r = (int)(qd * 32) + l;            // m
+    const int ih = (int)(qd * 16) + (l & 15);
+    const bool upper = l >= 16;
+    const uint32_t lb = (qd * 32u) << 16;
+    const int eb = (int)threadIdx.x - 192;
+    const float b = prm.b;
+    for (int n = 0; n < nc; ++n) {
+      const int s = n & 1;
+      const int64_t row0 = s0 + (int64_t)(nc - 1 - n) * kCB;
+      const uint8_t* k_t = smem + s * kStage + kT64;
+      // ---- E_R: b R_next -> sR
+      if (eb == 0) traceb(2, n, 0);
+      if (n >= 1) mbar_wait(r_full, (n - 1) & 1);
+      if (eb == 0) traceb(2, n, 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int j0 = 0; j0 < kD; j0 += 32) {
+        uint32_t x[32];
+        tmem_ld32(tmem + lb + kR + j0, x);
+        tmem_ld_wait();
 #pragma unroll
-      for (int i8 = 0; i8 < kCB; i8 += 8) {
-        const uint4 v4 = *(const uint4*)(w_t + sw128_off(r, i8, 128));
-        const uint32_t w4[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float2 f2 = unpack2<kBF16>(w4[q]);
-          cj += f2.x + f2.y;
+        for (int w8 = 0; w8 < 4; ++w8) {
+          uint4 v;
+          v.x = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 0]), b * __uint_as_float(x[8 * w8 + 1]));
+          v.y = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 2]), b * __uint_as_float(x[8 * w8 + 3]));
+          v.z = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 4]), b * __uint_as_float(x[8 * w8 + 5]));
+          v.w = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 6]), b * __uint_as_float(x[8 * w8 + 7]));
+          *(uint4*)(sR + sw128_off(r, j0 + 8 * w8, 128)) = v;
         }
       }
-      if (et == 0) traceb(1, n, 9);
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(sR_ready);
+      // ---- E_S: b S_prev -> sS
+      if (eb == 0) traceb(2, n, 2);
+      mbar_wait(s_full, n & 1);
+      if (eb == 0) traceb(2, n, 3);
+      tc_fence_after();
+#pragma unroll 1
+      for (int j0 = 0; j0 < kD; j0 += 32) {
+        uint32_t x[32];
+        tmem_ld32(tmem + lb + kS + j0, x);
+        tmem_ld_wait();
+#pragma unroll
+        for (int w8 = 0; w8 < 4; ++w8) {
+          uint4 v;
+          v.x = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 0]), b * __uint_as_float(x[8 * w8 + 1]));
+          v.y = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 2]), b * __uint_as_float(x[8 * w8 + 3]));
+          v.z = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 4]), b * __uint_as_float(x[8 * w8 + 5]));
+          v.w = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 6]), b * __uint_as_float(x[8 * w8 + 7]));
+          *(uint4*)(sS + sw128_off(r, j0 + 8 * w8, 128)) = v;
+        }
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(sS_ready);
+      // ---- z_prev: z -= sum_t k_t over this chunk (thread (mg, tg): columns 8 mg.., rows tg + 8 k)
+      {
+        const int mg = eb >> 3, tg = eb & 7;
+        float zs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int k8 = 0; k8 < kCB / 8; ++k8) {
+          const uint4 v4 = *(const uint4*)(k_t + sw128_off(tg + 8 * k8, 8 * mg, kCB));
+          const uint32_t xx[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 f2 = unpack2<kBF16>(xx[q]);
+            zs[2 * q] += f2.x;
+            zs[2 * q + 1] += f2.y;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          zs[q] += __shfl_xor_sync(0xffffffffu, zs[q], 1);
+          zs[q] += __shfl_xor_sync(0xffffffffu, zs[q], 2);
+          zs[q] += __shfl_xor_sync(0xffffffffu, zs[q], 4);
+        }
+        if (tg == 0) {
+          const float4 za = *(const float4*)(zq + 8 * mg), zb = *(const float4*)(zq + 8 * mg + 4);
+          *(float4*)(zq + 8 * mg) = make_float4(za.x - zs[0], za.y - zs[1], za.z - zs[2], za.w - zs[3]);
+          *(float4*)(zq + 8 * mg + 4) = make_float4(zb.x - zs[4], zb.y - zs[5], zb.z - zs[6], zb.w - zs[7]);
+        }
+        named_bar(2, 128);
+      }
+      // ---- dQ out (half lanes): dQ = acc - b s_i z_prev
+      mbar_wait(&a2b[s], (n >> 1) & 1);  // s of this chunk written by WG-A (per stage: no lapping)
+      if (eb == 0) traceb(2, n, 4);
+      mbar_wait(gr_full, n & 1);
+      if (eb == 0) traceb(2, n, 5);
+      tc_fence_after();
+      {
+        const float si = s_s[s * kCB + ih];
+        const int m0 = upper ? 64 : 0;
+        uint4 v[8];
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          uint32_t x[32];
+          tmem_ld32(tmem + lb + kDQ + c0, x);
+          tmem_ld_wait();
+#pragma unroll
+          for (int w4 = 0; w4 < 4; ++w4) {
+            uint32_t q4[4];
+            const float4 za = *(const float4*)(zq + m0 + c0 + 8 * w4);
+            const float4 zb = *(const float4*)(zq + m0 + c0 + 8 * w4 + 4);
+            const float z8[8] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              q4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) - si * b * z8[2 * q],
+                                   __uint_as_float(x[8 * w4 + 2 * q + 1]) - si * b * z8[2 * q + 1]);
+            v[c0 / 8 + w4] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(gr_empty);
+        // scratch: this warp's 4 KB of sS (dead until E_S of the next chunk)
+        uint8_t* scr_lo = sS + qd * 4096;
+        uint8_t* scr_hi = scr_lo + 2048;
+        uint16_t* dqb = (uint16_t*)prm.dq + (grp * prm.N + row0 + qd * 16) * kD;
+        warp_store_rows(scr_lo, scr_hi, v, [&](int seg) { return dqb + (seg & 15) * kD + (seg >> 4) * 64; });
+      }
+      if (eb == 0) traceb(2, n, 6);
       mbar_arrive(&empty[s]);
     }
   }
@@ -724,7 +830,7 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 constexpr size_t kAggSmemB = 2 * kStage + 512 + 1024;
-constexpr size_t kMainSmemB = 2 * kStage + 2 * 8192 + 2 * 32768 + 160 + (kCB + kD) * 4 + 1024;
+constexpr size_t kMainSmemB = 2 * kStage + 2 * 8192 + 2 * 32768 + 160 + (2 * kCB + 2 * kD) * 4 + 1024;
 
 int tcb_segments(int64_t G, int64_t N) { return tc_segments(G, N); }
 
@@ -779,7 +885,7 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
   }
   {
     ProfScope ps("la_bwd_causal", L.stream);
-    main_k<<<dim3(P, G), 192, kMainSmemB, L.stream>>>(mQ, mK, mV, mW, prm);
+    main_k<<<dim3(P, G), 320, kMainSmemB, L.stream>>>(mQ, mK, mV, mW, prm);
   }
   note_launch(3);
   return cudaGetLastError();

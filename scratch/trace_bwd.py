@@ -11,9 +11,10 @@ out = torch.empty(G, D, N, device=dev, dtype=torch.bfloat16); g = torch.empty(G,
 dq = torch.empty_like(q); dk = torch.empty_like(v); dv = torch.empty_like(v)
 wsf = torch.empty(L.la_forward_workspace_bytes(C.byref(p)), device=dev, dtype=torch.uint8)
 wsb = torch.empty(L.la_backward_workspace_bytes(C.byref(p)), device=dev, dtype=torch.uint8)
-L.la_forward(C.byref(p), q.data_ptr(), 1, k.data_ptr(), 1, v.data_ptr(), 0, out.data_ptr(), g.data_ptr(), wsf.data_ptr(), wsf.numel(), None, None)
+sv = torch.empty(L.la_saved_state_bytes(C.byref(p)), device=dev, dtype=torch.uint8)
+L.la_forward_save(C.byref(p), q.data_ptr(), 1, k.data_ptr(), 1, v.data_ptr(), 0, out.data_ptr(), g.data_ptr(), sv.data_ptr(), sv.numel(), wsf.data_ptr(), wsf.numel(), None, None)
 for _ in range(2):
-    L.la_backward(C.byref(p), q.data_ptr(), 1, k.data_ptr(), 1, v.data_ptr(), 0, out.data_ptr(), w.data_ptr(), 0, g.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), wsb.data_ptr(), wsb.numel(), None, None)
+    L.la_backward_saved(C.byref(p), q.data_ptr(), 1, k.data_ptr(), 1, v.data_ptr(), 0, out.data_ptr(), w.data_ptr(), 0, g.data_ptr(), sv.data_ptr(), sv.numel(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), wsb.data_ptr(), wsb.numel(), None, None)
 torch.cuda.synchronize()
 buf = (C.c_ulonglong * (4 * 64 * 10))()
 L.la_internal_trace_read_bwd(buf)
@@ -21,6 +22,8 @@ t = np.array(buf, dtype=np.int64).reshape(4, 64, 10)
 t0 = t[0, 10, 0]
 print("MMA: start,full,dpt_empty,w_ready,sS_ready,ps_ready,gr_empty,sR_ready")
 for c in range(10, 14): print(c, (t[0, c, :8] - t0).tolist())
-print("EPI: E0start,full,ERstart,r_full,ESstart,s_full... E1start,dpt_full,Eoutstart,gr_full,end")
-for c in range(10, 14): print(c, (t[1, c, :10] - t0).tolist())
-print("period", np.diff(t[0, 5:40, 0]).mean())
+print("WGA: E0start,full,w_ready-arr,dpt_full,ps_ready-arr,-,-,Eout-start,gr_full,end")
+for c in range(10, 14): print(c, (t[1, c, [0,1,2,3,4,7,8,9]] - t0).tolist())
+print("WGB: ER-start,r_full,ES-start,s_full,a2b,gr_full,end")
+for c in range(10, 14): print(c, (t[2, c, :7] - t0).tolist())
+print("period", np.diff(t[0, 5:60, 0]).mean())
