@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(320, 1)
              const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
              FwdParams prm) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = align1024(smem_raw);
   uint8_t* sP = smem + kFStages * kFStage;   // [2][8K]   P' (rows i, cols t)
   uint8_t* sO = sP + 2 * 8192;               // [2][16K]  O^T staging (rows j, cols i)
   uint64_t* bars = (uint64_t*)(sO + 2 * kFT);
@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(192, 1)
     k_fwd_agg_tc(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                  float* states, int64_t N, int64_t seg_len, int P) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = align1024(smem_raw);
   uint8_t* sK = smem;                  // [2][32K]
   uint8_t* sV = smem + 2 * kTile;      // [2][32K]
   uint64_t* bars = (uint64_t*)(smem + 4 * kTile);

@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(192, 1)
                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmW,
                  BwdParams prm) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = align1024(smem_raw);
   uint64_t* bars = (uint64_t*)(smem + 2 * kStage);
   uint64_t* full = bars;       // [2]
   uint64_t* empty = bars + 2;  // [2]
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(320, 1)
              const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmW,
              BwdParams prm) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = align1024(smem_raw);
   uint8_t* sP = smem + 2 * kStage;         // P  [64 rows i][64 t]     8 KB
   uint8_t* sdS = sP + 8192;                // dS [64 rows i][64 t]     8 KB
   uint8_t* sR = sdS + 8192;                // b R  [128 rows m][128 j] 32 KB
