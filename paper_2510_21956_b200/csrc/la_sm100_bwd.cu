@@ -655,31 +655,34 @@ __global__ void __launch_bounds__(320, 1)
         uint8_t* scr_lo = sP + qd * 2048;   // this warp's own P / dS rows are dead now
         uint8_t* scr_hi = sdS + qd * 2048;
         const float bu = b * u, ac = a * cj;
-        uint4 vk[8], vv[8];
-#pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 32) {
-          uint32_t xk[32], xv[32];
-          tmem_ld32(tmem + lb + kDK + c0, xk);
-          tmem_ld32(tmem + lb + kDV + c0, xv);
-          tmem_ld_wait();
-#pragma unroll
-          for (int w4 = 0; w4 < 4; ++w4) {
-            uint32_t k4[4], v4[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              k4[q] = pack2<kBF16>(__uint_as_float(xk[8 * w4 + 2 * q]) - bu, __uint_as_float(xk[8 * w4 + 2 * q + 1]) - bu);
-              v4[q] = pack2<kBF16>(__uint_as_float(xv[8 * w4 + 2 * q]) + ac, __uint_as_float(xv[8 * w4 + 2 * q + 1]) + ac);
-            }
-            vk[c0 / 8 + w4] = make_uint4(k4[0], k4[1], k4[2], k4[3]);
-            vv[c0 / 8 + w4] = make_uint4(v4[0], v4[1], v4[2], v4[3]);
-          }
-        }
-        tc_fence_before();
-        mbar_arrive(gr_empty);
         uint16_t* dkb = (uint16_t*)prm.dk + (grp * kD + qd * 32) * prm.N + row0;
         uint16_t* dvb = (uint16_t*)prm.dv + (grp * kD + qd * 32) * prm.N + row0;
-        warp_store_rows(scr_lo, scr_hi, vk, [&](int seg) { return dkb + seg * prm.N; });
-        warp_store_rows(scr_lo, scr_hi, vv, [&](int seg) { return dvb + seg * prm.N; });
+#pragma unroll 1
+        for (int which = 0; which < 2; ++which) {  // dK^T then dV^T: one tile live at a time
+          const uint32_t col = which ? kDV : kDK;
+          const float add = which ? ac : -bu;
+          uint4 vt[8];
+#pragma unroll
+          for (int c0 = 0; c0 < 64; c0 += 32) {
+            uint32_t x[32];
+            tmem_ld32(tmem + lb + col + c0, x);
+            tmem_ld_wait();
+#pragma unroll
+            for (int w4 = 0; w4 < 4; ++w4) {
+              uint32_t k4[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                k4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) + add, __uint_as_float(x[8 * w4 + 2 * q + 1]) + add);
+              vt[c0 / 8 + w4] = make_uint4(k4[0], k4[1], k4[2], k4[3]);
+            }
+          }
+          if (which) {
+            tc_fence_before();
+            mbar_arrive(gr_empty);
+          }
+          uint16_t* base = which ? dvb : dkb;
+          warp_store_rows(scr_lo, scr_hi, vt, [&](int seg) { return base + seg * prm.N; });
+        }
       }
       // apply this chunk's suffix increments: lane group leader (tg == 0) owns m = 8 mg .. 8 mg + 7
       {
