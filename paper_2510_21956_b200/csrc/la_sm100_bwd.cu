@@ -136,6 +136,60 @@ __device__ __forceinline__ void what_pass(uint8_t* w_t, const uint4 (&o8)[8], co
   }
 }
 
+// Half-tile variant used when both epilogue warpgroups share the pass: rows
+// j = jbase + 16 rr + jg (rr < 4); the partial s of this half goes to s_half.
+template <bool kBF16>
+__device__ __forceinline__ void what_pass_half(uint8_t* w_t, const uint4 (&o4)[4], const float4 (&g8)[2],
+                                               float* s_half, int et, int jbase) {
+  const int lane = et & 31, w = et >> 5;
+  const int jg = lane & 15, ig = 2 * w + (lane >> 4);
+  float ginv[8] = {1.f / g8[0].x, 1.f / g8[0].y, 1.f / g8[0].z, 1.f / g8[0].w,
+                   1.f / g8[1].x, 1.f / g8[1].y, 1.f / g8[1].z, 1.f / g8[1].w};
+  float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    const int j = jbase + 16 * rr + jg;
+    uint4* p = (uint4*)(w_t + sw128_off(j, 8 * ig, 128));
+    const uint4 wv = *p;
+    const uint32_t wa[4] = {wv.x, wv.y, wv.z, wv.w};
+    const uint32_t oa[4] = {o4[rr].x, o4[rr].y, o4[rr].z, o4[rr].w};
+    uint32_t res[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float2 wf = unpack2<kBF16>(wa[u]);
+      const float2 of = unpack2<kBF16>(oa[u]);
+      const float w0 = wf.x * ginv[2 * u], w1 = wf.y * ginv[2 * u + 1];
+      sp[2 * u] += of.x * w0;
+      sp[2 * u + 1] += of.y * w1;
+      res[u] = pack2<kBF16>(w0, w1);
+    }
+    *p = make_uint4(res[0], res[1], res[2], res[3]);
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+#pragma unroll
+    for (int off = 1; off < 16; off <<= 1) sp[u] += __shfl_xor_sync(0xffffffffu, sp[u], off);
+  }
+  if (jg == 0) {
+    *(float4*)(s_half + 8 * ig) = make_float4(sp[0], sp[1], sp[2], sp[3]);
+    *(float4*)(s_half + 8 * ig + 4) = make_float4(sp[4], sp[5], sp[6], sp[7]);
+  }
+}
+
+template <bool kBF16>
+__device__ __forceinline__ void what_prefetch_half(const BwdParams& prm, int64_t grp, int64_t row0, int et,
+                                                   int jbase, uint4 (&o4)[4], float4 (&g8)[2]) {
+  const int lane = et & 31, w = et >> 5;
+  const int jg = lane & 15, ig = 2 * w + (lane >> 4);
+  const uint16_t* o = (const uint16_t*)prm.o;
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr)
+    o4[rr] = __ldg((const uint4*)(o + (grp * kD + jbase + 16 * rr + jg) * prm.N + row0 + 8 * ig));
+  const float* gp = prm.g + grp * prm.N + row0 + 8 * ig;
+  g8[0] = __ldg((const float4*)gp);
+  g8[1] = __ldg((const float4*)(gp + 4));
+}
+
 // Prefetch of this thread's O^T slice (8 rows j x 8 columns i) and g for a chunk.
 template <bool kBF16>
 __device__ __forceinline__ void what_prefetch(const BwdParams& prm, int64_t grp, int64_t row0, int et,
@@ -378,10 +432,10 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* gr_full = bars + 11;
   uint64_t* gr_empty = bars + 12;
   uint64_t* r_full = bars + 13;
-  uint64_t* a2b = bars + 14;    // [2] per stage: WG-A wrote s of that chunk
   uint32_t* tslot = (uint32_t*)(bars + 16);
-  float* s_s = (float*)(bars + 20);   // [2][64]
-  float* zq = s_s + 2 * kCB;          // [128]
+  float* s_s = (float*)(bars + 20);   // [2 stages][2 halves][64]
+  float* du_s = s_s + 4 * kCB;        // [2][128]  WG-A -> WG-B suffix increments of u
+  float* zq = du_s + 2 * kD;          // [128]
 
   const int p = blockIdx.x;
   const int64_t grp = blockIdx.y;
@@ -408,8 +462,6 @@ __global__ void __launch_bounds__(320, 1)
     mbar_init(gr_full, 1);
     mbar_init(gr_empty, 256);
     mbar_init(r_full, 1);
-    mbar_init(&a2b[0], 128);
-    mbar_init(&a2b[1], 128);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
@@ -541,44 +593,44 @@ __global__ void __launch_bounds__(320, 1)
     }
   } else if (warp < 6) {
     // ------------------------------------------------------------ WG-A (warps 2..5)
+    // W_hat/s over feature rows 0..63, dS/P, du (handed to WG-B), dV^T out, c.
     const uint32_t qd = warp & 3;
     const int l = (int)lane_id();
-    const int r = (int)(qd * 32) + l;            // full-lane row: m (dK) or j (dV)
+    const int r = (int)(qd * 32) + l;            // j of dV^T
     const int ih = (int)(qd * 16) + (l & 15);    // half-lane row i of M=64 accumulators
     const bool upper = l >= 16;                  // lanes 16..31 of a quadrant: upper half
     const uint32_t lb = (qd * 32u) << 16;
     const int et = (int)threadIdx.x - 64;
     const float a = prm.a, b = prm.b;
     const float* recR = prm.stR + (grp * prm.P + p) * state_floats(kD);
-    float u = recR[kD * kD + r];        // u_next (m = r)
     float cj = recR[kD * kD + kD + r];  // c_next (j = r)
-    uint4 o8[8];
+    uint4 o4[4];
     float4 g8[2];
-    if (nc > 0) what_prefetch<kBF16>(prm, grp, s0 + (int64_t)(nc - 1) * kCB, et, o8, g8);
+    if (nc > 0) what_prefetch_half<kBF16>(prm, grp, s0 + (int64_t)(nc - 1) * kCB, et, 0, o4, g8);
     for (int n = 0; n < nc; ++n) {
       const int s = n & 1;
       const int64_t row0 = s0 + (int64_t)(nc - 1 - n) * kCB;
       uint8_t* st = smem + s * kStage;
       const uint8_t* q_t = st;
       uint8_t* w_t = st + 3 * kT64;
-      float* ss = s_s + s * kCB;
-      // ---- E0: W_hat, s
+      float* sA = s_s + s * 2 * kCB;
+      float* sB = sA + kCB;
+      // ---- E0 (rows 0..63): W_hat, partial s
       if (et == 0) traceb(1, n, 0);
       mbar_wait(&full[s], (n >> 1) & 1);
       if (et == 0) traceb(1, n, 1);
-      what_pass<kBF16>(w_t, o8, g8, ss, et);
-      if (n + 1 < nc) what_prefetch<kBF16>(prm, grp, row0 - kCB, et, o8, g8);
+      what_pass_half<kBF16>(w_t, o4, g8, sA, et, 0);
+      if (n + 1 < nc) what_prefetch_half<kBF16>(prm, grp, row0 - kCB, et, 0, o4, g8);
       fence_proxy_async();
-      named_bar(1, 128);  // s complete before any WG-A thread reads it
+      named_bar(3, 256);  // both halves of W_hat and s are complete
       mbar_arrive(w_ready);
-      mbar_arrive(&a2b[s]);
       if (et == 0) traceb(1, n, 2);
       // ---- E1: dPt -> dS (lower half lanes), T1 -> P (upper half lanes)
       mbar_wait(dpt_full, n & 1);
       if (et == 0) traceb(1, n, 3);
       tc_fence_after();
       {
-        const float si = ss[ih];
+        const float si = sA[ih] + sB[ih];
         uint8_t* dst = upper ? sP : sdS;
 #pragma unroll 1
         for (int t0 = 0; t0 < kCB; t0 += 32) {
@@ -611,15 +663,15 @@ __global__ void __launch_bounds__(320, 1)
       mbar_arrive(dpt_empty);
       mbar_arrive(ps_ready);
       if (et == 0) traceb(1, n, 4);
-      // ---- suffix-vector increments of this chunk (applied after its outputs):
-      //      du_m = sum_i q_im s_i ; dc_j = sum_i w_hat_ji
-      float du[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      // ---- du_m = sum_i q_im s_i of this chunk -> du_s[n & 1] for WG-B
       {
         const int mg = et >> 3, tg = et & 7;  // rows tg + 8k: conflict-free quarter-warps
+        float du[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
         for (int k8 = 0; k8 < kCB / 8; ++k8) {
           const int i = tg + 8 * k8;
           const uint4 v4 = *(const uint4*)(q_t + sw128_off(i, 8 * mg, kCB));
-          const float w = ss[i];
+          const float w = sA[i] + sB[i];
           const uint32_t xx[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -634,7 +686,13 @@ __global__ void __launch_bounds__(320, 1)
           du[q] += __shfl_xor_sync(0xffffffffu, du[q], 2);
           du[q] += __shfl_xor_sync(0xffffffffu, du[q], 4);
         }
+        if (tg == 0) {
+          float* dst = du_s + (n & 1) * kD + 8 * mg;
+          *(float4*)dst = make_float4(du[0], du[1], du[2], du[3]);
+          *(float4*)(dst + 4) = make_float4(du[4], du[5], du[6], du[7]);
+        }
       }
+      // ---- dc_j = sum_i w_hat_ji
       float dc = 0.f;
 #pragma unroll
       for (int i8 = 0; i8 < kCB; i8 += 8) {
@@ -646,7 +704,7 @@ __global__ void __launch_bounds__(320, 1)
           dc += f2.x + f2.y;
         }
       }
-      // ---- E_out: dK^T (lanes m), dV^T (lanes j)
+      // ---- dV^T out (lanes j): + a c_next
       if (et == 0) traceb(1, n, 7);
       mbar_wait(gr_full, n & 1);
       if (et == 0) traceb(1, n, 8);
@@ -654,47 +712,26 @@ __global__ void __launch_bounds__(320, 1)
       {
         uint8_t* scr_lo = sP + qd * 2048;   // this warp's own P / dS rows are dead now
         uint8_t* scr_hi = sdS + qd * 2048;
-        const float bu = b * u, ac = a * cj;
-        uint16_t* dkb = (uint16_t*)prm.dk + (grp * kD + qd * 32) * prm.N + row0;
+        const float ac = a * cj;
+        uint4 vt[8];
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          uint32_t x[32];
+          tmem_ld32(tmem + lb + kDV + c0, x);
+          tmem_ld_wait();
+#pragma unroll
+          for (int w4 = 0; w4 < 4; ++w4) {
+            uint32_t k4[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              k4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) + ac, __uint_as_float(x[8 * w4 + 2 * q + 1]) + ac);
+            vt[c0 / 8 + w4] = make_uint4(k4[0], k4[1], k4[2], k4[3]);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(gr_empty);
         uint16_t* dvb = (uint16_t*)prm.dv + (grp * kD + qd * 32) * prm.N + row0;
-#pragma unroll 1
-        for (int which = 0; which < 2; ++which) {  // dK^T then dV^T: one tile live at a time
-          const uint32_t col = which ? kDV : kDK;
-          const float add = which ? ac : -bu;
-          uint4 vt[8];
-#pragma unroll
-          for (int c0 = 0; c0 < 64; c0 += 32) {
-            uint32_t x[32];
-            tmem_ld32(tmem + lb + col + c0, x);
-            tmem_ld_wait();
-#pragma unroll
-            for (int w4 = 0; w4 < 4; ++w4) {
-              uint32_t k4[4];
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                k4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) + add, __uint_as_float(x[8 * w4 + 2 * q + 1]) + add);
-              vt[c0 / 8 + w4] = make_uint4(k4[0], k4[1], k4[2], k4[3]);
-            }
-          }
-          if (which) {
-            tc_fence_before();
-            mbar_arrive(gr_empty);
-          }
-          uint16_t* base = which ? dvb : dkb;
-          warp_store_rows(scr_lo, scr_hi, vt, [&](int seg) { return base + seg * prm.N; });
-        }
-      }
-      // apply this chunk's suffix increments: lane group leader (tg == 0) owns m = 8 mg .. 8 mg + 7
-      {
-        float* du_s = zq + kD;  // [128] scratch after z (WG-A only)
-        if ((et & 7) == 0) {
-          const int mg = et >> 3;
-          *(float4*)(du_s + 8 * mg) = make_float4(du[0], du[1], du[2], du[3]);
-          *(float4*)(du_s + 8 * mg + 4) = make_float4(du[4], du[5], du[6], du[7]);
-        }
-        named_bar(1, 128);
-        u += du_s[r];
-        named_bar(1, 128);
+        warp_store_rows(scr_lo, scr_hi, vt, [&](int seg) { return dvb + seg * prm.N; });
       }
       cj += dc;
       if (et == 0) traceb(1, n, 9);
@@ -702,6 +739,7 @@ __global__ void __launch_bounds__(320, 1)
     }
   } else {
     // ------------------------------------------------------------ WG-B (warps 6..9)
+    // bR/bS operand copies, W_hat/s over feature rows 64..127, z, dQ out, dK^T out, u.
     const uint32_t qd = warp & 3;
     const int l = (int)lane_id();
     const int r = (int)(qd * 32) + l;            // m
@@ -710,10 +748,19 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lb = (qd * 32u) << 16;
     const int eb = (int)threadIdx.x - 192;
     const float b = prm.b;
+    const float* recR = prm.stR + (grp * prm.P + p) * state_floats(kD);
+    float u = recR[kD * kD + r];  // u_next (m = r)
+    uint4 o4[4];
+    float4 g8[2];
+    if (nc > 0) what_prefetch_half<kBF16>(prm, grp, s0 + (int64_t)(nc - 1) * kCB, eb, 64, o4, g8);
     for (int n = 0; n < nc; ++n) {
       const int s = n & 1;
       const int64_t row0 = s0 + (int64_t)(nc - 1 - n) * kCB;
-      const uint8_t* k_t = smem + s * kStage + kT64;
+      uint8_t* st = smem + s * kStage;
+      const uint8_t* k_t = st + kT64;
+      uint8_t* w_t = st + 3 * kT64;
+      float* sA = s_s + s * 2 * kCB;
+      float* sB = sA + kCB;
       // ---- E_R: b R_next -> sR
       if (eb == 0) traceb(2, n, 0);
       if (n >= 1) mbar_wait(r_full, (n - 1) & 1);
@@ -760,10 +807,19 @@ __global__ void __launch_bounds__(320, 1)
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(sS_ready);
+      // ---- E0 (rows 64..127): W_hat, partial s
+      mbar_wait(&full[s], (n >> 1) & 1);
+      what_pass_half<kBF16>(w_t, o4, g8, sB, eb, 64);
+      if (n + 1 < nc) what_prefetch_half<kBF16>(prm, grp, row0 - kCB, eb, 64, o4, g8);
+      fence_proxy_async();
+      named_bar(3, 256);
+      if (eb == 0) traceb(2, n, 4);
+      if (n >= 1) u += du_s[((n - 1) & 1) * kD + r];  // suffix sum through the previous chunk
       // ---- z_prev: z -= sum_t k_t over this chunk (thread (mg, tg): columns 8 mg.., rows tg + 8 k)
       {
         const int mg = eb >> 3, tg = eb & 7;
         float zs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
         for (int k8 = 0; k8 < kCB / 8; ++k8) {
           const uint4 v4 = *(const uint4*)(k_t + sw128_off(tg + 8 * k8, 8 * mg, kCB));
           const uint32_t xx[4] = {v4.x, v4.y, v4.z, v4.w};
@@ -787,16 +843,17 @@ __global__ void __launch_bounds__(320, 1)
         }
         named_bar(2, 128);
       }
-      // ---- dQ out (half lanes): dQ = acc - b s_i z_prev
-      mbar_wait(&a2b[s], (n >> 1) & 1);  // s of this chunk written by WG-A (per stage: no lapping)
-      if (eb == 0) traceb(2, n, 4);
+      // ---- dQ (half lanes): acc - b s_i z_prev ; dK^T (lanes m): acc - b u_next
       mbar_wait(gr_full, n & 1);
       if (eb == 0) traceb(2, n, 5);
       tc_fence_after();
       {
-        const float si = s_s[s * kCB + ih];
+        // scratch: this warp's 4 KB of sS (dead until E_S of the next chunk)
+        uint8_t* scr_lo = sS + qd * 4096;
+        uint8_t* scr_hi = scr_lo + 2048;
+        const float si = sA[ih] + sB[ih];
         const int m0 = upper ? 64 : 0;
-        uint4 v[8];
+        uint4 vt[8];
 #pragma unroll
         for (int c0 = 0; c0 < 64; c0 += 32) {
           uint32_t x[32];
@@ -812,16 +869,30 @@ __global__ void __launch_bounds__(320, 1)
             for (int q = 0; q < 4; ++q)
               q4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) - si * b * z8[2 * q],
                                    __uint_as_float(x[8 * w4 + 2 * q + 1]) - si * b * z8[2 * q + 1]);
-            v[c0 / 8 + w4] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
+            vt[c0 / 8 + w4] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
+          }
+        }
+        uint16_t* dqb = (uint16_t*)prm.dq + (grp * prm.N + row0 + qd * 16) * kD;
+        warp_store_rows(scr_lo, scr_hi, vt, [&](int seg) { return dqb + (seg & 15) * kD + (seg >> 4) * 64; });
+        const float bu = b * u;
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          uint32_t x[32];
+          tmem_ld32(tmem + lb + kDK + c0, x);
+          tmem_ld_wait();
+#pragma unroll
+          for (int w4 = 0; w4 < 4; ++w4) {
+            uint32_t k4[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              k4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) - bu, __uint_as_float(x[8 * w4 + 2 * q + 1]) - bu);
+            vt[c0 / 8 + w4] = make_uint4(k4[0], k4[1], k4[2], k4[3]);
           }
         }
         tc_fence_before();
         mbar_arrive(gr_empty);
-        // scratch: this warp's 4 KB of sS (dead until E_S of the next chunk)
-        uint8_t* scr_lo = sS + qd * 4096;
-        uint8_t* scr_hi = scr_lo + 2048;
-        uint16_t* dqb = (uint16_t*)prm.dq + (grp * prm.N + row0 + qd * 16) * kD;
-        warp_store_rows(scr_lo, scr_hi, v, [&](int seg) { return dqb + (seg & 15) * kD + (seg >> 4) * 64; });
+        uint16_t* dkb = (uint16_t*)prm.dk + (grp * kD + qd * 32) * prm.N + row0;
+        warp_store_rows(scr_lo, scr_hi, vt, [&](int seg) { return dkb + seg * prm.N; });
       }
       if (eb == 0) traceb(2, n, 6);
       mbar_arrive(&empty[s]);
@@ -833,7 +904,7 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 constexpr size_t kAggSmemB = 2 * kStage + 512 + 1024;
-constexpr size_t kMainSmemB = 2 * kStage + 2 * 8192 + 2 * 32768 + 160 + (2 * kCB + 2 * kD) * 4 + 1024;
+constexpr size_t kMainSmemB = 2 * kStage + 2 * 8192 + 2 * 32768 + 160 + (4 * kCB + 3 * kD) * 4 + 1024;
 
 int tcb_segments(int64_t G, int64_t N) { return tc_segments(G, N); }
 
