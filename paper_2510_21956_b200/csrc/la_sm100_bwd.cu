@@ -761,6 +761,13 @@ __global__ void __launch_bounds__(320, 1)
       uint8_t* w_t = st + 3 * kT64;
       float* sA = s_s + s * 2 * kCB;
       float* sB = sA + kCB;
+      // ---- E0 (rows 64..127): W_hat, partial s
+      mbar_wait(&full[s], (n >> 1) & 1);
+      what_pass_half<kBF16>(w_t, o4, g8, sB, eb, 64);
+      if (n + 1 < nc) what_prefetch_half<kBF16>(prm, grp, row0 - kCB, eb, 64, o4, g8);
+      fence_proxy_async();
+      named_bar(3, 256);
+      if (eb == 0) traceb(2, n, 4);
       // ---- E_R: b R_next -> sR
       if (eb == 0) traceb(2, n, 0);
       if (n >= 1) mbar_wait(r_full, (n - 1) & 1);
@@ -807,13 +814,6 @@ __global__ void __launch_bounds__(320, 1)
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(sS_ready);
-      // ---- E0 (rows 64..127): W_hat, partial s
-      mbar_wait(&full[s], (n >> 1) & 1);
-      what_pass_half<kBF16>(w_t, o4, g8, sB, eb, 64);
-      if (n + 1 < nc) what_prefetch_half<kBF16>(prm, grp, row0 - kCB, eb, 64, o4, g8);
-      fence_proxy_async();
-      named_bar(3, 256);
-      if (eb == 0) traceb(2, n, 4);
       if (n >= 1) u += du_s[((n - 1) & 1) * kD + r];  // suffix sum through the previous chunk
       // ---- z_prev: z -= sum_t k_t over this chunk (thread (mg, tg): columns 8 mg.., rows tg + 8 k)
       {
