@@ -433,15 +433,16 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* gr_empty = bars + 12;
   uint64_t* r_full = bars + 13;
   uint32_t* tslot = (uint32_t*)(bars + 16);
-  float* s_s = (float*)(bars + 20);   // [2 stages][2 halves][64]
-  float* du_s = s_s + 4 * kCB;        // [2][128]  WG-A -> WG-B suffix increments of u
-  float* zq = du_s + 2 * kD;          // [128]
+  float* s_s = (float*)(bars + 20);   // [4 chunks][2 halves][64]  partial s (WG-A rows 0..63, WG-B 64..127)
+  float* du_s = s_s + 8 * kCB;        // [4][128]  WG-A -> WG-B suffix increments of u
+  float* zbuf = du_s + 4 * kD;        // [2][128]  z_prev per chunk parity
 
   const int p = blockIdx.x;
   const int64_t grp = blockIdx.y;
   const int64_t s0 = (int64_t)p * prm.seg_len;
   const int64_t s1 = lmin(prm.N, s0 + prm.seg_len);
   const int nc = (int)((s1 - s0) / kCB);
+  auto row_of = [&](int m) -> int64_t { return s0 + (int64_t)(nc - 1 - m) * kCB; };  // reverse sweep
   const uint32_t warp = warp_id();
   if (warp == 0 && elect_one()) {
     tma_prefetch(&tmQ);
@@ -452,7 +453,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1 + 256);
     }
-    mbar_init(w_ready, 128);
+    mbar_init(w_ready, 256);
     mbar_init(s_full, 1);
     mbar_init(dpt_full, 1);
     mbar_init(dpt_empty, 128);
@@ -492,7 +493,7 @@ __global__ void __launch_bounds__(320, 1)
       tmem_st32(tmem + lb + kS + j0, xs);
     }
     tmem_st_wait();
-    zq[r] = recS[kD * kD + r];  // z at the segment end
+    zbuf[kD + r] = recS[kD * kD + r];  // z at the segment end (read as chunk "-1")
   }
   tc_fence_before();
   __syncthreads();
@@ -593,10 +594,12 @@ __global__ void __launch_bounds__(320, 1)
     }
   } else if (warp < 6) {
     // ------------------------------------------------------------ WG-A (warps 2..5)
-    // W_hat/s over feature rows 0..63, dS/P, du (handed to WG-B), dV^T out, c.
+    // Iteration n: dV^T out of chunk n-1, bR -> sR (E_R), dS/P (E1), du, dc of
+    // chunk n, then the W_hat/s half (rows 0..63) of chunk n+1, so that the next
+    // chunk's dPt MMA is never waiting on the W_hat pass.
     const uint32_t qd = warp & 3;
     const int l = (int)lane_id();
-    const int r = (int)(qd * 32) + l;            // j of dV^T
+    const int r = (int)(qd * 32) + l;            // j of dV^T, m of R
     const int ih = (int)(qd * 16) + (l & 15);    // half-lane row i of M=64 accumulators
     const bool upper = l >= 16;                  // lanes 16..31 of a quadrant: upper half
     const uint32_t lb = (qd * 32u) << 16;
@@ -604,26 +607,80 @@ __global__ void __launch_bounds__(320, 1)
     const float a = prm.a, b = prm.b;
     const float* recR = prm.stR + (grp * prm.P + p) * state_floats(kD);
     float cj = recR[kD * kD + kD + r];  // c_next (j = r)
+    float dc_prev = 0.f;
     uint4 o4[4];
     float4 g8[2];
-    if (nc > 0) what_prefetch_half<kBF16>(prm, grp, s0 + (int64_t)(nc - 1) * kCB, et, 0, o4, g8);
-    for (int n = 0; n < nc; ++n) {
+    auto e0 = [&](int m) {  // W_hat / partial s of chunk m (rows 0..63)
+      const int sm = m & 1;
+      mbar_wait(&full[sm], (m >> 1) & 1);
+      what_pass_half<kBF16>(smem + sm * kStage + 3 * kT64, o4, g8, s_s + (m & 3) * 2 * kCB, et, 0);
+      if (m + 1 < nc) what_prefetch_half<kBF16>(prm, grp, row_of(m + 1), et, 0, o4, g8);
+      fence_proxy_async();
+      mbar_arrive(w_ready);
+    };
+    auto dv_out = [&](int m) {  // dV^T of chunk m (lanes j): acc + a c_next
+      mbar_wait(gr_full, m & 1);
+      tc_fence_after();
+      uint8_t* scr_lo = sP + qd * 2048;   // this warp's own P / dS rows are dead now
+      uint8_t* scr_hi = sdS + qd * 2048;
+      const float ac = a * cj;
+      uint4 vt[8];
+#pragma unroll
+      for (int c0 = 0; c0 < 64; c0 += 32) {
+        uint32_t x[32];
+        tmem_ld32(tmem + lb + kDV + c0, x);
+        tmem_ld_wait();
+#pragma unroll
+        for (int w4 = 0; w4 < 4; ++w4) {
+          uint32_t k4[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            k4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) + ac, __uint_as_float(x[8 * w4 + 2 * q + 1]) + ac);
+          vt[c0 / 8 + w4] = make_uint4(k4[0], k4[1], k4[2], k4[3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(gr_empty);
+      uint16_t* dvb = (uint16_t*)prm.dv + (grp * kD + qd * 32) * prm.N + row_of(m);
+      warp_store_rows(scr_lo, scr_hi, vt, [&](int seg) { return dvb + seg * prm.N; });
+      cj += dc_prev;
+    };
+    if (nc > 0) what_prefetch_half<kBF16>(prm, grp, row_of(0), et, 0, o4, g8);
+    // One call site per phase (the kernel's code must stay small for the I-cache):
+    // iteration n = -1 only runs E0(0); n = nc only drains dV^T(nc-1).
+    for (int n = -1; n <= nc; ++n) {
+      if (n >= 0 && et == 0) traceb(1, n, 0);
+      if (n >= 1) dv_out(n - 1);
+      if (n == nc) break;
+      if (n >= 0) {
       const int s = n & 1;
-      const int64_t row0 = s0 + (int64_t)(nc - 1 - n) * kCB;
       uint8_t* st = smem + s * kStage;
       const uint8_t* q_t = st;
-      uint8_t* w_t = st + 3 * kT64;
-      float* sA = s_s + s * 2 * kCB;
-      float* sB = sA + kCB;
-      // ---- E0 (rows 0..63): W_hat, partial s
-      if (et == 0) traceb(1, n, 0);
-      mbar_wait(&full[s], (n >> 1) & 1);
+      const uint8_t* w_t = st + 3 * kT64;
+      const float* sA = s_s + (n & 3) * 2 * kCB;
+      const float* sB = sA + kCB;
       if (et == 0) traceb(1, n, 1);
-      what_pass_half<kBF16>(w_t, o4, g8, sA, et, 0);
-      if (n + 1 < nc) what_prefetch_half<kBF16>(prm, grp, row0 - kCB, et, 0, o4, g8);
+      // ---- E_R: b R_next -> sR (R complete after the previous chunk's R += MMA)
+      if (n >= 1) mbar_wait(r_full, (n - 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int j0 = 0; j0 < kD; j0 += 32) {
+        uint32_t x[32];
+        tmem_ld32(tmem + lb + kR + j0, x);
+        tmem_ld_wait();
+#pragma unroll
+        for (int w8 = 0; w8 < 4; ++w8) {
+          uint4 v;
+          v.x = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 0]), b * __uint_as_float(x[8 * w8 + 1]));
+          v.y = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 2]), b * __uint_as_float(x[8 * w8 + 3]));
+          v.z = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 4]), b * __uint_as_float(x[8 * w8 + 5]));
+          v.w = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 6]), b * __uint_as_float(x[8 * w8 + 7]));
+          *(uint4*)(sR + sw128_off(r, j0 + 8 * w8, 128)) = v;
+        }
+      }
       fence_proxy_async();
-      named_bar(3, 256);  // both halves of W_hat and s are complete
-      mbar_arrive(w_ready);
+      tc_fence_before();
+      mbar_arrive(sR_ready);
       if (et == 0) traceb(1, n, 2);
       // ---- E1: dPt -> dS (lower half lanes), T1 -> P (upper half lanes)
       mbar_wait(dpt_full, n & 1);
@@ -663,7 +720,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_arrive(dpt_empty);
       mbar_arrive(ps_ready);
       if (et == 0) traceb(1, n, 4);
-      // ---- du_m = sum_i q_im s_i of this chunk -> du_s[n & 1] for WG-B
+      // ---- du_m = sum_i q_im s_i of this chunk -> du_s[n & 3] for WG-B
       {
         const int mg = et >> 3, tg = et & 7;  // rows tg + 8k: conflict-free quarter-warps
         float du[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -687,59 +744,36 @@ __global__ void __launch_bounds__(320, 1)
           du[q] += __shfl_xor_sync(0xffffffffu, du[q], 4);
         }
         if (tg == 0) {
-          float* dst = du_s + (n & 1) * kD + 8 * mg;
+          float* dst = du_s + (n & 3) * kD + 8 * mg;
           *(float4*)dst = make_float4(du[0], du[1], du[2], du[3]);
           *(float4*)(dst + 4) = make_float4(du[4], du[5], du[6], du[7]);
         }
       }
-      // ---- dc_j = sum_i w_hat_ji
-      float dc = 0.f;
-#pragma unroll
-      for (int i8 = 0; i8 < kCB; i8 += 8) {
-        const uint4 v4 = *(const uint4*)(w_t + sw128_off(r, i8, 128));
-        const uint32_t w4[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float2 f2 = unpack2<kBF16>(w4[q]);
-          dc += f2.x + f2.y;
-        }
-      }
-      // ---- dV^T out (lanes j): + a c_next
-      if (et == 0) traceb(1, n, 7);
-      mbar_wait(gr_full, n & 1);
-      if (et == 0) traceb(1, n, 8);
-      tc_fence_after();
+      // ---- dc_j = sum_i w_hat_ji (added to c after this chunk's dV^T is out)
       {
-        uint8_t* scr_lo = sP + qd * 2048;   // this warp's own P / dS rows are dead now
-        uint8_t* scr_hi = sdS + qd * 2048;
-        const float ac = a * cj;
-        uint4 vt[8];
+        float dc = 0.f;
 #pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 32) {
-          uint32_t x[32];
-          tmem_ld32(tmem + lb + kDV + c0, x);
-          tmem_ld_wait();
+        for (int i8 = 0; i8 < kCB; i8 += 8) {
+          const uint4 v4 = *(const uint4*)(w_t + sw128_off(r, i8, 128));
+          const uint32_t w4[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-          for (int w4 = 0; w4 < 4; ++w4) {
-            uint32_t k4[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              k4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) + ac, __uint_as_float(x[8 * w4 + 2 * q + 1]) + ac);
-            vt[c0 / 8 + w4] = make_uint4(k4[0], k4[1], k4[2], k4[3]);
+          for (int q = 0; q < 4; ++q) {
+            const float2 f2 = unpack2<kBF16>(w4[q]);
+            dc += f2.x + f2.y;
           }
         }
-        tc_fence_before();
-        mbar_arrive(gr_empty);
-        uint16_t* dvb = (uint16_t*)prm.dv + (grp * kD + qd * 32) * prm.N + row0;
-        warp_store_rows(scr_lo, scr_hi, vt, [&](int seg) { return dvb + seg * prm.N; });
+        dc_prev = dc;
       }
-      cj += dc;
-      if (et == 0) traceb(1, n, 9);
       mbar_arrive(&empty[s]);
+      if (et == 0) traceb(1, n, 5);
+      }
+      if (n + 1 < nc) e0(n + 1);
+      if (n >= 0 && et == 0) traceb(1, n, 6);
     }
   } else {
     // ------------------------------------------------------------ WG-B (warps 6..9)
-    // bR/bS operand copies, W_hat/s over feature rows 64..127, z, dQ out, dK^T out, u.
+    // Iteration n: dQ and dK^T out of chunk n-1, bS -> sS (E_S) and z of chunk n,
+    // then the W_hat/s half (rows 64..127) of chunk n+1.
     const uint32_t qd = warp & 3;
     const int l = (int)lane_id();
     const int r = (int)(qd * 32) + l;            // m
@@ -752,49 +786,79 @@ __global__ void __launch_bounds__(320, 1)
     float u = recR[kD * kD + r];  // u_next (m = r)
     uint4 o4[4];
     float4 g8[2];
-    if (nc > 0) what_prefetch_half<kBF16>(prm, grp, s0 + (int64_t)(nc - 1) * kCB, eb, 64, o4, g8);
-    for (int n = 0; n < nc; ++n) {
-      const int s = n & 1;
-      const int64_t row0 = s0 + (int64_t)(nc - 1 - n) * kCB;
-      uint8_t* st = smem + s * kStage;
-      const uint8_t* k_t = st + kT64;
-      uint8_t* w_t = st + 3 * kT64;
-      float* sA = s_s + s * 2 * kCB;
-      float* sB = sA + kCB;
-      // ---- E0 (rows 64..127): W_hat, partial s
-      mbar_wait(&full[s], (n >> 1) & 1);
-      what_pass_half<kBF16>(w_t, o4, g8, sB, eb, 64);
-      if (n + 1 < nc) what_prefetch_half<kBF16>(prm, grp, row0 - kCB, eb, 64, o4, g8);
+    auto e0 = [&](int m) {  // W_hat / partial s of chunk m (rows 64..127)
+      const int sm = m & 1;
+      mbar_wait(&full[sm], (m >> 1) & 1);
+      what_pass_half<kBF16>(smem + sm * kStage + 3 * kT64, o4, g8, s_s + (m & 3) * 2 * kCB + kCB, eb, 64);
+      if (m + 1 < nc) what_prefetch_half<kBF16>(prm, grp, row_of(m + 1), eb, 64, o4, g8);
       fence_proxy_async();
-      named_bar(3, 256);
-      if (eb == 0) traceb(2, n, 4);
-      // ---- E_R: b R_next -> sR
-      if (eb == 0) traceb(2, n, 0);
-      if (n >= 1) mbar_wait(r_full, (n - 1) & 1);
-      if (eb == 0) traceb(2, n, 1);
+      mbar_arrive(w_ready);
+    };
+    auto qk_out = [&](int m) {  // dQ (half lanes): acc - b s_i z_prev ; dK^T (lanes m): acc - b u_next
+      mbar_wait(gr_full, m & 1);
+      if (m >= 1) u += du_s[((m - 1) & 3) * kD + r];  // suffix sum through chunk m-1
       tc_fence_after();
-#pragma unroll 1
-      for (int j0 = 0; j0 < kD; j0 += 32) {
+      // scratch: this warp's 4 KB of sS (dead until E_S of the next chunk)
+      uint8_t* scr_lo = sS + qd * 4096;
+      uint8_t* scr_hi = scr_lo + 2048;
+      const float* sA = s_s + (m & 3) * 2 * kCB;
+      const float si = sA[ih] + sA[kCB + ih];
+      const float* zq = zbuf + (m & 1) * kD;
+      const int m0 = upper ? 64 : 0;
+      const int64_t row0 = row_of(m);
+      uint4 vt[8];
+#pragma unroll
+      for (int c0 = 0; c0 < 64; c0 += 32) {
         uint32_t x[32];
-        tmem_ld32(tmem + lb + kR + j0, x);
+        tmem_ld32(tmem + lb + kDQ + c0, x);
         tmem_ld_wait();
 #pragma unroll
-        for (int w8 = 0; w8 < 4; ++w8) {
-          uint4 v;
-          v.x = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 0]), b * __uint_as_float(x[8 * w8 + 1]));
-          v.y = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 2]), b * __uint_as_float(x[8 * w8 + 3]));
-          v.z = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 4]), b * __uint_as_float(x[8 * w8 + 5]));
-          v.w = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 6]), b * __uint_as_float(x[8 * w8 + 7]));
-          *(uint4*)(sR + sw128_off(r, j0 + 8 * w8, 128)) = v;
+        for (int w4 = 0; w4 < 4; ++w4) {
+          uint32_t q4[4];
+          const float4 za = *(const float4*)(zq + m0 + c0 + 8 * w4);
+          const float4 zb = *(const float4*)(zq + m0 + c0 + 8 * w4 + 4);
+          const float z8[8] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            q4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) - si * b * z8[2 * q],
+                                 __uint_as_float(x[8 * w4 + 2 * q + 1]) - si * b * z8[2 * q + 1]);
+          vt[c0 / 8 + w4] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
         }
       }
-      fence_proxy_async();
+      uint16_t* dqb = (uint16_t*)prm.dq + (grp * prm.N + row0 + qd * 16) * kD;
+      warp_store_rows(scr_lo, scr_hi, vt, [&](int seg) { return dqb + (seg & 15) * kD + (seg >> 4) * 64; });
+      const float bu = b * u;
+#pragma unroll
+      for (int c0 = 0; c0 < 64; c0 += 32) {
+        uint32_t x[32];
+        tmem_ld32(tmem + lb + kDK + c0, x);
+        tmem_ld_wait();
+#pragma unroll
+        for (int w4 = 0; w4 < 4; ++w4) {
+          uint32_t k4[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            k4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) - bu, __uint_as_float(x[8 * w4 + 2 * q + 1]) - bu);
+          vt[c0 / 8 + w4] = make_uint4(k4[0], k4[1], k4[2], k4[3]);
+        }
+      }
       tc_fence_before();
-      mbar_arrive(sR_ready);
+      mbar_arrive(gr_empty);
+      uint16_t* dkb = (uint16_t*)prm.dk + (grp * kD + qd * 32) * prm.N + row0;
+      warp_store_rows(scr_lo, scr_hi, vt, [&](int seg) { return dkb + seg * prm.N; });
+    };
+    if (nc > 0) what_prefetch_half<kBF16>(prm, grp, row_of(0), eb, 64, o4, g8);
+    for (int n = -1; n <= nc; ++n) {
+      if (n >= 0 && eb == 0) traceb(2, n, 0);
+      if (n >= 1) qk_out(n - 1);
+      if (n == nc) break;
+      if (n >= 0) {
+      const int s = n & 1;
+      const uint8_t* k_t = smem + s * kStage + kT64;
+      if (eb == 0) traceb(2, n, 1);
       // ---- E_S: b S_prev -> sS
-      if (eb == 0) traceb(2, n, 2);
       mbar_wait(s_full, n & 1);
-      if (eb == 0) traceb(2, n, 3);
+      if (eb == 0) traceb(2, n, 2);
       tc_fence_after();
 #pragma unroll 1
       for (int j0 = 0; j0 < kD; j0 += 32) {
@@ -814,10 +878,10 @@ __global__ void __launch_bounds__(320, 1)
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(sS_ready);
-      if (n >= 1) u += du_s[((n - 1) & 1) * kD + r];  // suffix sum through the previous chunk
-      // ---- z_prev: z -= sum_t k_t over this chunk (thread (mg, tg): columns 8 mg.., rows tg + 8 k)
+      if (eb == 0) traceb(2, n, 3);
+      // ---- z_prev(n) = z_prev(n-1) - sum_t k_t over this chunk -> zbuf[n & 1]
       {
-        const int mg = eb >> 3, tg = eb & 7;
+        const int mg = eb >> 3, tg = eb & 7;  // columns 8 mg.., rows tg + 8 k
         float zs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int k8 = 0; k8 < kCB / 8; ++k8) {
@@ -837,65 +901,19 @@ __global__ void __launch_bounds__(320, 1)
           zs[q] += __shfl_xor_sync(0xffffffffu, zs[q], 4);
         }
         if (tg == 0) {
-          const float4 za = *(const float4*)(zq + 8 * mg), zb = *(const float4*)(zq + 8 * mg + 4);
-          *(float4*)(zq + 8 * mg) = make_float4(za.x - zs[0], za.y - zs[1], za.z - zs[2], za.w - zs[3]);
-          *(float4*)(zq + 8 * mg + 4) = make_float4(zb.x - zs[4], zb.y - zs[5], zb.z - zs[6], zb.w - zs[7]);
+          const float* zin = zbuf + ((n - 1) & 1) * kD + 8 * mg;
+          float* zout = zbuf + (n & 1) * kD + 8 * mg;
+          const float4 za = *(const float4*)zin, zb = *(const float4*)(zin + 4);
+          *(float4*)zout = make_float4(za.x - zs[0], za.y - zs[1], za.z - zs[2], za.w - zs[3]);
+          *(float4*)(zout + 4) = make_float4(zb.x - zs[4], zb.y - zs[5], zb.z - zs[6], zb.w - zs[7]);
         }
         named_bar(2, 128);
       }
-      // ---- dQ (half lanes): acc - b s_i z_prev ; dK^T (lanes m): acc - b u_next
-      mbar_wait(gr_full, n & 1);
-      if (eb == 0) traceb(2, n, 5);
-      tc_fence_after();
-      {
-        // scratch: this warp's 4 KB of sS (dead until E_S of the next chunk)
-        uint8_t* scr_lo = sS + qd * 4096;
-        uint8_t* scr_hi = scr_lo + 2048;
-        const float si = sA[ih] + sB[ih];
-        const int m0 = upper ? 64 : 0;
-        uint4 vt[8];
-#pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 32) {
-          uint32_t x[32];
-          tmem_ld32(tmem + lb + kDQ + c0, x);
-          tmem_ld_wait();
-#pragma unroll
-          for (int w4 = 0; w4 < 4; ++w4) {
-            uint32_t q4[4];
-            const float4 za = *(const float4*)(zq + m0 + c0 + 8 * w4);
-            const float4 zb = *(const float4*)(zq + m0 + c0 + 8 * w4 + 4);
-            const float z8[8] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              q4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) - si * b * z8[2 * q],
-                                   __uint_as_float(x[8 * w4 + 2 * q + 1]) - si * b * z8[2 * q + 1]);
-            vt[c0 / 8 + w4] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
-          }
-        }
-        uint16_t* dqb = (uint16_t*)prm.dq + (grp * prm.N + row0 + qd * 16) * kD;
-        warp_store_rows(scr_lo, scr_hi, vt, [&](int seg) { return dqb + (seg & 15) * kD + (seg >> 4) * 64; });
-        const float bu = b * u;
-#pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 32) {
-          uint32_t x[32];
-          tmem_ld32(tmem + lb + kDK + c0, x);
-          tmem_ld_wait();
-#pragma unroll
-          for (int w4 = 0; w4 < 4; ++w4) {
-            uint32_t k4[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              k4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) - bu, __uint_as_float(x[8 * w4 + 2 * q + 1]) - bu);
-            vt[c0 / 8 + w4] = make_uint4(k4[0], k4[1], k4[2], k4[3]);
-          }
-        }
-        tc_fence_before();
-        mbar_arrive(gr_empty);
-        uint16_t* dkb = (uint16_t*)prm.dk + (grp * kD + qd * 32) * prm.N + row0;
-        warp_store_rows(scr_lo, scr_hi, vt, [&](int seg) { return dkb + seg * prm.N; });
-      }
-      if (eb == 0) traceb(2, n, 6);
       mbar_arrive(&empty[s]);
+      if (eb == 0) traceb(2, n, 4);
+      }
+      if (n + 1 < nc) e0(n + 1);
+      if (n >= 0 && eb == 0) traceb(2, n, 5);
     }
   }
   tc_fence_before();
@@ -904,7 +922,7 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 constexpr size_t kAggSmemB = 2 * kStage + 512 + 1024;
-constexpr size_t kMainSmemB = 2 * kStage + 2 * 8192 + 2 * 32768 + 160 + (4 * kCB + 3 * kD) * 4 + 1024;
+constexpr size_t kMainSmemB = 2 * kStage + 2 * 8192 + 2 * 32768 + 160 + (8 * kCB + 6 * kD) * 4 + 1024;
 
 int tcb_segments(int64_t G, int64_t N) { return tc_segments(G, N); }
 

@@ -22,8 +22,8 @@ t = np.array(buf, dtype=np.int64).reshape(4, 64, 10)
 t0 = t[0, 10, 0]
 print("MMA: start,full,dpt_empty,w_ready,sS_ready,ps_ready,gr_empty,sR_ready")
 for c in range(10, 14): print(c, (t[0, c, :8] - t0).tolist())
-print("WGA: E0start,full,w_ready-arr,dpt_full,ps_ready-arr,-,-,Eout-start,gr_full,end")
-for c in range(10, 14): print(c, (t[1, c, [0,1,2,3,4,7,8,9]] - t0).tolist())
-print("WGB: ER-start,r_full,ES-start,s_full,E0sync,gr_full,end")
-for c in range(10, 14): print(c, (t[2, c, :7] - t0).tolist())
+print("WGA: start,after dv_out(n-1),sR_ready,dpt_full,ps_ready,after du/dc,after E0(n+1)")
+for c in range(10, 14): print(c, (t[1, c, :7] - t0).tolist())
+print("WGB: start,after qk_out(n-1),after s_full wait,sS_ready,after z,after E0(n+1)")
+for c in range(10, 14): print(c, (t[2, c, :6] - t0).tolist())
 print("period", np.diff(t[0, 5:60, 0]).mean())
