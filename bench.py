@@ -48,43 +48,78 @@ def peaks():
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Polls NVML (SM clock, max SM clock, clock-event reasons) from a thread every
+    ~2 ms while the timed region runs; one sample is always taken on entry and exit,
+    so even a short region is covered."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, index):
-        self.index, self.rows, self.proc = index, [], None
+    def __init__(self, index, period_s=0.002):
+        self.index, self.period, self.rows, self.h, self.nv = index, period_s, [], None, None
+        self.stop = threading.Event()
+
+    def _handle(self):
+        import pynvml as nv
+        import torch
+        nv.nvmlInit()
+        self.nv = nv
+        try:  # match the CUDA device to its NVML handle by UUID (CUDA_VISIBLE_DEVICES safe)
+            uuid = str(torch.cuda.get_device_properties(self.index).uuid)
+            for i in range(nv.nvmlDeviceGetCount()):
+                h = nv.nvmlDeviceGetHandleByIndex(i)
+                u = nv.nvmlDeviceGetUUID(h)
+                u = u.decode() if isinstance(u, bytes) else u
+                if u.replace("GPU-", "") == uuid.replace("GPU-", ""):
+                    return h
+        except Exception:
+            pass
+        return nv.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _sample(self):
+        nv = self.nv
+        sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        try:
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        self.rows.append((sm, mx, rs))
+
+    def _loop(self):
+        while not self.stop.wait(self.period):
+            try:
+                self._sample()
+            except Exception:
+                return
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self.h = self._handle()
+            self._sample()
+            self.t = threading.Thread(target=self._loop, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.h = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            self.proc.wait()
+        if self.h is not None:
+            self.stop.set()
+            self.t.join()
+            try:
+                self._sample()
+            except Exception:
+                pass
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 4 + i and r[4 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        # the entry/exit samples bracket the region; the load samples are the inner ones
+        inner = self.rows[1:-1] or self.rows
+        reasons = sorted({n for _, _, r in self.rows for bit, n in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(s for s, _, _ in inner),
+                "sm_max_mhz": max(m for _, m, _ in self.rows), "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml"}
 
 
 # ----------------------------------------------------------------------------- CPU arms
@@ -306,13 +341,10 @@ def run_our_arm(args):
         hout, hdq, hdk, hdv = (torch.empty(x.shape, **pin) for x in (out, dq, dk, dv))
         hg = torch.empty((G, N), dtype=torch.float32, pin_memory=True)
 
-        def e2e_step():
-            st = L.la_host_forward(C.byref(p), hq.data_ptr(), SMj, hk.data_ptr(), SMj, hv.data_ptr(), FMj,
-                                   hout.data_ptr(), hg.data_ptr(), C.byref(err))
-            assert st == 0, err.message
-            st = L.la_host_backward(C.byref(p), hq.data_ptr(), SMj, hk.data_ptr(), SMj, hv.data_ptr(), FMj,
-                                    hout.data_ptr(), hw.data_ptr(), FMj, hg.data_ptr(), hdq.data_ptr(),
-                                    hdk.data_ptr(), hdv.data_ptr(), C.byref(err))
+        def e2e_step():  # one training step through the host-buffer C-ABI (la_host_step)
+            st = L.la_host_step(C.byref(p), hq.data_ptr(), SMj, hk.data_ptr(), SMj, hv.data_ptr(), FMj,
+                                hw.data_ptr(), FMj, hout.data_ptr(), hg.data_ptr(), hdq.data_ptr(),
+                                hdk.data_ptr(), hdv.data_ptr(), C.byref(err))
             assert st == 0, err.message
 
         e2e_step()
@@ -327,9 +359,10 @@ def run_our_arm(args):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             et = float(tt.item())
         T = G * N * D * e
-        e2e = {"value": tokens_step / et, "unit": UNIT, "h2d_bytes_per_step": 8 * T + 4 * G * N,
+        e2e = {"value": tokens_step / et, "unit": UNIT, "h2d_bytes_per_step": 4 * T,
                "d2h_bytes_per_step": 4 * T + 4 * G * N, "ms_per_step": et * 1e3,
-               "api": "la_host_forward + la_host_backward (pinned host buffers)"}
+               "api": "la_host_step: forward + backward over pinned host buffers (q, k, v, dO in; "
+                      "o, g, dq, dk, dv out), group blocks pipelined over H2D / compute / D2H streams"}
         L.la_host_release()
 
     cpu = None

@@ -14,6 +14,7 @@
  * la_backward(causal=1)            la::backward_causal  src/backward.cpp:93-96
  * la_backward(causal=0)            la::backward_full    src/backward.cpp:98-101
  * la_host_forward / _backward      the same, over host buffers (copies in/out)
+ * la_host_step                     forward then backward over host buffers, pipelined
  * la_forward_shard_state           (new) per-shard (S,z,sigma,count) totals for
  * la_backward_shard_state          (new) sequence sharding, exchanged by the
  *                                  caller over NCCL, fed back as carry-in/out
@@ -185,6 +186,15 @@ la_status la_host_backward(const la_problem* p, const void* q, la_layout lq, con
                            la_layout lk, const void* v, la_layout lv, const void* o,
                            const void* omega, la_layout lw, const float* g, void* dq, void* dk,
                            void* dv, la_error_info* err);
+/* One training step over host buffers: forward_causal/forward_full followed by
+ * backward_causal/backward_full on the same inputs (forward.cpp:133-142,
+ * backward.cpp:93-101, as bench.cpp:137-139 + :176-179 time them). Inputs q, k, v,
+ * omega are copied in once and out, g, dq, dk, dv copied back; the groups are
+ * processed in blocks so host->device copies, compute and device->host copies
+ * overlap (pinned host memory gives the full PCIe rate in both directions). */
+la_status la_host_step(const la_problem* p, const void* q, la_layout lq, const void* k,
+                       la_layout lk, const void* v, la_layout lv, const void* omega, la_layout lw,
+                       void* out, float* g, void* dq, void* dk, void* dv, la_error_info* err);
 void la_host_release(void);
 
 #ifdef __cplusplus

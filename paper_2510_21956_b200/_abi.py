@@ -25,7 +25,7 @@ EXPORTS = [
     "la_shard_state_floats", "la_validate_plan", "la_default_plan", "la_launch_count", "la_forward",
     "la_backward", "la_forward_sharded", "la_backward_sharded", "la_forward_shard_state",
     "la_backward_shard_state", "la_combine_shard_states", "la_query_status", "la_host_forward",
-    "la_host_backward", "la_host_release", "la_profile_enable", "la_profile_read",
+    "la_host_backward", "la_host_step", "la_host_release", "la_profile_enable", "la_profile_read",
     "la_saved_state_bytes", "la_forward_save", "la_backward_saved",
 ]
 
@@ -94,6 +94,8 @@ def lib():
         L.la_backward_saved.argtypes = [P, vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, C.c_int, vp, vp, sz,
                                         vp, vp, vp, vp, sz, vp, E]
         L.la_host_forward.argtypes = [P, vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, E]
+        L.la_host_step.argtypes = [P, vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, vp, vp,
+                                   vp, E]
         L.la_host_backward.argtypes = [P, vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, C.c_int, vp,
                                        vp, vp, vp, E]
         _lib = L

@@ -46,3 +46,19 @@ __host__ __device__ __forceinline__ int64_t lmax(int64_t a, int64_t b) { return 
 constexpr float kEpsF32 = 1e-4f;  // constants.hpp:15-18 (T = float)
 
 }  // namespace lab
+
+namespace lab {
+// In-kernel carry combine (replaces a separate scan launch): the CTA's threads
+// [tid, nthr) write dst[e] = (base ? base[e] : 0) + sum_{q in [q0, q1)} recs[q * SZ + e].
+__device__ __forceinline__ void combine_records(float* dst, const float* base, const float* recs, int q0,
+                                                int q1, int64_t SZ, int tid, int nthr) {
+  for (int64_t e = 4 * tid; e < SZ; e += 4 * nthr) {
+    float4 acc = base ? *(const float4*)(base + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = q0; q < q1; ++q) {
+      const float4 v = *(const float4*)(recs + q * SZ + e);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    *(float4*)(dst + e) = acc;
+  }
+}
+}  // namespace lab

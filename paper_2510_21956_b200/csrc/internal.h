@@ -41,6 +41,18 @@ inline int choose_segments(int64_t G, int64_t N, int num_sms = 148) {
   return bestP;
 }
 
+// Aggregate passes split each segment into A equal units (whole 128-row chunks)
+// so that the G x (segments aggregated) x A grid fills the SMs; records are kept
+// per unit and summed by the consumer's prologue.
+inline int agg_split(int64_t G, int64_t seg_rows, int segs_aggregated, int num_sms = 148) {
+  if (segs_aggregated <= 0) return 1;
+  int A = (int)(num_sms / (G * segs_aggregated));
+  if (A < 1) A = 1;
+  const int64_t chunks = seg_rows / 128;
+  while (A > 1 && chunks % A) --A;
+  return A;
+}
+
 struct Tensors {
   const void* q; int lq;
   const void* k; int lk;

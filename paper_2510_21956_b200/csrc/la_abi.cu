@@ -193,7 +193,7 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
                         const void* k, la_layout lk, const void* v, la_layout lv, const void* o,
                         const void* omega, la_layout lw, const float* g, void* dq, void* dk,
                         void* dv, void* ws, size_t ws_bytes, void* stream, la_error_info* err,
-                        const void* saved = nullptr, size_t saved_bytes = 0) {
+                        const void* saved = nullptr, size_t saved_bytes = 0, bool trust_saved = false) {
   // check_backward_inputs (backward.cpp:13-28)
   if (p && (!o || !q || !k || !v))
     return fail(err, LA_ERR_MISSING_FORWARD_STATE,
@@ -214,7 +214,11 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
   Tensors t{q, lq, k, lk, v, lv, o, LA_FEATURE_MAJOR, omega, lw, g};
   Workspace w = carve(ws, ws_bytes);
   const bool tc = use_tc(p, tc_backward_supported(L, t));
-  if (saved && tc) {
+  if (saved && tc && trust_saved) {
+    // written by this library's own forward of the same problem on the same stream
+    // (la_host_step): the header is known to match, no synchronous read
+    L.saved_in = (const float*)saved;
+  } else if (saved && tc) {
     // validate the saved-state header written by la_forward_save
     float hdr[kSavedHeader];
     if (saved_bytes < sizeof(hdr) ||
@@ -271,6 +275,68 @@ struct Arena {
   }
 };
 thread_local Arena t_arena;
+
+// Host-buffer training step (la_host_step): the groups are cut into blocks and
+// each block's H2D copy, fwd+bwd, and D2H copy run on their own streams through
+// a ring of device slots, so PCIe traffic in both directions overlaps compute.
+struct HostPipe {
+  static constexpr int R = 3;
+  cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
+  cudaEvent_t ev_in[R] = {}, ev_cmp[R] = {}, ev_out[R] = {};
+  void* slots = nullptr;
+  size_t slot_bytes = 0;
+  unsigned long long* hflags = nullptr;  // pinned: per block {forward flag, backward flag}
+  int nflags = 0;
+  ~HostPipe() { release(); }
+  void release() {
+    if (s_out) cudaStreamSynchronize(s_out);
+    if (slots) cudaFree(slots);
+    if (hflags) cudaFreeHost(hflags);
+    for (int i = 0; i < R; ++i) {
+      if (ev_in[i]) cudaEventDestroy(ev_in[i]);
+      if (ev_cmp[i]) cudaEventDestroy(ev_cmp[i]);
+      if (ev_out[i]) cudaEventDestroy(ev_out[i]);
+      ev_in[i] = ev_cmp[i] = ev_out[i] = nullptr;
+    }
+    for (cudaStream_t* st : {&s_in, &s_cmp, &s_out})
+      if (*st) {
+        cudaStreamDestroy(*st);
+        *st = nullptr;
+      }
+    slots = nullptr;
+    hflags = nullptr;
+    slot_bytes = 0;
+    nflags = 0;
+  }
+  cudaError_t reserve(size_t per_slot, int blocks) {
+    cudaError_t e = cudaSuccess;
+    if (!s_in) {
+      for (cudaStream_t* st : {&s_in, &s_cmp, &s_out})
+        if ((e = cudaStreamCreateWithFlags(st, cudaStreamNonBlocking)) != cudaSuccess) return e;
+      for (int i = 0; i < R; ++i)
+        if ((e = cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&ev_cmp[i], cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming)) != cudaSuccess)
+          return e;
+    }
+    if (per_slot > slot_bytes) {
+      if (slots) cudaFree(slots);
+      slots = nullptr;
+      slot_bytes = 0;
+      if ((e = cudaMalloc(&slots, per_slot * R)) != cudaSuccess) return e;
+      slot_bytes = per_slot;
+    }
+    if (2 * blocks > nflags) {
+      if (hflags) cudaFreeHost(hflags);
+      hflags = nullptr;
+      nflags = 0;
+      if ((e = cudaMallocHost((void**)&hflags, sizeof(unsigned long long) * 2 * blocks)) != cudaSuccess) return e;
+      nflags = 2 * blocks;
+    }
+    return e;
+  }
+};
+thread_local HostPipe t_pipe;
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -549,6 +615,89 @@ la_status la_host_backward(const la_problem* p, const void* q, la_layout lq, con
   return la_query_status(dws, st, err);
 }
 
-void la_host_release(void) { t_arena.release(); }
+void la_host_release(void) {
+  t_arena.release();
+  t_pipe.release();
+}
+
+la_status la_host_step(const la_problem* p, const void* q, la_layout lq, const void* k,
+                       la_layout lk, const void* v, la_layout lv, const void* omega, la_layout lw,
+                       void* out, float* g, void* dq, void* dk, void* dv, la_error_info* err) {
+  la_status s = check_problem(p, err);
+  if (s != LA_OK) return s;
+  if (!q || !k || !v || !omega || !out || !g || !dq || !dk || !dv)
+    return fail(err, LA_ERR_INVALID_SHAPE, "null host buffer");
+  if (!layout_ok(lq) || !layout_ok(lk) || !layout_ok(lv) || !layout_ok(lw))
+    return fail(err, LA_ERR_INVALID_ARGUMENT, "unknown layout");
+  const int64_t G = p->groups, N = p->seq_len, D = p->dim;
+  const int64_t Gb = (G + 7) / 8;  // up to 8 blocks of whole groups
+  const int nb = (int)((G + Gb - 1) / Gb);
+  la_problem pb = *p;
+  pb.groups = Gb;
+  pb.plan.groups = Gb;
+  const size_t eb = elem_bytes(p->dtype);
+  const size_t tb = align256((size_t)(Gb * N * D) * eb), gbb = align256(sizeof(float) * (size_t)(Gb * N));
+  const size_t sb = align256(la_saved_state_bytes(&pb));
+  const size_t wf = align256(la_forward_workspace_bytes(&pb)), wbk = align256(la_backward_workspace_bytes(&pb));
+  const size_t per_slot = 8 * tb + gbb + sb + wf + wbk;
+  cudaError_t e = t_pipe.reserve(per_slot, nb);
+  if (e != cudaSuccess) return cuda_fail(err, e);
+  HostPipe& hp = t_pipe;
+  for (int bi = 0; bi < nb; ++bi) {
+    const int slot = bi % HostPipe::R;
+    const int64_t g0 = bi * Gb, gn = (g0 + Gb <= G) ? Gb : G - g0;
+    pb.groups = gn;
+    pb.plan.groups = gn;
+    const size_t tbytes = (size_t)(gn * N * D) * eb, toff = (size_t)(g0 * N * D) * eb;
+    const size_t gbytes = sizeof(float) * (size_t)(gn * N), goff = (size_t)(g0 * N);
+    char* base = (char*)hp.slots + slot * hp.slot_bytes;
+    char* b[8];
+    for (int i = 0; i < 8; ++i) b[i] = base + i * tb;
+    float* dg = (float*)(base + 8 * tb);
+    char* dsaved = base + 8 * tb + gbb;
+    char* dwf = dsaved + sb;
+    char* dwb = dwf + wf;
+    // copy-in
+    if (bi >= HostPipe::R) cudaStreamWaitEvent(hp.s_in, hp.ev_out[slot], 0);
+    cudaMemcpyAsync(b[0], (const char*)q + toff, tbytes, cudaMemcpyHostToDevice, hp.s_in);
+    cudaMemcpyAsync(b[1], (const char*)k + toff, tbytes, cudaMemcpyHostToDevice, hp.s_in);
+    cudaMemcpyAsync(b[2], (const char*)v + toff, tbytes, cudaMemcpyHostToDevice, hp.s_in);
+    cudaMemcpyAsync(b[3], (const char*)omega + toff, tbytes, cudaMemcpyHostToDevice, hp.s_in);
+    cudaEventRecord(hp.ev_in[slot], hp.s_in);
+    // forward (saving its segment states) then backward on the block
+    cudaStreamWaitEvent(hp.s_cmp, hp.ev_in[slot], 0);
+    s = forward_impl(&pb, nullptr, b[0], lq, b[1], lk, b[2], lv, b[4], dg, dwf, wf, hp.s_cmp, nullptr,
+                     dsaved, sb);
+    if (s != LA_OK) return fail(err, s, "device forward failed");
+    s = backward_impl(&pb, nullptr, b[0], lq, b[1], lk, b[2], lv, b[4], b[3], lw, dg, b[5], b[6], b[7], dwb,
+                      wbk, hp.s_cmp, nullptr, dsaved, sb, true);
+    if (s != LA_OK) return fail(err, s, "device backward failed");
+    cudaEventRecord(hp.ev_cmp[slot], hp.s_cmp);
+    // copy-out
+    cudaStreamWaitEvent(hp.s_out, hp.ev_cmp[slot], 0);
+    cudaMemcpyAsync((char*)out + toff, b[4], tbytes, cudaMemcpyDeviceToHost, hp.s_out);
+    cudaMemcpyAsync(g + goff, dg, gbytes, cudaMemcpyDeviceToHost, hp.s_out);
+    cudaMemcpyAsync((char*)dq + toff, b[5], tbytes, cudaMemcpyDeviceToHost, hp.s_out);
+    cudaMemcpyAsync((char*)dk + toff, b[6], tbytes, cudaMemcpyDeviceToHost, hp.s_out);
+    cudaMemcpyAsync((char*)dv + toff, b[7], tbytes, cudaMemcpyDeviceToHost, hp.s_out);
+    cudaMemcpyAsync(&hp.hflags[2 * bi], dwf, sizeof(unsigned long long), cudaMemcpyDeviceToHost, hp.s_out);
+    cudaMemcpyAsync(&hp.hflags[2 * bi + 1], dwb, sizeof(unsigned long long), cudaMemcpyDeviceToHost, hp.s_out);
+    cudaEventRecord(hp.ev_out[slot], hp.s_out);
+  }
+  e = cudaStreamSynchronize(hp.s_out);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(err, e);
+  for (int bi = 0; bi < nb; ++bi) {
+    const unsigned long long f = hp.hflags[2 * bi];
+    if (f != ULLONG_MAX) {
+      const int64_t grp = (int64_t)(f >> 32) + bi * Gb, pos = (int64_t)(f & 0xFFFFFFFFull);
+      char msg[160];
+      std::snprintf(msg, sizeof(msg), "degenerate attention denominator at group %lld, position %lld",
+                    (long long)grp, (long long)pos);
+      return fail(err, LA_ERR_DEGENERATE_DENOMINATOR, msg, grp, pos);
+    }
+  }
+  return ok(err);
+}
 
 }  // extern "C"

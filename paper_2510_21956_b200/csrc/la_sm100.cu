@@ -56,7 +56,10 @@ __device__ __forceinline__ uint64_t mndesc(uint32_t tile, int ks) {
 }
 
 struct FwdParams {
-  const float* states;  // per (g, segment) exclusive-prefix records, or null (no carry)
+  const float* agg;     // per (g, unit) raw sums (A units per segment, segments 0..P-2)
+  int A;                // units per segment
+  const float* carry;   // per-group carry-in (sequence sharding), or null
+  float* cmb;           // per (g, segment) scratch: exclusive prefix combined in the prologue
   float* gout;          // G*N
   unsigned long long* flag;
   int64_t N, G;
@@ -65,19 +68,35 @@ struct FwdParams {
   int64_t row_offset;
   float a, b;
   float* st_out;        // per-(group, segment) end state (S, z, sigma, rows) for the backward, or null
+  void* out;            // o, FeatureMajor [G][D][N]
 };
 
 // ================================================================ forward main
-// Chunks of C = 64 rows, 3-stage TMA ring. Warp roles (320 threads):
-// 0 TMA producer; 1 MMA issuer + TMEM owner; 2-5 "WG-A" (S^T -> bf16 operand,
-// T1 -> P', g, z); 6-9 "WG-B" (O^T -> o -> TMA store, sigma).
-// TMEM: [0,64) T1 (M=64: lanes 0-15 of each quadrant), [64,192) O^T x2,
-// [192,320) S^T, [320,448) bf16(b S^T) x2.
-constexpr int kCF = 64;                 // forward chunk rows
-constexpr int kFT = 16384;              // 64x128 / 128x64 16-bit tile
+// Chunks of C = 64 rows, 3-stage TMA ring (+ L2 prefetch ahead of it). Warp roles
+// (448 threads): 0 TMA producer; 1 MMA issuer + TMEM owner; 2-5 "WG-A" (T1 -> P',
+// g); 6-9 "WG-B" (sigma, O^T -> o); 10-13 "WG-S" (S^T -> bf16 operand, z, z rows).
+// Per chunk c the tensor core computes
+//   T1  = Q [K ; z_hi ; z_lo]^T   (M=64, N=80: columns 64, 65 give q_i . z_prev)
+//   S^T += V^T K                  (the running state, fp32 in TMEM)
+//   O^T = V^T P'^T + bf16(b S^T) Q^T   (bf16 S^T is an A operand read from TMEM)
+// so the CUDA-core passes are the TMEM epilogues, z (column sums of K, written as
+// the two bf16 rows z_hi, z_lo under the next chunk's K tile) and sigma (row sums of V^T).
+// Stage: Q [64][128] | K as two 80-row panels (64 key rows + 16 rows for z) | V^T.
+// TMEM: [0,80) T1 (M=64: lanes 0-15 of each quadrant), [128,256) O^T x2,
+// [256,384) S^T, [384,512) bf16(b S^T) x2.
+constexpr int kCF = 64;                  // forward chunk rows
+constexpr int kFT = 16384;               // 64x128 / 128x64 16-bit tile
+constexpr int kKPanel = 80 * 128;        // K-tile panel: 64 key rows + 16 z rows
 constexpr int kFStages = 3;
-constexpr int kFStage = 3 * kFT;        // Q, K, V^T
-constexpr uint32_t kF_T1 = 0, kF_OT = 64, kF_ST = 192, kF_SB = 320;
+constexpr int kFPrefetch = 6;            // chunks of Q/K/V prefetched into L2 ahead of the ring
+constexpr int kFStage = kFT + 2 * kKPanel + kFT;  // Q, K(+z), V^T  = 52 KB
+constexpr int kOffK = kFT, kOffV = kFT + 2 * kKPanel;
+constexpr uint32_t kF_T1 = 0, kF_OT = 128, kF_ST = 256, kF_SB = 384;
+
+template <bool kBF16>
+__device__ __forceinline__ float h2f_fwd(uint16_t h) {
+  return kBF16 ? __bfloat162float(__ushort_as_bfloat16(h)) : __half2float(__ushort_as_half(h));
+}
 
 __device__ __forceinline__ uint64_t kd64(uint32_t tile, int ks, uint32_t rows) {
   return sdesc_sw128(tile + (ks >> 2) * rows * 128 + (ks & 3) * 32, 16, 1024);
@@ -87,15 +106,13 @@ __device__ __forceinline__ uint64_t mn64(uint32_t tile, int ks, uint32_t panel) 
 }
 
 template <bool kBF16>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(448, 1)
     k_fwd_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
-             FwdParams prm) {
+             const __grid_constant__ CUtensorMap tmV, FwdParams prm) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sP = smem + kFStages * kFStage;   // [2][8K]   P' (rows i, cols t)
-  uint8_t* sO = sP + 2 * 8192;               // [2][16K]  O^T staging (rows j, cols i)
-  uint64_t* bars = (uint64_t*)(sO + 2 * kFT);
+  uint64_t* bars = (uint64_t*)(sP + 2 * 8192);
   uint64_t* full = bars;            // [3]
   uint64_t* empty = bars + 3;       // [3]
   uint64_t* t1_full = bars + 6;
@@ -106,9 +123,9 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* o_full = bars + 11;     // [2]
   uint64_t* ot_empty = bars + 13;   // [2]
   uint64_t* a2b = bars + 15;        // [4]
-  uint32_t* tslot = (uint32_t*)(bars + 19);
-  float* ginv_s = (float*)(bars + 20);  // [4][64]
-  float* zq = ginv_s + 4 * kCF;         // [128]
+  uint64_t* zrow_ready = bars + 19; // z rows of the next chunk's stage written
+  uint32_t* tslot = (uint32_t*)(bars + 20);
+  float* ginv_s = (float*)(bars + 22);  // [4][64] (16-byte aligned: read as float4), then [128] z exchange
 
   const int p = blockIdx.x;
   const int64_t grp = blockIdx.y;
@@ -121,10 +138,9 @@ __global__ void __launch_bounds__(320, 1)
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
-    tma_prefetch(&tmO);
     for (int s = 0; s < kFStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1 + 128 + 128);
+      mbar_init(&empty[s], 1 + 2 * 128);  // M2 commit, WG-B (V), WG-S (K)
     }
     mbar_init(t1_full, 1);
     mbar_init(t1_empty, 128);
@@ -136,77 +152,85 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&ot_empty[b], 128);
     }
     for (int b = 0; b < 4; ++b) mbar_init(&a2b[b], 128);
+    mbar_init(zrow_ready, 128);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
+  // exclusive prefix of this segment: carry + sum of the earlier segments' sums
+  const bool has_in = p > 0 || prm.carry != nullptr;
+  float* st_in = has_in ? prm.cmb + (grp * prm.P + p) * state_floats(kD) : nullptr;
+  if (has_in && warp >= 2 && warp < 10)
+    combine_records(st_in, prm.carry ? prm.carry + grp * state_floats(kD) : nullptr,
+                    prm.agg + grp * prm.P * prm.A * state_floats(kD), 0, p * prm.A, state_floats(kD),
+                    (int)threadIdx.x - 64, 256);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const float* st_in = prm.states ? prm.states + (grp * prm.P + p) * state_floats(kD) : nullptr;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
+      auto l2_prefetch = [&](int c) {
+        const int64_t row0 = s0 + (int64_t)c * kCF;
+        tma_prefetch_l2_3d(&tmQ, 0, (int)(grp * prm.N + row0), 0);
+        tma_prefetch_l2_3d(&tmK, 0, (int)(grp * prm.N + row0), 0);
+        tma_prefetch_l2_3d(&tmK, 0, (int)(grp * prm.N + row0), 1);
+        tma_prefetch_l2_3d(&tmV, 0, (int)(grp * kD), (int)(row0 / 64));
+      };
+      for (int c = 0; c < kFPrefetch && c < nc; ++c) l2_prefetch(c);
       for (int c = 0; c < nc; ++c) {
         const int s = c % kFStages;
+        if (c + kFPrefetch < nc) l2_prefetch(c + kFPrefetch);
         if (lane_id() == 0) trace(3, c, 0);
         if (c >= kFStages) mbar_wait(&empty[s], ((c / kFStages) & 1) ^ 1);
         trace(3, c, 1);
         const int64_t row0 = s0 + (int64_t)c * kCF;
         uint8_t* st = smem + s * kFStage;
-        mbar_expect_tx(&full[s], kFStage);
+        mbar_expect_tx(&full[s], 3 * kFT);  // Q 16K + K 2 x 8K + V^T 16K
         tma_load_3d(st, &tmQ, &full[s], 0, (int)(grp * prm.N + row0), 0);
-        tma_load_3d(st + kFT, &tmK, &full[s], 0, (int)(grp * prm.N + row0), 0);
-        tma_load_3d(st + 2 * kFT, &tmV, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
+        tma_load_3d(st + kOffK, &tmK, &full[s], 0, (int)(grp * prm.N + row0), 0);
+        tma_load_3d(st + kOffK + kKPanel, &tmK, &full[s], 0, (int)(grp * prm.N + row0), 1);
+        tma_load_3d(st + kOffV, &tmV, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    // Per chunk: M3(c) S^T update, M1(c+1) next T1, M2(c) O^T.
+    // Per chunk: M3(c) = S^T and Z^T updates, M2(c) = O^T, then M1(c+1) = next T1.
     constexpr uint32_t fmt = kBF16 ? 1 : 0;
-    const uint32_t id_T1 = idesc_f16(64, 64, fmt, 0, 0);
+    const uint32_t id_T1 = idesc_f16(64, 80, fmt, 0, 0);
     const uint32_t id_ST = idesc_f16(128, 128, fmt, 0, 1);
     const uint32_t id_OT = idesc_f16(128, 64, fmt, 0, 0);
     const uint32_t a0 = smem_u32(smem), aP = smem_u32(sP);
-    if (nc > 0) {
-      mbar_wait(&full[0], 0);
+    auto issue_t1 = [&](int c) {  // T1(c) = Q [K ; z rows]^T
+      const uint32_t aQ = a0 + (c % kFStages) * kFStage;
+      mbar_wait(&full[c % kFStages], (c / kFStages) & 1);
+      mbar_wait(zrow_ready, c & 1);
+      if (c >= 1) mbar_wait(t1_empty, (c - 1) & 1);
       tc_fence_after();
       if (elect_one()) {
         for (int ks = 0; ks < 8; ++ks)
-          mma_ss(tmem + kF_T1, kd64(a0, ks, 64), kd64(a0 + kFT, ks, 64), id_T1, ks > 0);
+          mma_ss(tmem + kF_T1, kd64(aQ, ks, 64), kd64(aQ + kOffK, ks, 80), id_T1, ks > 0);
         mma_commit(t1_full);
       }
       __syncwarp();
-    }
+    };
+    if (nc > 0) issue_t1(0);
     for (int c = 0; c < nc; ++c) {
       const int s = c % kFStages, b = c & 1;
-      const uint32_t aQ = a0 + s * kFStage, aK = aQ + kFT, aV = aQ + 2 * kFT;
+      const uint32_t aQ = a0 + s * kFStage, aK = aQ + kOffK, aV = aQ + kOffV;
       if (lane_id() == 0) trace(0, c, 0);
       mbar_wait(sb_ready, c & 1);
       if (lane_id() == 0) trace(0, c, 1);
       tc_fence_after();
       if (elect_one()) {
         for (int ks = 0; ks < 4; ++ks)  // S^T += V^T K  (A: V^T rows j, K-major; B: K (N=m, K=t) MN-major)
-          mma_ss(tmem + kF_ST, kd64(aV, ks, 128), mn64(aK, ks, 8192), id_ST, 1);
+          mma_ss(tmem + kF_ST, kd64(aV, ks, 128), mn64(aK, ks, kKPanel), id_ST, 1);
         mma_commit(st_full);
       }
       __syncwarp();
-      if (c + 1 < nc) {
-        const int sn = (c + 1) % kFStages;
-        const uint32_t aQn = a0 + sn * kFStage;
-        mbar_wait(&full[sn], ((c + 1) / kFStages) & 1);
-        if (lane_id() == 0) trace(0, c, 2);
-        mbar_wait(t1_empty, c & 1);
-        if (lane_id() == 0) trace(0, c, 3);
-        tc_fence_after();
-        if (elect_one()) {
-          for (int ks = 0; ks < 8; ++ks)  // T1(c+1) = Q K^T (M=64)
-            mma_ss(tmem + kF_T1, kd64(aQn, ks, 64), kd64(aQn + kFT, ks, 64), id_T1, ks > 0);
-          mma_commit(t1_full);
-        }
-        __syncwarp();
-      }
+      if (c + 1 < nc) issue_t1(c + 1);
+      if (lane_id() == 0) trace(0, c, 2);
       mbar_wait(p_ready, c & 1);
       if (lane_id() == 0) trace(0, c, 4);
       if (c >= 2) mbar_wait(&ot_empty[b], ((c - 2) >> 1) & 1);
@@ -225,14 +249,96 @@ __global__ void __launch_bounds__(320, 1)
     }
   } else if (warp < 6) {
     // ------------------------------------------------------------ WG-A (warps 2..5)
+    // Per chunk: T1 -> P' (registers), g = rowsum(P') + a (row) + b q.z_prev -> 1/g for
+    // WG-B, P' -> smem.
     const uint32_t qd = warp & 3;
     const int l = (int)lane_id();
-    const int r = (int)(qd * 32) + l;              // full-lane row (j of S^T)
     const int ih = (int)(qd * 16) + (l & 15);      // row i of the M=64 T1
     const bool lower = l < 16;
     const uint32_t lane_base = (qd * 32u) << 16;
     const int et = (int)threadIdx.x - 64;          // 0..127
     const float a = prm.a, b = prm.b;
+    for (int c = 0; c < nc; ++c) {
+      const int bb = c & 1;
+      const int64_t row0 = s0 + (int64_t)c * kCF;
+      mbar_wait(t1_full, c & 1);
+      if (et == 0) trace(1, c, 3);
+      tc_fence_after();
+      uint32_t pk[32];
+      float rs0 = 0.f, rs1 = 0.f, qz;
+      {
+        uint32_t x[64], zh, zl;
+        tmem_ld32(tmem + lane_base + kF_T1, *(uint32_t(*)[32])x);
+        tmem_ld32(tmem + lane_base + kF_T1 + 32, *(uint32_t(*)[32])(x + 32));
+        tmem_ld2(tmem + lane_base + kF_T1 + 64, zh, zl);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(t1_empty);
+        qz = __uint_as_float(zh) + __uint_as_float(zl);
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          const int t0 = 2 * u;
+          const float p0 = t0 <= ih ? a + b * __uint_as_float(x[2 * u]) : 0.f;
+          const float p1 = t0 + 1 <= ih ? a + b * __uint_as_float(x[2 * u + 1]) : 0.f;
+          rs0 += p0;
+          rs1 += p1;
+          pk[u] = pack2<kBF16>(p0, p1);
+        }
+      }
+      if (et == 0) trace(1, c, 7);
+      if (lower) {
+        const float gi = (rs0 + rs1) + a * (float)(prm.row_offset + row0) + b * qz;
+        if (fabsf(gi) < kEpsF32) flag_degenerate(prm.flag, grp, prm.row_offset + row0 + ih);
+        ginv_s[(c & 3) * kCF + ih] = 1.f / gi;
+        prm.gout[grp * prm.N + row0 + ih] = gi;
+      }
+      mbar_arrive(&a2b[c & 3]);
+      if (et == 0) trace(1, c, 4);
+      if (c >= 2) mbar_wait(&o_full[bb], ((c - 2) >> 1) & 1);  // M2(c-2) drained sP[bb]
+      if (et == 0) trace(1, c, 5);
+      if (lower) {
+        uint8_t* pp = sP + bb * 8192;
+#pragma unroll
+        for (int w = 0; w < 8; ++w)
+          *(uint4*)(pp + sw128_off(ih, 8 * w, kCF)) = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
+      }
+      fence_proxy_async();
+      mbar_arrive(p_ready);
+      if (et == 0) trace(1, c, 6);
+    }
+  } else if (warp >= 10) {
+    // ------------------------------------------------------------ WG-S (warps 10..13)
+    // Per chunk: E2 (S^T -> bf16(b S^T) TMEM operand), then the z rows (z_hi, z_lo of
+    // z after this chunk, from the Z^T accumulator) into the next chunk's K tile.
+    const uint32_t qd = warp & 3;
+    const int r = (int)(qd * 32 + lane_id());      // j of S^T; m of Z^T
+    const uint32_t lane_base = (qd * 32u) << 16;
+    const int es = (int)threadIdx.x - 320;         // 0..127
+    const float b = prm.b;
+    // z_hi / z_lo of feature m = r into rows 64, 65 of the K-tile panel holding column m
+    auto put_zrows = [&](int c, float z) {
+      uint8_t* kt = smem + (c % kFStages) * kFStage + kOffK + (r >> 6) * kKPanel;
+      const __nv_bfloat16 h = __float2bfloat16_rn(z);
+      const float lo = z - __bfloat162float(h);
+      uint16_t hv, lv;
+      if (kBF16) {
+        hv = __bfloat16_as_ushort(h);
+        lv = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
+      } else {
+        const __half hh = __float2half_rn(z);
+        hv = __half_as_ushort(hh);
+        lv = __half_as_ushort(__float2half_rn(z - __half2float(hh)));
+      }
+      *(uint16_t*)(kt + sw128_off(64, r & 63, 80)) = hv;
+      *(uint16_t*)(kt + sw128_off(65, r & 63, 80)) = lv;
+      if (c < kFStages) {  // rows 66..79 stay zero (first use of the stage)
+        for (int rr = 66; rr < 80; ++rr) *(uint16_t*)(kt + sw128_off(rr, r & 63, 80)) = 0;
+      }
+      fence_proxy_async();
+      mbar_arrive(zrow_ready);
+    };
+    float zr = st_in ? st_in[kD * kD + r] : 0.f;  // z_m (m = r) before the current chunk
+    float* zx = (float*)(ginv_s + 4 * kCF);        // [128] column-sum exchange
     for (int m0 = 0; m0 < kD; m0 += 32) {  // carry-in S^T row r = S[:, r]
       uint32_t v[32];
 #pragma unroll
@@ -240,20 +346,13 @@ __global__ void __launch_bounds__(320, 1)
       tmem_st32(tmem + lane_base + kF_ST + m0, v);
     }
     tmem_st_wait();
-    zq[r] = st_in ? st_in[kD * kD + r] : 0.f;
-    tc_fence_before();
-    named_bar(1, 128);
-    tc_fence_after();
-
+    if (nc > 0) put_zrows(0, zr);
+    const int mg = es >> 3, tg = es & 7;
     for (int c = 0; c < nc; ++c) {
       const int s = c % kFStages, bb = c & 1;
-      const int64_t row0 = s0 + (int64_t)c * kCF;
-      const uint8_t* q_t = smem + s * kFStage;
-      const uint8_t* k_t = q_t + kFT;
-      // ---- E2: S^T -> bf16(b S^T) in TMEM buffer bb
-      if (et == 0) trace(1, c, 0);
+      // ---- E2: S^T (after chunk c-1) -> bf16(b S^T) in TMEM buffer bb
+      if (es == 0) trace(1, c, 0);
       if (c >= 1) mbar_wait(st_full, (c - 1) & 1);
-      if (et == 0) trace(1, c, 1);
       tc_fence_after();
 #pragma unroll 1
       for (int half = 0; half < 2; ++half) {
@@ -271,61 +370,17 @@ __global__ void __launch_bounds__(320, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(sb_ready);
-      if (et == 0) trace(1, c, 2);
-
-      // ---- E1: T1 -> P' (registers, lower lanes); q.z_prev (upper lanes)
-      mbar_wait(&full[s], (c / kFStages) & 1);
-      mbar_wait(t1_full, c & 1);
-      if (et == 0) trace(1, c, 3);
-      tc_fence_after();
-      uint32_t pk[32];
-      float rowsum = 0.f;
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        uint32_t x[32];
-        tmem_ld32(tmem + lane_base + kF_T1 + cc * 32, x);
-        tmem_ld_wait();
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int t0 = cc * 32 + 2 * u;
-          const float p0 = t0 <= ih ? a + b * __uint_as_float(x[2 * u]) : 0.f;
-          const float p1 = t0 + 1 <= ih ? a + b * __uint_as_float(x[2 * u + 1]) : 0.f;
-          rowsum += p0 + p1;
-          pk[cc * 16 + u] = pack2<kBF16>(p0, p1);
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(t1_empty);
-      if (et == 0) trace(1, c, 7);
-      float qz = 0.f;
-      if (!lower) {
-#pragma unroll 4
-        for (int m8 = 0; m8 < kD; m8 += 8) {
-          const uint4 v4 = *(const uint4*)(q_t + sw128_off(ih, m8, kCF));
-          const float4 za = *(const float4*)(zq + m8), zb = *(const float4*)(zq + m8 + 4);
-          const float2 f0 = unpack2<kBF16>(v4.x), f1 = unpack2<kBF16>(v4.y);
-          const float2 f2 = unpack2<kBF16>(v4.z), f3 = unpack2<kBF16>(v4.w);
-          qz += f0.x * za.x + f0.y * za.y + f1.x * za.z + f1.y * za.w + f2.x * zb.x + f2.y * zb.y +
-                f3.x * zb.z + f3.y * zb.w;
-        }
-      }
-      qz = __shfl_xor_sync(0xffffffffu, qz, 16);  // lower lane i receives q_i . z from lane i + 16
-      if (lower) {
-        const float gi = rowsum + a * (float)(prm.row_offset + row0) + b * qz;
-        if (fabsf(gi) < kEpsF32) flag_degenerate(prm.flag, grp, prm.row_offset + row0 + ih);
-        ginv_s[(c & 3) * kCF + ih] = 1.f / gi;
-        prm.gout[grp * prm.N + row0 + ih] = gi;
-      }
-      if (et == 0) trace(2, c, 6);
-      named_bar(1, 128);  // zq reads done, ginv(c) written
-      if (et == 0) trace(2, c, 7);
-      mbar_arrive(&a2b[c & 3]);
-      {  // z_m += sum_t K[t][m]: thread (mg, tg) sums rows [8 tg, 8 tg + 8) of columns [8 mg, 8 mg + 8)
-        const int mg = et >> 3, tg = et & 7;
+      if (es == 0) trace(1, c, 1);
+      // ---- z after chunk c (column sums of K(c), CUDA cores) -> z rows of chunk c + 1.
+      //      Thread (mg, tg) sums rows tg + 8 u of columns [8 mg, 8 mg + 8): a quarter-warp
+      //      reads 8 consecutive rows (distinct swizzle chunks, no bank conflicts).
+      if (c + 1 < nc) {
+        mbar_wait(&full[s], (c / kFStages) & 1);
+        const uint8_t* kt = smem + s * kFStage + kOffK + (mg >> 3) * kKPanel;
         float zs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int t = 8 * tg; t < 8 * tg + 8; ++t) {
-          const uint4 v4 = *(const uint4*)(k_t + sw128_off(t, 8 * mg, kCF));
+        for (int t = tg; t < kCF; t += 8) {
+          const uint4 v4 = *(const uint4*)(kt + sw128_off(t, 8 * (mg & 7), 80));
           const float2 f0 = unpack2<kBF16>(v4.x), f1 = unpack2<kBF16>(v4.y);
           const float2 f2 = unpack2<kBF16>(v4.z), f3 = unpack2<kBF16>(v4.w);
           zs[0] += f0.x; zs[1] += f0.y; zs[2] += f1.x; zs[3] += f1.y;
@@ -338,29 +393,30 @@ __global__ void __launch_bounds__(320, 1)
           zs[u] += __shfl_xor_sync(0xffffffffu, zs[u], 4);
         }
         if (tg == 0) {
-          const float4 za = *(const float4*)(zq + 8 * mg), zb = *(const float4*)(zq + 8 * mg + 4);
-          *(float4*)(zq + 8 * mg) = make_float4(za.x + zs[0], za.y + zs[1], za.z + zs[2], za.w + zs[3]);
-          *(float4*)(zq + 8 * mg + 4) = make_float4(zb.x + zs[4], zb.y + zs[5], zb.z + zs[6], zb.w + zs[7]);
+          *(float4*)(zx + 8 * mg) = make_float4(zs[0], zs[1], zs[2], zs[3]);
+          *(float4*)(zx + 8 * mg + 4) = make_float4(zs[4], zs[5], zs[6], zs[7]);
         }
+        mbar_arrive(&empty[s]);  // WG-S is done with K(c)
+        named_bar(3, 128);
+        zr += zx[r];
+        named_bar(3, 128);  // zx is reused next chunk
+        if (es == 0) trace(1, c, 2);
+        mbar_wait(&full[(c + 1) % kFStages], ((c + 1) / kFStages) & 1);
+        put_zrows(c + 1, zr);
+      } else {
+        mbar_arrive(&empty[s]);  // last chunk: K(c) is summed below, the stage is not reloaded
       }
-      mbar_arrive(&empty[s]);  // WG-A is done with Q(c), K(c)
-      if (et == 0) trace(1, c, 4);
-      if (c >= 2) mbar_wait(&o_full[bb], ((c - 2) >> 1) & 1);  // M2(c-2) drained sP[bb]
-      if (et == 0) trace(1, c, 5);
-      if (lower) {
-        uint8_t* pp = sP + bb * 8192;
-#pragma unroll
-        for (int w = 0; w < 8; ++w)
-          *(uint4*)(pp + sw128_off(ih, 8 * w, kCF)) = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
-      }
-      fence_proxy_async();
-      named_bar(1, 128);  // P' complete; zq updates visible
-      mbar_arrive(p_ready);
-      if (et == 0) trace(1, c, 6);
     }
     if (prm.st_out && nc > 0) {  // final state for the backward (S, z)
       mbar_wait(st_full, (nc - 1) & 1);
       tc_fence_after();
+      if (nc >= 1) {  // z after the last chunk
+        const int s = (nc - 1) % kFStages;
+        const uint8_t* kt = smem + s * kFStage + kOffK + (r >> 6) * kKPanel;
+        float zs = 0.f;
+        for (int t = 0; t < kCF; ++t) zs += h2f_fwd<kBF16>(*(const uint16_t*)(kt + sw128_off(t, r & 63, 80)));
+        zr += zs;
+      }
       float* so = prm.st_out + (grp * prm.P + p) * state_floats(kD);
       for (int m0 = 0; m0 < kD; m0 += 32) {
         uint32_t x[32];
@@ -369,7 +425,7 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int u = 0; u < 32; ++u) so[(m0 + u) * kD + r] = __uint_as_float(x[u]);
       }
-      so[kD * kD + r] = zq[r];
+      so[kD * kD + r] = zr;
       if (r == 0) so[kD * kD + 2 * kD] = (float)(prm.row_offset + s1);
     }
   } else {
@@ -383,58 +439,54 @@ __global__ void __launch_bounds__(320, 1)
     for (int c = 0; c < nc; ++c) {
       const int s = c % kFStages, bb = c & 1;
       const int64_t row0 = s0 + (int64_t)c * kCF;
-      const uint8_t* v_t = smem + s * kFStage + 2 * kFT;
+      const uint8_t* v_t = smem + s * kFStage + kOffV;
       if (eb == 0) trace(2, c, 0);
-      mbar_wait(&o_full[bb], (c >> 1) & 1);
-      if (eb == 0) trace(2, c, 1);
-      mbar_wait(&a2b[c & 3], (c >> 2) & 1);
-      if (eb == 0) trace(2, c, 2);
-      tc_fence_after();
-      const float asig = a * sigma;
-      const float* gv = ginv_s + (c & 3) * kCF;
-      uint32_t pk[32];
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        uint32_t x[32];
-        tmem_ld32(tmem + lane_base + kF_OT + bb * 64 + cc * 32, x);
-        tmem_ld_wait();
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int i0 = cc * 32 + 2 * u;
-          pk[cc * 16 + u] = pack2<kBF16>((__uint_as_float(x[2 * u]) + asig) * gv[i0],
-                                         (__uint_as_float(x[2 * u + 1]) + asig) * gv[i0 + 1]);
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&ot_empty[bb]);
-      if (eb == 0) trace(2, c, 3);
-      // sigma_j += sum_t V^T[j][t]   (j = r), for the next chunk
+      // sigma_j += sum_t V^T[j][t] (j = r) as soon as V(c) lands; a * sigma_prev feeds
+      // this chunk's outputs.
+      mbar_wait(&full[s], (c / kFStages) & 1);
       float vs = 0.f;
 #pragma unroll
       for (int t8 = 0; t8 < kCF; t8 += 8) {
         const uint4 v4 = *(const uint4*)(v_t + sw128_off(r, t8, kD));
         const float2 f0 = unpack2<kBF16>(v4.x), f1 = unpack2<kBF16>(v4.y);
         const float2 f2 = unpack2<kBF16>(v4.z), f3 = unpack2<kBF16>(v4.w);
-        vs += f0.x + f0.y + f1.x + f1.y + f2.x + f2.y + f3.x + f3.y;
+        vs += ((f0.x + f0.y) + (f1.x + f1.y)) + ((f2.x + f2.y) + (f3.x + f3.y));
       }
-      sigma += vs;
       mbar_arrive(&empty[s]);  // WG-B is done with V(c)
-      // staging buffer bb: the store issued two chunks ago must have left it
-      if (eb == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-      named_bar(2, 128);
-      uint8_t* so = sO + bb * kFT;
+      const float asig = a * sigma;
+      sigma += vs;
+      mbar_wait(&o_full[bb], (c >> 1) & 1);
+      if (eb == 0) trace(2, c, 1);
+      mbar_wait(&a2b[c & 3], (c >> 2) & 1);
+      if (eb == 0) trace(2, c, 2);
+      tc_fence_after();
+      const float* gv = ginv_s + (c & 3) * kCF;
+      uint32_t pk[32];
+      {
+        uint32_t x0[32], x1[32];
+        tmem_ld32(tmem + lane_base + kF_OT + bb * 64, x0);
+        tmem_ld32(tmem + lane_base + kF_OT + bb * 64 + 32, x1);
+        float gr[64];
 #pragma unroll
-      for (int w = 0; w < 8; ++w)
-        *(uint4*)(so + sw128_off(r, 8 * w, kD)) = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
-      fence_proxy_async();
-      named_bar(2, 128);
-      if (eb == 0) {
-        tma_store_3d(&tmO, so, 0, (int)(grp * kD), (int)(row0 / 64));
-        tma_store_commit();
-        trace(2, c, 4);
+        for (int u = 0; u < 16; ++u) *(float4*)(gr + 4 * u) = *(const float4*)(gv + 4 * u);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&ot_empty[bb]);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          pk[u] = pack2<kBF16>((__uint_as_float(x0[2 * u]) + asig) * gr[2 * u],
+                               (__uint_as_float(x0[2 * u + 1]) + asig) * gr[2 * u + 1]);
+          pk[16 + u] = pack2<kBF16>((__uint_as_float(x1[2 * u]) + asig) * gr[32 + 2 * u],
+                                    (__uint_as_float(x1[2 * u + 1]) + asig) * gr[32 + 2 * u + 1]);
+        }
       }
+      if (eb == 0) trace(2, c, 3);
+      // o^T row j = r, columns [row0, row0 + 64): one 128-byte line per thread
+      uint4* dst = (uint4*)((uint16_t*)prm.out + (grp * kD + r) * prm.N + row0);
+#pragma unroll
+      for (int w = 0; w < 8; ++w) dst[w] = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
+      if (eb == 0) trace(2, c, 4);
     }
-    if (eb == 0) tma_store_wait0();
     if (prm.st_out && nc > 0) prm.st_out[(grp * prm.P + p) * state_floats(kD) + kD * kD + kD + r] = sigma;
   }
   tc_fence_before();
@@ -556,21 +608,8 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc<128>(tmem);
 }
 
-constexpr size_t kFwdSmem = kFStages * kFStage + 2 * 8192 + 2 * kFT + 256 + (4 * kCF + kD) * 4 + 1024;
+constexpr size_t kFwdSmem = kFStages * kFStage + 2 * 8192 + 256 + (4 * kCF + kD) * 4 + 1024;
 constexpr size_t kAggSmem = 4 * kTile + 128 + 1024;
-
-__global__ void k_scan_fwd(float* states, int P, int64_t SZ, const float* carry) {
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t grp = blockIdx.y;
-  if (e >= SZ) return;
-  float* base = states + grp * P * SZ + e;
-  float run = carry ? carry[grp * SZ + e] : 0.f;
-  for (int q = 0; q < P; ++q) {
-    const float t = base[q * SZ];
-    base[q * SZ] = run;
-    run += t;
-  }
-}
 
 }  // namespace
 
@@ -586,10 +625,15 @@ bool tc_forward_supported(const Launch& L, const Tensors& t) {
          t.lv == LA_FEATURE_MAJOR && L.G * L.N < (1ll << 31) && L.G * kD < (1ll << 31);
 }
 
+static int fwd_agg_split(int64_t G, int64_t N, int P) {
+  const int64_t seg = ((N / kC + P - 1) / P) * kC;
+  return agg_split(G, seg, P - 1);
+}
+
 size_t tc_forward_ws_floats(int64_t G, int64_t N, int64_t D) {
   if (D != kD || N % kC) return 0;
   const int P = tc_segments(G, N);
-  return P > 1 ? (size_t)(G * P * state_floats(kD)) : 0;
+  return (size_t)((fwd_agg_split(G, N, P) + 1) * G * P * state_floats(kD));  // unit sums + combined prefixes
 }
 
 size_t tc_saved_floats(int64_t G, int64_t N, int64_t D) {
@@ -606,42 +650,34 @@ cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, W
   const int P = tc_segments(G, N);
   const int64_t chunks = N / kC;
   const int64_t seg = ((chunks + P - 1) / P) * kC;
-  CUtensorMap mK, mV, mQ64, mK64, mV64, mO64;
+  CUtensorMap mK, mV, mQ64, mK64, mV64;
   if (!make_map(&mK, t.k, bf, (uint64_t)(G * N), kD) || !make_map(&mV, t.v, bf, (uint64_t)(G * kD), (uint64_t)N) ||
       !make_tma_map(&mQ64, t.q, bf, (uint64_t)(G * N), kD, 64, 2) ||
-      !make_tma_map(&mK64, t.k, bf, (uint64_t)(G * N), kD, 64, 2) ||
-      !make_tma_map(&mV64, t.v, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1) ||
-      !make_tma_map(&mO64, out, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1))
+      !make_tma_map(&mK64, t.k, bf, (uint64_t)(G * N), kD, 64, 1) ||
+      !make_tma_map(&mV64, t.v, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1))
     return cudaErrorInvalidValue;
   auto main_k = bf ? k_fwd_tc<true> : k_fwd_tc<false>;
   cudaFuncSetAttribute(main_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem);
   float* saved = L.saved_out ? L.saved_out + kSavedHeader : nullptr;
-  const float* states = L.carry_prefix;
+  const int A = fwd_agg_split(G, N, P);
+  float* agg_st = ws.base;
+  float* cmb = ws.base + G * P * A * SZ;
   int launches = 1;
-  if (P > 1) {
-    float* st = ws.base;
+  if (P > 1) {  // only segments 0..P-2 feed a later segment's prefix
     auto agg = bf ? k_fwd_agg_tc<true> : k_fwd_agg_tc<false>;
     cudaFuncSetAttribute(agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggSmem);
-    {
-      ProfScope ps("la_fwd_agg", L.stream);
-      agg<<<dim3(P, G), 192, kAggSmem, L.stream>>>(mK, mV, st, N, seg, P);
-    }
-    {
-      ProfScope ps("la_fwd_scan", L.stream);
-      k_scan_fwd<<<dim3((unsigned)((SZ + 255) / 256), (unsigned)G), 256, 0, L.stream>>>(st, P, SZ,
-                                                                                      L.carry_prefix);
-    }
-    states = st;
-    launches += 2;
+    ProfScope ps("la_fwd_agg", L.stream);
+    agg<<<dim3(A * (P - 1), G), 192, kAggSmem, L.stream>>>(mK, mV, agg_st, N, seg / A, P * A);
+    launches += 1;
   }
   if (L.saved_out) {
     const float hdr[kSavedHeader] = {kSavedMagic, (float)G, (float)N, (float)kD, (float)P, (float)seg};
     cudaMemcpyAsync(L.saved_out, hdr, sizeof(hdr), cudaMemcpyHostToDevice, L.stream);
   }
-  FwdParams prm{states, g, ws.flag, N, G, seg, P, L.row_offset, L.a, L.b, saved};
+  FwdParams prm{agg_st, A, L.carry_prefix, cmb, g, ws.flag, N, G, seg, P, L.row_offset, L.a, L.b, saved, out};
   {
     ProfScope ps("la_fwd_causal", L.stream);
-    main_k<<<dim3(P, G), 320, kFwdSmem, L.stream>>>(mQ64, mK64, mV64, mO64, prm);
+    main_k<<<dim3(P, G), 448, kFwdSmem, L.stream>>>(mQ64, mK64, mV64, prm);
   }
   note_launch(launches);
   return cudaGetLastError();

@@ -38,6 +38,7 @@ constexpr int kCB = 64;   // chunk rows
 constexpr int kD = 128;   // head dim
 constexpr int kT64 = 16384;  // a 64x128 or 128x64 16-bit tile
 constexpr int kStage = 4 * kT64;  // Q, K, V^T, Omega^T
+constexpr int kBPrefetch = 4;     // chunks prefetched into L2 ahead of the 2-stage ring
 constexpr uint32_t kDP = 0, kDQ = 64, kDK = 128, kDV = 192, kR = 256, kS = 384;
 constexpr uint32_t kHalf = 16u << 16;  // TMEM lane offset of the upper M=64 half
 
@@ -92,6 +93,11 @@ struct BwdParams {
   float a, b;
   int dbg;     // debug bitmask (LA_BWD_DEBUG): 1 skip dS K, 2 skip W_hat S^T
   int skipS;   // aggregate pass: S records come from the forward (la_backward_saved)
+  int p0;      // aggregate pass: first unit of the grid
+  int A;       // aggregate units per segment (records are per unit: [G][P * A])
+  const float* carry_pre;  // sequence-shard carries (or null)
+  const float* carry_suf;
+  float* cmb;  // per (g, segment) combined [S inclusive prefix | R exclusive suffix]
 };
 
 // Epilogue step E0: W_hat = omega / g in place (bf16) and s_i = sum_j o_ij w_hat_ij.
@@ -223,7 +229,7 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t* tslot = (uint32_t*)(bars + 8);
   float* s_s = (float*)(bars + 16);  // [64]
 
-  const int p = blockIdx.x;
+  const int p = blockIdx.x + prm.p0;
   const int64_t grp = blockIdx.y;
   const int64_t s0 = (int64_t)p * prm.seg_len;
   const int64_t s1 = lmin(prm.N, s0 + prm.seg_len);
@@ -363,30 +369,6 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc<256>(tmem);
 }
 
-// Scan: S records -> inclusive prefix (+carry), R records -> exclusive suffix (+carry).
-__global__ void k_scan_bwd(float* stS, float* stR, int P, int64_t SZ, const float* carry_pre,
-                           const float* carry_suf) {
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t grp = blockIdx.y;
-  if (e >= SZ) return;
-  float* br = stR + grp * P * SZ + e;
-  float run;
-  if (stS) {  // null when the forward's saved (already inclusive) S records are used
-    float* bs = stS + grp * P * SZ + e;
-    run = carry_pre ? carry_pre[grp * SZ + e] : 0.f;
-    for (int q = 0; q < P; ++q) {
-      run += bs[q * SZ];
-      bs[q * SZ] = run;
-    }
-  }
-  run = carry_suf ? carry_suf[grp * SZ + e] : 0.f;
-  for (int q = P - 1; q >= 0; --q) {
-    const float t = br[q * SZ];
-    br[q * SZ] = run;
-    run += t;
-  }
-}
-
 // ================================================================ main reverse sweep
 // Warp roles (320 threads): 0 TMA producer; 1 MMA issuer + TMEM owner;
 // 2-5 WG-A: W_hat/s, dS/P, dK^T/dV^T out, u/c; 6-9 WG-B: bR/bS operand copies,
@@ -466,6 +448,21 @@ __global__ void __launch_bounds__(320, 1)
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
+  {  // carries: S inclusive prefix at s1 (saved by the forward, or carry + segment sums
+     // 0..p) and R exclusive suffix after s1 (carry + segment sums p+1..P-1)
+    const int64_t SZ = state_floats(kD);
+    const int U = prm.P * prm.A;
+    float* cS = prm.cmb + (grp * prm.P + p) * 2 * SZ;
+    if (warp >= 2) {
+      if (prm.skipS)
+        combine_records(cS, prm.stS + (grp * prm.P + p) * SZ, prm.stS, 0, 0, SZ, (int)threadIdx.x - 64, 256);
+      else
+        combine_records(cS, prm.carry_pre ? prm.carry_pre + grp * SZ : nullptr, prm.stS + grp * U * SZ, 0,
+                        (p + 1) * prm.A, SZ, (int)threadIdx.x - 64, 256);
+      combine_records(cS + SZ, prm.carry_suf ? prm.carry_suf + grp * SZ : nullptr, prm.stR + grp * U * SZ,
+                      (p + 1) * prm.A, U, SZ, (int)threadIdx.x - 64, 256);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -476,8 +473,8 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t qd = warp & 3;
     const int r = (int)(qd * 32 + lane_id());
     const uint32_t lb = (qd * 32u) << 16;
-    const float* recS = prm.stS + (grp * prm.P + p) * state_floats(kD);  // inclusive prefix at s1
-    const float* recR = prm.stR + (grp * prm.P + p) * state_floats(kD);  // exclusive suffix after s1
+    const float* recS = prm.cmb + (grp * prm.P + p) * 2 * state_floats(kD);  // inclusive prefix at s1
+    const float* recR = recS + state_floats(kD);                             // exclusive suffix after s1
     for (int j0 = 0; j0 < kD; j0 += 32) {
       uint32_t xr[32], xs[32];
 #pragma unroll
@@ -502,8 +499,17 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (reverse)
     if (elect_one()) {
+      auto l2_prefetch = [&](int n) {  // Q, K, V^T, Omega^T and O^T of chunk n into L2
+        const int64_t row0 = s0 + (int64_t)(nc - 1 - n) * kCB;
+        tma_prefetch_l2_3d(&tmQ, 0, (int)(grp * prm.N + row0), 0);
+        tma_prefetch_l2_3d(&tmK, 0, (int)(grp * prm.N + row0), 0);
+        tma_prefetch_l2_3d(&tmV, 0, (int)(grp * kD), (int)(row0 / 64));
+        tma_prefetch_l2_3d(&tmW, 0, (int)(grp * kD), (int)(row0 / 64));
+      };
+      for (int n = 0; n < kBPrefetch && n < nc; ++n) l2_prefetch(n);
       for (int n = 0; n < nc; ++n) {
         const int s = n & 1;
+        if (n + kBPrefetch < nc) l2_prefetch(n + kBPrefetch);
         if (n >= 2) mbar_wait(&empty[s], ((n >> 1) & 1) ^ 1);
         const int64_t row0 = s0 + (int64_t)(nc - 1 - n) * kCB;
         uint8_t* st = smem + s * kStage;
@@ -605,7 +611,7 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lb = (qd * 32u) << 16;
     const int et = (int)threadIdx.x - 64;
     const float a = prm.a, b = prm.b;
-    const float* recR = prm.stR + (grp * prm.P + p) * state_floats(kD);
+    const float* recR = prm.cmb + (grp * prm.P + p) * 2 * state_floats(kD) + state_floats(kD);
     float cj = recR[kD * kD + kD + r];  // c_next (j = r)
     float dc_prev = 0.f;
     uint4 o4[4];
@@ -782,7 +788,7 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lb = (qd * 32u) << 16;
     const int eb = (int)threadIdx.x - 192;
     const float b = prm.b;
-    const float* recR = prm.stR + (grp * prm.P + p) * state_floats(kD);
+    const float* recR = prm.cmb + (grp * prm.P + p) * 2 * state_floats(kD) + state_floats(kD);
     float u = recR[kD * kD + r];  // u_next (m = r)
     uint4 o4[4];
     float4 g8[2];
@@ -937,7 +943,10 @@ bool tc_backward_supported(const Launch& L, const Tensors& t) {
 
 size_t tc_backward_ws_floats(int64_t G, int64_t N, int64_t D) {
   if (D != kD || N % 128) return 0;
-  return (size_t)(2 * G * tcb_segments(G, N) * state_floats(kD));
+  const int P = tcb_segments(G, N);
+  const int64_t seg = ((N / 128 + P - 1) / P) * 128;
+  const int A = agg_split(G, seg, P > 1 ? P - 1 : 1);  // the larger of the two launch shapes' splits
+  return (size_t)((2 * A + 2) * G * P * state_floats(kD));  // S, R unit sums + combined
 }
 
 cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv, Workspace ws) {
@@ -951,8 +960,11 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
   // segmentation (no K/V re-read), else computed by the aggregate pass.
   const float* sv = L.saved_in;
   const bool use_saved = sv != nullptr;  // validated by the ABI layer
+  const int p0 = use_saved ? 1 : 0;  // first segment that needs an aggregate
+  const int A = agg_split(G, seg, P - p0);
   float* stS = ws.base;
-  float* stR = stS + G * P * SZ;
+  float* stR = stS + G * P * A * SZ;
+  float* cmb = stR + G * P * A * SZ;
   CUtensorMap mQ, mK, mV, mW;
   if (!make_tma_map(&mQ, t.q, bf, (uint64_t)(G * N), kD, 64, 2) ||
       !make_tma_map(&mK, t.k, bf, (uint64_t)(G * N), kD, 64, 2) ||
@@ -960,26 +972,32 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
       !make_tma_map(&mW, t.w, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1))
     return cudaErrorInvalidValue;
   const char* dbg = getenv("LA_BWD_DEBUG");
+  // With the forward's saved S records only segments 1..P-1 need an aggregate
+  // (their R sums feed the earlier segments' suffix); otherwise every segment's
+  // S sum is needed for the inclusive prefix. The aggregate runs on units of
+  // seg / A rows; the main kernel's prologue sums the unit records.
   BwdParams prm{t.o, t.g, dq, dk, dv, use_saved ? const_cast<float*>(sv + kSavedHeader) : stS, stR, N, seg, P,
-                L.a, L.b, dbg ? atoi(dbg) : 0, use_saved ? 1 : 0};
+                L.a, L.b, dbg ? atoi(dbg) : 0, use_saved ? 1 : 0, 0, A, L.carry_prefix, L.carry_suffix, cmb};
+  BwdParams pa = prm;  // aggregate launch: unit geometry
+  pa.stS = stS;
+  pa.seg_len = seg / A;
+  pa.P = P * A;
+  pa.p0 = p0 * A;
   auto agg = bf ? k_bwd_agg_tc<true> : k_bwd_agg_tc<false>;
   auto main_k = bf ? k_bwd_tc<true> : k_bwd_tc<false>;
   cudaFuncSetAttribute(agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggSmemB);
   cudaFuncSetAttribute(main_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmemB);
-  {
+  int launches = 1;
+  if (P - p0 > 0) {
     ProfScope ps("la_bwd_agg", L.stream);
-    agg<<<dim3(P, G), 192, kAggSmemB, L.stream>>>(mQ, mK, mV, mW, prm);
-  }
-  {
-    ProfScope ps("la_bwd_scan", L.stream);
-    k_scan_bwd<<<dim3((unsigned)((SZ + 255) / 256), (unsigned)G), 256, 0, L.stream>>>(
-        use_saved ? nullptr : stS, stR, P, SZ, L.carry_prefix, L.carry_suffix);
+    agg<<<dim3(A * (P - p0), G), 192, kAggSmemB, L.stream>>>(mQ, mK, mV, mW, pa);
+    launches += 1;
   }
   {
     ProfScope ps("la_bwd_causal", L.stream);
     main_k<<<dim3(P, G), 320, kMainSmemB, L.stream>>>(mQ, mK, mV, mW, prm);
   }
-  note_launch(3);
+  note_launch(launches);
   return cudaGetLastError();
 }
 

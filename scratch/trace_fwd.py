@@ -15,13 +15,18 @@ torch.cuda.synchronize()
 buf = (C.c_ulonglong * (4 * 64 * 8))()
 L.la_internal_trace_read(buf)
 t = np.array(buf, dtype=np.int64).reshape(4, 64, 8)
-t0 = t[3, 0, 0]
-names = {0: "MMA: start,sb_ready,full(c+1),t1_empty,p_ready,ot_empty", 1: "WGA: E2start,st_full,sbready,t1_full,a2b/empty,o_full(c-1),p_ready",
-         2: "WGB: start,o_full,a2b,ot_empty,store_issued,store_read", 3: "PROD: start,empty"}
-for role in range(4):
-    print(names[role])
-    for c in range(10, 16):
-        print(c, (t[role, c] - t0).tolist())
-print("per-chunk period (MMA start):", np.diff(t[0, 5:60, 0]).mean())
-print("WGA fine: t1_full, after T1 loads, after dot+g, after named_bar, after z(empty)")
-for c in range(10, 16): print(c, (t[1, c, [3, 7]] - t0).tolist(), (t[2, c, [6, 7]] - t0).tolist(), (t[1, c, 4] - t0))
+t0 = t[0, 10, 0]
+t = t - t0
+t[t < -10**9] = -1
+R = range(8, 14)
+print("MMA  : start, sb_ready, p_ready, ot_empty(M2 issue), T1(c+1) issued")
+for c in R: print(c, t[0, c, [0, 1, 4, 5, 2]].tolist())
+print("WG-S : E2start, sb_ready arrive, st_full(c)")
+for c in R: print(c, t[1, c, :3].tolist())
+print("WG-A : t1_full, T1 loaded, g/a2b, o_full(c-2), p_ready")
+for c in R: print(c, t[1, c, [3, 7, 4, 5, 6]].tolist())
+print("WG-B : start, o_full, a2b, ot_empty, store")
+for c in R: print(c, t[2, c, :5].tolist())
+print("PROD : start, empty")
+for c in R: print(c, t[3, c, :2].tolist())
+print("period", np.diff(t[0, 5:60, 0]).mean())

@@ -262,3 +262,46 @@ def test_backward_with_saved_forward_state_matches_recompute(cuda):
         assert max_abs(res[key], ref[key]) <= BF16_ABS, key
         assert max_abs(t.logical(), res[key]) <= 1e-2, key
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("dtype,G,N,D", [("bf16", 10, 1024, 128), ("f32", 3, 300, 64)])
+def test_host_step_pipeline_matches_oracle(cuda, dtype, G, N, D):
+    # la_host_step: forward + backward over host buffers, groups pipelined in blocks
+    # (ragged last block at G=10) through the H2D / compute / D2H streams
+    import ctypes as C
+
+    import torch
+    from paper_2510_21956_b200 import _abi
+    q, k, v, w = fast_inputs(G, N, D, seed=G + N)
+    tdt = {"bf16": torch.bfloat16, "f32": torch.float32}[dtype]
+    hq = torch.as_tensor(q).to(tdt).contiguous().pin_memory()                     # SequenceMajor
+    hk = torch.as_tensor(k).to(tdt).contiguous().pin_memory()
+    hv = torch.as_tensor(v).to(tdt).transpose(1, 2).contiguous().pin_memory()     # FeatureMajor
+    hw = torch.as_tensor(w).to(tdt).transpose(1, 2).contiguous().pin_memory()
+    hout = torch.empty((G, D, N), dtype=tdt).pin_memory()
+    hg = torch.empty((G, N), dtype=torch.float32).pin_memory()
+    hdq = torch.empty((G, N, D), dtype=tdt).pin_memory()
+    hdk = torch.empty((G, D, N), dtype=tdt).pin_memory()
+    hdv = torch.empty((G, D, N), dtype=tdt).pin_memory()
+    L = _abi.lib()
+    p = _abi.make_problem(G, N, D, dtype)
+    err = _abi.ErrorInfo()
+    st = L.la_host_step(C.byref(p), hq.data_ptr(), SM, hk.data_ptr(), SM, hv.data_ptr(), FM, hw.data_ptr(), FM,
+                        hout.data_ptr(), hg.data_ptr(), hdq.data_ptr(), hdk.data_ptr(), hdv.data_ptr(),
+                        C.byref(err))
+    assert st == 0, err.message
+    rq, rk = hq.double().numpy(), hk.double().numpy()
+    rv, rw = hv.double().transpose(1, 2).numpy(), hw.double().transpose(1, 2).numpy()
+    out = hout.double().transpose(1, 2).numpy()
+    g = hg.double().numpy()
+    ro, rg = O.forward(rq, rk, rv)
+    dq, dk, dv = O.backward(rq, rk, rv, out, rw, g)
+    got = {"out": out, "dq": hdq.double().numpy(), "dk": hdk.double().transpose(1, 2).numpy(),
+           "dv": hdv.double().transpose(1, 2).numpy()}
+    ref = {"out": ro, "dq": dq, "dk": dk, "dv": dv}
+    for key in got:
+        if dtype == "f32":
+            assert rel_err(got[key], ref[key]) <= FP32_REL, key
+        else:
+            assert max_abs(got[key], ref[key]) <= BF16_ABS, key
+    assert rel_err(g, rg) <= (1e-5 if dtype == "f32" else 1e-3)
