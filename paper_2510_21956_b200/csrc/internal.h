@@ -46,11 +46,20 @@ inline int choose_segments(int64_t G, int64_t N, int num_sms = 148) {
 // per unit and summed by the consumer's prologue.
 inline int agg_split(int64_t G, int64_t seg_rows, int segs_aggregated, int num_sms = 148) {
   if (segs_aggregated <= 0) return 1;
-  int A = (int)(num_sms / (G * segs_aggregated));
-  if (A < 1) A = 1;
-  const int64_t chunks = seg_rows / 128;
-  while (A > 1 && chunks % A) --A;
-  return A;
+  const int64_t units = G * segs_aggregated, chunks = seg_rows / 128;
+  int best = 1;
+  double best_t = 1e300;
+  for (int A = 1; A <= 8; ++A) {
+    if (chunks % A) continue;
+    // makespan in whole-segment times: waves of A-way split units, plus a small
+    // per-CTA overhead that keeps the split from growing without need
+    const double t = (double)((units * A + num_sms - 1) / num_sms) / A + 0.02 * A;
+    if (t < best_t - 1e-9) {
+      best_t = t;
+      best = A;
+    }
+  }
+  return best;
 }
 
 struct Tensors {

@@ -369,6 +369,182 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc<256>(tmem);
 }
 
+// ================================================================ lean R aggregate
+// Used when the forward's saved S records are available (la_backward_saved): per
+// unit of rows, R^T = sum W_hat^T Q, c = sum_i w_hat (a ones panel appended to Q as
+// extra N columns of the same MMA) and u = Q^T s (a second small MMA against two bf16
+// rows s_hi, s_lo). The only CUDA-core work is the W_hat / s pass, spread over 256
+// threads. Stage: Q [64 i][128 m] (2 panels) | ones panel | W_hat^T [128 j][64 i] | s rows
+// | O^T [128 j][64 i] (all by TMA, L2-prefetched ahead of the ring).
+constexpr int kAStages = 3;
+constexpr int kAStage = 2 * 8192 + 8192 + kT64 + 2048 + kT64;  // 58 KB
+constexpr int kAOffOnes = 16384, kAOffW = 24576, kAOffS = 24576 + kT64, kAOffO = kAOffS + 2048;
+constexpr size_t kAggRSmem = kAStages * kAStage + 128 + 4 * 2 * kCB * 4 + 1024;
+
+template <bool kBF16>
+__global__ void __launch_bounds__(320, 1)
+    k_bwd_aggR_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmW,
+                  const __grid_constant__ CUtensorMap tmO, BwdParams prm) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* bars = (uint64_t*)(smem + kAStages * kAStage);
+  uint64_t* full = bars;                 // [4]
+  uint64_t* empty = bars + kAStages;     // [4]
+  uint64_t* w_ready = bars + 2 * kAStages;
+  uint64_t* done = bars + 2 * kAStages + 1;
+  uint32_t* tslot = (uint32_t*)(bars + 2 * kAStages + 2);
+  float* s_part = (float*)(bars + 16);   // [2 parity][2 halves][64]
+
+  const int p = blockIdx.x + prm.p0;
+  const int64_t grp = blockIdx.y;
+  const int64_t s0 = (int64_t)p * prm.seg_len;
+  const int64_t s1 = lmin(prm.N, s0 + prm.seg_len);
+  const int nc = (int)((s1 - s0) / kCB);
+  const uint32_t warp = warp_id();
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmW);
+    tma_prefetch(&tmO);
+    for (int s = 0; s < kAStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(w_ready, 256);
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<256>(tslot);
+  if (warp >= 2) {  // constant ones panels and the zero rows 2..15 of every s-rows tile
+    const uint32_t one2 = kBF16 ? 0x3F803F80u : 0x3C003C00u;
+    const int t = (int)threadIdx.x - 64;
+    for (int s = 0; s < kAStages; ++s) {
+      uint4* op = (uint4*)(smem + s * kAStage + kAOffOnes);
+      for (int e = t; e < 8192 / 16; e += 256) op[e] = make_uint4(one2, one2, one2, one2);
+      uint4* sp = (uint4*)(smem + s * kAStage + kAOffS);
+      for (int e = t; e < 2048 / 16; e += 256) sp[e] = make_uint4(0, 0, 0, 0);
+    }
+    fence_proxy_async();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;  // [0,144) R^T | c, [160,176) U
+  if (warp == 0) {
+    if (elect_one()) {
+      auto l2_prefetch = [&](int c) {
+        const int64_t row0 = s0 + (int64_t)c * kCB;
+        tma_prefetch_l2_3d(&tmQ, 0, (int)(grp * prm.N + row0), 0);
+        tma_prefetch_l2_3d(&tmW, 0, (int)(grp * kD), (int)(row0 / 64));
+        tma_prefetch_l2_3d(&tmO, 0, (int)(grp * kD), (int)(row0 / 64));
+      };
+      for (int c = 0; c < 2 * kAStages && c < nc; ++c) l2_prefetch(c);
+      for (int c = 0; c < nc; ++c) {
+        const int s = c % kAStages;
+        if (c + 2 * kAStages < nc) l2_prefetch(c + 2 * kAStages);
+        if (c >= kAStages) mbar_wait(&empty[s], ((c / kAStages) & 1) ^ 1);
+        const int64_t row0 = s0 + (int64_t)c * kCB;
+        uint8_t* st = smem + s * kAStage;
+        mbar_expect_tx(&full[s], 3 * kT64);
+        tma_load_3d(st, &tmQ, &full[s], 0, (int)(grp * prm.N + row0), 0);
+        tma_load_3d(st + kAOffW, &tmW, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
+        tma_load_3d(st + kAOffO, &tmO, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t f = kBF16 ? 1 : 0;
+    const uint32_t id_RT = idesc_f16(128, 144, f, 0, 1);  // A = W_hat^T (K-major), B = [Q | 1] (MN-major)
+    const uint32_t id_U = idesc_f16(128, 16, f, 1, 0);    // A = Q^T (MN-major), B = s rows (K-major)
+    for (int c = 0; c < nc; ++c) {
+      const int s = c % kAStages;
+      const uint32_t st = smem_u32(smem + s * kAStage);
+      mbar_wait(w_ready, c & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        for (int ks = 0; ks < 4; ++ks)
+          mma_ss(tmem, kd(st + kAOffW, ks, 128), mn(st, ks, 8192), id_RT, (c > 0 || ks > 0) ? 1u : 0u);
+        for (int ks = 0; ks < 4; ++ks)
+          mma_ss(tmem + 160, mn(st, ks, 8192), kd(st + kAOffS, ks, 16), id_U, (c > 0 || ks > 0) ? 1u : 0u);
+        mma_commit(&empty[s]);
+        if (c == nc - 1) mma_commit(done);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int et = (int)threadIdx.x - 64;        // 0..255
+    const int half = et >> 7, eh = et & 127;
+    const uint32_t qd = warp & 3;
+    const int r = (int)(qd * 32 + lane_id());
+    const int jg = eh & 15, ig = 2 * (eh >> 5) + ((eh & 31) >> 4);  // what_pass_half's mapping
+    float4 g8[2];
+    auto g_prefetch = [&](int c) {
+      const float* gp = prm.g + grp * prm.N + s0 + (int64_t)c * kCB + 8 * ig;
+      g8[0] = __ldg((const float4*)gp);
+      g8[1] = __ldg((const float4*)(gp + 4));
+    };
+    if (nc > 0) g_prefetch(0);
+    for (int c = 0; c < nc; ++c) {
+      const int s = c % kAStages;
+      uint8_t* st = smem + s * kAStage;
+      float* sp = s_part + (c & 1) * 2 * kCB;
+      mbar_wait(&full[s], (c / kAStages) & 1);
+      uint4 o4[4];
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr)
+        o4[rr] = *(const uint4*)(st + kAOffO + sw128_off(64 * half + 16 * rr + jg, 8 * ig, 128));
+      const float4 gc[2] = {g8[0], g8[1]};
+      if (c + 1 < nc) g_prefetch(c + 1);
+      what_pass_half<kBF16>(st + kAOffW, o4, gc, sp + half * kCB, eh, 64 * half);
+      named_bar(1, 256);  // both halves' partial s of chunk c are in s_part
+      if (et < kCB) {     // s rows (hi, lo) of the U = Q^T s MMA
+        const float si = sp[et] + sp[kCB + et];
+        uint16_t hv, lv;
+        if (kBF16) {
+          const __nv_bfloat16 h = __float2bfloat16_rn(si);
+          hv = __bfloat16_as_ushort(h);
+          lv = __bfloat16_as_ushort(__float2bfloat16_rn(si - __bfloat162float(h)));
+        } else {
+          const __half h = __float2half_rn(si);
+          hv = __half_as_ushort(h);
+          lv = __half_as_ushort(__float2half_rn(si - __half2float(h)));
+        }
+        *(uint16_t*)(st + kAOffS + sw128_off(0, et, 16)) = hv;
+        *(uint16_t*)(st + kAOffS + sw128_off(1, et, 16)) = lv;
+      }
+      fence_proxy_async();
+      mbar_arrive(w_ready);
+    }
+    if (half == 0) {  // records: R (X[m][j]), u, c, count
+      float* rR = prm.stR + (grp * prm.P + p) * state_floats(kD);
+      const uint32_t lb = (qd * 32u) << 16;
+      if (nc > 0) {
+        mbar_wait(done, 0);
+        tc_fence_after();
+        for (int m0 = 0; m0 < kD; m0 += 32) {  // lane r = j of R^T: column j of X
+          uint32_t x[32];
+          tmem_ld32(tmem + lb + m0, x);
+          tmem_ld_wait();
+#pragma unroll
+          for (int u = 0; u < 32; ++u) rR[(m0 + u) * kD + r] = __uint_as_float(x[u]);
+        }
+        uint32_t cc, c1, u0, u1;
+        tmem_ld2(tmem + lb + 128, cc, c1);
+        tmem_ld2(tmem + lb + 160, u0, u1);
+        tmem_ld_wait();
+        rR[kD * kD + r] = __uint_as_float(u0) + __uint_as_float(u1);  // u_m (lane r = m of U)
+        rR[kD * kD + kD + r] = __uint_as_float(cc);                   // c_j
+      } else {
+        for (int m = 0; m < kD; ++m) rR[m * kD + r] = 0.f;
+        rR[kD * kD + r] = 0.f;
+        rR[kD * kD + kD + r] = 0.f;
+      }
+      if (r == 0) rR[kD * kD + 2 * kD] = (float)(s1 - s0);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<256>(tmem);
+}
+
 // ================================================================ main reverse sweep
 // Warp roles (320 threads): 0 TMA producer; 1 MMA issuer + TMEM owner;
 // 2-5 WG-A: W_hat/s, dS/P, dK^T/dV^T out, u/c; 6-9 WG-B: bR/bS operand copies,
@@ -965,8 +1141,9 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
   float* stS = ws.base;
   float* stR = stS + G * P * A * SZ;
   float* cmb = stR + G * P * A * SZ;
-  CUtensorMap mQ, mK, mV, mW;
-  if (!make_tma_map(&mQ, t.q, bf, (uint64_t)(G * N), kD, 64, 2) ||
+  CUtensorMap mQ, mK, mV, mW, mO;
+  if (!make_tma_map(&mO, t.o, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1) ||
+      !make_tma_map(&mQ, t.q, bf, (uint64_t)(G * N), kD, 64, 2) ||
       !make_tma_map(&mK, t.k, bf, (uint64_t)(G * N), kD, 64, 2) ||
       !make_tma_map(&mV, t.v, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1) ||
       !make_tma_map(&mW, t.w, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1))
@@ -988,7 +1165,13 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
   cudaFuncSetAttribute(agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggSmemB);
   cudaFuncSetAttribute(main_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmemB);
   int launches = 1;
-  if (P - p0 > 0) {
+  if (P - p0 > 0 && use_saved) {
+    auto aggR = bf ? k_bwd_aggR_tc<true> : k_bwd_aggR_tc<false>;
+    cudaFuncSetAttribute(aggR, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggRSmem);
+    ProfScope ps("la_bwd_agg", L.stream);
+    aggR<<<dim3(A * (P - p0), G), 320, kAggRSmem, L.stream>>>(mQ, mW, mO, pa);
+    launches += 1;
+  } else if (P - p0 > 0) {
     ProfScope ps("la_bwd_agg", L.stream);
     agg<<<dim3(A * (P - p0), G), 192, kAggSmemB, L.stream>>>(mQ, mK, mV, mW, pa);
     launches += 1;

@@ -110,12 +110,13 @@ def test_backward_argument_errors():
 
 def test_workspace_is_flat_in_sequence_length():
     # O(ND) memory: the forward workspace holds per-(group, segment) state records
-    # only (segment sums + combined prefixes), bounded by 2 * G * 64 segments * state
-    # size whatever N is (test_backward.cpp:329-347 "backward memory bound is flat in N").
+    # only (sums of at most 8 units per segment + combined prefixes), bounded by
+    # 9 * G * 64 segments * state size whatever N is (test_backward.cpp:329-347
+    # "backward memory bound is flat in N").
     lib = _abi.lib()
     G, D = 64, 128
     sz = (D * D + 2 * D + 1 + 3) // 4 * 4
-    bound = 256 + 4 * 2 * G * 64 * sz
+    bound = 256 + 4 * 9 * G * 64 * sz
     for n in (1 << 16, 1 << 18, 1 << 20, 1 << 22):
         p = _abi.make_problem(G, n, D, "bf16")
         assert lib.la_forward_workspace_bytes(C.byref(p)) <= bound
