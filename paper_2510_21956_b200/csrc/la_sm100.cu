@@ -108,11 +108,13 @@ __device__ __forceinline__ uint64_t mn64(uint32_t tile, int ks, uint32_t panel) 
 template <bool kBF16>
 __global__ void __launch_bounds__(448, 1)
     k_fwd_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-             const __grid_constant__ CUtensorMap tmV, FwdParams prm) {
+             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+             FwdParams prm) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sP = smem + kFStages * kFStage;   // [2][8K]   P' (rows i, cols t)
-  uint64_t* bars = (uint64_t*)(sP + 2 * 8192);
+  uint8_t* sO = sP + 2 * 8192;               // [2][16K]  o^T staging (rows j, cols i) for TMA stores
+  uint64_t* bars = (uint64_t*)(sO + 2 * kFT);
   uint64_t* full = bars;            // [3]
   uint64_t* empty = bars + 3;       // [3]
   uint64_t* t1_full = bars + 6;
@@ -138,6 +140,7 @@ __global__ void __launch_bounds__(448, 1)
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
+    tma_prefetch(&tmO);
     for (int s = 0; s < kFStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1 + 2 * 128);  // M2 commit, WG-B (V), WG-S (K)
@@ -482,11 +485,22 @@ __global__ void __launch_bounds__(448, 1)
       }
       if (eb == 0) trace(2, c, 3);
       // o^T row j = r, columns [row0, row0 + 64): one 128-byte line per thread
-      uint4* dst = (uint4*)((uint16_t*)prm.out + (grp * kD + r) * prm.N + row0);
+      // o^T rows j, columns [row0, row0 + 64) -> staging buffer bb -> one TMA store
+      if (eb == 0) tma_store_wait_read1();  // the store issued two chunks ago has left buffer bb
+      named_bar(2, 128);
+      uint8_t* so = sO + bb * kFT;
 #pragma unroll
-      for (int w = 0; w < 8; ++w) dst[w] = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
+      for (int w = 0; w < 8; ++w)
+        *(uint4*)(so + sw128_off(r, 8 * w, kD)) = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
+      fence_proxy_async();
+      named_bar(2, 128);
+      if (eb == 0) {
+        tma_store_3d(&tmO, so, 0, (int)(grp * kD), (int)(row0 / 64));
+        tma_store_commit();
+      }
       if (eb == 0) trace(2, c, 4);
     }
+    if (eb == 0) tma_store_wait0();
     if (prm.st_out && nc > 0) prm.st_out[(grp * prm.P + p) * state_floats(kD) + kD * kD + kD + r] = sigma;
   }
   tc_fence_before();
@@ -608,7 +622,7 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc<128>(tmem);
 }
 
-constexpr size_t kFwdSmem = kFStages * kFStage + 2 * 8192 + 256 + (4 * kCF + kD) * 4 + 1024;
+constexpr size_t kFwdSmem = kFStages * kFStage + 2 * 8192 + 2 * kFT + 256 + (4 * kCF + kD) * 4 + 1024;
 constexpr size_t kAggSmem = 4 * kTile + 128 + 1024;
 
 }  // namespace
@@ -650,11 +664,12 @@ cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, W
   const int P = tc_segments(G, N);
   const int64_t chunks = N / kC;
   const int64_t seg = ((chunks + P - 1) / P) * kC;
-  CUtensorMap mK, mV, mQ64, mK64, mV64;
+  CUtensorMap mK, mV, mQ64, mK64, mV64, mO64;
   if (!make_map(&mK, t.k, bf, (uint64_t)(G * N), kD) || !make_map(&mV, t.v, bf, (uint64_t)(G * kD), (uint64_t)N) ||
       !make_tma_map(&mQ64, t.q, bf, (uint64_t)(G * N), kD, 64, 2) ||
       !make_tma_map(&mK64, t.k, bf, (uint64_t)(G * N), kD, 64, 1) ||
-      !make_tma_map(&mV64, t.v, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1))
+      !make_tma_map(&mV64, t.v, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1) ||
+      !make_tma_map(&mO64, out, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1))
     return cudaErrorInvalidValue;
   auto main_k = bf ? k_fwd_tc<true> : k_fwd_tc<false>;
   cudaFuncSetAttribute(main_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem);
@@ -677,7 +692,7 @@ cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, W
   FwdParams prm{agg_st, A, L.carry_prefix, cmb, g, ws.flag, N, G, seg, P, L.row_offset, L.a, L.b, saved, out};
   {
     ProfScope ps("la_fwd_causal", L.stream);
-    main_k<<<dim3(P, G), 448, kFwdSmem, L.stream>>>(mQ64, mK64, mV64, prm);
+    main_k<<<dim3(P, G), 448, kFwdSmem, L.stream>>>(mQ64, mK64, mV64, mO64, prm);
   }
   note_launch(launches);
   return cudaGetLastError();
