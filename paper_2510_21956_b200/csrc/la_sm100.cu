@@ -69,6 +69,7 @@ struct FwdParams {
   float a, b;
   float* st_out;        // per-(group, segment) end state (S, z, sigma, rows) for the backward, or null
   void* out;            // o, FeatureMajor [G][D][N]
+  int pf;               // chunks prefetched into L2 ahead of the ring
 };
 
 // ================================================================ forward main
@@ -88,7 +89,8 @@ constexpr int kCF = 64;                  // forward chunk rows
 constexpr int kFT = 16384;               // 64x128 / 128x64 16-bit tile
 constexpr int kKPanel = 80 * 128;        // K-tile panel: 64 key rows + 16 z rows
 constexpr int kFStages = 3;
-constexpr int kFPrefetch = 6;            // chunks of Q/K/V prefetched into L2 ahead of the ring
+constexpr int kFPrefetch = 0;            // L2 prefetch distance (chunks) ahead of the ring: measured
+                                         // to cost extra DRAM re-reads at 148 CTAs, so off (LA_PREFETCH)
 constexpr int kFStage = kFT + 2 * kKPanel + kFT;  // Q, K(+z), V^T  = 52 KB
 constexpr int kOffK = kFT, kOffV = kFT + 2 * kKPanel;
 constexpr uint32_t kF_T1 = 0, kF_OT = 128, kF_ST = 256, kF_SB = 384;
@@ -181,10 +183,10 @@ __global__ void __launch_bounds__(448, 1)
         tma_prefetch_l2_3d(&tmK, 0, (int)(grp * prm.N + row0), 1);
         tma_prefetch_l2_3d(&tmV, 0, (int)(grp * kD), (int)(row0 / 64));
       };
-      for (int c = 0; c < kFPrefetch && c < nc; ++c) l2_prefetch(c);
+      for (int c = 0; c < prm.pf && c < nc; ++c) l2_prefetch(c);
       for (int c = 0; c < nc; ++c) {
         const int s = c % kFStages;
-        if (c + kFPrefetch < nc) l2_prefetch(c + kFPrefetch);
+        if (c + prm.pf < nc) l2_prefetch(c + prm.pf);
         if (lane_id() == 0) trace(3, c, 0);
         if (c >= kFStages) mbar_wait(&empty[s], ((c / kFStages) & 1) ^ 1);
         trace(3, c, 1);
@@ -689,7 +691,9 @@ cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, W
     const float hdr[kSavedHeader] = {kSavedMagic, (float)G, (float)N, (float)kD, (float)P, (float)seg};
     cudaMemcpyAsync(L.saved_out, hdr, sizeof(hdr), cudaMemcpyHostToDevice, L.stream);
   }
-  FwdParams prm{agg_st, A, L.carry_prefix, cmb, g, ws.flag, N, G, seg, P, L.row_offset, L.a, L.b, saved, out};
+  const char* pfe = getenv("LA_PREFETCH");
+  FwdParams prm{agg_st, A, L.carry_prefix, cmb, g, ws.flag, N, G, seg, P, L.row_offset, L.a, L.b, saved, out,
+                pfe ? atoi(pfe) : kFPrefetch};
   {
     ProfScope ps("la_fwd_causal", L.stream);
     main_k<<<dim3(P, G), 448, kFwdSmem, L.stream>>>(mQ64, mK64, mV64, mO64, prm);

@@ -38,7 +38,7 @@ constexpr int kCB = 64;   // chunk rows
 constexpr int kD = 128;   // head dim
 constexpr int kT64 = 16384;  // a 64x128 or 128x64 16-bit tile
 constexpr int kStage = 4 * kT64;  // Q, K, V^T, Omega^T
-constexpr int kBPrefetch = 4;     // chunks prefetched into L2 ahead of the 2-stage ring
+constexpr int kBPrefetch = 0;     // L2 prefetch distance (chunks): off by default, see la_sm100.cu
 constexpr uint32_t kDP = 0, kDQ = 64, kDK = 128, kDV = 192, kR = 256, kS = 384;
 constexpr uint32_t kHalf = 16u << 16;  // TMEM lane offset of the upper M=64 half
 
@@ -98,6 +98,7 @@ struct BwdParams {
   const float* carry_pre;  // sequence-shard carries (or null)
   const float* carry_suf;
   float* cmb;  // per (g, segment) combined [S inclusive prefix | R exclusive suffix]
+  int pf;      // chunks prefetched into L2 ahead of the ring
 };
 
 // Epilogue step E0: W_hat = omega / g in place (bf16) and s_i = sum_j o_ij w_hat_ij.
@@ -437,10 +438,10 @@ __global__ void __launch_bounds__(320, 1)
         tma_prefetch_l2_3d(&tmW, 0, (int)(grp * kD), (int)(row0 / 64));
         tma_prefetch_l2_3d(&tmO, 0, (int)(grp * kD), (int)(row0 / 64));
       };
-      for (int c = 0; c < 2 * kAStages && c < nc; ++c) l2_prefetch(c);
+      for (int c = 0; c < prm.pf && c < nc; ++c) l2_prefetch(c);
       for (int c = 0; c < nc; ++c) {
         const int s = c % kAStages;
-        if (c + 2 * kAStages < nc) l2_prefetch(c + 2 * kAStages);
+        if (c + prm.pf < nc) l2_prefetch(c + prm.pf);
         if (c >= kAStages) mbar_wait(&empty[s], ((c / kAStages) & 1) ^ 1);
         const int64_t row0 = s0 + (int64_t)c * kCB;
         uint8_t* st = smem + s * kAStage;
@@ -682,10 +683,10 @@ __global__ void __launch_bounds__(320, 1)
         tma_prefetch_l2_3d(&tmV, 0, (int)(grp * kD), (int)(row0 / 64));
         tma_prefetch_l2_3d(&tmW, 0, (int)(grp * kD), (int)(row0 / 64));
       };
-      for (int n = 0; n < kBPrefetch && n < nc; ++n) l2_prefetch(n);
+      for (int n = 0; n < prm.pf && n < nc; ++n) l2_prefetch(n);
       for (int n = 0; n < nc; ++n) {
         const int s = n & 1;
-        if (n + kBPrefetch < nc) l2_prefetch(n + kBPrefetch);
+        if (n + prm.pf < nc) l2_prefetch(n + prm.pf);
         if (n >= 2) mbar_wait(&empty[s], ((n >> 1) & 1) ^ 1);
         const int64_t row0 = s0 + (int64_t)(nc - 1 - n) * kCB;
         uint8_t* st = smem + s * kStage;
@@ -1154,7 +1155,8 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
   // S sum is needed for the inclusive prefix. The aggregate runs on units of
   // seg / A rows; the main kernel's prologue sums the unit records.
   BwdParams prm{t.o, t.g, dq, dk, dv, use_saved ? const_cast<float*>(sv + kSavedHeader) : stS, stR, N, seg, P,
-                L.a, L.b, dbg ? atoi(dbg) : 0, use_saved ? 1 : 0, 0, A, L.carry_prefix, L.carry_suffix, cmb};
+                L.a, L.b, dbg ? atoi(dbg) : 0, use_saved ? 1 : 0, 0, A, L.carry_prefix, L.carry_suffix, cmb,
+                getenv("LA_PREFETCH") ? atoi(getenv("LA_PREFETCH")) : kBPrefetch};
   BwdParams pa = prm;  // aggregate launch: unit geometry
   pa.stS = stS;
   pa.seg_len = seg / A;
