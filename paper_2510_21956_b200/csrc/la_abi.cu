@@ -279,6 +279,13 @@ thread_local Arena t_arena;
 // Host-buffer training step (la_host_step): the groups are cut into blocks and
 // each block's H2D copy, fwd+bwd, and D2H copy run on their own streams through
 // a ring of device slots, so PCIe traffic in both directions overlaps compute.
+// Up to this many group blocks per step: more blocks shorten the pipeline's fill
+// (first H2D) and drain (last D2H), which are the only unoverlapped copies.
+int kHostBlocks = [] {
+  const char* e = getenv("LA_HOST_BLOCKS");
+  return e ? (atoi(e) > 0 ? atoi(e) : 16) : 16;
+}();
+
 struct HostPipe {
   static constexpr int R = 3;
   cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
@@ -630,7 +637,7 @@ la_status la_host_step(const la_problem* p, const void* q, la_layout lq, const v
   if (!layout_ok(lq) || !layout_ok(lk) || !layout_ok(lv) || !layout_ok(lw))
     return fail(err, LA_ERR_INVALID_ARGUMENT, "unknown layout");
   const int64_t G = p->groups, N = p->seq_len, D = p->dim;
-  const int64_t Gb = (G + 7) / 8;  // up to 8 blocks of whole groups
+  const int64_t Gb = (G + kHostBlocks - 1) / kHostBlocks;  // blocks of whole groups
   const int nb = (int)((G + Gb - 1) / Gb);
   la_problem pb = *p;
   pb.groups = Gb;

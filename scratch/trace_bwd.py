@@ -20,15 +20,10 @@ buf = (C.c_ulonglong * (4 * 64 * 10))()
 L.la_internal_trace_read_bwd(buf)
 t = np.array(buf, dtype=np.int64).reshape(4, 64, 10)
 t0 = t[0, 10, 0]
-t = t - t0
-t[t < -10**9] = -1
-R = range(10, 14)
-print("MMA : start, full+dpt_empty, w_ready, sR_ready, sS_ready, ps_ready, gr_empty, issued-all")
-for c in R: print(c, t[0, c, :8].tolist())
-print("WG-A: start, E_R done, dV(n) out [logged at n], aux ready(w_ready passed), aux done")
-for c in R: print(c, t[1, c, :5].tolist())
-print("WG-B: start, E_S done, qk_out(n) done")
-for c in R: print(c, t[2, c, :3].tolist())
-print("WG-C: dpt_full, gr_full(n-1) passed, ps_ready, e0(n+1) done")
-for c in R: print(c, t[3, c, :4].tolist())
+print("MMA: start,full,dpt_empty,w_ready,sS_ready,ps_ready,gr_empty,sR_ready")
+for c in range(10, 14): print(c, (t[0, c, :8] - t0).tolist())
+print("WGA: start,after dv_out(n-1),sR_ready,dpt_full,ps_ready,after du/dc,after E0(n+1)")
+for c in range(10, 14): print(c, (t[1, c, :7] - t0).tolist())
+print("WGB: start,after qk_out(n-1),after s_full wait,sS_ready,after z,after E0(n+1)")
+for c in range(10, 14): print(c, (t[2, c, :6] - t0).tolist())
 print("period", np.diff(t[0, 5:60, 0]).mean())
