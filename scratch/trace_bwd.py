@@ -20,10 +20,15 @@ buf = (C.c_ulonglong * (4 * 64 * 10))()
 L.la_internal_trace_read_bwd(buf)
 t = np.array(buf, dtype=np.int64).reshape(4, 64, 10)
 t0 = t[0, 10, 0]
-print("MMA: start,full,dpt_empty,w_ready,sS_ready,ps_ready,gr_empty,sR_ready")
-for c in range(10, 14): print(c, (t[0, c, :8] - t0).tolist())
-print("WGA: start,after dv_out(n-1),sR_ready,dpt_full,ps_ready,after du/dc,after E0(n+1)")
-for c in range(10, 14): print(c, (t[1, c, :7] - t0).tolist())
-print("WGB: start,after qk_out(n-1),after s_full wait,sS_ready,after z,after E0(n+1)")
-for c in range(10, 14): print(c, (t[2, c, :6] - t0).tolist())
+t = t - t0
+t[t < -10**9] = -1
+R = range(10, 14)
+print("MMA : start, sS_ready, ps_ready, dQ+T(n+1) issued, sR_ready, v_empty, all issued")
+for c in R: print(c, t[0, c, :7].tolist())
+print("WG-A: E_R(n) done, dV(n) out, dc+e0(n+1) done")
+for c in R: print(c, t[1, c, :3].tolist())
+print("WG-B: dQ(n) out, E_S(n) done, dK(n) out, z/du(n) done")
+for c in R: print(c, t[2, c, :4].tolist())
+print("WG-C: t_full(n), v_full(n-1) passed, ps_ready, e0(n+1) done")
+for c in R: print(c, t[3, c, :4].tolist())
 print("period", np.diff(t[0, 5:60, 0]).mean())
