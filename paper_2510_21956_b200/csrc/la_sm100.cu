@@ -28,7 +28,9 @@ using namespace sm100;
 // chunk and event; read back with la_internal_trace_read (not part of the ABI).
 __device__ unsigned long long g_trace[4][64][8];
 __device__ __forceinline__ void trace(int role, int c, int ev) {
+#ifdef LA_TRACE  // compiled out by default: the kernels are I-cache sensitive
   if (blockIdx.x == 0 && blockIdx.y == 0 && c < 64) g_trace[role][c][ev] = clock64();
+#endif
 }
 
 namespace {
