@@ -909,7 +909,7 @@ __global__ void __launch_bounds__(320, 1)
       {
         const int mg = et >> 3, tg = et & 7;  // rows tg + 8k: conflict-free quarter-warps
         float du[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
+#pragma unroll 2
         for (int k8 = 0; k8 < kCB / 8; ++k8) {
           const int i = tg + 8 * k8;
           const uint4 v4 = *(const uint4*)(q_t + sw128_off(i, 8 * mg, kCB));
@@ -937,7 +937,7 @@ __global__ void __launch_bounds__(320, 1)
       // ---- dc_j = sum_i w_hat_ji (added to c after this chunk's dV^T is out)
       {
         float dc = 0.f;
-#pragma unroll
+#pragma unroll 2
         for (int i8 = 0; i8 < kCB; i8 += 8) {
           const uint4 v4 = *(const uint4*)(w_t + sw128_off(r, i8, 128));
           const uint32_t w4[4] = {v4.x, v4.y, v4.z, v4.w};
@@ -1068,7 +1068,7 @@ __global__ void __launch_bounds__(320, 1)
       {
         const int mg = eb >> 3, tg = eb & 7;  // columns 8 mg.., rows tg + 8 k
         float zs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
+#pragma unroll 2
         for (int k8 = 0; k8 < kCB / 8; ++k8) {
           const uint4 v4 = *(const uint4*)(k_t + sw128_off(tg + 8 * k8, 8 * mg, kCB));
           const uint32_t xx[4] = {v4.x, v4.y, v4.z, v4.w};
