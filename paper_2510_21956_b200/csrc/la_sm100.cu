@@ -50,11 +50,11 @@ bool make_map(CUtensorMap* m, const void* base, bool bf16, uint64_t rows, uint64
 
 // K-major SW128 descriptor for k-step ks (16 elements) of a 128-row tile.
 __device__ __forceinline__ uint64_t kdesc(uint32_t tile, int ks) {
-  return sdesc_sw128(tile + (ks >> 2) * kPanel + (ks & 3) * 32, 16, 1024);
+  return sdesc_sw128(tile, 16, 1024) + (uint64_t)(((ks >> 2) * kPanel + (ks & 3) * 32) >> 4);
 }
 // MN-major SW128 descriptor for k-step ks: K rows of 128 B, MN panels kPanel apart.
 __device__ __forceinline__ uint64_t mndesc(uint32_t tile, int ks) {
-  return sdesc_sw128(tile + ks * 2048, kPanel, 1024);
+  return sdesc_sw128(tile, kPanel, 1024) + (uint64_t)((ks * 2048) >> 4);
 }
 
 struct FwdParams {
@@ -103,10 +103,10 @@ __device__ __forceinline__ float h2f_fwd(uint16_t h) {
 }
 
 __device__ __forceinline__ uint64_t kd64(uint32_t tile, int ks, uint32_t rows) {
-  return sdesc_sw128(tile + (ks >> 2) * rows * 128 + (ks & 3) * 32, 16, 1024);
+  return sdesc_sw128(tile, 16, 1024) + (uint64_t)(((ks >> 2) * rows * 128 + (ks & 3) * 32) >> 4);
 }
 __device__ __forceinline__ uint64_t mn64(uint32_t tile, int ks, uint32_t panel) {
-  return sdesc_sw128(tile + ks * 2048, panel, 1024);
+  return sdesc_sw128(tile, panel, 1024) + (uint64_t)((ks * 2048) >> 4);
 }
 
 template <bool kBF16>

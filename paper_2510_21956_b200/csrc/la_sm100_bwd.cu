@@ -46,12 +46,14 @@ constexpr uint32_t kHalf = 16u << 16;  // TMEM lane offset of the upper M=64 hal
 
 // descriptors ---------------------------------------------------------------
 // K-major tile with `rows` rows and 64-column panels `rows*128` bytes apart.
+// The tile's base descriptor plus the k-step's byte offset (>> 4) in the start-address
+// field: the base is common to a whole MMA chain, so each MMA costs one add (small hot code).
 __device__ __forceinline__ uint64_t kd(uint32_t tile, int ks, uint32_t rows) {
-  return sdesc_sw128(tile + (ks >> 2) * rows * 128 + (ks & 3) * 32, 16, 1024);
+  return sdesc_sw128(tile, 16, 1024) + (uint64_t)(((ks >> 2) * rows * 128 + (ks & 3) * 32) >> 4);
 }
 // MN-major tile: K rows of 128 B (16 per k-step), MN panels `panel` bytes apart.
 __device__ __forceinline__ uint64_t mn(uint32_t tile, int ks, uint32_t panel) {
-  return sdesc_sw128(tile + ks * 2048, panel, 1024);
+  return sdesc_sw128(tile, panel, 1024) + (uint64_t)((ks * 2048) >> 4);
 }
 
 // Per-warp transpose of 32 row segments (128 B each) through a 4 KB smem scratch
