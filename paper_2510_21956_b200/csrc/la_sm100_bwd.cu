@@ -176,15 +176,27 @@ __device__ __forceinline__ void what_pass_half(uint8_t* w_t, const uint4 (&o4)[4
     }
     *p = make_uint4(res[0], res[1], res[2], res[3]);
   }
+  // Reduce-scatter of the 8 partial sums over the 16 lanes sharing ig: each exchange
+  // step halves the values a lane keeps (8 shuffles instead of 32). Afterwards lanes
+  // jg and jg^1 hold the full sum of value (jg >> 1).
+  const bool b3 = (jg & 8) != 0, b2 = (jg & 4) != 0, b1 = (jg & 2) != 0;
+  float s4[4], s2v[2], s1v;
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
+  for (int k = 0; k < 4; ++k) {
+    const float mine = b3 ? sp[4 + k] : sp[k], other = b3 ? sp[k] : sp[4 + k];
+    s4[k] = mine + __shfl_xor_sync(0xffffffffu, other, 8);
+  }
 #pragma unroll
-    for (int off = 1; off < 16; off <<= 1) sp[u] += __shfl_xor_sync(0xffffffffu, sp[u], off);
+  for (int k = 0; k < 2; ++k) {
+    const float mine = b2 ? s4[2 + k] : s4[k], other = b2 ? s4[k] : s4[2 + k];
+    s2v[k] = mine + __shfl_xor_sync(0xffffffffu, other, 4);
   }
-  if (jg == 0) {
-    *(float4*)(s_half + 8 * ig) = make_float4(sp[0], sp[1], sp[2], sp[3]);
-    *(float4*)(s_half + 8 * ig + 4) = make_float4(sp[4], sp[5], sp[6], sp[7]);
+  {
+    const float mine = b1 ? s2v[1] : s2v[0], other = b1 ? s2v[0] : s2v[1];
+    s1v = mine + __shfl_xor_sync(0xffffffffu, other, 2);
   }
+  s1v += __shfl_xor_sync(0xffffffffu, s1v, 1);
+  if ((jg & 1) == 0) s_half[8 * ig + (jg >> 1)] = s1v;
 }
 
 template <bool kBF16>
