@@ -393,16 +393,7 @@ __global__ void __launch_bounds__(448, 1)
           zs[0] += f0.x; zs[1] += f0.y; zs[2] += f1.x; zs[3] += f1.y;
           zs[4] += f2.x; zs[5] += f2.y; zs[6] += f3.x; zs[7] += f3.y;
         }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          zs[u] += __shfl_xor_sync(0xffffffffu, zs[u], 1);
-          zs[u] += __shfl_xor_sync(0xffffffffu, zs[u], 2);
-          zs[u] += __shfl_xor_sync(0xffffffffu, zs[u], 4);
-        }
-        if (tg == 0) {
-          *(float4*)(zx + 8 * mg) = make_float4(zs[0], zs[1], zs[2], zs[3]);
-          *(float4*)(zx + 8 * mg + 4) = make_float4(zs[4], zs[5], zs[6], zs[7]);
-        }
+        zx[8 * mg + tg] = reduce_scatter8(zs, tg);
         mbar_arrive(&empty[s]);  // WG-S is done with K(c)
         named_bar(3, 128);
         zr += zx[r];

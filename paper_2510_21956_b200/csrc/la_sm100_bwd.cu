@@ -936,17 +936,7 @@ __global__ void __launch_bounds__(320, 1)
             du[2 * q + 1] += w * f2.y;
           }
         }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          du[q] += __shfl_xor_sync(0xffffffffu, du[q], 1);
-          du[q] += __shfl_xor_sync(0xffffffffu, du[q], 2);
-          du[q] += __shfl_xor_sync(0xffffffffu, du[q], 4);
-        }
-        if (tg == 0) {
-          float* dst = du_s + (n & 3) * kD + 8 * mg;
-          *(float4*)dst = make_float4(du[0], du[1], du[2], du[3]);
-          *(float4*)(dst + 4) = make_float4(du[4], du[5], du[6], du[7]);
-        }
+        du_s[(n & 3) * kD + 8 * mg + tg] = reduce_scatter8(du, tg);
       }
       // ---- dc_j = sum_i w_hat_ji (added to c after this chunk's dV^T is out)
       {
@@ -1093,18 +1083,9 @@ __global__ void __launch_bounds__(320, 1)
             zs[2 * q + 1] += f2.y;
           }
         }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          zs[q] += __shfl_xor_sync(0xffffffffu, zs[q], 1);
-          zs[q] += __shfl_xor_sync(0xffffffffu, zs[q], 2);
-          zs[q] += __shfl_xor_sync(0xffffffffu, zs[q], 4);
-        }
-        if (tg == 0) {
-          const float* zin = zbuf + ((n - 1) & 1) * kD + 8 * mg;
-          float* zout = zbuf + (n & 1) * kD + 8 * mg;
-          const float4 za = *(const float4*)zin, zb = *(const float4*)(zin + 4);
-          *(float4*)zout = make_float4(za.x - zs[0], za.y - zs[1], za.z - zs[2], za.w - zs[3]);
-          *(float4*)(zout + 4) = make_float4(zb.x - zs[4], zb.y - zs[5], zb.z - zs[6], zb.w - zs[7]);
+        {
+          const int m = 8 * mg + tg;
+          zbuf[(n & 1) * kD + m] = zbuf[((n - 1) & 1) * kD + m] - reduce_scatter8(zs, tg);
         }
         named_bar(2, 128);
       }

@@ -257,5 +257,19 @@ __device__ __forceinline__ float2 unpack2(uint32_t v) {
   return __half22float2(h);
 }
 
+// Reduce-scatter of 8 per-lane partial sums over the 8 lanes that differ in lane bits
+// 0..2 (t = lane & 7): returns the full sum of value t (7 shuffles instead of 24).
+__device__ __forceinline__ float reduce_scatter8(const float (&v)[8], int t) {
+  const bool b2 = (t & 4) != 0, b1 = (t & 2) != 0, b0 = (t & 1) != 0;
+  float s4[4], s2[2];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    s4[k] = (b2 ? v[4 + k] : v[k]) + __shfl_xor_sync(0xffffffffu, b2 ? v[k] : v[4 + k], 4);
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+    s2[k] = (b1 ? s4[2 + k] : s4[k]) + __shfl_xor_sync(0xffffffffu, b1 ? s4[k] : s4[2 + k], 2);
+  return (b0 ? s2[1] : s2[0]) + __shfl_xor_sync(0xffffffffu, b0 ? s2[0] : s2[1], 1);
+}
+
 }  // namespace sm100
 }  // namespace lab
