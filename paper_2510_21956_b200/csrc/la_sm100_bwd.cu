@@ -887,6 +887,7 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_after();
       {
         const float si = sA[ih] + sB[ih];
+        const float alpha = upper ? a : -b * si;
         uint8_t* dst = upper ? sP : sdS;
 #pragma unroll 1
         for (int t0 = 0; t0 < kCB; t0 += 32) {
@@ -900,14 +901,9 @@ __global__ void __launch_bounds__(320, 1)
             for (int q = 0; q < 4; ++q) {
               const int t = t0 + 8 * w8 + 2 * q;
               const float x0 = __uint_as_float(x[8 * w8 + 2 * q]), x1 = __uint_as_float(x[8 * w8 + 2 * q + 1]);
-              float v0, v1;
-              if (upper) {
-                v0 = t <= ih ? a + b * x0 : 0.f;
-                v1 = t + 1 <= ih ? a + b * x1 : 0.f;
-              } else {
-                v0 = t <= ih ? b * (x0 - si) : 0.f;
-                v1 = t + 1 <= ih ? b * (x1 - si) : 0.f;
-              }
+              // P = a + b T1 (upper lanes), dS = b dPt - b s (lower lanes): one FFMA, no divergence
+              const float v0 = t <= ih ? fmaf(b, x0, alpha) : 0.f;
+              const float v1 = t + 1 <= ih ? fmaf(b, x1, alpha) : 0.f;
               pk[q] = pack2<kBF16>(v0, v1);
             }
             *(uint4*)(dst + sw128_off(ih, t0 + 8 * w8, kCB)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
