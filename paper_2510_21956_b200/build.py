@@ -20,6 +20,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-v" if os.environ.get("LA_PTXAS_VERBOSE") else "-O3"]
+if os.environ.get("LA_TRACE"):  # clock64 pipeline traces (diagnostics, la_internal_trace_read*)
+    FLAGS.append("-DLA_TRACE")
 
 
 def _newest(paths):

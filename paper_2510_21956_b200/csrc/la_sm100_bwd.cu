@@ -567,22 +567,6 @@ __global__ void __launch_bounds__(320, 1)
 // 2-5 WG-A: W_hat/s, dS/P, dK^T/dV^T out, u/c; 6-9 WG-B: bR/bS operand copies,
 // z, dQ out. Each epilogue column sum uses 16-byte loads over a conflict-free
 // (rows-by-lane) mapping and a shuffle reduction.
-__device__ __forceinline__ void colsum8(const uint8_t* tile, int rows_tile, int c0, int r_begin, int nrows,
-                                        const float* wrow, float (&acc)[8], bool bf) {
-  // acc[u] += sum_{r in [r_begin, r_begin + nrows)} w[r] * tile[r][c0 + u]
-  for (int r = r_begin; r < r_begin + nrows; ++r) {
-    const uint4 v4 = *(const uint4*)(tile + sw128_off(r, c0, rows_tile));
-    const float w = wrow ? wrow[r] : 1.f;
-    const uint32_t x[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float2 f = bf ? unpack2<true>(x[q]) : unpack2<false>(x[q]);
-      acc[2 * q] += w * f.x;
-      acc[2 * q + 1] += w * f.y;
-    }
-  }
-}
-
 template <bool kBF16>
 __global__ void __launch_bounds__(320, 1)
     k_bwd_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,

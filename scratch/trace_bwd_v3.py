@@ -1,0 +1,29 @@
+import ctypes as C, sys, numpy as np, torch
+sys.path.insert(0, '.')
+from paper_2510_21956_b200 import _abi
+L = _abi.lib()
+dev = torch.device('cuda')
+G, N, D = 64, 65536, 128
+p = _abi.make_problem(G, N, D, "bf16")
+q = torch.randn(G, N, D, device=dev); q = (q / q.norm(dim=-1, keepdim=True)).bfloat16()
+k = q.clone(); v = (torch.rand(G, D, N, device=dev) * 2 - 1).bfloat16(); w = v.clone()
+out = torch.empty(G, D, N, device=dev, dtype=torch.bfloat16); g = torch.empty(G, N, device=dev)
+dq = torch.empty_like(q); dk = torch.empty_like(v); dv = torch.empty_like(v)
+wsf = torch.empty(L.la_forward_workspace_bytes(C.byref(p)), device=dev, dtype=torch.uint8)
+wsb = torch.empty(L.la_backward_workspace_bytes(C.byref(p)), device=dev, dtype=torch.uint8)
+sv = torch.empty(L.la_saved_state_bytes(C.byref(p)), device=dev, dtype=torch.uint8)
+L.la_forward_save(C.byref(p), q.data_ptr(), 1, k.data_ptr(), 1, v.data_ptr(), 0, out.data_ptr(), g.data_ptr(), sv.data_ptr(), sv.numel(), wsf.data_ptr(), wsf.numel(), None, None)
+for _ in range(2):
+    L.la_backward_saved(C.byref(p), q.data_ptr(), 1, k.data_ptr(), 1, v.data_ptr(), 0, out.data_ptr(), w.data_ptr(), 0, g.data_ptr(), sv.data_ptr(), sv.numel(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), wsb.data_ptr(), wsb.numel(), None, None)
+torch.cuda.synchronize()
+buf = (C.c_ulonglong * (4 * 64 * 10))()
+L.la_internal_trace_read_bwd(buf)
+t = np.array(buf, dtype=np.int64).reshape(4, 64, 10)
+t0 = t[0, 10, 0]
+print("MMA: start,full,dpt_empty,w_ready,sS_ready,ps_ready,gr_empty,sR_ready")
+for c in range(10, 14): print(c, (t[0, c, :8] - t0).tolist())
+print("WGA: start,after dv_out(n-1),sR_ready,dpt_full,ps_ready,after du/dc,after E0(n+1)")
+for c in range(10, 14): print(c, (t[1, c, :7] - t0).tolist())
+print("WGB: start,after qk_out(n-1),after s_full wait,sS_ready,after z,after E0(n+1)")
+for c in range(10, 14): print(c, (t[2, c, :6] - t0).tolist())
+print("period", np.diff(t[0, 5:60, 0]).mean())
