@@ -172,7 +172,7 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
   cudaError_t e;
   const bool tc = use_tc(p, tc_forward_supported(L, t));
   if (saved) {
-    if (tc) {
+    if (tc && p->causal) {  // prefix states per segment (the non-causal path keeps no prefixes)
       L.saved_out = (float*)saved;
     } else {  // header only: the backward recomputes its prefix states
       const float hdr[kSavedHeader] = {kSavedMagic, (float)p->groups, (float)p->seq_len, (float)p->dim, 0.f};

@@ -620,6 +620,202 @@ __global__ void __launch_bounds__(192, 1)
 constexpr size_t kFwdSmem = kFStages * kFStage + 2 * 8192 + 2 * kFT + 256 + (4 * kCF + kD) * 4 + 1024;
 constexpr size_t kAggSmem = 4 * kTile + 128 + 1024;
 
+// ================================================================ non-causal forward
+// forward_full (forward_kernels.hpp:133-206): with the totals S = sum k^T v, z = sum k,
+// sigma = sum v over all N (aggregate pass + k_sum_units),
+//   O^T = bf16(b S^T) Q^T        (bf16 S^T is a constant A operand in TMEM)
+//   g   = a N + b Q [z_hi; z_lo]^T   (M=64, N=16 against two bf16 rows of z)
+//   o   = (O^T + a sigma) / g  -> staging -> TMA store.
+// One CTA per (group, segment) of 64-row chunks; 4-stage Q ring; 192 threads:
+// 0 TMA producer, 1 MMA issuer + TMEM owner, 2-5 epilogue.
+constexpr int kQStages = 4;
+constexpr uint32_t kFF_SB = 0, kFF_OT = 64, kFF_GZ = 192;  // TMEM: bf16 S^T | O^T x2 | q.z x2
+constexpr size_t kFwdFullSmem = kQStages * kFT + 4096 + 2 * kFT + 128 + 2 * kCF * 4 + 1024;
+
+__global__ void k_sum_units(const float* recs, int U, int64_t SZ, float* tot) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t grp = blockIdx.y;
+  if (e >= SZ) return;
+  const float* r = recs + grp * U * SZ + e;
+  float acc = 0.f;
+  for (int u = 0; u < U; ++u) acc += r[u * SZ];
+  tot[grp * SZ + e] = acc;
+}
+
+struct FwdFullParams {
+  const float* tot;     // per-group totals (S, z, sigma, count)
+  float* gout;
+  unsigned long long* flag;
+  int64_t N, n_total, seg_len;
+  float a, b;
+};
+
+template <bool kBF16>
+__global__ void __launch_bounds__(192, 1)
+    k_fwd_full_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO,
+                  FwdFullParams prm) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sZ = smem + kQStages * kFT;   // [16 rows][128 m] z_hi, z_lo, zeros (K-major, 2 panels)
+  uint8_t* sO = sZ + 4096;               // [2][16K] o^T staging
+  uint64_t* bars = (uint64_t*)(sO + 2 * kFT);
+  uint64_t* full = bars;                 // [4]
+  uint64_t* empty = bars + 4;            // [4]
+  uint64_t* o_full = bars + 8;           // [2]
+  uint64_t* ot_empty = bars + 10;        // [2]
+  uint32_t* tslot = (uint32_t*)(bars + 12);
+  float* ginv_s = (float*)(bars + 16);   // [2][64]
+
+  const int p = blockIdx.x;
+  const int64_t grp = blockIdx.y;
+  const int64_t s0 = (int64_t)p * prm.seg_len;
+  const int64_t s1 = lmin(prm.N, s0 + prm.seg_len);
+  const int nc = s1 > s0 ? (int)((s1 - s0) / kCF) : 0;
+  const uint32_t warp = warp_id();
+  const float* tot = prm.tot + grp * state_floats(kD);
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmO);
+    for (int s = 0; s < kQStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&o_full[b], 1);
+      mbar_init(&ot_empty[b], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<256>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  if (warp >= 2) {  // constants: bf16(b S^T) into TMEM, z rows into smem
+    const uint32_t qd = warp & 3;
+    const int r = (int)(qd * 32 + lane_id());
+    const uint32_t lb = (qd * 32u) << 16;
+    const float b = prm.b;
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+      uint32_t pk[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u)
+        pk[u] = pack2<kBF16>(b * tot[(half * 64 + 2 * u) * kD + r], b * tot[(half * 64 + 2 * u + 1) * kD + r]);
+      tmem_st32(tmem + lb + kFF_SB + half * 32, pk);
+    }
+    tmem_st_wait();
+    const float z = tot[kD * kD + r];
+    uint16_t hv, lv;
+    if (kBF16) {
+      const __nv_bfloat16 h = __float2bfloat16_rn(z);
+      hv = __bfloat16_as_ushort(h);
+      lv = __bfloat16_as_ushort(__float2bfloat16_rn(z - __bfloat162float(h)));
+    } else {
+      const __half h = __float2half_rn(z);
+      hv = __half_as_ushort(h);
+      lv = __half_as_ushort(__float2half_rn(z - __half2float(h)));
+    }
+    uint8_t* zp = sZ + (r >> 6) * 2048;
+    *(uint16_t*)(zp + sw128_off(0, r & 63, 16)) = hv;
+    *(uint16_t*)(zp + sw128_off(1, r & 63, 16)) = lv;
+    for (int rr = 2; rr < 16; ++rr) *(uint16_t*)(zp + sw128_off(rr, r & 63, 16)) = 0;
+    fence_proxy_async();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int c = 0; c < nc; ++c) {
+        const int s = c % kQStages;
+        if (c >= kQStages) mbar_wait(&empty[s], ((c / kQStages) & 1) ^ 1);
+        mbar_expect_tx(&full[s], kFT);
+        tma_load_3d(smem + s * kFT, &tmQ, &full[s], 0, (int)(grp * prm.N + s0 + (int64_t)c * kCF), 0);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t fmt = kBF16 ? 1 : 0;
+    const uint32_t id_OT = idesc_f16(128, 64, fmt, 0, 0);
+    const uint32_t id_GZ = idesc_f16(64, 16, fmt, 0, 0);
+    const uint32_t aZ = smem_u32(sZ);
+    for (int c = 0; c < nc; ++c) {
+      const int s = c % kQStages, b = c & 1;
+      const uint32_t aQ = smem_u32(smem + s * kFT);
+      mbar_wait(&full[s], (c / kQStages) & 1);
+      if (c >= 2) mbar_wait(&ot_empty[b], ((c - 2) >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        for (int ks = 0; ks < 8; ++ks)  // O^T = bf16(b S^T) Q^T  (A from TMEM)
+          mma_ts(tmem + kFF_OT + b * 64, tmem + kFF_SB + ks * 8, kd64(aQ, ks, 64), id_OT, ks > 0);
+        for (int ks = 0; ks < 8; ++ks)  // q . [z_hi, z_lo]
+          mma_ss(tmem + kFF_GZ + b * 16, kd64(aQ, ks, 64), kd64(aZ, ks, 16), id_GZ, ks > 0);
+        mma_commit(&o_full[b]);
+        mma_commit(&empty[s]);
+      }
+      __syncwarp();
+    }
+  } else {
+    const uint32_t qd = warp & 3;
+    const int l = (int)lane_id();
+    const int r = (int)(qd * 32) + l;              // j of O^T
+    const int ih = (int)(qd * 16) + (l & 15);      // row i of the M=64 q.z accumulator
+    const bool lower = l < 16;
+    const uint32_t lb = (qd * 32u) << 16;
+    const int et = (int)threadIdx.x - 64;
+    const float a = prm.a, b = prm.b;
+    const float asig = a * tot[kD * kD + kD + r];
+    const float an = a * (float)prm.n_total;
+    for (int c = 0; c < nc; ++c) {
+      const int bb = c & 1;
+      const int64_t row0 = s0 + (int64_t)c * kCF;
+      mbar_wait(&o_full[bb], (c >> 1) & 1);
+      tc_fence_after();
+      uint32_t x0[32], x1[32], zh, zl;
+      tmem_ld32(tmem + lb + kFF_OT + bb * 64, x0);
+      tmem_ld32(tmem + lb + kFF_OT + bb * 64 + 32, x1);
+      tmem_ld2(tmem + lb + kFF_GZ + bb * 16, zh, zl);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&ot_empty[bb]);
+      if (lower) {
+        const float gi = an + b * (__uint_as_float(zh) + __uint_as_float(zl));
+        if (fabsf(gi) < kEpsF32) flag_degenerate(prm.flag, grp, row0 + ih);
+        ginv_s[bb * kCF + ih] = 1.f / gi;
+        prm.gout[grp * prm.N + row0 + ih] = gi;
+      }
+      if (et == 0) tma_store_wait_read1();  // the store issued two chunks ago has left buffer bb
+      named_bar(1, 128);                     // ginv of chunk c complete; staging bb free
+      const float* gv = ginv_s + bb * kCF;
+      uint8_t* so = sO + bb * kFT;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        uint32_t p0[4], p1[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i0 = 8 * w + 2 * q;
+          p0[q] = pack2<kBF16>((__uint_as_float(x0[i0]) + asig) * gv[i0], (__uint_as_float(x0[i0 + 1]) + asig) * gv[i0 + 1]);
+          p1[q] = pack2<kBF16>((__uint_as_float(x1[i0]) + asig) * gv[32 + i0],
+                               (__uint_as_float(x1[i0 + 1]) + asig) * gv[32 + i0 + 1]);
+        }
+        *(uint4*)(so + sw128_off(r, 8 * w, kD)) = make_uint4(p0[0], p0[1], p0[2], p0[3]);
+        *(uint4*)(so + sw128_off(r, 32 + 8 * w, kD)) = make_uint4(p1[0], p1[1], p1[2], p1[3]);
+      }
+      fence_proxy_async();
+      named_bar(1, 128);
+      if (et == 0) {
+        tma_store_3d(&tmO, so, 0, (int)(grp * kD), (int)(row0 / 64));
+        tma_store_commit();
+      }
+    }
+    if (et == 0) tma_store_wait0();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<256>(tmem);
+}
+
 }  // namespace
 
 int tc_segments(int64_t G, int64_t N) {
@@ -629,7 +825,8 @@ int tc_segments(int64_t G, int64_t N) {
 }
 
 bool tc_forward_supported(const Launch& L, const Tensors& t) {
-  return (L.dtype == LA_BF16 || L.dtype == LA_F16) && L.D == kD && L.causal && L.fault == LA_FAULT_NONE &&
+  return (L.dtype == LA_BF16 || L.dtype == LA_F16) && L.D == kD && L.fault == LA_FAULT_NONE &&
+         (L.causal || (L.carry_prefix == nullptr && L.row_offset == 0)) &&
          L.N % kC == 0 && t.lq == LA_SEQUENCE_MAJOR && t.lk == LA_SEQUENCE_MAJOR &&
          t.lv == LA_FEATURE_MAJOR && L.G * L.N < (1ll << 31) && L.G * kD < (1ll << 31);
 }
@@ -642,7 +839,54 @@ static int fwd_agg_split(int64_t G, int64_t N, int P) {
 size_t tc_forward_ws_floats(int64_t G, int64_t N, int64_t D) {
   if (D != kD || N % kC) return 0;
   const int P = tc_segments(G, N);
-  return (size_t)((fwd_agg_split(G, N, P) + 1) * G * P * state_floats(kD));  // unit sums + combined prefixes
+  const int64_t seg = ((N / kC + P - 1) / P) * kC;
+  const int Af = agg_split(G, seg, P);  // non-causal: every segment is aggregated
+  const int A = fwd_agg_split(G, N, P);
+  const size_t causal = (size_t)((A + 1) * G * P), full = (size_t)(Af * G * P + G);
+  return (causal > full ? causal : full) * state_floats(kD);  // unit sums + combined prefixes / totals
+}
+
+// Non-causal forward: aggregate every segment, sum the unit records per group, then
+// the apply pass over 64-row chunks.
+static cudaError_t tc_forward_full(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws) {
+  const bool bf = L.dtype == LA_BF16;
+  const int64_t G = L.G, N = L.N, SZ = state_floats(kD);
+  const int P = tc_segments(G, N);
+  const int64_t seg = ((N / kC + P - 1) / P) * kC;
+  const int A = agg_split(G, seg, P);
+  float* units = ws.base;
+  float* tot = ws.base + G * P * A * SZ;
+  CUtensorMap mK, mV, mQ64, mO64;
+  if (!make_map(&mK, t.k, bf, (uint64_t)(G * N), kD) || !make_map(&mV, t.v, bf, (uint64_t)(G * kD), (uint64_t)N) ||
+      !make_tma_map(&mQ64, t.q, bf, (uint64_t)(G * N), kD, 64, 2) ||
+      !make_tma_map(&mO64, out, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1))
+    return cudaErrorInvalidValue;
+  auto agg = bf ? k_fwd_agg_tc<true> : k_fwd_agg_tc<false>;
+  cudaFuncSetAttribute(agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggSmem);
+  {
+    ProfScope ps("la_fwd_agg", L.stream);
+    agg<<<dim3(A * P, G), 192, kAggSmem, L.stream>>>(mK, mV, units, N, seg / A, P * A);
+  }
+  {
+    ProfScope ps("la_fwd_sum", L.stream);
+    k_sum_units<<<dim3((unsigned)((SZ + 255) / 256), (unsigned)G), 256, 0, L.stream>>>(units, P * A, SZ, tot);
+  }
+  // apply pass: segments of whole 64-row chunks, about two CTAs per SM
+  const int64_t c64 = N / kCF;
+  int64_t P2 = (2 * 148 + G - 1) / G;
+  if (P2 > c64) P2 = c64;
+  if (P2 < 1) P2 = 1;
+  const int64_t seg2 = ((c64 + P2 - 1) / P2) * kCF;
+  P2 = (N + seg2 - 1) / seg2;
+  auto main_k = bf ? k_fwd_full_tc<true> : k_fwd_full_tc<false>;
+  cudaFuncSetAttribute(main_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdFullSmem);
+  FwdFullParams prm{tot, g, ws.flag, N, L.n_total > 0 ? L.n_total : N, seg2, L.a, L.b};
+  {
+    ProfScope ps("la_fwd_full", L.stream);
+    main_k<<<dim3((unsigned)P2, (unsigned)G), 192, kFwdFullSmem, L.stream>>>(mQ64, mO64, prm);
+  }
+  note_launch(3);
+  return cudaGetLastError();
 }
 
 size_t tc_saved_floats(int64_t G, int64_t N, int64_t D) {
@@ -653,6 +897,7 @@ size_t tc_saved_floats(int64_t G, int64_t N, int64_t D) {
 // One CTA per (group, segment). P = 1 walks whole sequences (no carries, no
 // aggregate pass); P > 1 takes exclusive-prefix carries from k_fwd_agg_tc + scan.
 cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws) {
+  if (!L.causal) return tc_forward_full(L, t, out, g, ws);
   const bool bf = L.dtype == LA_BF16;
   const int64_t G = L.G, N = L.N;
   const int64_t SZ = state_floats(kD);

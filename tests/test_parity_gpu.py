@@ -305,3 +305,14 @@ def test_host_step_pipeline_matches_oracle(cuda, dtype, G, N, D):
         else:
             assert max_abs(got[key], ref[key]) <= BF16_ABS, key
     assert rel_err(g, rg) <= (1e-5 if dtype == "f32" else 1e-3)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+@pytest.mark.parametrize("N", [128, 4096])
+def test_tcgen05_noncausal_forward_parity(cuda, dtype, N):
+    # the sm_100a non-causal forward (forced): aggregate totals + apply pass
+    q, k, v, _ = fast_inputs(3, N, 128, seed=N + 3 * len(dtype))
+    res = run_dev(q, k, v, None, dtype, cuda, causal=False, impl="tcgen05")
+    ref = oracle_all(res, False)
+    assert max_abs(res["out"], ref["out"]) <= BF16_ABS
+    assert rel_err(res["g"], ref["g"]) <= 1e-3
