@@ -123,6 +123,10 @@ int tc_segments(int64_t G, int64_t N);
 cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws);
 cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv,
                         Workspace ws);
+// Non-causal helpers shared by the forward and backward files.
+int tc_kv_units(int64_t G, int64_t N);
+cudaError_t tc_sum_units(const float* recs, int64_t G, int U, float* tot, cudaStream_t st);
+cudaError_t tc_kv_totals(const Launch& L, const Tensors& t, float* units, float* tot);
 
 void note_launch(int n = 1);
 

@@ -896,6 +896,39 @@ size_t tc_saved_floats(int64_t G, int64_t N, int64_t D) {
 
 // One CTA per (group, segment). P = 1 walks whole sequences (no carries, no
 // aggregate pass); P > 1 takes exclusive-prefix carries from k_fwd_agg_tc + scan.
+int tc_kv_units(int64_t G, int64_t N) {
+  const int P = tc_segments(G, N);
+  const int64_t seg = ((N / kC + P - 1) / P) * kC;
+  return P * agg_split(G, seg, P);
+}
+
+cudaError_t tc_sum_units(const float* recs, int64_t G, int U, float* tot, cudaStream_t st) {
+  const int64_t SZ = state_floats(kD);
+  k_sum_units<<<dim3((unsigned)((SZ + 255) / 256), (unsigned)G), 256, 0, st>>>(recs, U, SZ, tot);
+  note_launch(1);
+  return cudaGetLastError();
+}
+
+// Totals over the whole sequence of S = sum k^T v, z, sigma (count) per group.
+cudaError_t tc_kv_totals(const Launch& L, const Tensors& t, float* units, float* tot) {
+  const bool bf = L.dtype == LA_BF16;
+  const int64_t G = L.G, N = L.N;
+  const int P = tc_segments(G, N);
+  const int64_t seg = ((N / kC + P - 1) / P) * kC;
+  const int A = agg_split(G, seg, P);
+  CUtensorMap mK, mV;
+  if (!make_map(&mK, t.k, bf, (uint64_t)(G * N), kD) || !make_map(&mV, t.v, bf, (uint64_t)(G * kD), (uint64_t)N))
+    return cudaErrorInvalidValue;
+  auto agg = bf ? k_fwd_agg_tc<true> : k_fwd_agg_tc<false>;
+  cudaFuncSetAttribute(agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggSmem);
+  {
+    ProfScope ps("la_kv_agg", L.stream);
+    agg<<<dim3(A * P, G), 192, kAggSmem, L.stream>>>(mK, mV, units, N, seg / A, P * A);
+  }
+  note_launch(1);
+  return tc_sum_units(units, G, P * A, tot, L.stream);
+}
+
 cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws) {
   if (!L.causal) return tc_forward_full(L, t, out, g, ws);
   const bool bf = L.dtype == LA_BF16;

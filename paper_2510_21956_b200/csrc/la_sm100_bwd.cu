@@ -1081,6 +1081,245 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
+// ================================================================ non-causal backward
+// backward_full (backward_kernels.hpp:173-288): with the totals S, z (keys/values) and
+// R = sum q^T w_hat, u = sum s q, c = sum w_hat over all N, every 64-row chunk is
+// independent:
+//   dQ   = W_hat (b S)^T - b s z^T          (M=64 halves; bS a constant smem operand)
+//   dK^T = (b R) V^T - b u                  (bR constant)
+//   dV^T = (b R)^T K^T + a c
+// Stage: K [64 t][128 m] | V^T | Omega^T (-> W_hat in place) | O^T. Two epilogue
+// warpgroups share the W_hat / s pass (rows j 0..63 / 64..127); WG-A drains dV^T, WG-B
+// dQ and dK^T. TMEM: [dQ | dK^T | dV^T] x 2 buffers.
+struct BwdFullParams {
+  const float* totS;  // per group: S (X[m][j]), z, sigma, count
+  const float* totR;  // per group: R (X[m][j]), u, c, count
+  const void* o;
+  const float* g;
+  void* dq;
+  void* dk;
+  void* dv;
+  int64_t N;
+  int64_t seg_len;
+  float a, b;
+};
+
+constexpr int kFStageB = 4 * kT64;  // K, V^T, Omega^T, O^T
+constexpr size_t kBwdFullSmem = 2 * kFStageB + 2 * 32768 + 128 + 4 * kCB * 2 * 4 + 1024;
+
+template <bool kBF16>
+__global__ void __launch_bounds__(320, 1)
+    k_bwd_full_tc(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                  const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmO,
+                  BwdFullParams prm) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sR = smem + 2 * kFStageB;       // b R [128 rows m][128 j]
+  uint8_t* sS = sR + 32768;                // b S [128 rows m][128 j]
+  uint64_t* bars = (uint64_t*)(sS + 32768);
+  uint64_t* full = bars;         // [2]
+  uint64_t* empty = bars + 2;    // [2]
+  uint64_t* w_ready = bars + 4;  // [2] by chunk parity
+  uint64_t* acc_full = bars + 6; // [2]
+  uint64_t* acc_empty = bars + 8;// [2]
+  uint32_t* tslot = (uint32_t*)(bars + 10);
+  float* s_s = (float*)(bars + 16);  // [4][2][64]
+
+  const int p = blockIdx.x;
+  const int64_t grp = blockIdx.y;
+  const int64_t s0 = (int64_t)p * prm.seg_len;
+  const int64_t s1 = lmin(prm.N, s0 + prm.seg_len);
+  const int nc = s1 > s0 ? (int)((s1 - s0) / kCB) : 0;
+  auto row_of = [&](int m) -> int64_t { return s0 + (int64_t)m * kCB; };
+  const uint32_t warp = warp_id();
+  const float* tS = prm.totS + grp * state_floats(kD);
+  const float* tR = prm.totR + grp * state_floats(kD);
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmW);
+    tma_prefetch(&tmO);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], 1 + 256);
+      mbar_init(&w_ready[b], 256);
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 256);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  if (warp >= 2) {  // constants bR, bS -> smem (row m = r, bf16, K-major over j)
+    const int t = (int)threadIdx.x - 64;
+    const int r = t & 127;
+    const float* src = t < 128 ? tR : tS;
+    uint8_t* dst = t < 128 ? sR : sS;
+    const float b = prm.b;
+#pragma unroll 1
+    for (int j0 = 0; j0 < kD; j0 += 8) {
+      const float4 x0 = *(const float4*)(src + r * kD + j0), x1 = *(const float4*)(src + r * kD + j0 + 4);
+      *(uint4*)(dst + sw128_off(r, j0, 128)) =
+          make_uint4(pack2<kBF16>(b * x0.x, b * x0.y), pack2<kBF16>(b * x0.z, b * x0.w),
+                     pack2<kBF16>(b * x1.x, b * x1.y), pack2<kBF16>(b * x1.z, b * x1.w));
+    }
+    fence_proxy_async();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int n = 0; n < nc; ++n) {
+        const int s = n & 1;
+        if (n >= 2) mbar_wait(&empty[s], ((n >> 1) & 1) ^ 1);
+        const int64_t row0 = row_of(n);
+        uint8_t* st = smem + s * kFStageB;
+        mbar_expect_tx(&full[s], kFStageB);
+        tma_load_3d(st, &tmK, &full[s], 0, (int)(grp * prm.N + row0), 0);
+        tma_load_3d(st + kT64, &tmV, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
+        tma_load_3d(st + 2 * kT64, &tmW, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
+        tma_load_3d(st + 3 * kT64, &tmO, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t f = kBF16 ? 1 : 0;
+    const uint32_t id_dQ2 = idesc_f16(64, 64, f, 1, 0);
+    const uint32_t id_dK2 = idesc_f16(128, 64, f, 0, 1);
+    const uint32_t id_dV2 = idesc_f16(128, 64, f, 1, 0);
+    const uint32_t aR = smem_u32(sR), aS = smem_u32(sS);
+    for (int n = 0; n < nc; ++n) {
+      const int s = n & 1, bb = n & 1;
+      const uint32_t aK = smem_u32(smem + s * kFStageB), aV = aK + kT64, aW = aK + 2 * kT64;
+      mbar_wait(&w_ready[s], (n >> 1) & 1);
+      if (n >= 2) mbar_wait(&acc_empty[bb], ((n - 2) >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t base = tmem + bb * 192;
+        for (int h = 0; h < 2; ++h)  // dQ[:, 64h:64h+64] = W_hat (b S)^T
+          for (int ks = 0; ks < 8; ++ks)
+            mma_ss(base + (h ? kHalf : 0u), mn(aW, ks, 8192), kd(aS + h * 8192, ks, 128), id_dQ2, ks > 0);
+        for (int ks = 0; ks < 8; ++ks)  // dK^T = (b R) V^T
+          mma_ss(base + 64, kd(aR, ks, 128), mn(aV, ks, 8192), id_dK2, ks > 0);
+        for (int ks = 0; ks < 8; ++ks)  // dV^T = (b R)^T K^T
+          mma_ss(base + 128, mn(aR, ks, 16384), kd(aK, ks, 64), id_dV2, ks > 0);
+        mma_commit(&acc_full[bb]);
+        mma_commit(&empty[s]);
+      }
+      __syncwarp();
+    }
+  } else {
+    const bool is_a = warp < 6;
+    const uint32_t qd = warp & 3;
+    const int l = (int)lane_id();
+    const int r = (int)(qd * 32) + l;              // j (WG-A: dV^T) / m (WG-B: dK^T)
+    const int ih = (int)(qd * 16) + (l & 15);
+    const bool upper = l >= 16;
+    const uint32_t lb = (qd * 32u) << 16;
+    const int et = (int)threadIdx.x - (is_a ? 64 : 192);
+    const int jbase = is_a ? 0 : 64;
+    const float a = prm.a, b = prm.b;
+    const float ac = a * tR[kD * kD + kD + r];     // WG-A: a c_j
+    const float bu = b * tR[kD * kD + r];          // WG-B: b u_m
+    uint4 o4[4];
+    float4 g8[2];
+    auto e0 = [&](int m) {  // W_hat / partial s of chunk m (rows jbase..jbase+63), O^T from the stage
+      const int sm = m & 1;
+      mbar_wait(&full[sm], (m >> 1) & 1);
+      uint8_t* st = smem + sm * kFStageB;
+      const int jg = et & 15, ig = 2 * (et >> 5) + ((et & 31) >> 4);
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr)
+        o4[rr] = *(const uint4*)(st + 3 * kT64 + sw128_off(jbase + 16 * rr + jg, 8 * ig, 128));
+      const float* gp = prm.g + grp * prm.N + row_of(m) + 8 * ig;
+      g8[0] = __ldg((const float4*)gp);
+      g8[1] = __ldg((const float4*)(gp + 4));
+      what_pass_half<kBF16>(st + 2 * kT64, o4, g8, s_s + (m & 3) * 2 * kCB + (jbase ? kCB : 0), et, jbase);
+      fence_proxy_async();
+      mbar_arrive(&w_ready[sm]);
+      mbar_arrive(&empty[sm]);
+    };
+    if (nc > 0) e0(0);
+    for (int n = 0; n < nc; ++n) {
+      if (n + 1 < nc) e0(n + 1);
+      const int bb = n & 1;
+      const int64_t row0 = row_of(n);
+      mbar_wait(&acc_full[bb], (n >> 1) & 1);
+      tc_fence_after();
+      const uint32_t base = tmem + bb * 192;
+      uint32_t x0[32], x1[32];
+      uint4 vt[8];
+      if (is_a) {  // dV^T (lanes j) + a c_j
+        tmem_ld32(base + lb + 128, x0);
+        tmem_ld32(base + lb + 128 + 32, x1);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&acc_empty[bb]);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          vt[w] = make_uint4(pack2<kBF16>(__uint_as_float(x0[8 * w]) + ac, __uint_as_float(x0[8 * w + 1]) + ac),
+                             pack2<kBF16>(__uint_as_float(x0[8 * w + 2]) + ac, __uint_as_float(x0[8 * w + 3]) + ac),
+                             pack2<kBF16>(__uint_as_float(x0[8 * w + 4]) + ac, __uint_as_float(x0[8 * w + 5]) + ac),
+                             pack2<kBF16>(__uint_as_float(x0[8 * w + 6]) + ac, __uint_as_float(x0[8 * w + 7]) + ac));
+          vt[4 + w] = make_uint4(pack2<kBF16>(__uint_as_float(x1[8 * w]) + ac, __uint_as_float(x1[8 * w + 1]) + ac),
+                                 pack2<kBF16>(__uint_as_float(x1[8 * w + 2]) + ac, __uint_as_float(x1[8 * w + 3]) + ac),
+                                 pack2<kBF16>(__uint_as_float(x1[8 * w + 4]) + ac, __uint_as_float(x1[8 * w + 5]) + ac),
+                                 pack2<kBF16>(__uint_as_float(x1[8 * w + 6]) + ac, __uint_as_float(x1[8 * w + 7]) + ac));
+        }
+        uint4* dst = (uint4*)((uint16_t*)prm.dv + (grp * kD + r) * prm.N + row0);
+#pragma unroll
+        for (int w = 0; w < 8; ++w) dst[w] = vt[w];
+      } else {  // dQ (half lanes) - b s_i z_m, then dK^T (lanes m) - b u_m
+        const float* sA = s_s + (n & 3) * 2 * kCB;
+        const float bsi = b * (sA[ih] + sA[kCB + ih]);
+        const float* zq = tS + kD * kD + (upper ? 64 : 0);
+        tmem_ld32(base + lb, x0);
+        tmem_ld32(base + lb + 32, x1);
+        tmem_ld_wait();
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const float4 za = *(const float4*)(zq + 8 * w), zb = *(const float4*)(zq + 8 * w + 4);
+          vt[w] = make_uint4(pack2<kBF16>(__uint_as_float(x0[8 * w]) - bsi * za.x, __uint_as_float(x0[8 * w + 1]) - bsi * za.y),
+                             pack2<kBF16>(__uint_as_float(x0[8 * w + 2]) - bsi * za.z, __uint_as_float(x0[8 * w + 3]) - bsi * za.w),
+                             pack2<kBF16>(__uint_as_float(x0[8 * w + 4]) - bsi * zb.x, __uint_as_float(x0[8 * w + 5]) - bsi * zb.y),
+                             pack2<kBF16>(__uint_as_float(x0[8 * w + 6]) - bsi * zb.z, __uint_as_float(x0[8 * w + 7]) - bsi * zb.w));
+          const float4 zc = *(const float4*)(zq + 32 + 8 * w), zd = *(const float4*)(zq + 32 + 8 * w + 4);
+          vt[4 + w] = make_uint4(pack2<kBF16>(__uint_as_float(x1[8 * w]) - bsi * zc.x, __uint_as_float(x1[8 * w + 1]) - bsi * zc.y),
+                                 pack2<kBF16>(__uint_as_float(x1[8 * w + 2]) - bsi * zc.z, __uint_as_float(x1[8 * w + 3]) - bsi * zc.w),
+                                 pack2<kBF16>(__uint_as_float(x1[8 * w + 4]) - bsi * zd.x, __uint_as_float(x1[8 * w + 5]) - bsi * zd.y),
+                                 pack2<kBF16>(__uint_as_float(x1[8 * w + 6]) - bsi * zd.z, __uint_as_float(x1[8 * w + 7]) - bsi * zd.w));
+        }
+        uint4* dqr = (uint4*)((uint16_t*)prm.dq + (grp * prm.N + row0 + ih) * kD + (upper ? 64 : 0));
+#pragma unroll
+        for (int w = 0; w < 8; ++w) dqr[w] = vt[w];
+        tmem_ld32(base + lb + 64, x0);
+        tmem_ld32(base + lb + 64 + 32, x1);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&acc_empty[bb]);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          vt[w] = make_uint4(pack2<kBF16>(__uint_as_float(x0[8 * w]) - bu, __uint_as_float(x0[8 * w + 1]) - bu),
+                             pack2<kBF16>(__uint_as_float(x0[8 * w + 2]) - bu, __uint_as_float(x0[8 * w + 3]) - bu),
+                             pack2<kBF16>(__uint_as_float(x0[8 * w + 4]) - bu, __uint_as_float(x0[8 * w + 5]) - bu),
+                             pack2<kBF16>(__uint_as_float(x0[8 * w + 6]) - bu, __uint_as_float(x0[8 * w + 7]) - bu));
+          vt[4 + w] = make_uint4(pack2<kBF16>(__uint_as_float(x1[8 * w]) - bu, __uint_as_float(x1[8 * w + 1]) - bu),
+                                 pack2<kBF16>(__uint_as_float(x1[8 * w + 2]) - bu, __uint_as_float(x1[8 * w + 3]) - bu),
+                                 pack2<kBF16>(__uint_as_float(x1[8 * w + 4]) - bu, __uint_as_float(x1[8 * w + 5]) - bu),
+                                 pack2<kBF16>(__uint_as_float(x1[8 * w + 6]) - bu, __uint_as_float(x1[8 * w + 7]) - bu));
+        }
+        uint4* dkr = (uint4*)((uint16_t*)prm.dk + (grp * kD + r) * prm.N + row0);
+#pragma unroll
+        for (int w = 0; w < 8; ++w) dkr[w] = vt[w];
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
 constexpr size_t kAggSmemB = 2 * kStage + 512 + 1024;
 constexpr size_t kMainSmemB = 2 * kStage + 2 * 8192 + 2 * 32768 + 160 + (8 * kCB + 6 * kD) * 4 + 1024;
 
@@ -1089,7 +1328,8 @@ int tcb_segments(int64_t G, int64_t N) { return tc_segments(G, N); }
 }  // namespace
 
 bool tc_backward_supported(const Launch& L, const Tensors& t) {
-  return (L.dtype == LA_BF16 || L.dtype == LA_F16) && L.D == kD && L.causal && L.fault == LA_FAULT_NONE &&
+  return (L.dtype == LA_BF16 || L.dtype == LA_F16) && L.D == kD && L.fault == LA_FAULT_NONE &&
+         (L.causal || (L.carry_prefix == nullptr && L.carry_suffix == nullptr && L.row_offset == 0)) &&
          L.N % 128 == 0 && t.lq == LA_SEQUENCE_MAJOR && t.lk == LA_SEQUENCE_MAJOR &&
          t.lv == LA_FEATURE_MAJOR && t.lw == LA_FEATURE_MAJOR && t.lo == LA_FEATURE_MAJOR &&
          L.G * L.N < (1ll << 31) && L.G * kD < (1ll << 31);
@@ -1100,10 +1340,64 @@ size_t tc_backward_ws_floats(int64_t G, int64_t N, int64_t D) {
   const int P = tcb_segments(G, N);
   const int64_t seg = ((N / 128 + P - 1) / P) * 128;
   const int A = agg_split(G, seg, P > 1 ? P - 1 : 1);  // the larger of the two launch shapes' splits
-  return (size_t)((2 * A + 2) * G * P * state_floats(kD));  // S, R unit sums + combined
+  const size_t causal = (size_t)((2 * A + 2) * G * P);  // S, R unit sums + combined
+  const int Af = agg_split(G, seg, P);
+  const size_t full = (size_t)(tc_kv_units(G, N) * G + Af * P * G + 2 * G);  // non-causal unit sums + totals
+  return (causal > full ? causal : full) * state_floats(kD);
+}
+
+// Non-causal backward: totals (S, z from K, V; R, u, c from Q, dO, O, g), then one
+// independent pass over 64-row chunks.
+static cudaError_t tc_backward_full(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv,
+                                    Workspace ws) {
+  const bool bf = L.dtype == LA_BF16;
+  const int64_t G = L.G, N = L.N, SZ = state_floats(kD);
+  const int P = tcb_segments(G, N);
+  const int64_t seg = ((N / 128 + P - 1) / P) * 128;
+  const int A = agg_split(G, seg, P);
+  const int Ukv = tc_kv_units(G, N);
+  float* unitsS = ws.base;
+  float* totS = unitsS + G * Ukv * SZ;
+  float* unitsR = totS + G * SZ;
+  float* totR = unitsR + G * P * A * SZ;
+  cudaError_t e = tc_kv_totals(L, t, unitsS, totS);
+  if (e != cudaSuccess) return e;
+  CUtensorMap mQ, mK, mV, mW, mO;
+  if (!make_tma_map(&mO, t.o, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1) ||
+      !make_tma_map(&mQ, t.q, bf, (uint64_t)(G * N), kD, 64, 2) ||
+      !make_tma_map(&mK, t.k, bf, (uint64_t)(G * N), kD, 64, 2) ||
+      !make_tma_map(&mV, t.v, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1) ||
+      !make_tma_map(&mW, t.w, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1))
+    return cudaErrorInvalidValue;
+  BwdParams pa{t.o, t.g, dq, dk, dv, unitsS, unitsR, N, seg / A, P * A, L.a, L.b, 0, 1, 0, A, nullptr, nullptr,
+               nullptr, 0};
+  auto aggR = bf ? k_bwd_aggR_tc<true> : k_bwd_aggR_tc<false>;
+  cudaFuncSetAttribute(aggR, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggRSmem);
+  {
+    ProfScope ps("la_bwd_agg", L.stream);
+    aggR<<<dim3(A * P, G), 320, kAggRSmem, L.stream>>>(mQ, mW, mO, pa);
+  }
+  e = tc_sum_units(unitsR, G, P * A, totR, L.stream);
+  if (e != cudaSuccess) return e;
+  const int64_t c64 = N / kCB;
+  int64_t P2 = (148 + G - 1) / G;
+  if (P2 > c64) P2 = c64;
+  if (P2 < 1) P2 = 1;
+  const int64_t seg2 = ((c64 + P2 - 1) / P2) * kCB;
+  P2 = (N + seg2 - 1) / seg2;
+  BwdFullParams prm{totS, totR, t.o, t.g, dq, dk, dv, N, seg2, L.a, L.b};
+  auto main_k = bf ? k_bwd_full_tc<true> : k_bwd_full_tc<false>;
+  cudaFuncSetAttribute(main_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdFullSmem);
+  {
+    ProfScope ps("la_bwd_full", L.stream);
+    main_k<<<dim3((unsigned)P2, (unsigned)G), 320, kBwdFullSmem, L.stream>>>(mK, mV, mW, mO, prm);
+  }
+  note_launch(2);
+  return cudaGetLastError();
 }
 
 cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv, Workspace ws) {
+  if (!L.causal) return tc_backward_full(L, t, dq, dk, dv, ws);
   const bool bf = L.dtype == LA_BF16;
   const int64_t G = L.G, N = L.N;
   const int P = tcb_segments(G, N);

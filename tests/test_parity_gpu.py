@@ -316,3 +316,14 @@ def test_tcgen05_noncausal_forward_parity(cuda, dtype, N):
     ref = oracle_all(res, False)
     assert max_abs(res["out"], ref["out"]) <= BF16_ABS
     assert rel_err(res["g"], ref["g"]) <= 1e-3
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+@pytest.mark.parametrize("N", [128, 4096])
+def test_tcgen05_noncausal_backward_parity(cuda, dtype, N):
+    # the sm_100a non-causal backward (forced): totals + independent chunk pass
+    q, k, v, w = fast_inputs(2, N, 128, seed=N + 5 * len(dtype))
+    res = run_dev(q, k, v, w, dtype, cuda, causal=False, impl="tcgen05")
+    ref = oracle_all(res, False)
+    for key in ("out", "dq", "dk", "dv"):
+        assert max_abs(res[key], ref[key]) <= BF16_ABS, key
