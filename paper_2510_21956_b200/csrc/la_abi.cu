@@ -149,6 +149,69 @@ size_t bwd_floats(const la_problem* p) {
   return m > c ? m : c;
 }
 
+// Head dimensions below 128 on the tensor-core path: zero-pad D to 128 in device
+// scratch (exact: padded key features add nothing to S or z, padded value features
+// are dropped on the way out), run the D = 128 kernels, copy the D columns back.
+bool pad_eligible(const la_problem* p, const la_shard* sh, int lq, int lk, int lv, int lw) {
+  return p->impl != LA_IMPL_SIMT && (p->dtype == LA_BF16 || p->dtype == LA_F16) && p->dim < 128 &&
+         p->dim % 8 == 0 && p->fault == LA_FAULT_NONE && p->seq_len % 128 == 0 && sh == nullptr &&
+         lq == LA_SEQUENCE_MAJOR && lk == LA_SEQUENCE_MAJOR && lv == LA_FEATURE_MAJOR &&
+         (lw < 0 || lw == LA_FEATURE_MAJOR) && p->groups * p->seq_len < (1ll << 31);
+}
+la_problem padded_problem(const la_problem* p) {
+  la_problem q = *p;
+  q.dim = 128;
+  la_default_plan(q.groups, 128, p->plan.workers > 0 ? p->plan.workers : 1, &q.plan);
+  return q;
+}
+// [rows][D] <-> [rows][128] (SequenceMajor) and [G][D][N] <-> [G][128][N] (FeatureMajor),
+// 16-byte vectors, zero fill of the padded part on the way in.
+__global__ void k_pad_seq(uint4* dst, const uint4* src, int64_t rows, int dv, int to_padded) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // 16-byte vector of the 128-wide row
+  if (e >= rows * 16) return;
+  const int64_t r = e >> 4;
+  const int c = (int)(e & 15);
+  if (to_padded) dst[e] = c < dv ? src[r * dv + c] : make_uint4(0, 0, 0, 0);
+  else if (c < dv) dst[r * dv + c] = src[e];
+}
+__global__ void k_pad_feat(uint4* dst, const uint4* src, int64_t G, int D, int64_t nv, int to_padded) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // vector of the [G][128][N] tensor
+  if (e >= G * 128 * nv) return;
+  const int64_t g = e / (128 * nv), rem = e % (128 * nv);
+  const int j = (int)(rem / nv);
+  const int64_t i = rem % nv;
+  if (to_padded) dst[e] = j < D ? src[(g * D + j) * nv + i] : make_uint4(0, 0, 0, 0);
+  else if (j < D) dst[(g * D + j) * nv + i] = src[e];
+}
+void pad_copy(void* dst, const void* src, const la_problem* p, bool seq_major, bool to_padded, cudaStream_t st) {
+  const int64_t G = p->groups, N = p->seq_len;
+  const int D = (int)p->dim;
+  if (seq_major) {
+    const int64_t n = G * N * 16;
+    k_pad_seq<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((uint4*)dst, (const uint4*)src, G * N, D / 8,
+                                                           to_padded ? 1 : 0);
+  } else {
+    const int64_t n = G * 128 * (N / 8);
+    k_pad_feat<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((uint4*)dst, (const uint4*)src, G, D, N / 8,
+                                                            to_padded ? 1 : 0);
+  }
+  note_launch(1);
+}
+// Keep the stream-ordered pool's freed blocks for reuse (the padded path allocates
+// per call); without this every call would map fresh pages.
+void keep_pool_memory() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
+
 la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, la_layout lq,
                        const void* k, la_layout lk, const void* v, la_layout lv, void* out,
                        float* g, void* ws, size_t ws_bytes, void* stream, la_error_info* err,
@@ -163,6 +226,27 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
     return fail(err, LA_ERR_WORKSPACE, "workspace smaller than la_forward_workspace_bytes");
   if (sh && !p->causal && (sh->carry_in || sh->row_offset))
     return fail(err, LA_ERR_UNSUPPORTED, "sequence sharding is defined for the causal mask");
+  if (pad_eligible(p, sh, lq, lk, lv, -1)) {
+    const la_problem p2 = padded_problem(p);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t T = (size_t)p->groups * p->seq_len * 128 * 2;
+    char* buf = nullptr;
+    keep_pool_memory();
+    if (cudaMallocAsync((void**)&buf, 4 * T, st) != cudaSuccess) return cuda_fail(err, cudaErrorMemoryAllocation);
+    pad_copy(buf, q, p, true, true, st);
+    pad_copy(buf + T, k, p, true, true, st);
+    pad_copy(buf + 2 * T, v, p, false, true, st);
+    if (saved) {  // no per-segment states on this path: header only, the backward recomputes
+      const float hdr[kSavedHeader] = {kSavedMagic, (float)p->groups, (float)p->seq_len, (float)p->dim, 0.f};
+      cudaMemcpyAsync(saved, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st);
+    }
+    s = forward_impl(&p2, nullptr, buf, LA_SEQUENCE_MAJOR, buf + T, LA_SEQUENCE_MAJOR, buf + 2 * T,
+                     LA_FEATURE_MAJOR, buf + 3 * T, g, ws, ws_bytes, stream, nullptr);
+    if (s == LA_OK) pad_copy(out, buf + 3 * T, p, false, false, st);
+    cudaFreeAsync(buf, st);
+    if (s != LA_OK) return fail(err, s, "padded forward failed");
+    return finish(ws, st, err);
+  }
   Launch L = make_launch(p, sh, stream);
   Tensors t{q, lq, k, lk, v, lv, nullptr, 0, nullptr, 0, nullptr};
   Workspace w = carve(ws, ws_bytes);
@@ -210,6 +294,30 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
     return fail(err, LA_ERR_WORKSPACE, "workspace smaller than la_backward_workspace_bytes");
   if (sh && !p->causal && (sh->carry_in || sh->carry_suffix || sh->row_offset))
     return fail(err, LA_ERR_UNSUPPORTED, "sequence sharding is defined for the causal mask");
+  if (pad_eligible(p, sh, lq, lk, lv, lw)) {
+    const la_problem p2 = padded_problem(p);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t T = (size_t)p->groups * p->seq_len * 128 * 2;
+    char* buf = nullptr;
+    keep_pool_memory();
+    if (cudaMallocAsync((void**)&buf, 8 * T, st) != cudaSuccess) return cuda_fail(err, cudaErrorMemoryAllocation);
+    pad_copy(buf, q, p, true, true, st);
+    pad_copy(buf + T, k, p, true, true, st);
+    pad_copy(buf + 2 * T, v, p, false, true, st);
+    pad_copy(buf + 3 * T, o, p, false, true, st);
+    pad_copy(buf + 4 * T, omega, p, false, true, st);
+    la_status s2 = backward_impl(&p2, nullptr, buf, LA_SEQUENCE_MAJOR, buf + T, LA_SEQUENCE_MAJOR, buf + 2 * T,
+                                 LA_FEATURE_MAJOR, buf + 3 * T, buf + 4 * T, LA_FEATURE_MAJOR, g, buf + 5 * T,
+                                 buf + 6 * T, buf + 7 * T, ws, ws_bytes, stream, nullptr);
+    if (s2 == LA_OK) {
+      pad_copy(dq, buf + 5 * T, p, true, false, st);
+      pad_copy(dk, buf + 6 * T, p, false, false, st);
+      pad_copy(dv, buf + 7 * T, p, false, false, st);
+    }
+    cudaFreeAsync(buf, st);
+    if (s2 != LA_OK) return fail(err, s2, "padded backward failed");
+    return finish(ws, st, err);
+  }
   Launch L = make_launch(p, sh, stream);
   Tensors t{q, lq, k, lk, v, lv, o, LA_FEATURE_MAJOR, omega, lw, g};
   Workspace w = carve(ws, ws_bytes);
@@ -428,12 +536,24 @@ la_status la_backward_saved(const la_problem* p, const void* q, la_layout lq, co
 
 size_t la_forward_workspace_bytes(const la_problem* p) {
   if (!p || p->groups <= 0 || p->seq_len <= 0 || p->dim <= 0) return kFlagBytes;
-  return ws_bytes_for(fwd_floats(p));
+  size_t f = fwd_floats(p);
+  if (pad_eligible(p, nullptr, LA_SEQUENCE_MAJOR, LA_SEQUENCE_MAJOR, LA_FEATURE_MAJOR, -1)) {
+    const la_problem p2 = padded_problem(p);
+    const size_t f2 = fwd_floats(&p2);
+    if (f2 > f) f = f2;
+  }
+  return ws_bytes_for(f);
 }
 
 size_t la_backward_workspace_bytes(const la_problem* p) {
   if (!p || p->groups <= 0 || p->seq_len <= 0 || p->dim <= 0) return kFlagBytes;
-  return ws_bytes_for(bwd_floats(p));
+  size_t f = bwd_floats(p);
+  if (pad_eligible(p, nullptr, LA_SEQUENCE_MAJOR, LA_SEQUENCE_MAJOR, LA_FEATURE_MAJOR, LA_FEATURE_MAJOR)) {
+    const la_problem p2 = padded_problem(p);
+    const size_t f2 = bwd_floats(&p2);
+    if (f2 > f) f = f2;
+  }
+  return ws_bytes_for(f);
 }
 
 // validate_plan (plan.cpp:49-62), same order of checks and messages.
