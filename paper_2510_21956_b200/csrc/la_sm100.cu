@@ -97,6 +97,11 @@ constexpr int kFStage = kFT + 2 * kKPanel + kFT;  // Q, K(+z), V^T  = 52 KB
 constexpr int kOffK = kFT, kOffV = kFT + 2 * kKPanel;
 constexpr uint32_t kF_T1 = 0, kF_OT = 128, kF_ST = 256, kF_SB = 384;
 
+// z (a sum of up to N keys) is handed to the tensor core as two 16-bit rows; fp16
+// would overflow at |z| > 65504, so fp16 rows carry z / 256 and g multiplies back.
+template <bool kBF16>
+__host__ __device__ constexpr float z_row_scale() { return kBF16 ? 1.f : 1.f / 256.f; }
+
 template <bool kBF16>
 __device__ __forceinline__ float h2f_fwd(uint16_t h) {
   return kBF16 ? __bfloat162float(__ushort_as_bfloat16(h)) : __half2float(__ushort_as_half(h));
@@ -281,7 +286,7 @@ __global__ void __launch_bounds__(448, 1)
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(t1_empty);
-        qz = __uint_as_float(zh) + __uint_as_float(zl);
+        qz = (__uint_as_float(zh) + __uint_as_float(zl)) * (1.f / z_row_scale<kBF16>());
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
           const int t0 = 2 * u;
@@ -324,6 +329,7 @@ __global__ void __launch_bounds__(448, 1)
     const float b = prm.b;
     // z_hi / z_lo of feature m = r into rows 64, 65 of the K-tile panel holding column m
     auto put_zrows = [&](int c, float z) {
+      z *= z_row_scale<kBF16>();
       uint8_t* kt = smem + (c % kFStages) * kFStage + kOffK + (r >> 6) * kKPanel;
       const __nv_bfloat16 h = __float2bfloat16_rn(z);
       const float lo = z - __bfloat162float(h);
@@ -705,7 +711,7 @@ __global__ void __launch_bounds__(192, 1)
       tmem_st32(tmem + lb + kFF_SB + half * 32, pk);
     }
     tmem_st_wait();
-    const float z = tot[kD * kD + r];
+    const float z = tot[kD * kD + r] * z_row_scale<kBF16>();
     uint16_t hv, lv;
     if (kBF16) {
       const __nv_bfloat16 h = __float2bfloat16_rn(z);
@@ -780,7 +786,7 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_before();
       mbar_arrive(&ot_empty[bb]);
       if (lower) {
-        const float gi = an + b * (__uint_as_float(zh) + __uint_as_float(zl));
+        const float gi = an + b * (__uint_as_float(zh) + __uint_as_float(zl)) * (1.f / z_row_scale<kBF16>());
         if (fabsf(gi) < kEpsF32) flag_degenerate(prm.flag, grp, row0 + ih);
         ginv_s[bb * kCF + ih] = 1.f / gi;
         prm.gout[grp * prm.N + row0 + ih] = gi;

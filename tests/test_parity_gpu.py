@@ -340,3 +340,20 @@ def test_bf16_small_head_dim_padded_tcgen05(cuda, causal, D):
     for key in ("out", "dq", "dk", "dv"):
         assert max_abs(res[key], ref[key]) <= BF16_ABS, (D, key)
     assert rel_err(res["g"], ref["g"]) <= 1e-3
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_f16_key_sum_beyond_half_range(cuda, causal):
+    # every key is e_0, so z_0 = N = 131072 > 65504 (the fp16 maximum): the q.z term
+    # must not overflow on the fp16 tensor-core path
+    G, N, D = 1, 131072, 128
+    rng = np.random.default_rng(11)
+    q = O.normalize_rows(rng.uniform(-1, 1, (G, N, D)))
+    k = np.zeros((G, N, D))
+    k[..., 0] = 1.0
+    v = rng.uniform(-1, 1, (G, N, D))
+    res = run_dev(q, k, v, None, "f16", cuda, causal=causal)
+    ref = oracle_all(res, causal, dtype=np.float32)
+    assert np.isfinite(res["out"]).all() and np.isfinite(res["g"]).all()
+    assert max_abs(res["out"], ref["out"]) <= BF16_ABS
+    assert rel_err(res["g"], ref["g"]) <= 1e-3
