@@ -510,17 +510,23 @@ __global__ void __launch_bounds__(448, 1)
 }
 
 // ================================================================ segment aggregates
-// Per (g, segment): S = sum_t k_t^T v_t (stored X[m][j]), z = sum k, sigma = sum v,
-// count; the record layout of la_simt.cu's k_seg_sums (internal.h).
+// Per (g, unit): S = sum_t k_t^T v_t (stored X[m][j]), z = sum k, sigma = sum v,
+// count; the record layout of la_simt.cu's k_seg_sums (internal.h). Everything is on
+// the tensor core: S^T|sigma = V^T [K | 1] (a constant ones panel appended to the K
+// tile gives N = 144, column 128 = sigma) and Z = K^T 1 (M=128 lanes m, N=16 against
+// a constant ones tile), so the epilogue warps only read TMEM once per unit.
+// Stage: K [128 t][128 m] (2 panels) | ones panel | V^T [128 j][128 t] (2 panels).
+constexpr int kAggStage = 2 * kTile + kPanel;  // 80 KB
+constexpr int kAggOffOnes = kTile, kAggOffV = kTile + kPanel;
+
 template <bool kBF16>
 __global__ void __launch_bounds__(192, 1)
     k_fwd_agg_tc(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                  float* states, int64_t N, int64_t seg_len, int P) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint8_t* sK = smem;                  // [2][32K]
-  uint8_t* sV = smem + 2 * kTile;      // [2][32K]
-  uint64_t* bars = (uint64_t*)(smem + 4 * kTile);
+  uint8_t* sOnesZ = smem + 2 * kAggStage;   // [16 rows][128 t] ones (K-major B of the Z MMA)
+  uint64_t* bars = (uint64_t*)(sOnesZ + 4096);
   uint64_t* full = bars;
   uint64_t* empty = bars + 2;
   uint64_t* done = bars + 4;
@@ -529,44 +535,60 @@ __global__ void __launch_bounds__(192, 1)
   const int64_t grp = blockIdx.y;
   const int64_t s0 = (int64_t)p * seg_len;
   const int64_t s1 = lmin(N, s0 + seg_len);
-  const int nc = (int)((s1 - s0) / kC);
+  const int nc = s1 > s0 ? (int)((s1 - s0) / kC) : 0;
   const uint32_t warp = warp_id();
   if (warp == 0 && elect_one()) {
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1 + 128);
+      mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<128>(tslot);
+  if (warp == 1) tmem_alloc<256>(tslot);
+  if (warp >= 2) {  // constant ones: the N-augmentation panel of each stage and the Z tile
+    const uint32_t one2 = kBF16 ? 0x3F803F80u : 0x3C003C00u;
+    const int t = (int)threadIdx.x - 64;
+    for (int st = 0; st < 2; ++st) {
+      uint4* op = (uint4*)(smem + st * kAggStage + kAggOffOnes);
+      for (int e = t; e < kPanel / 16; e += 128) op[e] = make_uint4(one2, one2, one2, one2);
+    }
+    for (int e = t; e < 4096 / 16; e += 128) ((uint4*)sOnesZ)[e] = make_uint4(one2, one2, one2, one2);
+    fence_proxy_async();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tslot;
+  const uint32_t tmem = *tslot;  // [0,144) S^T | sigma, [160,176) Z
   if (warp == 0) {
     if (elect_one()) {
       for (int c = 0; c < nc; ++c) {
         const int s = c & 1;
         if (c >= 2) mbar_wait(&empty[s], ((c >> 1) & 1) ^ 1);
         const int64_t row0 = s0 + (int64_t)c * kC;
+        uint8_t* st = smem + s * kAggStage;
         mbar_expect_tx(&full[s], 2 * kTile);
-        tma_load_3d(sK + s * kTile, &tmK, &full[s], 0, (int)(grp * N + row0), 0);
-        tma_load_3d(sV + s * kTile, &tmV, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
+        tma_load_3d(st, &tmK, &full[s], 0, (int)(grp * N + row0), 0);
+        tma_load_3d(st + kAggOffV, &tmV, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
       }
     }
   } else if (warp == 1) {
-    const uint32_t id_kmn = idesc_f16(128, 128, kBF16 ? 1 : 0, 0, 1);
-    const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
+    const uint32_t id_S = idesc_f16(128, 144, kBF16 ? 1 : 0, 0, 1);  // A = V^T (K-major), B = [K | 1] (MN-major)
+    const uint32_t id_Z = idesc_f16(128, 16, kBF16 ? 1 : 0, 1, 0);   // A = K^T (MN-major), B = ones (K-major)
+    const uint32_t aZ = smem_u32(sOnesZ);
     for (int c = 0; c < nc; ++c) {
       const int s = c & 1;
+      const uint32_t aK = smem_u32(smem + s * kAggStage), aV = aK + kAggOffV;
       mbar_wait(&full[s], (c >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
         for (int ks = 0; ks < 8; ++ks)
-          mma_ss(tmem, kdesc(aV + s * kTile, ks), mndesc(aK + s * kTile, ks), id_kmn,
+          mma_ss(tmem, kdesc(aV, ks), mndesc(aK, ks), id_S, (c > 0 || ks > 0) ? 1u : 0u);
+        for (int ks = 0; ks < 8; ++ks)
+          mma_ss(tmem + 160, mndesc(aK, ks),
+                 sdesc_sw128(aZ, 16, 1024) + (uint64_t)(((ks >> 2) * 16 * 128 + (ks & 3) * 32) >> 4), id_Z,
                  (c > 0 || ks > 0) ? 1u : 0u);
         mma_commit(&empty[s]);
         if (c == nc - 1) mma_commit(done);
@@ -576,29 +598,6 @@ __global__ void __launch_bounds__(192, 1)
   } else {
     const uint32_t qd = warp & 3;
     const int r = (int)(qd * 32 + lane_id());
-    float zs = 0.f, vs = 0.f;
-    for (int c = 0; c < nc; ++c) {
-      const int s = c & 1;
-      mbar_wait(&full[s], (c >> 1) & 1);
-      const uint8_t* k_t = sK + s * kTile;
-      const uint8_t* v_t = sV + s * kTile;
-#pragma unroll 4
-      for (int t8 = 0; t8 < kC; t8 += 8) {
-        const uint4 v4 = *(const uint4*)(v_t + sw128_off(r, t8, kD));
-        const uint32_t w4[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float2 f = unpack2<kBF16>(w4[u]);
-          vs += f.x + f.y;
-        }
-      }
-#pragma unroll 8
-      for (int t = 0; t < kC; ++t) {
-        const uint16_t h = *(const uint16_t*)(k_t + sw128_off(t, r, kC));
-        zs += kBF16 ? __bfloat162float(__ushort_as_bfloat16(h)) : __half2float(__ushort_as_half(h));
-      }
-      mbar_arrive(&empty[s]);
-    }
     float* st = states + (grp * P + p) * state_floats(kD);
     if (nc > 0) {
       mbar_wait(done, 0);
@@ -611,20 +610,26 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int u = 0; u < 32; ++u) st[(m0 + u) * kD + r] = __uint_as_float(x[u]);  // X[m][j=r]
       }
+      uint32_t sg, s2_, zz, z2;
+      tmem_ld2(tmem + lane_base + 128, sg, s2_);
+      tmem_ld2(tmem + lane_base + 160, zz, z2);
+      tmem_ld_wait();
+      st[kD * kD + r] = __uint_as_float(zz);        // z_m (lane r = m of Z)
+      st[kD * kD + kD + r] = __uint_as_float(sg);   // sigma_j (lane r = j of S^T)
     } else {
       for (int m = 0; m < kD; ++m) st[m * kD + r] = 0.f;
+      st[kD * kD + r] = 0.f;
+      st[kD * kD + kD + r] = 0.f;
     }
-    st[kD * kD + r] = zs;
-    st[kD * kD + kD + r] = vs;
-    if (r == 0) st[kD * kD + 2 * kD] = (float)(s1 - s0);
+    if (r == 0) st[kD * kD + 2 * kD] = (float)(s1 > s0 ? s1 - s0 : 0);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<128>(tmem);
+  if (warp == 1) tmem_dealloc<256>(tmem);
 }
 
 constexpr size_t kFwdSmem = kFStages * kFStage + 2 * 8192 + 2 * kFT + 256 + (4 * kCF + kD) * 4 + 1024;
-constexpr size_t kAggSmem = 4 * kTile + 128 + 1024;
+constexpr size_t kAggSmem = 2 * kAggStage + 4096 + 128 + 1024;
 
 // ================================================================ non-causal forward
 // forward_full (forward_kernels.hpp:133-206): with the totals S = sum k^T v, z = sum k,
