@@ -96,6 +96,7 @@ constexpr int kFPrefetch = 0;            // L2 prefetch distance (chunks) ahead 
 constexpr int kFStage = kFT + 2 * kKPanel + kFT;  // Q, K(+z), V^T  = 52 KB
 constexpr int kOffK = kFT, kOffV = kFT + 2 * kKPanel;
 constexpr uint32_t kF_T1 = 0, kF_OT = 128, kF_ST = 256, kF_SB = 384;
+constexpr uint32_t kHalfLanes = 16u << 16;  // TMEM lane offset of the upper M=64 half
 
 // z (a sum of up to N keys) is handed to the tensor core as two 16-bit rows; fp16
 // would overflow at |z| > 65504, so fp16 rows carry z / 256 and g multiplies back.
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(448, 1)
     // ------------------------------------------------------------ MMA issuer
     // Per chunk: M3(c) = S^T and Z^T updates, M2(c) = O^T, then M1(c+1) = next T1.
     constexpr uint32_t fmt = kBF16 ? 1 : 0;
-    const uint32_t id_T1 = idesc_f16(64, 80, fmt, 0, 0);
+    const uint32_t id_T1 = idesc_f16(64, 40, fmt, 0, 0);
     const uint32_t id_ST = idesc_f16(128, 128, fmt, 0, 1);
     const uint32_t id_OT = idesc_f16(128, 64, fmt, 0, 0);
     const uint32_t a0 = smem_u32(smem), aP = smem_u32(sP);
@@ -220,9 +221,11 @@ __global__ void __launch_bounds__(448, 1)
       mbar_wait(zrow_ready, c & 1);
       if (c >= 1) mbar_wait(t1_empty, (c - 1) & 1);
       tc_fence_after();
-      if (elect_one()) {
+      if (elect_one()) {  // key rows 0..39 -> lower lane half, rows 40..79 (incl. z) -> upper half
         for (int ks = 0; ks < 8; ++ks)
           mma_ss(tmem + kF_T1, kd64(aQ, ks, 64), kd64(aQ + kOffK, ks, 80), id_T1, ks > 0);
+        for (int ks = 0; ks < 8; ++ks)
+          mma_ss(tmem + kF_T1 + kHalfLanes, kd64(aQ, ks, 64), kd64(aQ + kOffK + 40 * 128, ks, 80), id_T1, ks > 0);
         mma_commit(t1_full);
       }
       __syncwarp();
@@ -276,30 +279,34 @@ __global__ void __launch_bounds__(448, 1)
       mbar_wait(t1_full, c & 1);
       if (et == 0) trace(1, c, 3);
       tc_fence_after();
-      uint32_t pk[32];
+      // lower lanes hold T1 columns t = 0..39 of row ih, upper lanes t = 40..79 (t = 64, 65:
+      // q . z_hi, q . z_lo); each half builds its part of P' and of the row sum
+      uint32_t pk[20];
       float rs0 = 0.f, rs1 = 0.f, qz;
       {
-        uint32_t x[64], zh, zl;
+        uint32_t x[40];
         tmem_ld32(tmem + lane_base + kF_T1, *(uint32_t(*)[32])x);
-        tmem_ld32(tmem + lane_base + kF_T1 + 32, *(uint32_t(*)[32])(x + 32));
-        tmem_ld2(tmem + lane_base + kF_T1 + 64, zh, zl);
+        tmem_ld8(tmem + lane_base + kF_T1 + 32, *(uint32_t(*)[8])(x + 32));
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(t1_empty);
-        qz = (__uint_as_float(zh) + __uint_as_float(zl)) * (1.f / z_row_scale<kBF16>());
+        const int tb = lower ? 0 : 40;
+        qz = lower ? 0.f : (__uint_as_float(x[24]) + __uint_as_float(x[25])) * (1.f / z_row_scale<kBF16>());
 #pragma unroll
-        for (int u = 0; u < 32; ++u) {
-          const int t0 = 2 * u;
-          const float p0 = t0 <= ih ? a + b * __uint_as_float(x[2 * u]) : 0.f;
+        for (int u = 0; u < 20; ++u) {
+          const int t0 = tb + 2 * u;
+          const float p0 = t0 <= ih ? a + b * __uint_as_float(x[2 * u]) : 0.f;  // t >= 64 never passes
           const float p1 = t0 + 1 <= ih ? a + b * __uint_as_float(x[2 * u + 1]) : 0.f;
           rs0 += p0;
           rs1 += p1;
           pk[u] = pack2<kBF16>(p0, p1);
         }
       }
+      const float rs = (rs0 + rs1) + __shfl_xor_sync(0xffffffffu, rs0 + rs1, 16);
+      qz += __shfl_xor_sync(0xffffffffu, qz, 16);
       if (et == 0) trace(1, c, 7);
       if (lower) {
-        const float gi = (rs0 + rs1) + a * (float)(prm.row_offset + row0) + b * qz;
+        const float gi = rs + a * (float)(prm.row_offset + row0) + b * qz;
         if (fabsf(gi) < kEpsF32) flag_degenerate(prm.flag, grp, prm.row_offset + row0 + ih);
         ginv_s[(c & 3) * kCF + ih] = 1.f / gi;
         prm.gout[grp * prm.N + row0 + ih] = gi;
@@ -308,11 +315,14 @@ __global__ void __launch_bounds__(448, 1)
       if (et == 0) trace(1, c, 4);
       if (c >= 2) mbar_wait(&o_full[bb], ((c - 2) >> 1) & 1);  // M2(c-2) drained sP[bb]
       if (et == 0) trace(1, c, 5);
-      if (lower) {
+      {  // P' row ih: lower lanes columns 0..39 (5 chunks), upper lanes 40..63 (3 chunks)
         uint8_t* pp = sP + bb * 8192;
+        const int w0 = lower ? 0 : 5, nw = lower ? 5 : 3;
 #pragma unroll
-        for (int w = 0; w < 8; ++w)
-          *(uint4*)(pp + sw128_off(ih, 8 * w, kCF)) = make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
+        for (int w = 0; w < 5; ++w)
+          if (w < nw)
+            *(uint4*)(pp + sw128_off(ih, 8 * (w0 + w), kCF)) =
+                make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
       }
       fence_proxy_async();
       mbar_arrive(p_ready);
