@@ -563,12 +563,15 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ================================================================ main reverse sweep
-// Warp roles (320 threads): 0 TMA producer; 1 MMA issuer + TMEM owner;
-// 2-5 WG-A: W_hat/s, dS/P, dK^T/dV^T out, u/c; 6-9 WG-B: bR/bS operand copies,
-// z, dQ out. Each epilogue column sum uses 16-byte loads over a conflict-free
-// (rows-by-lane) mapping and a shuffle reduction.
+// Warp roles (512 threads): 0 TMA producer; 1 MMA issuer + TMEM owner; 2-3 idle
+// (warpgroup 0 hands its registers to the epilogue warpgroups with setmaxnreg);
+// 4-7 WG-A: bR -> sR, dS/P, dV^T out, u/c increments; 8-11 WG-B: bS -> sS, z, dQ and
+// dK^T out; 12-15 WG-C: the W_hat / s pass, running up to two chunks ahead. Each
+// epilogue column sum uses 16-byte loads over a conflict-free (rows-by-lane)
+// mapping and a shuffle reduction.
+constexpr int kBwdThreads = 512;
 template <bool kBF16>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(kBwdThreads, 1)
     k_bwd_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
              const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmW,
              BwdParams prm) {
@@ -612,7 +615,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1 + 256);
     }
-    mbar_init(w_ready, 256);
+    mbar_init(w_ready, 128);
     mbar_init(s_full, 1);
     mbar_init(dpt_full, 1);
     mbar_init(dpt_empty, 128);
@@ -630,14 +633,15 @@ __global__ void __launch_bounds__(320, 1)
     const int64_t SZ = state_floats(kD);
     const int U = prm.P * prm.A;
     float* cS = prm.cmb + (grp * prm.P + p) * 2 * SZ;
-    if (warp >= 2) {
+    if (warp >= 4) {
+      const int ct = (int)threadIdx.x - 128, cn = kBwdThreads - 128;
       if (prm.skipS)
-        combine_records(cS, prm.stS + (grp * prm.P + p) * SZ, prm.stS, 0, 0, SZ, (int)threadIdx.x - 64, 256);
+        combine_records(cS, prm.stS + (grp * prm.P + p) * SZ, prm.stS, 0, 0, SZ, ct, cn);
       else
         combine_records(cS, prm.carry_pre ? prm.carry_pre + grp * SZ : nullptr, prm.stS + grp * U * SZ, 0,
-                        (p + 1) * prm.A, SZ, (int)threadIdx.x - 64, 256);
+                        (p + 1) * prm.A, SZ, ct, cn);
       combine_records(cS + SZ, prm.carry_suf ? prm.carry_suf + grp * SZ : nullptr, prm.stR + grp * U * SZ,
-                      (p + 1) * prm.A, U, SZ, (int)threadIdx.x - 64, 256);
+                      (p + 1) * prm.A, U, SZ, ct, cn);
     }
   }
   tc_fence_before();
@@ -646,7 +650,7 @@ __global__ void __launch_bounds__(320, 1)
   const uint32_t tmem = *tslot;
   // Carries (R_next, S_end, u, c, z) are written into TMEM by WG-B before any role
   // starts: the first S -= K^T V must see S_end.
-  if (warp >= 6) {
+  if (warp >= 8 && warp < 12) {
     const uint32_t qd = warp & 3;
     const int r = (int)(qd * 32 + lane_id());
     const uint32_t lb = (qd * 32u) << 16;
@@ -673,6 +677,8 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
 
+  if (warp < 4) {
+  regs_dec<96>();
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (reverse)
     if (elect_one()) {
@@ -775,32 +781,23 @@ __global__ void __launch_bounds__(320, 1)
       }
       __syncwarp();
     }
-  } else if (warp < 6) {
-    // ------------------------------------------------------------ WG-A (warps 2..5)
-    // Iteration n: dV^T out of chunk n-1, bR -> sR (E_R), dS/P (E1), du, dc of
-    // chunk n, then the W_hat/s half (rows 0..63) of chunk n+1, so that the next
-    // chunk's dPt MMA is never waiting on the W_hat pass.
+  }
+  } else {
+  regs_inc<136>();
+  if (warp < 8) {
+    // ------------------------------------------------------------ WG-A (warps 4..7)
+    // Iteration n: dV^T out of chunk n-1, bR -> sR (E_R), dS/P (E1), du, dc of chunk n.
     const uint32_t qd = warp & 3;
     const int l = (int)lane_id();
     const int r = (int)(qd * 32) + l;            // j of dV^T, m of R
     const int ih = (int)(qd * 16) + (l & 15);    // half-lane row i of M=64 accumulators
     const bool upper = l >= 16;                  // lanes 16..31 of a quadrant: upper half
     const uint32_t lb = (qd * 32u) << 16;
-    const int et = (int)threadIdx.x - 64;
+    const int et = (int)threadIdx.x - 128;
     const float a = prm.a, b = prm.b;
     const float* recR = prm.cmb + (grp * prm.P + p) * 2 * state_floats(kD) + state_floats(kD);
     float cj = recR[kD * kD + kD + r];  // c_next (j = r)
     float dc_prev = 0.f;
-    uint4 o4[4];
-    float4 g8[2];
-    auto e0 = [&](int m) {  // W_hat / partial s of chunk m (rows 0..63)
-      const int sm = m & 1;
-      mbar_wait(&full[sm], (m >> 1) & 1);
-      what_pass_half<kBF16>(smem + sm * kStage + 3 * kT64, o4, g8, s_s + (m & 3) * 2 * kCB, et, 0);
-      if (m + 1 < nc) what_prefetch_half<kBF16>(prm, grp, row_of(m + 1), et, 0, o4, g8);
-      fence_proxy_async();
-      mbar_arrive(w_ready);
-    };
     auto dv_out = [&](int m) {  // dV^T of chunk m (lanes j): acc + a c_next
       mbar_wait(gr_full, m & 1);
       tc_fence_after();
@@ -828,14 +825,13 @@ __global__ void __launch_bounds__(320, 1)
       warp_store_rows(scr_lo, scr_hi, vt, [&](int seg) { return dvb + seg * prm.N; });
       cj += dc_prev;
     };
-    if (nc > 0) what_prefetch_half<kBF16>(prm, grp, row_of(0), et, 0, o4, g8);
     // One call site per phase (the kernel's code must stay small for the I-cache):
-    // iteration n = -1 only runs E0(0); n = nc only drains dV^T(nc-1).
-    for (int n = -1; n <= nc; ++n) {
-      if (n >= 0 && et == 0) traceb(1, n, 0);
+    // iteration n = nc only drains dV^T(nc-1).
+    for (int n = 0; n <= nc; ++n) {
+      if (et == 0) traceb(1, n, 0);
       if (n >= 1) dv_out(n - 1);
       if (n == nc) break;
-      if (n >= 0) {
+      {
       const int s = n & 1;
       uint8_t* st = smem + s * kStage;
       const uint8_t* q_t = st;
@@ -936,33 +932,20 @@ __global__ void __launch_bounds__(320, 1)
       mbar_arrive(&empty[s]);
       if (et == 0) traceb(1, n, 5);
       }
-      if (n + 1 < nc) e0(n + 1);
-      if (n >= 0 && et == 0) traceb(1, n, 6);
     }
-  } else {
-    // ------------------------------------------------------------ WG-B (warps 6..9)
-    // Iteration n: dQ and dK^T out of chunk n-1, bS -> sS (E_S) and z of chunk n,
-    // then the W_hat/s half (rows 64..127) of chunk n+1.
+  } else if (warp < 12) {
+    // ------------------------------------------------------------ WG-B (warps 8..11)
+    // Iteration n: dQ and dK^T out of chunk n-1, bS -> sS (E_S) and z of chunk n.
     const uint32_t qd = warp & 3;
     const int l = (int)lane_id();
     const int r = (int)(qd * 32) + l;            // m
     const int ih = (int)(qd * 16) + (l & 15);
     const bool upper = l >= 16;
     const uint32_t lb = (qd * 32u) << 16;
-    const int eb = (int)threadIdx.x - 192;
+    const int eb = (int)threadIdx.x - 256;
     const float b = prm.b;
     const float* recR = prm.cmb + (grp * prm.P + p) * 2 * state_floats(kD) + state_floats(kD);
     float u = recR[kD * kD + r];  // u_next (m = r)
-    uint4 o4[4];
-    float4 g8[2];
-    auto e0 = [&](int m) {  // W_hat / partial s of chunk m (rows 64..127)
-      const int sm = m & 1;
-      mbar_wait(&full[sm], (m >> 1) & 1);
-      what_pass_half<kBF16>(smem + sm * kStage + 3 * kT64, o4, g8, s_s + (m & 3) * 2 * kCB + kCB, eb, 64);
-      if (m + 1 < nc) what_prefetch_half<kBF16>(prm, grp, row_of(m + 1), eb, 64, o4, g8);
-      fence_proxy_async();
-      mbar_arrive(w_ready);
-    };
     auto qk_out = [&](int m) {  // dQ (half lanes): acc - b s_i z_prev ; dK^T (lanes m): acc - b u_next
       mbar_wait(gr_full, m & 1);
       if (m >= 1) u += du_s[((m - 1) & 3) * kD + r];  // suffix sum through chunk m-1
@@ -1016,12 +999,11 @@ __global__ void __launch_bounds__(320, 1)
       uint16_t* dkb = (uint16_t*)prm.dk + (grp * kD + qd * 32) * prm.N + row0;
       warp_store_rows(scr_lo, scr_hi, vt, [&](int seg) { return dkb + seg * prm.N; });
     };
-    if (nc > 0) what_prefetch_half<kBF16>(prm, grp, row_of(0), eb, 64, o4, g8);
-    for (int n = -1; n <= nc; ++n) {
-      if (n >= 0 && eb == 0) traceb(2, n, 0);
+    for (int n = 0; n <= nc; ++n) {
+      if (eb == 0) traceb(2, n, 0);
       if (n >= 1) qk_out(n - 1);
       if (n == nc) break;
-      if (n >= 0) {
+      {
       const int s = n & 1;
       const uint8_t* k_t = smem + s * kStage + kT64;
       if (eb == 0) traceb(2, n, 1);
@@ -1072,9 +1054,31 @@ __global__ void __launch_bounds__(320, 1)
       mbar_arrive(&empty[s]);
       if (eb == 0) traceb(2, n, 4);
       }
-      if (n + 1 < nc) e0(n + 1);
-      if (n >= 0 && eb == 0) traceb(2, n, 5);
     }
+  } else {
+    // ------------------------------------------------------------ WG-C (warps 12..15)
+    // W_hat = Omega^T / g in place and the partial s_i = sum_j o_ji w_hat_ji of both
+    // row halves, chunk by chunk as the stages land (s_s ring of 4: slot m & 3 is
+    // rewritten only after the stage of chunk m + 2 was released by WG-A / WG-B).
+    const int ec = (int)threadIdx.x - 384;
+    uint4 o8[8];
+    float4 g8[2];
+    if (nc > 0) what_prefetch<kBF16>(prm, grp, row_of(0), ec, o8, g8);
+    for (int m = 0; m < nc; ++m) {
+      const int sm = m & 1;
+      if (ec == 0) traceb(3, m, 0);
+      mbar_wait(&full[sm], (m >> 1) & 1);
+      if (ec == 0) traceb(3, m, 1);
+      uint8_t* w_t = smem + sm * kStage + 3 * kT64;
+      float* sp = s_s + (m & 3) * 2 * kCB;
+      what_pass_half<kBF16>(w_t, *(const uint4(*)[4])&o8[0], g8, sp, ec, 0);
+      what_pass_half<kBF16>(w_t, *(const uint4(*)[4])&o8[4], g8, sp + kCB, ec, 64);
+      fence_proxy_async();
+      mbar_arrive(w_ready);
+      if (m + 1 < nc) what_prefetch<kBF16>(prm, grp, row_of(m + 1), ec, o8, g8);
+      if (ec == 0) traceb(3, m, 2);
+    }
+  }
   }
   tc_fence_before();
   __syncthreads();
@@ -1451,7 +1455,7 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
   }
   {
     ProfScope ps("la_bwd_causal", L.stream);
-    main_k<<<dim3(P, G), 320, kMainSmemB, L.stream>>>(mQ, mK, mV, mW, prm);
+    main_k<<<dim3(P, G), kBwdThreads, kMainSmemB, L.stream>>>(mQ, mK, mV, mW, prm);
   }
   note_launch(launches);
   return cudaGetLastError();
