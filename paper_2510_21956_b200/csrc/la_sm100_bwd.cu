@@ -59,6 +59,29 @@ __device__ __forceinline__ uint64_t mn(uint32_t tile, int ks, uint32_t panel) {
 // Per-warp transpose of 32 row segments (128 B each) through a 4 KB smem scratch
 // (XOR-swizzled 16 B chunks), then coalesced 128 B-row global stores: lane L holds
 // segment L in v[8]; dst(seg) gives the segment's global address.
+// Same with one 2 KB scratch: lanes 0-15, then lanes 16-31.
+template <typename DstFn>
+__device__ __forceinline__ void warp_store_rows_2k(uint8_t* scratch, const uint4 (&v)[8], DstFn dst) {
+  const int lane = (int)lane_id();
+  auto slot = [&](int seg, int ch) -> uint4* {
+    return (uint4*)(scratch + (seg & 15) * 128 + ((ch ^ (seg & 7)) << 4));
+  };
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if ((lane >> 4) == h) {
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) *slot(lane, ch) = v[ch];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int seg = 16 * h + 4 * k + (lane >> 3), ch = lane & 7;
+      *(uint4*)((uint8_t*)dst(seg) + ch * 16) = *slot(seg, ch);
+    }
+    __syncwarp();
+  }
+}
+
 template <typename DstFn>
 __device__ __forceinline__ void warp_store_rows(uint8_t* scratch_lo, uint8_t* scratch_hi,
                                                 const uint4 (&v)[8], DstFn dst) {
@@ -147,11 +170,12 @@ __device__ __forceinline__ void what_pass(uint8_t* w_t, const uint4 (&o8)[8], co
   }
 }
 
-// Half-tile variant used when both epilogue warpgroups share the pass: rows
-// j = jbase + 16 rr + jg (rr < 4); the partial s of this half goes to s_half.
+// Half-tile variant: rows j = jbase + 16 rr + jg (rr < 4); the partial s of this
+// half goes to s_half, and rs[rr] returns this thread's partial row sum of W_hat
+// (its 8 columns of row j).
 template <bool kBF16>
 __device__ __forceinline__ void what_pass_half(uint8_t* w_t, const uint4 (&o4)[4], const float4 (&g8)[2],
-                                               float* s_half, int et, int jbase) {
+                                               float* s_half, int et, int jbase, float (&rs)[4]) {
   const int lane = et & 31, w = et >> 5;
   const int jg = lane & 15, ig = 2 * w + (lane >> 4);
   float ginv[8] = {1.f / g8[0].x, 1.f / g8[0].y, 1.f / g8[0].z, 1.f / g8[0].w,
@@ -165,6 +189,7 @@ __device__ __forceinline__ void what_pass_half(uint8_t* w_t, const uint4 (&o4)[4
     const uint32_t wa[4] = {wv.x, wv.y, wv.z, wv.w};
     const uint32_t oa[4] = {o4[rr].x, o4[rr].y, o4[rr].z, o4[rr].w};
     uint32_t res[4];
+    float rsum = 0.f;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const float2 wf = unpack2<kBF16>(wa[u]);
@@ -172,8 +197,10 @@ __device__ __forceinline__ void what_pass_half(uint8_t* w_t, const uint4 (&o4)[4
       const float w0 = wf.x * ginv[2 * u], w1 = wf.y * ginv[2 * u + 1];
       sp[2 * u] += of.x * w0;
       sp[2 * u + 1] += of.y * w1;
+      rsum += w0 + w1;
       res[u] = pack2<kBF16>(w0, w1);
     }
+    rs[rr] = rsum;
     *p = make_uint4(res[0], res[1], res[2], res[3]);
   }
   // Reduce-scatter of the 8 partial sums over the 16 lanes sharing ig: each exchange
@@ -510,7 +537,8 @@ __global__ void __launch_bounds__(320, 1)
         o4[rr] = *(const uint4*)(st + kAOffO + sw128_off(64 * half + 16 * rr + jg, 8 * ig, 128));
       const float4 gc[2] = {g8[0], g8[1]};
       if (c + 1 < nc) g_prefetch(c + 1);
-      what_pass_half<kBF16>(st + kAOffW, o4, gc, sp + half * kCB, eh, 64 * half);
+      float rs_unused[4];
+      what_pass_half<kBF16>(st + kAOffW, o4, gc, sp + half * kCB, eh, 64 * half, rs_unused);
       named_bar(1, 256);  // both halves' partial s of chunk c are in s_part
       if (et < kCB) {     // s rows (hi, lo) of the U = Q^T s MMA
         const float si = sp[et] + sp[kCB + et];
@@ -594,10 +622,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* gr_full = bars + 11;
   uint64_t* gr_empty = bars + 12;
   uint64_t* r_full = bars + 13;
+  uint64_t* s_rdy = bars + 14;  // [2] partial s of chunk m in s_s (WG-C -> WG-B's du)
   uint32_t* tslot = (uint32_t*)(bars + 16);
-  float* s_s = (float*)(bars + 20);   // [4 chunks][2 halves][64]  partial s (WG-A rows 0..63, WG-B 64..127)
+  float* s_s = (float*)(bars + 20);   // [4 chunks][2 halves][64]  partial s (rows j 0..63, 64..127)
   float* du_s = s_s + 8 * kCB;        // [4][128]  WG-A -> WG-B suffix increments of u
   float* zbuf = du_s + 4 * kD;        // [2][128]  z_prev per chunk parity
+  float* dcp = zbuf + 2 * kD;         // [4][4][128] WG-C per-warp partial row sums of W_hat
 
   const int p = blockIdx.x;
   const int64_t grp = blockIdx.y;
@@ -613,7 +643,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     tma_prefetch(&tmW);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1 + 256);
+      mbar_init(&empty[s], 1 + 128);
     }
     mbar_init(w_ready, 128);
     mbar_init(s_full, 1);
@@ -625,6 +655,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(gr_full, 1);
     mbar_init(gr_empty, 256);
     mbar_init(r_full, 1);
+    mbar_init(&s_rdy[0], 128);
+    mbar_init(&s_rdy[1], 128);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
@@ -786,7 +818,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   regs_inc<136>();
   if (warp < 8) {
     // ------------------------------------------------------------ WG-A (warps 4..7)
-    // Iteration n: dV^T out of chunk n-1, bR -> sR (E_R), dS/P (E1), du, dc of chunk n.
+    // Iteration n: dV^T out of chunk n-1 (then c += dc(n-1)), bR -> sR (E_R) and
+    // dS/P (E1) of chunk n.
     const uint32_t qd = warp & 3;
     const int l = (int)lane_id();
     const int r = (int)(qd * 32) + l;            // j of dV^T, m of R
@@ -797,7 +830,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const float a = prm.a, b = prm.b;
     const float* recR = prm.cmb + (grp * prm.P + p) * 2 * state_floats(kD) + state_floats(kD);
     float cj = recR[kD * kD + kD + r];  // c_next (j = r)
-    float dc_prev = 0.f;
     auto dv_out = [&](int m) {  // dV^T of chunk m (lanes j): acc + a c_next
       mbar_wait(gr_full, m & 1);
       tc_fence_after();
@@ -823,7 +855,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_arrive(gr_empty);
       uint16_t* dvb = (uint16_t*)prm.dv + (grp * kD + qd * 32) * prm.N + row_of(m);
       warp_store_rows(scr_lo, scr_hi, vt, [&](int seg) { return dvb + seg * prm.N; });
-      cj += dc_prev;
+      const float* dq4 = dcp + (m & 3) * 4 * kD;  // WG-C's partial row sums of W_hat (chunk m)
+      cj += (dq4[r] + dq4[kD + r]) + (dq4[2 * kD + r] + dq4[3 * kD + r]);
     };
     // One call site per phase (the kernel's code must stay small for the I-cache):
     // iteration n = nc only drains dV^T(nc-1).
@@ -832,10 +865,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (n >= 1) dv_out(n - 1);
       if (n == nc) break;
       {
-      const int s = n & 1;
-      uint8_t* st = smem + s * kStage;
-      const uint8_t* q_t = st;
-      const uint8_t* w_t = st + 3 * kT64;
       const float* sA = s_s + (n & 3) * 2 * kCB;
       const float* sB = sA + kCB;
       if (et == 0) traceb(1, n, 1);
@@ -895,41 +924,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_arrive(dpt_empty);
       mbar_arrive(ps_ready);
       if (et == 0) traceb(1, n, 4);
-      // ---- du_m = sum_i q_im s_i of this chunk -> du_s[n & 3] for WG-B
-      {
-        const int mg = et >> 3, tg = et & 7;  // rows tg + 8k: conflict-free quarter-warps
-        float du[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
-        for (int k8 = 0; k8 < kCB / 8; ++k8) {
-          const int i = tg + 8 * k8;
-          const uint4 v4 = *(const uint4*)(q_t + sw128_off(i, 8 * mg, kCB));
-          const float w = sA[i] + sB[i];
-          const uint32_t xx[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float2 f2 = unpack2<kBF16>(xx[q]);
-            du[2 * q] += w * f2.x;
-            du[2 * q + 1] += w * f2.y;
-          }
-        }
-        du_s[(n & 3) * kD + 8 * mg + tg] = reduce_scatter8(du, tg);
-      }
-      // ---- dc_j = sum_i w_hat_ji (added to c after this chunk's dV^T is out)
-      {
-        float dc = 0.f;
-#pragma unroll 2
-        for (int i8 = 0; i8 < kCB; i8 += 8) {
-          const uint4 v4 = *(const uint4*)(w_t + sw128_off(r, i8, 128));
-          const uint32_t w4[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float2 f2 = unpack2<kBF16>(w4[q]);
-            dc += f2.x + f2.y;
-          }
-        }
-        dc_prev = dc;
-      }
-      mbar_arrive(&empty[s]);
       if (et == 0) traceb(1, n, 5);
       }
     }
@@ -1005,7 +999,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (n == nc) break;
       {
       const int s = n & 1;
-      const uint8_t* k_t = smem + s * kStage + kT64;
+      const uint8_t* q_t = smem + s * kStage;
+      const uint8_t* k_t = q_t + kT64;
+      const float* sA = s_s + (n & 3) * 2 * kCB;
+      const float* sB = sA + kCB;
       if (eb == 0) traceb(2, n, 1);
       // ---- E_S: b S_prev -> sS
       mbar_wait(s_full, n & 1);
@@ -1030,6 +1027,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       mbar_arrive(sS_ready);
       if (eb == 0) traceb(2, n, 3);
+      // ---- du_m = sum_i q_im s_i of this chunk -> du_s[n & 3] (read by qk_out after the barrier below)
+      mbar_wait(&s_rdy[s], (n >> 1) & 1);  // slot s next completes at chunk n + 2, after our empty arrival
+      {
+        const int mg = eb >> 3, tg = eb & 7;  // rows tg + 8k: conflict-free quarter-warps
+        float du[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 2
+        for (int k8 = 0; k8 < kCB / 8; ++k8) {
+          const int i = tg + 8 * k8;
+          const uint4 v4 = *(const uint4*)(q_t + sw128_off(i, 8 * mg, kCB));
+          const float w = sA[i] + sB[i];
+          const uint32_t xx[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 f2 = unpack2<kBF16>(xx[q]);
+            du[2 * q] += w * f2.x;
+            du[2 * q + 1] += w * f2.y;
+          }
+        }
+        du_s[(n & 3) * kD + 8 * mg + tg] = reduce_scatter8(du, tg);
+      }
       // ---- z_prev(n) = z_prev(n-1) - sum_t k_t over this chunk -> zbuf[n & 1]
       {
         const int mg = eb >> 3, tg = eb & 7;  // columns 8 mg.., rows tg + 8 k
@@ -1060,7 +1077,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // W_hat = Omega^T / g in place and the partial s_i = sum_j o_ji w_hat_ji of both
     // row halves, chunk by chunk as the stages land (s_s ring of 4: slot m & 3 is
     // rewritten only after the stage of chunk m + 2 was released by WG-A / WG-B).
+    // W_hat = Omega^T / g in place, the partial s_i = sum_j o_ji w_hat_ji of both row
+    // halves and per-warp partial row sums of W_hat (dc, dcp[m & 3]), chunk by chunk
+    // as the stages land. Rings of 4: slot m & 3 is rewritten only after the stage
+    // of chunk m + 2 was released, i.e. after its readers finished chunk m.
     const int ec = (int)threadIdx.x - 384;
+    const uint32_t qd = warp & 3;
+    const int l = (int)lane_id();
     uint4 o8[8];
     float4 g8[2];
     if (nc > 0) what_prefetch<kBF16>(prm, grp, row_of(0), ec, o8, g8);
@@ -1071,10 +1094,23 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (ec == 0) traceb(3, m, 1);
       uint8_t* w_t = smem + sm * kStage + 3 * kT64;
       float* sp = s_s + (m & 3) * 2 * kCB;
-      what_pass_half<kBF16>(w_t, *(const uint4(*)[4])&o8[0], g8, sp, ec, 0);
-      what_pass_half<kBF16>(w_t, *(const uint4(*)[4])&o8[4], g8, sp + kCB, ec, 64);
+      float* dq4 = dcp + (m & 3) * 4 * kD + qd * kD;
+      float rs[4];
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        uint4 o4[4];
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) o4[rr] = h ? o8[4 + rr] : o8[rr];
+        what_pass_half<kBF16>(w_t, o4, g8, sp + h * kCB, ec, 64 * h, rs);
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+          const float v = rs[rr] + __shfl_xor_sync(0xffffffffu, rs[rr], 16);
+          if (l < 16) dq4[64 * h + 16 * rr + l] = v;
+        }
+      }
       fence_proxy_async();
       mbar_arrive(w_ready);
+      mbar_arrive(&s_rdy[sm]);
       if (m + 1 < nc) what_prefetch<kBF16>(prm, grp, row_of(m + 1), ec, o8, g8);
       if (ec == 0) traceb(3, m, 2);
     }
@@ -1239,7 +1275,9 @@ __global__ void __launch_bounds__(320, 1)
       const float* gp = prm.g + grp * prm.N + row_of(m) + 8 * ig;
       g8[0] = __ldg((const float4*)gp);
       g8[1] = __ldg((const float4*)(gp + 4));
-      what_pass_half<kBF16>(st + 2 * kT64, o4, g8, s_s + (m & 3) * 2 * kCB + (jbase ? kCB : 0), et, jbase);
+      float rs_unused[4];
+      what_pass_half<kBF16>(st + 2 * kT64, o4, g8, s_s + (m & 3) * 2 * kCB + (jbase ? kCB : 0), et, jbase,
+                            rs_unused);
       fence_proxy_async();
       mbar_arrive(&w_ready[sm]);
       mbar_arrive(&empty[sm]);
@@ -1325,7 +1363,8 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 constexpr size_t kAggSmemB = 2 * kStage + 512 + 1024;
-constexpr size_t kMainSmemB = 2 * kStage + 2 * 8192 + 2 * 32768 + 160 + (8 * kCB + 6 * kD) * 4 + 1024;
+constexpr size_t kMainSmemB = 2 * kStage + 2 * 8192 + 2 * 32768 + 160 + (8 * kCB + 22 * kD) * 4 + 1024;
+static_assert(kMainSmemB <= 232448, "backward smem");
 
 int tcb_segments(int64_t G, int64_t N) { return tc_segments(G, N); }
 

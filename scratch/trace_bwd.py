@@ -23,12 +23,12 @@ t0 = t[0, 10, 0]
 t = t - t0
 t[t < -10**9] = -1
 R = range(10, 14)
-print("MMA : start, sS_ready, ps_ready, dQ+T(n+1) issued, sR_ready, v_empty, all issued")
-for c in R: print(c, t[0, c, :7].tolist())
-print("WG-A: E_R(n) done, dV(n) out, dc+e0(n+1) done")
-for c in R: print(c, t[1, c, :3].tolist())
-print("WG-B: dQ(n) out, E_S(n) done, dK(n) out, z/du(n) done")
-for c in R: print(c, t[2, c, :4].tolist())
-print("WG-C: t_full(n), v_full(n-1) passed, ps_ready, e0(n+1) done")
-for c in R: print(c, t[3, c, :4].tolist())
+print("MMA : start, full, dpt_empty, w_ready, sS_ready, ps_ready, gr_empty, sR_ready")
+for c in R: print(c, t[0, c, :8].tolist())
+print("WG-A: start, dv_out done, E_R done, dpt_full, E1 done, du/dc done")
+for c in R: print(c, t[1, c, :6].tolist())
+print("WG-B: start, qk_out done, s_full, E_S done, z done")
+for c in R: print(c, t[2, c, :5].tolist())
+print("WG-C: start, full, done")
+for c in R: print(c, t[3, c, :3].tolist())
 print("period", np.diff(t[0, 5:60, 0]).mean())
