@@ -619,15 +619,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* sS_ready = bars + 8;
   uint64_t* ps_ready = bars + 9;
   uint64_t* sR_ready = bars + 10;
-  uint64_t* gr_full = bars + 11;
-  uint64_t* gr_empty = bars + 12;
+  uint64_t* gkv_full = bars + 11;   // dK^T, dV^T accumulators complete
+  uint64_t* gkv_empty = bars + 12;  // ... drained (WG-A dV^T, WG-B dK^T)
   uint64_t* r_full = bars + 13;
   uint64_t* s_rdy = bars + 14;  // [2] partial s of chunk m in s_s (WG-C -> WG-B's du)
   uint32_t* tslot = (uint32_t*)(bars + 16);
+  uint64_t* gq_full = bars + 17;    // dQ accumulator complete
+  uint64_t* gq_empty = bars + 18;   // ... drained (WG-B)
   float* s_s = (float*)(bars + 20);   // [4 chunks][2 halves][64]  partial s (rows j 0..63, 64..127)
-  float* du_s = s_s + 8 * kCB;        // [4][128]  WG-A -> WG-B suffix increments of u
-  float* zbuf = du_s + 4 * kD;        // [2][128]  z_prev per chunk parity
-  float* dcp = zbuf + 2 * kD;         // [4][4][128] WG-C per-warp partial row sums of W_hat
+  float* du_s = s_s + 8 * kCB;        // [4][128]  du per chunk (WG-B)
+  float* zbuf = du_s + 4 * kD;        // [4][128]  z_prev per chunk (WG-A -> WG-B's dQ drain)
+  float* dcp = zbuf + 4 * kD;         // [4][4][128] WG-C per-warp partial row sums of W_hat
 
   const int p = blockIdx.x;
   const int64_t grp = blockIdx.y;
@@ -643,7 +645,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     tma_prefetch(&tmW);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1 + 128);
+      mbar_init(&empty[s], 1 + 256);
     }
     mbar_init(w_ready, 128);
     mbar_init(s_full, 1);
@@ -651,9 +653,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(dpt_empty, 128);
     mbar_init(sS_ready, 128);
     mbar_init(ps_ready, 128);
-    mbar_init(sR_ready, 128);
-    mbar_init(gr_full, 1);
-    mbar_init(gr_empty, 256);
+    mbar_init(sR_ready, 256);
+    mbar_init(gkv_full, 1);
+    mbar_init(gkv_empty, 256);
+    mbar_init(gq_full, 1);
+    mbar_init(gq_empty, 128);
     mbar_init(r_full, 1);
     mbar_init(&s_rdy[0], 128);
     mbar_init(&s_rdy[1], 128);
@@ -703,7 +707,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tmem_st32(tmem + lb + kS + j0, xs);
     }
     tmem_st_wait();
-    zbuf[kD + r] = recS[kD * kD + r];  // z at the segment end (read as chunk "-1")
+    zbuf[3 * kD + r] = recS[kD * kD + r];  // z at the segment end (read as chunk "-1")
   }
   tc_fence_before();
   __syncthreads();
@@ -737,6 +741,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
+    // Block n: dK^T / dV^T (+ R) as soon as E1(n), E_R(n) and the previous drains are
+    // done, then dQ(n); then S -= K^T V, T1 and dPt of chunk n+1, which feed the next
+    // E1 while this chunk's outputs drain.
     constexpr uint32_t f = kBF16 ? 1 : 0;
     const uint32_t id_T1 = idesc_f16(64, 64, f, 0, 0);
     const uint32_t id_dPt = idesc_f16(64, 64, f, 1, 1);
@@ -749,92 +756,117 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t id_dV2 = idesc_f16(128, 64, f, 1, 0);
     const uint32_t id_R = idesc_f16(128, 128, f, 1, 0);
     const uint32_t aP = smem_u32(sP), adS = smem_u32(sdS), aR = smem_u32(sR), aS = smem_u32(sS);
-    for (int n = 0; n < nc; ++n) {
-      const int s = n & 1;
-      const uint32_t aQ = smem_u32(smem + s * kStage), aK = aQ + kT64, aV = aQ + 2 * kT64,
-                     aW = aQ + 3 * kT64;
-      if (lane_id() == 0) traceb(0, n, 0);
-      mbar_wait(&full[s], (n >> 1) & 1);
-      if (lane_id() == 0) traceb(0, n, 1);
-      if (n >= 1) mbar_wait(dpt_empty, (n - 1) & 1);
-      if (lane_id() == 0) traceb(0, n, 2);
-      tc_fence_after();
-      if (elect_one()) {
-        for (int ks = 0; ks < 8; ++ks)  // T1 = Q K^T -> upper lane half
-          mma_ss(tmem + kDP + kHalf, kd(aQ, ks, 64), kd(aK, ks, 64), id_T1, ks > 0);
-        for (int ks = 0; ks < 4; ++ks)  // S -= K^T V
-          mma_ss(tmem + kS, mn(aK, ks, 8192), kd(aV, ks, 128), id_Sneg, 1);
-        mma_commit(s_full);
-      }
-      __syncwarp();
-      mbar_wait(w_ready, n & 1);
-      if (lane_id() == 0) traceb(0, n, 3);
-      tc_fence_after();
-      if (elect_one()) {
-        for (int ks = 0; ks < 8; ++ks)  // dPt = W_hat V^T -> lower lane half
-          mma_ss(tmem + kDP, mn(aW, ks, 8192), mn(aV, ks, 8192), id_dPt, ks > 0);
-        mma_commit(dpt_full);
-      }
-      __syncwarp();
-      mbar_wait(sS_ready, n & 1);
-      if (lane_id() == 0) traceb(0, n, 4);
-      mbar_wait(ps_ready, n & 1);
-      if (lane_id() == 0) traceb(0, n, 5);
-      if (n >= 1) mbar_wait(gr_empty, (n - 1) & 1);
-      if (lane_id() == 0) traceb(0, n, 6);
-      tc_fence_after();
-      if (elect_one()) {
-        for (int h = 0; h < 2; ++h) {  // dQ[:, 64h:64h+64]
-          const uint32_t d = tmem + kDQ + (h ? kHalf : 0u);
-          for (int ks = 0; ks < 4; ++ks)  // dS K
-            mma_ss(d, kd(adS, ks, 64), mn(aK + h * 8192, ks, 8192), id_dQ1, ks > 0);
-          for (int ks = 0; ks < 8; ++ks)  // W_hat (b S)^T
-            mma_ss(d, mn(aW, ks, 8192), kd(aS + h * 8192, ks, 128), id_dQ2, 1);
+    for (int n = -1; n < nc; ++n) {
+      if (n >= 0) {
+        const uint32_t aQ = smem_u32(smem + (n & 1) * kStage), aK = aQ + kT64, aV = aQ + 2 * kT64,
+                       aW = aQ + 3 * kT64;
+        if (lane_id() == 0) traceb(0, n, 0);
+        mbar_wait(ps_ready, n & 1);
+        mbar_wait(sR_ready, n & 1);
+        if (n >= 1) mbar_wait(gkv_empty, (n - 1) & 1);
+        if (lane_id() == 0) traceb(0, n, 1);
+        tc_fence_after();
+        if (elect_one()) {
+          for (int ks = 0; ks < 4; ++ks)  // dK^T = Q^T dS^T
+            mma_ss(tmem + kDK, mn(aQ, ks, 8192), mn(adS, ks, 8192), id_dK1, ks > 0);
+          for (int ks = 0; ks < 8; ++ks)  //      + (b R) V^T
+            mma_ss(tmem + kDK, kd(aR, ks, 128), mn(aV, ks, 8192), id_dK2, 1);
+          for (int ks = 0; ks < 4; ++ks)  // dV^T = W_hat^T P
+            mma_ss(tmem + kDV, kd(aW, ks, 128), mn(aP, ks, 8192), id_dV1, ks > 0);
+          for (int ks = 0; ks < 8; ++ks)  //      + (b R)^T K^T
+            mma_ss(tmem + kDV, mn(aR, ks, 16384), kd(aK, ks, 64), id_dV2, 1);
+          mma_commit(gkv_full);
+          for (int ks = 0; ks < 4; ++ks)  // R += Q^T W_hat
+            mma_ss(tmem + kR, mn(aQ, ks, 8192), kd(aW, ks, 128), id_R, 1);
+          mma_commit(r_full);
         }
+        __syncwarp();
+        mbar_wait(sS_ready, n & 1);
+        if (n >= 1) mbar_wait(gq_empty, (n - 1) & 1);
+        if (lane_id() == 0) traceb(0, n, 2);
+        tc_fence_after();
+        if (elect_one()) {
+          for (int h = 0; h < 2; ++h) {  // dQ[:, 64h:64h+64]
+            const uint32_t d = tmem + kDQ + (h ? kHalf : 0u);
+            for (int ks = 0; ks < 4; ++ks)  // dS K
+              mma_ss(d, kd(adS, ks, 64), mn(aK + h * 8192, ks, 8192), id_dQ1, ks > 0);
+            for (int ks = 0; ks < 8; ++ks)  // W_hat (b S)^T
+              mma_ss(d, mn(aW, ks, 8192), kd(aS + h * 8192, ks, 128), id_dQ2, 1);
+          }
+          mma_commit(gq_full);
+          mma_commit(&empty[n & 1]);
+        }
+        __syncwarp();
       }
-      __syncwarp();
-      mbar_wait(sR_ready, n & 1);
-      if (lane_id() == 0) traceb(0, n, 7);
-      tc_fence_after();
-      if (elect_one()) {
-        for (int ks = 0; ks < 4; ++ks)  // dK^T = Q^T dS^T
-          mma_ss(tmem + kDK, mn(aQ, ks, 8192), mn(adS, ks, 8192), id_dK1, ks > 0);
-        for (int ks = 0; ks < 8; ++ks)  //      + (b R) V^T
-          mma_ss(tmem + kDK, kd(aR, ks, 128), mn(aV, ks, 8192), id_dK2, 1);
-        for (int ks = 0; ks < 4; ++ks)  // dV^T = W_hat^T P
-          mma_ss(tmem + kDV, kd(aW, ks, 128), mn(aP, ks, 8192), id_dV1, ks > 0);
-        for (int ks = 0; ks < 8; ++ks)  //      + (b R)^T K^T
-          mma_ss(tmem + kDV, mn(aR, ks, 16384), kd(aK, ks, 64), id_dV2, 1);
-        mma_commit(gr_full);
-        for (int ks = 0; ks < 4; ++ks)  // R += Q^T W_hat
-          mma_ss(tmem + kR, mn(aQ, ks, 8192), kd(aW, ks, 128), id_R, 1);
-        mma_commit(r_full);
-        mma_commit(&empty[s]);
+      if (n + 1 < nc) {
+        const int m = n + 1;
+        const uint32_t aQ = smem_u32(smem + (m & 1) * kStage), aK = aQ + kT64, aV = aQ + 2 * kT64,
+                       aW = aQ + 3 * kT64;
+        mbar_wait(&full[m & 1], (m >> 1) & 1);
+        if (m >= 1) mbar_wait(dpt_empty, (m - 1) & 1);  // E1(m-1) has read T1 / dPt
+        if (lane_id() == 0) traceb(0, m, 3);
+        tc_fence_after();
+        if (elect_one()) {
+          for (int ks = 0; ks < 4; ++ks)  // S -= K^T V (E_S(m-1) is done: sS_ready above)
+            mma_ss(tmem + kS, mn(aK, ks, 8192), kd(aV, ks, 128), id_Sneg, 1);
+          mma_commit(s_full);
+          for (int ks = 0; ks < 8; ++ks)  // T1 = Q K^T -> upper lane half
+            mma_ss(tmem + kDP + kHalf, kd(aQ, ks, 64), kd(aK, ks, 64), id_T1, ks > 0);
+        }
+        __syncwarp();
+        mbar_wait(w_ready, m & 1);
+        if (lane_id() == 0) traceb(0, m, 4);
+        tc_fence_after();
+        if (elect_one()) {
+          for (int ks = 0; ks < 8; ++ks)  // dPt = W_hat V^T -> lower lane half
+            mma_ss(tmem + kDP, mn(aW, ks, 8192), mn(aV, ks, 8192), id_dPt, ks > 0);
+          mma_commit(dpt_full);
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
   }
   } else {
   regs_inc<136>();
+  const uint32_t qd = warp & 3;
+  const int l = (int)lane_id();
+  const int r = (int)(qd * 32) + l;            // lane of the M=128 accumulators (j or m)
+  const uint32_t lb = (qd * 32u) << 16;
+  const float a = prm.a, b = prm.b;
+  const float* recR = prm.cmb + (grp * prm.P + p) * 2 * state_floats(kD) + state_floats(kD);
+  // b R_next -> sR for columns [jb, jb + 64) (R complete after the previous chunk's R +=)
+  auto er_half = [&](int n, int jb) {
+    if (n >= 1) mbar_wait(r_full, (n - 1) & 1);
+    tc_fence_after();
+#pragma unroll 1
+    for (int j0 = jb; j0 < jb + 64; j0 += 32) {
+      uint32_t x[32];
+      tmem_ld32(tmem + lb + kR + j0, x);
+      tmem_ld_wait();
+#pragma unroll
+      for (int w8 = 0; w8 < 4; ++w8) {
+        uint4 v;
+        v.x = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 0]), b * __uint_as_float(x[8 * w8 + 1]));
+        v.y = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 2]), b * __uint_as_float(x[8 * w8 + 3]));
+        v.z = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 4]), b * __uint_as_float(x[8 * w8 + 5]));
+        v.w = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 6]), b * __uint_as_float(x[8 * w8 + 7]));
+        *(uint4*)(sR + sw128_off(r, j0 + 8 * w8, 128)) = v;
+      }
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    mbar_arrive(sR_ready);
+  };
   if (warp < 8) {
     // ------------------------------------------------------------ WG-A (warps 4..7)
-    // Iteration n: dV^T out of chunk n-1 (then c += dc(n-1)), bR -> sR (E_R) and
-    // dS/P (E1) of chunk n.
-    const uint32_t qd = warp & 3;
-    const int l = (int)lane_id();
-    const int r = (int)(qd * 32) + l;            // j of dV^T, m of R
-    const int ih = (int)(qd * 16) + (l & 15);    // half-lane row i of M=64 accumulators
-    const bool upper = l >= 16;                  // lanes 16..31 of a quadrant: upper half
-    const uint32_t lb = (qd * 32u) << 16;
+    // Iteration n: dV^T drain of chunk n-1 (then c += dc(n-1)); bR -> sR for j < 64,
+    // z and bS -> sS (E_S) of chunk n.
     const int et = (int)threadIdx.x - 128;
-    const float a = prm.a, b = prm.b;
-    const float* recR = prm.cmb + (grp * prm.P + p) * 2 * state_floats(kD) + state_floats(kD);
     float cj = recR[kD * kD + kD + r];  // c_next (j = r)
     auto dv_out = [&](int m) {  // dV^T of chunk m (lanes j): acc + a c_next
-      mbar_wait(gr_full, m & 1);
+      mbar_wait(gkv_full, m & 1);
+      if (et == 0) traceb(1, m, 0);
       tc_fence_after();
-      uint8_t* scr_lo = sP + qd * 2048;   // this warp's own P / dS rows are dead now
-      uint8_t* scr_hi = sdS + qd * 2048;
       const float ac = a * cj;
       uint4 vt[8];
 #pragma unroll
@@ -852,29 +884,49 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(gr_empty);
       uint16_t* dvb = (uint16_t*)prm.dv + (grp * kD + qd * 32) * prm.N + row_of(m);
-      warp_store_rows(scr_lo, scr_hi, vt, [&](int seg) { return dvb + seg * prm.N; });
+      warp_store_rows_2k(sP + qd * 2048, vt, [&](int seg) { return dvb + seg * prm.N; });
+      mbar_arrive(gkv_empty);  // after the staging: E1(m+1) rewrites sP
       const float* dq4 = dcp + (m & 3) * 4 * kD;  // WG-C's partial row sums of W_hat (chunk m)
       cj += (dq4[r] + dq4[kD + r]) + (dq4[2 * kD + r] + dq4[3 * kD + r]);
     };
     // One call site per phase (the kernel's code must stay small for the I-cache):
     // iteration n = nc only drains dV^T(nc-1).
     for (int n = 0; n <= nc; ++n) {
-      if (et == 0) traceb(1, n, 0);
       if (n >= 1) dv_out(n - 1);
       if (n == nc) break;
-      {
-      const float* sA = s_s + (n & 3) * 2 * kCB;
-      const float* sB = sA + kCB;
+      const int s = n & 1;
+      er_half(n, 0);
       if (et == 0) traceb(1, n, 1);
-      // ---- E_R: b R_next -> sR (R complete after the previous chunk's R += MMA)
-      if (n >= 1) mbar_wait(r_full, (n - 1) & 1);
+      // ---- z_prev(n) = z_prev(n-1) - sum_t k_t over this chunk -> zbuf[n & 3]
+      mbar_wait(&full[s], (n >> 1) & 1);
+      {
+        const uint8_t* k_t = smem + s * kStage + kT64;
+        const int mg = et >> 3, tg = et & 7;  // columns 8 mg.., rows tg + 8 k
+        float zs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 2
+        for (int k8 = 0; k8 < kCB / 8; ++k8) {
+          const uint4 v4 = *(const uint4*)(k_t + sw128_off(tg + 8 * k8, 8 * mg, kCB));
+          const uint32_t xx[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 f2 = unpack2<kBF16>(xx[q]);
+            zs[2 * q] += f2.x;
+            zs[2 * q + 1] += f2.y;
+          }
+        }
+        const int m = 8 * mg + tg;
+        zbuf[(n & 3) * kD + m] = zbuf[((n - 1) & 3) * kD + m] - reduce_scatter8(zs, tg);
+      }
+      // ---- E_S: b S_prev -> sS (after the dQ drain of chunk n-1 used sS as scratch)
+      mbar_wait(s_full, n & 1);
+      if (n >= 1) mbar_wait(gq_empty, (n - 1) & 1);
+      if (et == 0) traceb(1, n, 2);
       tc_fence_after();
 #pragma unroll 1
       for (int j0 = 0; j0 < kD; j0 += 32) {
         uint32_t x[32];
-        tmem_ld32(tmem + lb + kR + j0, x);
+        tmem_ld32(tmem + lb + kS + j0, x);
         tmem_ld_wait();
 #pragma unroll
         for (int w8 = 0; w8 < 4; ++w8) {
@@ -883,19 +935,177 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           v.y = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 2]), b * __uint_as_float(x[8 * w8 + 3]));
           v.z = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 4]), b * __uint_as_float(x[8 * w8 + 5]));
           v.w = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 6]), b * __uint_as_float(x[8 * w8 + 7]));
-          *(uint4*)(sR + sw128_off(r, j0 + 8 * w8, 128)) = v;
+          *(uint4*)(sS + sw128_off(r, j0 + 8 * w8, 128)) = v;
         }
       }
       fence_proxy_async();
       tc_fence_before();
-      mbar_arrive(sR_ready);
-      if (et == 0) traceb(1, n, 2);
-      // ---- E1: dPt -> dS (lower half lanes), T1 -> P (upper half lanes)
-      mbar_wait(dpt_full, n & 1);
+      mbar_arrive(sS_ready);  // z(n) above is published with it (read by dq_out(n))
+      mbar_arrive(&empty[s]);
       if (et == 0) traceb(1, n, 3);
+    }
+  } else if (warp < 12) {
+    // ------------------------------------------------------------ WG-B (warps 8..11)
+    // Iteration n: bR -> sR for j >= 64 of chunk n, dK^T and dQ drains of chunk n-1,
+    // du of chunk n.
+    const int ih = (int)(qd * 16) + (l & 15);
+    const bool upper = l >= 16;
+    const int eb = (int)threadIdx.x - 256;
+    float u = recR[kD * kD + r];  // u_next (m = r)
+    auto dk_out = [&](int m) {  // dK^T (lanes m): acc - b u_next
+      mbar_wait(gkv_full, m & 1);
+      if (m >= 1) u += du_s[((m - 1) & 3) * kD + r];  // suffix sum through chunk m-1
+      tc_fence_after();
+      const float bu = b * u;
+      uint4 vt[8];
+#pragma unroll
+      for (int c0 = 0; c0 < 64; c0 += 32) {
+        uint32_t x[32];
+        tmem_ld32(tmem + lb + kDK + c0, x);
+        tmem_ld_wait();
+#pragma unroll
+        for (int w4 = 0; w4 < 4; ++w4) {
+          uint32_t k4[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            k4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) - bu, __uint_as_float(x[8 * w4 + 2 * q + 1]) - bu);
+          vt[c0 / 8 + w4] = make_uint4(k4[0], k4[1], k4[2], k4[3]);
+        }
+      }
+      tc_fence_before();
+      mbar_wait(gq_full, m & 1);  // dQ(m) has read dS: sdS is free as scratch
+      uint16_t* dkb = (uint16_t*)prm.dk + (grp * kD + qd * 32) * prm.N + row_of(m);
+      warp_store_rows_2k(sdS + qd * 2048, vt, [&](int seg) { return dkb + seg * prm.N; });
+      mbar_arrive(gkv_empty);  // after the staging: E1(m+1) rewrites sdS
+    };
+    auto dq_out = [&](int m) {  // dQ (half lanes): acc - b s_i z_prev
+      mbar_wait(gq_full, m & 1);
+      if (eb == 0) traceb(2, m, 0);
+      tc_fence_after();
+      const float* sA = s_s + (m & 3) * 2 * kCB;
+      const float si = sA[ih] + sA[kCB + ih];
+      const float* zq = zbuf + (m & 3) * kD;
+      const int m0 = upper ? 64 : 0;
+      uint4 vt[8];
+#pragma unroll
+      for (int c0 = 0; c0 < 64; c0 += 32) {
+        uint32_t x[32];
+        tmem_ld32(tmem + lb + kDQ + c0, x);
+        tmem_ld_wait();
+#pragma unroll
+        for (int w4 = 0; w4 < 4; ++w4) {
+          uint32_t q4[4];
+          const float4 za = *(const float4*)(zq + m0 + c0 + 8 * w4);
+          const float4 zb = *(const float4*)(zq + m0 + c0 + 8 * w4 + 4);
+          const float z8[8] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            q4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) - si * b * z8[2 * q],
+                                 __uint_as_float(x[8 * w4 + 2 * q + 1]) - si * b * z8[2 * q + 1]);
+          vt[c0 / 8 + w4] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
+        }
+      }
+      tc_fence_before();
+      // scratch: this warp's 4 KB of sS (E_S of the next chunk waits for gq_empty)
+      uint8_t* scr_lo = sS + qd * 4096;
+      uint16_t* dqb = (uint16_t*)prm.dq + (grp * prm.N + row_of(m) + qd * 16) * kD;
+      warp_store_rows(scr_lo, scr_lo + 2048, vt, [&](int seg) { return dqb + (seg & 15) * kD + (seg >> 4) * 64; });
+      mbar_arrive(gq_empty);
+    };
+    for (int n = 0; n <= nc; ++n) {
+      if (n < nc) er_half(n, 64);
+      if (n >= 1) dk_out(n - 1);
+      if (n >= 1) dq_out(n - 1);
+      if (n == nc) break;
+      const int s = n & 1;
+      // ---- du_m = sum_i q_im s_i of this chunk -> du_s[n & 3]
+      mbar_wait(&full[s], (n >> 1) & 1);
+      mbar_wait(&s_rdy[s], (n >> 1) & 1);  // slot s next completes at chunk n + 2, after our empty arrival
+      {
+        const uint8_t* q_t = smem + s * kStage;
+        const float* sA = s_s + (n & 3) * 2 * kCB;
+        const float* sB = sA + kCB;
+        const int mg = eb >> 3, tg = eb & 7;  // rows tg + 8k: conflict-free quarter-warps
+        float du[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 2
+        for (int k8 = 0; k8 < kCB / 8; ++k8) {
+          const int i = tg + 8 * k8;
+          const uint4 v4 = *(const uint4*)(q_t + sw128_off(i, 8 * mg, kCB));
+          const float w = sA[i] + sB[i];
+          const uint32_t xx[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 f2 = unpack2<kBF16>(xx[q]);
+            du[2 * q] += w * f2.x;
+            du[2 * q + 1] += w * f2.y;
+          }
+        }
+        du_s[(n & 3) * kD + 8 * mg + tg] = reduce_scatter8(du, tg);
+      }
+      named_bar(2, 128);  // du(n) visible to dk_out(n + 1)
+      mbar_arrive(&empty[s]);
+      if (eb == 0) traceb(2, n, 1);
+    }
+  } else {
+    // ------------------------------------------------------------ WG-C (warps 12..15)
+    // E1 of chunk n (dPt -> dS, T1 -> P), then the W_hat / s / dc pass of chunk n+1:
+    // W_hat = Omega^T / g in place, partial s_i = sum_j o_ji w_hat_ji of both row
+    // halves, per-warp partial row sums of W_hat (dcp[m & 3]). Rings of 4: slot m & 3
+    // is rewritten only after the stage of chunk m + 2 was released, i.e. after its
+    // readers finished chunk m.
+    const int ec = (int)threadIdx.x - 384;
+    const int ih = (int)(qd * 16) + (l & 15);    // half-lane row i of M=64 accumulators
+    const bool upper = l >= 16;                  // lanes 16..31 of a quadrant: upper half
+    uint4 o8[8];
+    float4 g8[2];
+    auto e0 = [&](int m) {
+      const int sm = m & 1;
+      mbar_wait(&full[sm], (m >> 1) & 1);
+      if (ec == 0) traceb(3, m, 0);
+      uint8_t* w_t = smem + sm * kStage + 3 * kT64;
+      float* sp = s_s + (m & 3) * 2 * kCB;
+      float* dq4 = dcp + (m & 3) * 4 * kD + qd * kD;
+      float rs[4];
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        uint4 o4[4];
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) o4[rr] = h ? o8[4 + rr] : o8[rr];
+        what_pass_half<kBF16>(w_t, o4, g8, sp + h * kCB, ec, 64 * h, rs);
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+          const float v = rs[rr] + __shfl_xor_sync(0xffffffffu, rs[rr], 16);
+          if (l < 16) dq4[64 * h + 16 * rr + l] = v;
+        }
+      }
+      fence_proxy_async();
+      mbar_arrive(w_ready);
+      mbar_arrive(&s_rdy[sm]);
+      if (m + 2 < nc) {  // O^T rows (128 B each) and g of chunk m+2 into L2
+        const int64_t row2 = row_of(m + 2);
+        prefetch_l2((const uint16_t*)prm.o + (grp * kD + ec) * prm.N + row2);
+        if (ec < 2) prefetch_l2(prm.g + grp * prm.N + row2 + 32 * ec);
+      }
+      if (m + 1 < nc) what_prefetch<kBF16>(prm, grp, row_of(m + 1), ec, o8, g8);
+      if (ec == 0) traceb(3, m, 1);
+    };
+    if (nc > 0) {
+      what_prefetch<kBF16>(prm, grp, row_of(0), ec, o8, g8);
+      e0(0);
+    }
+    for (int n = 0; n < nc; ++n) {
+      // ---- E1: dPt -> dS (lower half lanes), T1 -> P (upper half lanes); sP / sdS are
+      // free once dQ(n-1) has run and the dK^T / dV^T drains (scratch) are done
+      mbar_wait(dpt_full, n & 1);
+      if (n >= 1) {
+        mbar_wait(gq_full, (n - 1) & 1);
+        mbar_wait(gkv_empty, (n - 1) & 1);
+      }
+      if (ec == 0) traceb(3, n, 2);
       tc_fence_after();
       {
-        const float si = sA[ih] + sB[ih];
+        const float* sA = s_s + (n & 3) * 2 * kCB;
+        const float si = sA[ih] + sA[kCB + ih];
         const float alpha = upper ? a : -b * si;
         uint8_t* dst = upper ? sP : sdS;
 #pragma unroll 1
@@ -923,196 +1133,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       mbar_arrive(dpt_empty);
       mbar_arrive(ps_ready);
-      if (et == 0) traceb(1, n, 4);
-      if (et == 0) traceb(1, n, 5);
-      }
-    }
-  } else if (warp < 12) {
-    // ------------------------------------------------------------ WG-B (warps 8..11)
-    // Iteration n: dQ and dK^T out of chunk n-1, bS -> sS (E_S) and z of chunk n.
-    const uint32_t qd = warp & 3;
-    const int l = (int)lane_id();
-    const int r = (int)(qd * 32) + l;            // m
-    const int ih = (int)(qd * 16) + (l & 15);
-    const bool upper = l >= 16;
-    const uint32_t lb = (qd * 32u) << 16;
-    const int eb = (int)threadIdx.x - 256;
-    const float b = prm.b;
-    const float* recR = prm.cmb + (grp * prm.P + p) * 2 * state_floats(kD) + state_floats(kD);
-    float u = recR[kD * kD + r];  // u_next (m = r)
-    auto qk_out = [&](int m) {  // dQ (half lanes): acc - b s_i z_prev ; dK^T (lanes m): acc - b u_next
-      mbar_wait(gr_full, m & 1);
-      if (m >= 1) u += du_s[((m - 1) & 3) * kD + r];  // suffix sum through chunk m-1
-      tc_fence_after();
-      // scratch: this warp's 4 KB of sS (dead until E_S of the next chunk)
-      uint8_t* scr_lo = sS + qd * 4096;
-      uint8_t* scr_hi = scr_lo + 2048;
-      const float* sA = s_s + (m & 3) * 2 * kCB;
-      const float si = sA[ih] + sA[kCB + ih];
-      const float* zq = zbuf + (m & 1) * kD;
-      const int m0 = upper ? 64 : 0;
-      const int64_t row0 = row_of(m);
-      uint4 vt[8];
-#pragma unroll
-      for (int c0 = 0; c0 < 64; c0 += 32) {
-        uint32_t x[32];
-        tmem_ld32(tmem + lb + kDQ + c0, x);
-        tmem_ld_wait();
-#pragma unroll
-        for (int w4 = 0; w4 < 4; ++w4) {
-          uint32_t q4[4];
-          const float4 za = *(const float4*)(zq + m0 + c0 + 8 * w4);
-          const float4 zb = *(const float4*)(zq + m0 + c0 + 8 * w4 + 4);
-          const float z8[8] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            q4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) - si * b * z8[2 * q],
-                                 __uint_as_float(x[8 * w4 + 2 * q + 1]) - si * b * z8[2 * q + 1]);
-          vt[c0 / 8 + w4] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
-        }
-      }
-      uint16_t* dqb = (uint16_t*)prm.dq + (grp * prm.N + row0 + qd * 16) * kD;
-      warp_store_rows(scr_lo, scr_hi, vt, [&](int seg) { return dqb + (seg & 15) * kD + (seg >> 4) * 64; });
-      const float bu = b * u;
-#pragma unroll
-      for (int c0 = 0; c0 < 64; c0 += 32) {
-        uint32_t x[32];
-        tmem_ld32(tmem + lb + kDK + c0, x);
-        tmem_ld_wait();
-#pragma unroll
-        for (int w4 = 0; w4 < 4; ++w4) {
-          uint32_t k4[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            k4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) - bu, __uint_as_float(x[8 * w4 + 2 * q + 1]) - bu);
-          vt[c0 / 8 + w4] = make_uint4(k4[0], k4[1], k4[2], k4[3]);
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(gr_empty);
-      uint16_t* dkb = (uint16_t*)prm.dk + (grp * kD + qd * 32) * prm.N + row0;
-      warp_store_rows(scr_lo, scr_hi, vt, [&](int seg) { return dkb + seg * prm.N; });
-    };
-    for (int n = 0; n <= nc; ++n) {
-      if (eb == 0) traceb(2, n, 0);
-      if (n >= 1) qk_out(n - 1);
-      if (n == nc) break;
-      {
-      const int s = n & 1;
-      const uint8_t* q_t = smem + s * kStage;
-      const uint8_t* k_t = q_t + kT64;
-      const float* sA = s_s + (n & 3) * 2 * kCB;
-      const float* sB = sA + kCB;
-      if (eb == 0) traceb(2, n, 1);
-      // ---- E_S: b S_prev -> sS
-      mbar_wait(s_full, n & 1);
-      if (eb == 0) traceb(2, n, 2);
-      tc_fence_after();
-#pragma unroll 1
-      for (int j0 = 0; j0 < kD; j0 += 32) {
-        uint32_t x[32];
-        tmem_ld32(tmem + lb + kS + j0, x);
-        tmem_ld_wait();
-#pragma unroll
-        for (int w8 = 0; w8 < 4; ++w8) {
-          uint4 v;
-          v.x = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 0]), b * __uint_as_float(x[8 * w8 + 1]));
-          v.y = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 2]), b * __uint_as_float(x[8 * w8 + 3]));
-          v.z = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 4]), b * __uint_as_float(x[8 * w8 + 5]));
-          v.w = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 6]), b * __uint_as_float(x[8 * w8 + 7]));
-          *(uint4*)(sS + sw128_off(r, j0 + 8 * w8, 128)) = v;
-        }
-      }
-      fence_proxy_async();
-      tc_fence_before();
-      mbar_arrive(sS_ready);
-      if (eb == 0) traceb(2, n, 3);
-      // ---- du_m = sum_i q_im s_i of this chunk -> du_s[n & 3] (read by qk_out after the barrier below)
-      mbar_wait(&s_rdy[s], (n >> 1) & 1);  // slot s next completes at chunk n + 2, after our empty arrival
-      {
-        const int mg = eb >> 3, tg = eb & 7;  // rows tg + 8k: conflict-free quarter-warps
-        float du[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
-        for (int k8 = 0; k8 < kCB / 8; ++k8) {
-          const int i = tg + 8 * k8;
-          const uint4 v4 = *(const uint4*)(q_t + sw128_off(i, 8 * mg, kCB));
-          const float w = sA[i] + sB[i];
-          const uint32_t xx[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float2 f2 = unpack2<kBF16>(xx[q]);
-            du[2 * q] += w * f2.x;
-            du[2 * q + 1] += w * f2.y;
-          }
-        }
-        du_s[(n & 3) * kD + 8 * mg + tg] = reduce_scatter8(du, tg);
-      }
-      // ---- z_prev(n) = z_prev(n-1) - sum_t k_t over this chunk -> zbuf[n & 1]
-      {
-        const int mg = eb >> 3, tg = eb & 7;  // columns 8 mg.., rows tg + 8 k
-        float zs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
-        for (int k8 = 0; k8 < kCB / 8; ++k8) {
-          const uint4 v4 = *(const uint4*)(k_t + sw128_off(tg + 8 * k8, 8 * mg, kCB));
-          const uint32_t xx[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float2 f2 = unpack2<kBF16>(xx[q]);
-            zs[2 * q] += f2.x;
-            zs[2 * q + 1] += f2.y;
-          }
-        }
-        {
-          const int m = 8 * mg + tg;
-          zbuf[(n & 1) * kD + m] = zbuf[((n - 1) & 1) * kD + m] - reduce_scatter8(zs, tg);
-        }
-        named_bar(2, 128);
-      }
-      mbar_arrive(&empty[s]);
-      if (eb == 0) traceb(2, n, 4);
-      }
-    }
-  } else {
-    // ------------------------------------------------------------ WG-C (warps 12..15)
-    // W_hat = Omega^T / g in place and the partial s_i = sum_j o_ji w_hat_ji of both
-    // row halves, chunk by chunk as the stages land (s_s ring of 4: slot m & 3 is
-    // rewritten only after the stage of chunk m + 2 was released by WG-A / WG-B).
-    // W_hat = Omega^T / g in place, the partial s_i = sum_j o_ji w_hat_ji of both row
-    // halves and per-warp partial row sums of W_hat (dc, dcp[m & 3]), chunk by chunk
-    // as the stages land. Rings of 4: slot m & 3 is rewritten only after the stage
-    // of chunk m + 2 was released, i.e. after its readers finished chunk m.
-    const int ec = (int)threadIdx.x - 384;
-    const uint32_t qd = warp & 3;
-    const int l = (int)lane_id();
-    uint4 o8[8];
-    float4 g8[2];
-    if (nc > 0) what_prefetch<kBF16>(prm, grp, row_of(0), ec, o8, g8);
-    for (int m = 0; m < nc; ++m) {
-      const int sm = m & 1;
-      if (ec == 0) traceb(3, m, 0);
-      mbar_wait(&full[sm], (m >> 1) & 1);
-      if (ec == 0) traceb(3, m, 1);
-      uint8_t* w_t = smem + sm * kStage + 3 * kT64;
-      float* sp = s_s + (m & 3) * 2 * kCB;
-      float* dq4 = dcp + (m & 3) * 4 * kD + qd * kD;
-      float rs[4];
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
-        uint4 o4[4];
-#pragma unroll
-        for (int rr = 0; rr < 4; ++rr) o4[rr] = h ? o8[4 + rr] : o8[rr];
-        what_pass_half<kBF16>(w_t, o4, g8, sp + h * kCB, ec, 64 * h, rs);
-#pragma unroll
-        for (int rr = 0; rr < 4; ++rr) {
-          const float v = rs[rr] + __shfl_xor_sync(0xffffffffu, rs[rr], 16);
-          if (l < 16) dq4[64 * h + 16 * rr + l] = v;
-        }
-      }
-      fence_proxy_async();
-      mbar_arrive(w_ready);
-      mbar_arrive(&s_rdy[sm]);
-      if (m + 1 < nc) what_prefetch<kBF16>(prm, grp, row_of(m + 1), ec, o8, g8);
-      if (ec == 0) traceb(3, m, 2);
+      if (ec == 0) traceb(3, n, 3);
+      if (n + 1 < nc) e0(n + 1);
     }
   }
   }
@@ -1363,7 +1385,7 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 constexpr size_t kAggSmemB = 2 * kStage + 512 + 1024;
-constexpr size_t kMainSmemB = 2 * kStage + 2 * 8192 + 2 * 32768 + 160 + (8 * kCB + 22 * kD) * 4 + 1024;
+constexpr size_t kMainSmemB = 2 * kStage + 2 * 8192 + 2 * 32768 + 160 + (8 * kCB + 24 * kD) * 4 + 1024;
 static_assert(kMainSmemB <= 232448, "backward smem");
 
 int tcb_segments(int64_t G, int64_t N) { return tc_segments(G, N); }

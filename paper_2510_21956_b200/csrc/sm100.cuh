@@ -66,6 +66,10 @@ __device__ __forceinline__ void fence_proxy_async() {
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+// L2 prefetch of the 128-byte line holding p (no register result).
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 // Register re-distribution between warpgroups (all four warps of a warpgroup execute
 // the same instruction): producer / MMA warpgroups give registers back, epilogue
 // warpgroups take them.

@@ -23,12 +23,12 @@ t0 = t[0, 10, 0]
 t = t - t0
 t[t < -10**9] = -1
 R = range(10, 14)
-print("MMA : start, full, dpt_empty, w_ready, sS_ready, ps_ready, gr_empty, sR_ready")
-for c in R: print(c, t[0, c, :8].tolist())
-print("WG-A: start, dv_out done, E_R done, dpt_full, E1 done, du/dc done")
-for c in R: print(c, t[1, c, :6].tolist())
-print("WG-B: start, qk_out done, s_full, E_S done, z done")
-for c in R: print(c, t[2, c, :5].tolist())
-print("WG-C: start, full, done")
-for c in R: print(c, t[3, c, :3].tolist())
-print("period", np.diff(t[0, 5:60, 0]).mean())
+names = {0: "MMA : blk n start, dKdV issue(n), dQ issue(n), T1/S issue(n), dPt issue(n)",
+         1: "WG-A: gkv_full(n) seen, E_R half done, E_S start, E_S done",
+         2: "WG-B: gq_full(n) seen, du done",
+         3: "WG-C: e0 start(n), e0 done(n), E1 start(n), E1 done(n)"}
+cols = {0: 5, 1: 4, 2: 2, 3: 4}
+for role in range(4):
+    print(names[role])
+    for c in R: print(c, t[role, c, :cols[role]].tolist())
+print("period", np.diff(t[0, 5:60, 1]).mean())
