@@ -16,6 +16,7 @@
 //   [0,64) dPt (lanes 0-15,32-47,..) + T1 (other half), [64,128) dQ halves,
 //   [128,192) dK^T, [192,256) dV^T, [256,384) R, [384,512) S.
 // Segment carries: an aggregate pass (R, u, c and S, z per segment) + scan.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -126,6 +127,7 @@ struct BwdParams {
   const float* carry_suf;
   float* cmb;  // per (g, segment) combined [S inclusive prefix | R exclusive suffix]
   int pf;      // chunks prefetched into L2 ahead of the ring
+  int store_w = 0;  // W_hat pass: store W_hat^T (into dv) and s (into dq rows) for the sweep
 };
 
 // Epilogue step E0: W_hat = omega / g in place (bf16) and s_i = sum_j o_ij w_hat_ij.
@@ -413,13 +415,15 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc<256>(tmem);
 }
 
-// ================================================================ lean R aggregate
-// Used when the forward's saved S records are available (la_backward_saved): per
-// unit of rows, R^T = sum W_hat^T Q, c = sum_i w_hat (a ones panel appended to Q as
-// extra N columns of the same MMA) and u = Q^T s (a second small MMA against two bf16
-// rows s_hi, s_lo). The only CUDA-core work is the W_hat / s pass, spread over 256
-// threads. Stage: Q [64 i][128 m] (2 panels) | ones panel | W_hat^T [128 j][64 i] | s rows
-// | O^T [128 j][64 i] (all by TMA, L2-prefetched ahead of the ring).
+// ================================================================ W_hat pass + R aggregate
+// Runs over every unit of rows before the reverse sweep: W_hat = Omega^T / g and
+// s_i = sum_j o_ji w_hat_ji per 64-row chunk, stored for the sweep (W_hat^T by TMA
+// into the dV output, s as the first 256 bytes of the chunk's dQ rows: both are
+// overwritten by the sweep after it has read them), and per unit R^T = sum W_hat^T Q,
+// c = sum_i w_hat (a ones panel appended to Q as extra N columns of the same MMA) and
+// u = Q^T s (a second small MMA against two bf16 rows s_hi, s_lo). The only CUDA-core
+// work is the W_hat / s pass, spread over 256 threads. Stage: Q [64 i][128 m]
+// (2 panels) | ones panel | W_hat^T [128 j][64 i] | s rows | O^T [128 j][64 i] (by TMA).
 constexpr int kAStages = 3;
 constexpr int kAStage = 2 * 8192 + 8192 + kT64 + 2048 + kT64;  // 58 KB
 constexpr int kAOffOnes = 16384, kAOffW = 24576, kAOffS = 24576 + kT64, kAOffO = kAOffS + 2048;
@@ -428,7 +432,8 @@ constexpr size_t kAggRSmem = kAStages * kAStage + 128 + 4 * 2 * kCB * 4 + 1024;
 template <bool kBF16>
 __global__ void __launch_bounds__(320, 1)
     k_bwd_aggR_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmW,
-                  const __grid_constant__ CUtensorMap tmO, BwdParams prm) {
+                  const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmWo,
+                  BwdParams prm) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint64_t* bars = (uint64_t*)(smem + kAStages * kAStage);
@@ -451,7 +456,7 @@ __global__ void __launch_bounds__(320, 1)
     tma_prefetch(&tmO);
     for (int s = 0; s < kAStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], 2);  // MMA commit + the W_hat^T store having read the stage
     }
     mbar_init(w_ready, 256);
     mbar_init(done, 1);
@@ -539,9 +544,16 @@ __global__ void __launch_bounds__(320, 1)
       if (c + 1 < nc) g_prefetch(c + 1);
       float rs_unused[4];
       what_pass_half<kBF16>(st + kAOffW, o4, gc, sp + half * kCB, eh, 64 * half, rs_unused);
-      named_bar(1, 256);  // both halves' partial s of chunk c are in s_part
+      fence_proxy_async();
+      named_bar(1, 256);  // W_hat^T and both halves' partial s of chunk c are complete
+      const int64_t row0 = s0 + (int64_t)c * kCB;
+      if (prm.store_w && et == 0) {
+        tma_store_3d(&tmWo, st + kAOffW, 0, (int)(grp * kD), (int)(row0 / 64));
+        tma_store_commit();
+      }
       if (et < kCB) {     // s rows (hi, lo) of the U = Q^T s MMA
         const float si = sp[et] + sp[kCB + et];
+        if (prm.store_w) ((float*)((uint16_t*)prm.dq + (grp * prm.N + row0) * kD))[et] = si;
         uint16_t hv, lv;
         if (kBF16) {
           const __nv_bfloat16 h = __float2bfloat16_rn(si);
@@ -557,7 +569,12 @@ __global__ void __launch_bounds__(320, 1)
       }
       fence_proxy_async();
       mbar_arrive(w_ready);
+      if (et == 0) {  // the previous chunk's W_hat^T store has read its stage
+        tma_store_wait_read1();
+        if (c >= 1) mbar_arrive(&empty[(c - 1) % kAStages]);
+      }
     }
+    if (et == 0) tma_store_wait0();
     if (half == 0) {  // records: R (X[m][j]), u, c, count
       float* rR = prm.stR + (grp * prm.P + p) * state_floats(kD);
       const uint32_t lb = (qd * 32u) << 16;
@@ -591,12 +608,15 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ================================================================ main reverse sweep
-// Warp roles (512 threads): 0 TMA producer; 1 MMA issuer + TMEM owner; 2-3 idle
+// Inputs per 64-row chunk (reverse order): Q, K, V^T and the W_hat^T / s written by the
+// aggregate pass (W_hat^T in the dV buffer, s in the chunk's first dQ row), all by
+// TMA. Warp roles (512 threads): 0 TMA producer; 1 MMA issuer + TMEM owner; 2-3 idle
 // (warpgroup 0 hands its registers to the epilogue warpgroups with setmaxnreg);
-// 4-7 WG-A: bR -> sR, dS/P, dV^T out, u/c increments; 8-11 WG-B: bS -> sS, z, dQ and
-// dK^T out; 12-15 WG-C: the W_hat / s pass, running up to two chunks ahead. Each
-// epilogue column sum uses 16-byte loads over a conflict-free (rows-by-lane)
-// mapping and a shuffle reduction.
+// 4-7 WG-A: dV^T drain, bR -> sR (j < 64), bS -> sS; 8-11 WG-B: bR -> sR (j >= 64),
+// dK^T and dQ drains, du; 12-15 WG-C: dc, E1 (dPt -> dS, T1 -> P), z.
+// MMA order per chunk n: dK^T / dV^T, R +=, dQ, then T1 / dPt and S -= of chunk n+1:
+// the chain from one chunk's dK^T / dV^T to the next is the drains and E_R in
+// parallel with E1.
 constexpr int kBwdThreads = 512;
 template <bool kBF16>
 __global__ void __launch_bounds__(kBwdThreads, 1)
@@ -612,7 +632,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* bars = (uint64_t*)(sS + 32768);
   uint64_t* full = bars;        // [2]
   uint64_t* empty = bars + 2;   // [2]
-  uint64_t* w_ready = bars + 4;
   uint64_t* s_full = bars + 5;
   uint64_t* dpt_full = bars + 6;
   uint64_t* dpt_empty = bars + 7;
@@ -622,14 +641,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* gkv_full = bars + 11;   // dK^T, dV^T accumulators complete
   uint64_t* gkv_empty = bars + 12;  // ... drained (WG-A dV^T, WG-B dK^T)
   uint64_t* r_full = bars + 13;
-  uint64_t* s_rdy = bars + 14;  // [2] partial s of chunk m in s_s (WG-C -> WG-B's du)
   uint32_t* tslot = (uint32_t*)(bars + 16);
   uint64_t* gq_full = bars + 17;    // dQ accumulator complete
   uint64_t* gq_empty = bars + 18;   // ... drained (WG-B)
-  float* s_s = (float*)(bars + 20);   // [4 chunks][2 halves][64]  partial s (rows j 0..63, 64..127)
-  float* du_s = s_s + 8 * kCB;        // [4][128]  du per chunk (WG-B)
-  float* zbuf = du_s + 4 * kD;        // [4][128]  z_prev per chunk (WG-A -> WG-B's dQ drain)
-  float* dcp = zbuf + 4 * kD;         // [4][4][128] WG-C per-warp partial row sums of W_hat
+  float* s_s = (float*)(bars + 20);   // [2 stages][64]  s of the staged chunk (TMA)
+  float* du_s = s_s + 2 * kCB;        // [4][128]  du per chunk (WG-B)
+  float* zbuf = du_s + 4 * kD;        // [4][128]  z_prev per chunk (WG-C -> WG-B's dQ drain)
+  float* dcp = zbuf + 4 * kD;         // [4][128]  dc per chunk (WG-C -> WG-A's dV^T drain)
 
   const int p = blockIdx.x;
   const int64_t grp = blockIdx.y;
@@ -647,11 +665,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1 + 256);
     }
-    mbar_init(w_ready, 128);
     mbar_init(s_full, 1);
     mbar_init(dpt_full, 1);
     mbar_init(dpt_empty, 128);
-    mbar_init(sS_ready, 128);
+    mbar_init(sS_ready, 256);
     mbar_init(ps_ready, 128);
     mbar_init(sR_ready, 256);
     mbar_init(gkv_full, 1);
@@ -659,8 +676,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(gq_full, 1);
     mbar_init(gq_empty, 128);
     mbar_init(r_full, 1);
-    mbar_init(&s_rdy[0], 128);
-    mbar_init(&s_rdy[1], 128);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
@@ -718,8 +733,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (reverse)
     if (elect_one()) {
-      auto l2_prefetch = [&](int n) {  // Q, K, V^T, Omega^T and O^T of chunk n into L2
-        const int64_t row0 = s0 + (int64_t)(nc - 1 - n) * kCB;
+      auto l2_prefetch = [&](int n) {  // Q, K, V^T, W_hat^T of chunk n into L2
+        const int64_t row0 = row_of(n);
         tma_prefetch_l2_3d(&tmQ, 0, (int)(grp * prm.N + row0), 0);
         tma_prefetch_l2_3d(&tmK, 0, (int)(grp * prm.N + row0), 0);
         tma_prefetch_l2_3d(&tmV, 0, (int)(grp * kD), (int)(row0 / 64));
@@ -730,20 +745,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int s = n & 1;
         if (n + prm.pf < nc) l2_prefetch(n + prm.pf);
         if (n >= 2) mbar_wait(&empty[s], ((n >> 1) & 1) ^ 1);
-        const int64_t row0 = s0 + (int64_t)(nc - 1 - n) * kCB;
+        const int64_t row0 = row_of(n);
         uint8_t* st = smem + s * kStage;
-        mbar_expect_tx(&full[s], kStage);
+        mbar_expect_tx(&full[s], kStage + kCB * 4);
         tma_load_3d(st, &tmQ, &full[s], 0, (int)(grp * prm.N + row0), 0);
         tma_load_3d(st + kT64, &tmK, &full[s], 0, (int)(grp * prm.N + row0), 0);
         tma_load_3d(st + 2 * kT64, &tmV, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
         tma_load_3d(st + 3 * kT64, &tmW, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
+        bulk_load(s_s + s * kCB, (const uint16_t*)prm.dq + (grp * prm.N + row0) * kD, kCB * 4, &full[s]);
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    // Block n: dK^T / dV^T (+ R) as soon as E1(n), E_R(n) and the previous drains are
-    // done, then dQ(n); then S -= K^T V, T1 and dPt of chunk n+1, which feed the next
-    // E1 while this chunk's outputs drain.
     constexpr uint32_t f = kBF16 ? 1 : 0;
     const uint32_t id_T1 = idesc_f16(64, 64, f, 0, 0);
     const uint32_t id_dPt = idesc_f16(64, 64, f, 1, 1);
@@ -757,9 +770,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t id_R = idesc_f16(128, 128, f, 1, 0);
     const uint32_t aP = smem_u32(sP), adS = smem_u32(sdS), aR = smem_u32(sR), aS = smem_u32(sS);
     for (int n = -1; n < nc; ++n) {
+      const uint32_t aQ = smem_u32(smem + (n & 1) * kStage), aK = aQ + kT64, aV = aQ + 2 * kT64,
+                     aW = aQ + 3 * kT64;
+      const uint32_t bQ = smem_u32(smem + ((n + 1) & 1) * kStage), bK = bQ + kT64, bV = bQ + 2 * kT64,
+                     bW = bQ + 3 * kT64;  // chunk n+1
       if (n >= 0) {
-        const uint32_t aQ = smem_u32(smem + (n & 1) * kStage), aK = aQ + kT64, aV = aQ + 2 * kT64,
-                       aW = aQ + 3 * kT64;
         if (lane_id() == 0) traceb(0, n, 0);
         mbar_wait(ps_ready, n & 1);
         mbar_wait(sR_ready, n & 1);
@@ -781,9 +796,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           mma_commit(r_full);
         }
         __syncwarp();
+      }
+      if (n >= 0) {
         mbar_wait(sS_ready, n & 1);
         if (n >= 1) mbar_wait(gq_empty, (n - 1) & 1);
-        if (lane_id() == 0) traceb(0, n, 2);
+        if (lane_id() == 0) traceb(0, n, 3);
         tc_fence_after();
         if (elect_one()) {
           for (int h = 0; h < 2; ++h) {  // dQ[:, 64h:64h+64]
@@ -798,29 +815,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         __syncwarp();
       }
-      if (n + 1 < nc) {
-        const int m = n + 1;
-        const uint32_t aQ = smem_u32(smem + (m & 1) * kStage), aK = aQ + kT64, aV = aQ + 2 * kT64,
-                       aW = aQ + 3 * kT64;
-        mbar_wait(&full[m & 1], (m >> 1) & 1);
-        if (m >= 1) mbar_wait(dpt_empty, (m - 1) & 1);  // E1(m-1) has read T1 / dPt
-        if (lane_id() == 0) traceb(0, m, 3);
+      if (n + 1 < nc) {  // T1 and dPt of chunk n+1 (E1(n) has read the previous ones)
+        mbar_wait(&full[(n + 1) & 1], ((n + 1) >> 1) & 1);
+        if (n >= 0) mbar_wait(dpt_empty, n & 1);
+        if (lane_id() == 0) traceb(0, n + 1, 2);
         tc_fence_after();
         if (elect_one()) {
-          for (int ks = 0; ks < 4; ++ks)  // S -= K^T V (E_S(m-1) is done: sS_ready above)
-            mma_ss(tmem + kS, mn(aK, ks, 8192), kd(aV, ks, 128), id_Sneg, 1);
-          mma_commit(s_full);
           for (int ks = 0; ks < 8; ++ks)  // T1 = Q K^T -> upper lane half
-            mma_ss(tmem + kDP + kHalf, kd(aQ, ks, 64), kd(aK, ks, 64), id_T1, ks > 0);
+            mma_ss(tmem + kDP + kHalf, kd(bQ, ks, 64), kd(bK, ks, 64), id_T1, ks > 0);
+          for (int ks = 0; ks < 8; ++ks)  // dPt = W_hat V^T -> lower lane half
+            mma_ss(tmem + kDP, mn(bW, ks, 8192), mn(bV, ks, 8192), id_dPt, ks > 0);
+          mma_commit(dpt_full);
         }
         __syncwarp();
-        mbar_wait(w_ready, m & 1);
-        if (lane_id() == 0) traceb(0, m, 4);
+      }
+      if (n + 1 < nc) {  // S -= K^T V of chunk n+1 (E_S(n) has read S: sS_ready above)
         tc_fence_after();
         if (elect_one()) {
-          for (int ks = 0; ks < 8; ++ks)  // dPt = W_hat V^T -> lower lane half
-            mma_ss(tmem + kDP, mn(aW, ks, 8192), mn(aV, ks, 8192), id_dPt, ks > 0);
-          mma_commit(dpt_full);
+          for (int ks = 0; ks < 4; ++ks)
+            mma_ss(tmem + kS, mn(bK, ks, 8192), kd(bV, ks, 128), id_Sneg, 1);
+          mma_commit(s_full);
         }
         __syncwarp();
       }
@@ -831,6 +845,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const uint32_t qd = warp & 3;
   const int l = (int)lane_id();
   const int r = (int)(qd * 32) + l;            // lane of the M=128 accumulators (j or m)
+  const int ih = (int)(qd * 16) + (l & 15);    // half-lane row i of M=64 accumulators
+  const bool upper = l >= 16;                  // lanes 16..31 of a quadrant: upper half
   const uint32_t lb = (qd * 32u) << 16;
   const float a = prm.a, b = prm.b;
   const float* recR = prm.cmb + (grp * prm.P + p) * 2 * state_floats(kD) + state_floats(kD);
@@ -859,8 +875,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   };
   if (warp < 8) {
     // ------------------------------------------------------------ WG-A (warps 4..7)
-    // Iteration n: dV^T drain of chunk n-1 (then c += dc(n-1)); bR -> sR for j < 64,
-    // z and bS -> sS (E_S) of chunk n.
+    // Iteration n: dV^T drain of chunk n-1 (then c += dc(n-1)); bR -> sR for j < 64 and
+    // bS -> sS (E_S) of chunk n.
     const int et = (int)threadIdx.x - 128;
     float cj = recR[kD * kD + kD + r];  // c_next (j = r)
     auto dv_out = [&](int m) {  // dV^T of chunk m (lanes j): acc + a c_next
@@ -887,37 +903,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       uint16_t* dvb = (uint16_t*)prm.dv + (grp * kD + qd * 32) * prm.N + row_of(m);
       warp_store_rows_2k(sP + qd * 2048, vt, [&](int seg) { return dvb + seg * prm.N; });
       mbar_arrive(gkv_empty);  // after the staging: E1(m+1) rewrites sP
-      const float* dq4 = dcp + (m & 3) * 4 * kD;  // WG-C's partial row sums of W_hat (chunk m)
-      cj += (dq4[r] + dq4[kD + r]) + (dq4[2 * kD + r] + dq4[3 * kD + r]);
+      cj += dcp[(m & 3) * kD + r];
     };
     // One call site per phase (the kernel's code must stay small for the I-cache):
     // iteration n = nc only drains dV^T(nc-1).
     for (int n = 0; n <= nc; ++n) {
       if (n >= 1) dv_out(n - 1);
       if (n == nc) break;
-      const int s = n & 1;
       er_half(n, 0);
       if (et == 0) traceb(1, n, 1);
-      // ---- z_prev(n) = z_prev(n-1) - sum_t k_t over this chunk -> zbuf[n & 3]
-      mbar_wait(&full[s], (n >> 1) & 1);
-      {
-        const uint8_t* k_t = smem + s * kStage + kT64;
-        const int mg = et >> 3, tg = et & 7;  // columns 8 mg.., rows tg + 8 k
-        float zs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
-        for (int k8 = 0; k8 < kCB / 8; ++k8) {
-          const uint4 v4 = *(const uint4*)(k_t + sw128_off(tg + 8 * k8, 8 * mg, kCB));
-          const uint32_t xx[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float2 f2 = unpack2<kBF16>(xx[q]);
-            zs[2 * q] += f2.x;
-            zs[2 * q + 1] += f2.y;
-          }
-        }
-        const int m = 8 * mg + tg;
-        zbuf[(n & 3) * kD + m] = zbuf[((n - 1) & 3) * kD + m] - reduce_scatter8(zs, tg);
-      }
       // ---- E_S: b S_prev -> sS (after the dQ drain of chunk n-1 used sS as scratch)
       mbar_wait(s_full, n & 1);
       if (n >= 1) mbar_wait(gq_empty, (n - 1) & 1);
@@ -940,18 +934,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       fence_proxy_async();
       tc_fence_before();
-      mbar_arrive(sS_ready);  // z(n) above is published with it (read by dq_out(n))
-      mbar_arrive(&empty[s]);
+      mbar_arrive(sS_ready);
       if (et == 0) traceb(1, n, 3);
     }
   } else if (warp < 12) {
     // ------------------------------------------------------------ WG-B (warps 8..11)
     // Iteration n: bR -> sR for j >= 64 of chunk n, dK^T and dQ drains of chunk n-1,
     // du of chunk n.
-    const int ih = (int)(qd * 16) + (l & 15);
-    const bool upper = l >= 16;
     const int eb = (int)threadIdx.x - 256;
     float u = recR[kD * kD + r];  // u_next (m = r)
+    float si_prev = 0.f;          // s_i (i = ih) of the chunk whose dQ drains next
     auto dk_out = [&](int m) {  // dK^T (lanes m): acc - b u_next
       mbar_wait(gkv_full, m & 1);
       if (m >= 1) u += du_s[((m - 1) & 3) * kD + r];  // suffix sum through chunk m-1
@@ -982,10 +974,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(gq_full, m & 1);
       if (eb == 0) traceb(2, m, 0);
       tc_fence_after();
-      const float* sA = s_s + (m & 3) * 2 * kCB;
-      const float si = sA[ih] + sA[kCB + ih];
       const float* zq = zbuf + (m & 3) * kD;
       const int m0 = upper ? 64 : 0;
+      const float bs = b * si_prev;
       uint4 vt[8];
 #pragma unroll
       for (int c0 = 0; c0 < 64; c0 += 32) {
@@ -1000,8 +991,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           const float z8[8] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            q4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) - si * b * z8[2 * q],
-                                 __uint_as_float(x[8 * w4 + 2 * q + 1]) - si * b * z8[2 * q + 1]);
+            q4[q] = pack2<kBF16>(__uint_as_float(x[8 * w4 + 2 * q]) - bs * z8[2 * q],
+                                 __uint_as_float(x[8 * w4 + 2 * q + 1]) - bs * z8[2 * q + 1]);
           vt[c0 / 8 + w4] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
         }
       }
@@ -1020,18 +1011,23 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int s = n & 1;
       // ---- du_m = sum_i q_im s_i of this chunk -> du_s[n & 3]
       mbar_wait(&full[s], (n >> 1) & 1);
-      mbar_wait(&s_rdy[s], (n >> 1) & 1);  // slot s next completes at chunk n + 2, after our empty arrival
       {
         const uint8_t* q_t = smem + s * kStage;
-        const float* sA = s_s + (n & 3) * 2 * kCB;
-        const float* sB = sA + kCB;
+        const float* sc = s_s + s * kCB;
+        si_prev = sc[ih];
         const int mg = eb >> 3, tg = eb & 7;  // rows tg + 8k: conflict-free quarter-warps
         float du[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
+        uint4 qv[kCB / 8];  // all loads first: smem latency is long under the MMA traffic
+        float wv[kCB / 8];
+#pragma unroll
         for (int k8 = 0; k8 < kCB / 8; ++k8) {
-          const int i = tg + 8 * k8;
-          const uint4 v4 = *(const uint4*)(q_t + sw128_off(i, 8 * mg, kCB));
-          const float w = sA[i] + sB[i];
+          qv[k8] = *(const uint4*)(q_t + sw128_off(tg + 8 * k8, 8 * mg, kCB));
+          wv[k8] = sc[tg + 8 * k8];
+        }
+#pragma unroll
+        for (int k8 = 0; k8 < kCB / 8; ++k8) {
+          const uint4 v4 = qv[k8];
+          const float w = wv[k8];
           const uint32_t xx[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -1048,64 +1044,41 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ WG-C (warps 12..15)
-    // E1 of chunk n (dPt -> dS, T1 -> P), then the W_hat / s / dc pass of chunk n+1:
-    // W_hat = Omega^T / g in place, partial s_i = sum_j o_ji w_hat_ji of both row
-    // halves, per-warp partial row sums of W_hat (dcp[m & 3]). Rings of 4: slot m & 3
-    // is rewritten only after the stage of chunk m + 2 was released, i.e. after its
-    // readers finished chunk m.
+    // Chunk n: dc_j = sum_i w_hat_ji (-> dcp for WG-A), E1 (dPt -> dS on the lower
+    // lane half, T1 -> P on the upper half), z_prev(n) = z_prev(n-1) - sum_t k_t.
     const int ec = (int)threadIdx.x - 384;
-    const int ih = (int)(qd * 16) + (l & 15);    // half-lane row i of M=64 accumulators
-    const bool upper = l >= 16;                  // lanes 16..31 of a quadrant: upper half
-    uint4 o8[8];
-    float4 g8[2];
-    auto e0 = [&](int m) {
-      const int sm = m & 1;
-      mbar_wait(&full[sm], (m >> 1) & 1);
-      if (ec == 0) traceb(3, m, 0);
-      uint8_t* w_t = smem + sm * kStage + 3 * kT64;
-      float* sp = s_s + (m & 3) * 2 * kCB;
-      float* dq4 = dcp + (m & 3) * 4 * kD + qd * kD;
-      float rs[4];
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
-        uint4 o4[4];
-#pragma unroll
-        for (int rr = 0; rr < 4; ++rr) o4[rr] = h ? o8[4 + rr] : o8[rr];
-        what_pass_half<kBF16>(w_t, o4, g8, sp + h * kCB, ec, 64 * h, rs);
-#pragma unroll
-        for (int rr = 0; rr < 4; ++rr) {
-          const float v = rs[rr] + __shfl_xor_sync(0xffffffffu, rs[rr], 16);
-          if (l < 16) dq4[64 * h + 16 * rr + l] = v;
-        }
-      }
-      fence_proxy_async();
-      mbar_arrive(w_ready);
-      mbar_arrive(&s_rdy[sm]);
-      if (m + 2 < nc) {  // O^T rows (128 B each) and g of chunk m+2 into L2
-        const int64_t row2 = row_of(m + 2);
-        prefetch_l2((const uint16_t*)prm.o + (grp * kD + ec) * prm.N + row2);
-        if (ec < 2) prefetch_l2(prm.g + grp * prm.N + row2 + 32 * ec);
-      }
-      if (m + 1 < nc) what_prefetch<kBF16>(prm, grp, row_of(m + 1), ec, o8, g8);
-      if (ec == 0) traceb(3, m, 1);
-    };
-    if (nc > 0) {
-      what_prefetch<kBF16>(prm, grp, row_of(0), ec, o8, g8);
-      e0(0);
-    }
     for (int n = 0; n < nc; ++n) {
-      // ---- E1: dPt -> dS (lower half lanes), T1 -> P (upper half lanes); sP / sdS are
-      // free once dQ(n-1) has run and the dK^T / dV^T drains (scratch) are done
+      const int s = n & 1;
+      uint8_t* st = smem + s * kStage;
+      mbar_wait(&full[s], (n >> 1) & 1);
+      {  // row j = r of W_hat^T: 8 conflict-free 16-byte chunks
+        const uint8_t* w_t = st + 3 * kT64;
+        uint4 wv[8];
+#pragma unroll
+        for (int c8 = 0; c8 < 8; ++c8) wv[c8] = *(const uint4*)(w_t + sw128_off(r, 8 * c8, 128));
+        float dc = 0.f;
+#pragma unroll
+        for (int c8 = 0; c8 < 8; ++c8) {
+          const uint32_t w4[4] = {wv[c8].x, wv[c8].y, wv[c8].z, wv[c8].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 f2 = unpack2<kBF16>(w4[q]);
+            dc += f2.x + f2.y;
+          }
+        }
+        dcp[(n & 3) * kD + r] = dc;
+      }
+      // ---- E1: sP / sdS are free once dQ(n-1) has run and the dK^T / dV^T drains
+      // (scratch) are done
       mbar_wait(dpt_full, n & 1);
       if (n >= 1) {
         mbar_wait(gq_full, (n - 1) & 1);
         mbar_wait(gkv_empty, (n - 1) & 1);
       }
-      if (ec == 0) traceb(3, n, 2);
+      if (ec == 0) traceb(3, n, 0);
       tc_fence_after();
       {
-        const float* sA = s_s + (n & 3) * 2 * kCB;
-        const float si = sA[ih] + sA[kCB + ih];
+        const float si = s_s[s * kCB + ih];
         const float alpha = upper ? a : -b * si;
         uint8_t* dst = upper ? sP : sdS;
 #pragma unroll 1
@@ -1133,8 +1106,31 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       mbar_arrive(dpt_empty);
       mbar_arrive(ps_ready);
-      if (ec == 0) traceb(3, n, 3);
-      if (n + 1 < nc) e0(n + 1);
+      if (ec == 0) traceb(3, n, 1);
+      // ---- z_prev(n) = z_prev(n-1) - sum_t k_t over this chunk -> zbuf[n & 3]
+      {
+        const uint8_t* k_t = st + kT64;
+        const int mg = ec >> 3, tg = ec & 7;  // columns 8 mg.., rows tg + 8 k
+        float zs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        uint4 kv[kCB / 8];
+#pragma unroll
+        for (int k8 = 0; k8 < kCB / 8; ++k8) kv[k8] = *(const uint4*)(k_t + sw128_off(tg + 8 * k8, 8 * mg, kCB));
+#pragma unroll
+        for (int k8 = 0; k8 < kCB / 8; ++k8) {
+          const uint32_t xx[4] = {kv[k8].x, kv[k8].y, kv[k8].z, kv[k8].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 f2 = unpack2<kBF16>(xx[q]);
+            zs[2 * q] += f2.x;
+            zs[2 * q + 1] += f2.y;
+          }
+        }
+        const int m = 8 * mg + tg;
+        zbuf[(n & 3) * kD + m] = zbuf[((n - 1) & 3) * kD + m] - reduce_scatter8(zs, tg);
+      }
+      mbar_arrive(sS_ready);  // publishes z(n) for dq_out(n) (dQ(n) waits sS_ready)
+      mbar_arrive(&empty[s]);
+      if (ec == 0) traceb(3, n, 2);
     }
   }
   }
@@ -1385,7 +1381,7 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 constexpr size_t kAggSmemB = 2 * kStage + 512 + 1024;
-constexpr size_t kMainSmemB = 2 * kStage + 2 * 8192 + 2 * 32768 + 160 + (8 * kCB + 24 * kD) * 4 + 1024;
+constexpr size_t kMainSmemB = 2 * kStage + 2 * 8192 + 2 * 32768 + 160 + (2 * kCB + 16 * kD) * 4 + 1024;
 static_assert(kMainSmemB <= 232448, "backward smem");
 
 int tcb_segments(int64_t G, int64_t N) { return tc_segments(G, N); }
@@ -1404,7 +1400,7 @@ size_t tc_backward_ws_floats(int64_t G, int64_t N, int64_t D) {
   if (D != kD || N % 128) return 0;
   const int P = tcb_segments(G, N);
   const int64_t seg = ((N / 128 + P - 1) / P) * 128;
-  const int A = agg_split(G, seg, P > 1 ? P - 1 : 1);  // the larger of the two launch shapes' splits
+  const int A = std::max(agg_split(G, seg, P > 1 ? P - 1 : 1), agg_split(G, seg, P));
   const size_t causal = (size_t)((2 * A + 2) * G * P);  // S, R unit sums + combined
   const int Af = agg_split(G, seg, P);
   const size_t full = (size_t)(tc_kv_units(G, N) * G + Af * P * G + 2 * G);  // non-causal unit sums + totals
@@ -1440,7 +1436,7 @@ static cudaError_t tc_backward_full(const Launch& L, const Tensors& t, void* dq,
   cudaFuncSetAttribute(aggR, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggRSmem);
   {
     ProfScope ps("la_bwd_agg", L.stream);
-    aggR<<<dim3(A * P, G), 320, kAggRSmem, L.stream>>>(mQ, mW, mO, pa);
+    aggR<<<dim3(A * P, G), 320, kAggRSmem, L.stream>>>(mQ, mW, mO, mW, pa);
   }
   e = tc_sum_units(unitsR, G, P * A, totR, L.stream);
   if (e != cudaSuccess) return e;
@@ -1473,23 +1469,24 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
   // segmentation (no K/V re-read), else computed by the aggregate pass.
   const float* sv = L.saved_in;
   const bool use_saved = sv != nullptr;  // validated by the ABI layer
-  const int p0 = use_saved ? 1 : 0;  // first segment that needs an aggregate
-  const int A = agg_split(G, seg, P - p0);
+  const int A = agg_split(G, seg, P);  // the W_hat pass covers every segment
   float* stS = ws.base;
   float* stR = stS + G * P * A * SZ;
   float* cmb = stR + G * P * A * SZ;
-  CUtensorMap mQ, mK, mV, mW, mO;
+  CUtensorMap mQ, mK, mV, mW, mO, mWh;
   if (!make_tma_map(&mO, t.o, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1) ||
       !make_tma_map(&mQ, t.q, bf, (uint64_t)(G * N), kD, 64, 2) ||
       !make_tma_map(&mK, t.k, bf, (uint64_t)(G * N), kD, 64, 2) ||
       !make_tma_map(&mV, t.v, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1) ||
-      !make_tma_map(&mW, t.w, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1))
+      !make_tma_map(&mW, t.w, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1) ||
+      !make_tma_map(&mWh, dv, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1))  // W_hat^T staged in dV
     return cudaErrorInvalidValue;
   const char* dbg = getenv("LA_BWD_DEBUG");
-  // With the forward's saved S records only segments 1..P-1 need an aggregate
-  // (their R sums feed the earlier segments' suffix); otherwise every segment's
-  // S sum is needed for the inclusive prefix. The aggregate runs on units of
-  // seg / A rows; the main kernel's prologue sums the unit records.
+  // The W_hat pass + R aggregate runs over every unit of seg / A rows (the sweep
+  // reads W_hat^T and s from it; the R sums of segments 1..P-1 feed the earlier
+  // segments' suffix). Without the forward's saved S records a second aggregate
+  // sums S per unit for the inclusive prefix. The main kernel's prologue sums the
+  // unit records.
   BwdParams prm{t.o, t.g, dq, dk, dv, use_saved ? const_cast<float*>(sv + kSavedHeader) : stS, stR, N, seg, P,
                 L.a, L.b, dbg ? atoi(dbg) : 0, use_saved ? 1 : 0, 0, A, L.carry_prefix, L.carry_suffix, cmb,
                 getenv("LA_PREFETCH") ? atoi(getenv("LA_PREFETCH")) : kBPrefetch};
@@ -1497,26 +1494,27 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
   pa.stS = stS;
   pa.seg_len = seg / A;
   pa.P = P * A;
-  pa.p0 = p0 * A;
+  pa.p0 = 0;
+  pa.store_w = 1;
   auto agg = bf ? k_bwd_agg_tc<true> : k_bwd_agg_tc<false>;
   auto main_k = bf ? k_bwd_tc<true> : k_bwd_tc<false>;
   cudaFuncSetAttribute(agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggSmemB);
   cudaFuncSetAttribute(main_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmemB);
-  int launches = 1;
-  if (P - p0 > 0 && use_saved) {
-    auto aggR = bf ? k_bwd_aggR_tc<true> : k_bwd_aggR_tc<false>;
-    cudaFuncSetAttribute(aggR, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggRSmem);
-    ProfScope ps("la_bwd_agg", L.stream);
-    aggR<<<dim3(A * (P - p0), G), 320, kAggRSmem, L.stream>>>(mQ, mW, mO, pa);
-    launches += 1;
-  } else if (P - p0 > 0) {
-    ProfScope ps("la_bwd_agg", L.stream);
-    agg<<<dim3(A * (P - p0), G), 192, kAggSmemB, L.stream>>>(mQ, mK, mV, mW, pa);
+  int launches = 2;
+  if (!use_saved) {
+    ProfScope ps("la_bwd_agg_s", L.stream);
+    agg<<<dim3(A * P, G), 192, kAggSmemB, L.stream>>>(mQ, mK, mV, mW, pa);
     launches += 1;
   }
   {
+    auto aggR = bf ? k_bwd_aggR_tc<true> : k_bwd_aggR_tc<false>;
+    cudaFuncSetAttribute(aggR, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggRSmem);
+    ProfScope ps("la_bwd_agg", L.stream);
+    aggR<<<dim3(A * P, G), 320, kAggRSmem, L.stream>>>(mQ, mW, mO, mWh, pa);
+  }
+  {
     ProfScope ps("la_bwd_causal", L.stream);
-    main_k<<<dim3(P, G), kBwdThreads, kMainSmemB, L.stream>>>(mQ, mK, mV, mW, prm);
+    main_k<<<dim3(P, G), kBwdThreads, kMainSmemB, L.stream>>>(mQ, mK, mV, mWh, prm);
   }
   note_launch(launches);
   return cudaGetLastError();

@@ -23,11 +23,11 @@ t0 = t[0, 10, 0]
 t = t - t0
 t[t < -10**9] = -1
 R = range(10, 14)
-names = {0: "MMA : blk n start, dKdV issue(n), dQ issue(n), T1/S issue(n), dPt issue(n)",
+names = {0: "MMA : blk n start, dKdV issue(n), T1/dPt issue(n), dQ issue(n)",
          1: "WG-A: gkv_full(n) seen, E_R half done, E_S start, E_S done",
          2: "WG-B: gq_full(n) seen, du done",
-         3: "WG-C: e0 start(n), e0 done(n), E1 start(n), E1 done(n)"}
-cols = {0: 5, 1: 4, 2: 2, 3: 4}
+         3: "WG-C: E1 start(n), E1 done(n), z done(n)"}
+cols = {0: 4, 1: 4, 2: 2, 3: 3}
 for role in range(4):
     print(names[role])
     for c in R: print(c, t[role, c, :cols[role]].tolist())
