@@ -22,6 +22,8 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxe
          "-Xptxas", "-v" if os.environ.get("LA_PTXAS_VERBOSE") else "-O3"]
 if os.environ.get("LA_TRACE"):  # clock64 pipeline traces (diagnostics, la_internal_trace_read*)
     FLAGS.append("-DLA_TRACE")
+    if os.environ.get("LA_TRACE_G"):
+        FLAGS.append("-DLA_TRACE_G=" + os.environ["LA_TRACE_G"])
 
 
 def _newest(paths):

@@ -30,8 +30,11 @@ using namespace sm100;
 
 __device__ unsigned long long g_trace_b[4][64][10];
 __device__ __forceinline__ void traceb(int role, int n, int ev) {
+#ifndef LA_TRACE_G
+#define LA_TRACE_G 0  // traced group (blockIdx.y) of segment 0
+#endif
 #ifdef LA_TRACE  // compiled out by default: the kernels are I-cache sensitive
-  if (blockIdx.x == 0 && blockIdx.y == 0 && n < 64) g_trace_b[role][n][ev] = clock64();
+  if (blockIdx.x == 0 && blockIdx.y == LA_TRACE_G && n < 64) g_trace_b[role][n][ev] = clock64();
 #endif
 }
 
@@ -612,8 +615,9 @@ __global__ void __launch_bounds__(320, 1)
 // aggregate pass (W_hat^T in the dV buffer, s in the chunk's first dQ row), all by
 // TMA. Warp roles (512 threads): 0 TMA producer; 1 MMA issuer + TMEM owner; 2-3 idle
 // (warpgroup 0 hands its registers to the epilogue warpgroups with setmaxnreg);
-// 4-7 WG-A: dV^T drain, bR -> sR (j < 64), bS -> sS; 8-11 WG-B: bR -> sR (j >= 64),
-// dK^T and dQ drains, du; 12-15 WG-C: dc, E1 (dPt -> dS, T1 -> P), z.
+// 4-7 WG-A: dV^T drain, bR -> sR (j < 64), E1 columns 32..63; 8-11 WG-B: dK^T drain,
+// bR -> sR (j >= 64), dQ drain, bS -> sS; 12-15 WG-C: dc, s, E1 columns 0..31, z, du.
+// E1: dPt -> dS (lower TMEM lane half), T1 -> P (upper half).
 // MMA order per chunk n: dK^T / dV^T, R +=, dQ, then T1 / dPt and S -= of chunk n+1:
 // the chain from one chunk's dK^T / dV^T to the next is the drains and E_R in
 // parallel with E1.
@@ -645,9 +649,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* gq_full = bars + 17;    // dQ accumulator complete
   uint64_t* gq_empty = bars + 18;   // ... drained (WG-B)
   float* s_s = (float*)(bars + 20);   // [2 stages][64]  s of the staged chunk (TMA)
-  float* du_s = s_s + 2 * kCB;        // [4][128]  du per chunk (WG-B)
+  float* du_s = s_s + 2 * kCB;        // [4][128]  du per chunk (WG-C -> WG-B's dK^T drain)
   float* zbuf = du_s + 4 * kD;        // [4][128]  z_prev per chunk (WG-C -> WG-B's dQ drain)
   float* dcp = zbuf + 4 * kD;         // [4][128]  dc per chunk (WG-C -> WG-A's dV^T drain)
+  float* s_ring = dcp + 4 * kD;       // [4][64]   s per chunk (WG-C -> WG-B's dQ drain)
+  uint8_t* dkscr = (uint8_t*)(s_ring + 4 * kCB);  // [4 warps][2 KB] dK^T store staging
 
   const int p = blockIdx.x;
   const int64_t grp = blockIdx.y;
@@ -656,6 +662,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int nc = (int)((s1 - s0) / kCB);
   auto row_of = [&](int m) -> int64_t { return s0 + (int64_t)(nc - 1 - m) * kCB; };  // reverse sweep
   const uint32_t warp = warp_id();
+  if (threadIdx.x == 0) traceb(0, 63, 8);
   if (warp == 0 && elect_one()) {
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
@@ -663,13 +670,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     tma_prefetch(&tmW);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1 + 256);
+      mbar_init(&empty[s], 1 + 128);
     }
     mbar_init(s_full, 1);
     mbar_init(dpt_full, 1);
-    mbar_init(dpt_empty, 128);
+    mbar_init(dpt_empty, 256);
     mbar_init(sS_ready, 256);
-    mbar_init(ps_ready, 128);
+    mbar_init(ps_ready, 256);
     mbar_init(sR_ready, 256);
     mbar_init(gkv_full, 1);
     mbar_init(gkv_empty, 256);
@@ -727,6 +734,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) traceb(0, 63, 9);
 
   if (warp < 4) {
   regs_dec<96>();
@@ -873,10 +881,40 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     tc_fence_before();
     mbar_arrive(sR_ready);
   };
+  // E1 for columns [t0, t0 + 32) of chunk n: P = a + b T1 (upper lanes), dS = b dPt - b s
+  // (lower lanes), one FFMA per element, no divergence
+  auto e1_half = [&](int n, int t0) {
+    mbar_wait(dpt_full, n & 1);
+    if (n >= 1) mbar_wait(gq_full, (n - 1) & 1);  // dK^T/dV^T(n-1) and dQ(n-1) have read sP / sdS
+    tc_fence_after();
+    const float si = s_s[(n & 1) * kCB + ih];
+    const float alpha = upper ? a : -b * si;
+    uint8_t* dst = upper ? sP : sdS;
+    uint32_t x[32];
+    tmem_ld32(tmem + lb + kDP + t0, x);
+    tmem_ld_wait();
+#pragma unroll
+    for (int w8 = 0; w8 < 4; ++w8) {
+      uint32_t pk[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int t = t0 + 8 * w8 + 2 * q;
+        const float x0 = __uint_as_float(x[8 * w8 + 2 * q]), x1 = __uint_as_float(x[8 * w8 + 2 * q + 1]);
+        const float v0 = t <= ih ? fmaf(b, x0, alpha) : 0.f;
+        const float v1 = t + 1 <= ih ? fmaf(b, x1, alpha) : 0.f;
+        pk[q] = pack2<kBF16>(v0, v1);
+      }
+      *(uint4*)(dst + sw128_off(ih, t0 + 8 * w8, kCB)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    mbar_arrive(dpt_empty);
+    mbar_arrive(ps_ready);
+  };
   if (warp < 8) {
     // ------------------------------------------------------------ WG-A (warps 4..7)
     // Iteration n: dV^T drain of chunk n-1 (then c += dc(n-1)); bR -> sR for j < 64 and
-    // bS -> sS (E_S) of chunk n.
+    // E1 columns 32..63 of chunk n.
     const int et = (int)threadIdx.x - 128;
     float cj = recR[kD * kD + kD + r];  // c_next (j = r)
     auto dv_out = [&](int m) {  // dV^T of chunk m (lanes j): acc + a c_next
@@ -902,7 +940,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       uint16_t* dvb = (uint16_t*)prm.dv + (grp * kD + qd * 32) * prm.N + row_of(m);
       warp_store_rows_2k(sP + qd * 2048, vt, [&](int seg) { return dvb + seg * prm.N; });
-      mbar_arrive(gkv_empty);  // after the staging: E1(m+1) rewrites sP
+      mbar_arrive(gkv_empty);  // after the staging: WG-C's E1(m+1) rewrites these sP rows
       cj += dcp[(m & 3) * kD + r];
     };
     // One call site per phase (the kernel's code must stay small for the I-cache):
@@ -912,38 +950,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (n == nc) break;
       er_half(n, 0);
       if (et == 0) traceb(1, n, 1);
-      // ---- E_S: b S_prev -> sS (after the dQ drain of chunk n-1 used sS as scratch)
-      mbar_wait(s_full, n & 1);
-      if (n >= 1) mbar_wait(gq_empty, (n - 1) & 1);
+      e1_half(n, 32);  // after dv_out: this warp's sP rows were its staging scratch
       if (et == 0) traceb(1, n, 2);
-      tc_fence_after();
-#pragma unroll 1
-      for (int j0 = 0; j0 < kD; j0 += 32) {
-        uint32_t x[32];
-        tmem_ld32(tmem + lb + kS + j0, x);
-        tmem_ld_wait();
-#pragma unroll
-        for (int w8 = 0; w8 < 4; ++w8) {
-          uint4 v;
-          v.x = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 0]), b * __uint_as_float(x[8 * w8 + 1]));
-          v.y = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 2]), b * __uint_as_float(x[8 * w8 + 3]));
-          v.z = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 4]), b * __uint_as_float(x[8 * w8 + 5]));
-          v.w = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 6]), b * __uint_as_float(x[8 * w8 + 7]));
-          *(uint4*)(sS + sw128_off(r, j0 + 8 * w8, 128)) = v;
-        }
-      }
-      fence_proxy_async();
-      tc_fence_before();
-      mbar_arrive(sS_ready);
-      if (et == 0) traceb(1, n, 3);
     }
   } else if (warp < 12) {
     // ------------------------------------------------------------ WG-B (warps 8..11)
-    // Iteration n: bR -> sR for j >= 64 of chunk n, dK^T and dQ drains of chunk n-1,
-    // du of chunk n.
+    // Iteration n: dK^T drain of chunk n-1, bR -> sR for j >= 64 of chunk n, dQ drain
+    // of chunk n-1, bS -> sS (E_S) of chunk n.
     const int eb = (int)threadIdx.x - 256;
     float u = recR[kD * kD + r];  // u_next (m = r)
-    float si_prev = 0.f;          // s_i (i = ih) of the chunk whose dQ drains next
     auto dk_out = [&](int m) {  // dK^T (lanes m): acc - b u_next
       mbar_wait(gkv_full, m & 1);
       if (m >= 1) u += du_s[((m - 1) & 3) * kD + r];  // suffix sum through chunk m-1
@@ -965,10 +980,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_wait(gq_full, m & 1);  // dQ(m) has read dS: sdS is free as scratch
+      mbar_arrive(gkv_empty);
       uint16_t* dkb = (uint16_t*)prm.dk + (grp * kD + qd * 32) * prm.N + row_of(m);
-      warp_store_rows_2k(sdS + qd * 2048, vt, [&](int seg) { return dkb + seg * prm.N; });
-      mbar_arrive(gkv_empty);  // after the staging: E1(m+1) rewrites sdS
+      warp_store_rows_2k(dkscr + qd * 2048, vt, [&](int seg) { return dkb + seg * prm.N; });
     };
     auto dq_out = [&](int m) {  // dQ (half lanes): acc - b s_i z_prev
       mbar_wait(gq_full, m & 1);
@@ -976,7 +990,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_after();
       const float* zq = zbuf + (m & 3) * kD;
       const int m0 = upper ? 64 : 0;
-      const float bs = b * si_prev;
+      const float bs = b * s_ring[(m & 3) * kCB + ih];
       uint4 vt[8];
 #pragma unroll
       for (int c0 = 0; c0 < 64; c0 += 32) {
@@ -1004,49 +1018,41 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_arrive(gq_empty);
     };
     for (int n = 0; n <= nc; ++n) {
-      if (n < nc) er_half(n, 64);
       if (n >= 1) dk_out(n - 1);
+      if (n < nc) er_half(n, 64);
       if (n >= 1) dq_out(n - 1);
       if (n == nc) break;
-      const int s = n & 1;
-      // ---- du_m = sum_i q_im s_i of this chunk -> du_s[n & 3]
-      mbar_wait(&full[s], (n >> 1) & 1);
-      {
-        const uint8_t* q_t = smem + s * kStage;
-        const float* sc = s_s + s * kCB;
-        si_prev = sc[ih];
-        const int mg = eb >> 3, tg = eb & 7;  // rows tg + 8k: conflict-free quarter-warps
-        float du[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        uint4 qv[kCB / 8];  // all loads first: smem latency is long under the MMA traffic
-        float wv[kCB / 8];
-#pragma unroll
-        for (int k8 = 0; k8 < kCB / 8; ++k8) {
-          qv[k8] = *(const uint4*)(q_t + sw128_off(tg + 8 * k8, 8 * mg, kCB));
-          wv[k8] = sc[tg + 8 * k8];
-        }
-#pragma unroll
-        for (int k8 = 0; k8 < kCB / 8; ++k8) {
-          const uint4 v4 = qv[k8];
-          const float w = wv[k8];
-          const uint32_t xx[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float2 f2 = unpack2<kBF16>(xx[q]);
-            du[2 * q] += w * f2.x;
-            du[2 * q + 1] += w * f2.y;
-          }
-        }
-        du_s[(n & 3) * kD + 8 * mg + tg] = reduce_scatter8(du, tg);
-      }
-      named_bar(2, 128);  // du(n) visible to dk_out(n + 1)
-      mbar_arrive(&empty[s]);
+      // ---- E_S: b S_prev -> sS (after every warp's dQ staging in sS: gq_empty)
+      mbar_wait(s_full, n & 1);
+      if (n >= 1) mbar_wait(gq_empty, (n - 1) & 1);
       if (eb == 0) traceb(2, n, 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int j0 = 0; j0 < kD; j0 += 32) {
+        uint32_t x[32];
+        tmem_ld32(tmem + lb + kS + j0, x);
+        tmem_ld_wait();
+#pragma unroll
+        for (int w8 = 0; w8 < 4; ++w8) {
+          uint4 v;
+          v.x = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 0]), b * __uint_as_float(x[8 * w8 + 1]));
+          v.y = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 2]), b * __uint_as_float(x[8 * w8 + 3]));
+          v.z = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 4]), b * __uint_as_float(x[8 * w8 + 5]));
+          v.w = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 6]), b * __uint_as_float(x[8 * w8 + 7]));
+          *(uint4*)(sS + sw128_off(r, j0 + 8 * w8, 128)) = v;
+        }
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(sS_ready);
+      if (eb == 0) traceb(2, n, 2);
     }
   } else {
     // ------------------------------------------------------------ WG-C (warps 12..15)
-    // Chunk n: dc_j = sum_i w_hat_ji (-> dcp for WG-A), E1 (dPt -> dS on the lower
-    // lane half, T1 -> P on the upper half), z_prev(n) = z_prev(n-1) - sum_t k_t.
+    // Chunk n: dc_j = sum_i w_hat_ji (-> dcp for WG-A), s (-> s_ring for WG-B), E1
+    // columns 0..31, z_prev(n) = z_prev(n-1) - sum_t k_t, du_m = sum_i q_im s_i.
     const int ec = (int)threadIdx.x - 384;
+    const int mg = ec >> 3, tg = ec & 7;  // column sums: columns 8 mg.., rows tg + 8 k
     for (int n = 0; n < nc; ++n) {
       const int s = n & 1;
       uint8_t* st = smem + s * kStage;
@@ -1067,50 +1073,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
         }
         dcp[(n & 3) * kD + r] = dc;
+        if (ec < kCB) s_ring[(n & 3) * kCB + ec] = s_s[s * kCB + ec];
       }
-      // ---- E1: sP / sdS are free once dQ(n-1) has run and the dK^T / dV^T drains
-      // (scratch) are done
-      mbar_wait(dpt_full, n & 1);
-      if (n >= 1) {
-        mbar_wait(gq_full, (n - 1) & 1);
-        mbar_wait(gkv_empty, (n - 1) & 1);
-      }
+      if (n >= 1) mbar_wait(gkv_empty, (n - 1) & 1);  // WG-A's dV^T staging in sP is done
       if (ec == 0) traceb(3, n, 0);
-      tc_fence_after();
-      {
-        const float si = s_s[s * kCB + ih];
-        const float alpha = upper ? a : -b * si;
-        uint8_t* dst = upper ? sP : sdS;
-#pragma unroll 1
-        for (int t0 = 0; t0 < kCB; t0 += 32) {
-          uint32_t x[32];
-          tmem_ld32(tmem + lb + kDP + t0, x);
-          tmem_ld_wait();
-#pragma unroll
-          for (int w8 = 0; w8 < 4; ++w8) {
-            uint32_t pk[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int t = t0 + 8 * w8 + 2 * q;
-              const float x0 = __uint_as_float(x[8 * w8 + 2 * q]), x1 = __uint_as_float(x[8 * w8 + 2 * q + 1]);
-              // P = a + b T1 (upper lanes), dS = b dPt - b s (lower lanes): one FFMA, no divergence
-              const float v0 = t <= ih ? fmaf(b, x0, alpha) : 0.f;
-              const float v1 = t + 1 <= ih ? fmaf(b, x1, alpha) : 0.f;
-              pk[q] = pack2<kBF16>(v0, v1);
-            }
-            *(uint4*)(dst + sw128_off(ih, t0 + 8 * w8, kCB)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          }
-        }
-      }
-      fence_proxy_async();
-      tc_fence_before();
-      mbar_arrive(dpt_empty);
-      mbar_arrive(ps_ready);
+      e1_half(n, 0);
       if (ec == 0) traceb(3, n, 1);
-      // ---- z_prev(n) = z_prev(n-1) - sum_t k_t over this chunk -> zbuf[n & 3]
+      // ---- z_prev(n) -> zbuf[n & 3]
       {
         const uint8_t* k_t = st + kT64;
-        const int mg = ec >> 3, tg = ec & 7;  // columns 8 mg.., rows tg + 8 k
         float zs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         uint4 kv[kCB / 8];
 #pragma unroll
@@ -1128,7 +1099,31 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int m = 8 * mg + tg;
         zbuf[(n & 3) * kD + m] = zbuf[((n - 1) & 3) * kD + m] - reduce_scatter8(zs, tg);
       }
-      mbar_arrive(sS_ready);  // publishes z(n) for dq_out(n) (dQ(n) waits sS_ready)
+      mbar_arrive(sS_ready);  // publishes z(n), s(n) for dq_out(n) (dQ(n) waits sS_ready)
+      // ---- du_m = sum_i q_im s_i of this chunk -> du_s[n & 3] (read by dk_out(n + 1))
+      {
+        const uint8_t* q_t = st;
+        const float* sc = s_s + s * kCB;
+        float du[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        uint4 qv[kCB / 8];  // all loads first: smem latency is long under the MMA traffic
+        float wv[kCB / 8];
+#pragma unroll
+        for (int k8 = 0; k8 < kCB / 8; ++k8) {
+          qv[k8] = *(const uint4*)(q_t + sw128_off(tg + 8 * k8, 8 * mg, kCB));
+          wv[k8] = sc[tg + 8 * k8];
+        }
+#pragma unroll
+        for (int k8 = 0; k8 < kCB / 8; ++k8) {
+          const uint32_t xx[4] = {qv[k8].x, qv[k8].y, qv[k8].z, qv[k8].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 f2 = unpack2<kBF16>(xx[q]);
+            du[2 * q] += wv[k8] * f2.x;
+            du[2 * q + 1] += wv[k8] * f2.y;
+          }
+        }
+        du_s[(n & 3) * kD + 8 * mg + tg] = reduce_scatter8(du, tg);
+      }
       mbar_arrive(&empty[s]);
       if (ec == 0) traceb(3, n, 2);
     }
@@ -1136,6 +1131,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) traceb(0, 63, 7);
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
@@ -1381,7 +1377,7 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 constexpr size_t kAggSmemB = 2 * kStage + 512 + 1024;
-constexpr size_t kMainSmemB = 2 * kStage + 2 * 8192 + 2 * 32768 + 160 + (2 * kCB + 16 * kD) * 4 + 1024;
+constexpr size_t kMainSmemB = 2 * kStage + 2 * 8192 + 2 * 32768 + 160 + (6 * kCB + 16 * kD) * 4 + 8192 + 1024;
 static_assert(kMainSmemB <= 232448, "backward smem");
 
 int tcb_segments(int64_t G, int64_t N) { return tc_segments(G, N); }

@@ -20,15 +20,18 @@ buf = (C.c_ulonglong * (4 * 64 * 10))()
 L.la_internal_trace_read_bwd(buf)
 t = np.array(buf, dtype=np.int64).reshape(4, 64, 10)
 t0 = t[0, 10, 0]
+ent, pro, fin = t[0, 63, 8], t[0, 63, 9], t[0, 63, 7]
+print("prologue", pro - ent, "first chunk", t[0, 0, 1] - pro, "total", fin - ent)
 t = t - t0
 t[t < -10**9] = -1
 R = range(10, 14)
 names = {0: "MMA : blk n start, dKdV issue(n), T1/dPt issue(n), dQ issue(n)",
-         1: "WG-A: gkv_full(n) seen, E_R half done, E_S start, E_S done",
-         2: "WG-B: gq_full(n) seen, du done",
-         3: "WG-C: E1 start(n), E1 done(n), z done(n)"}
-cols = {0: 4, 1: 4, 2: 2, 3: 3}
+         1: "WG-A: gkv_full(n) seen, E_R half done, E1 half done",
+         2: "WG-B: gq_full(n) seen, E_S start, E_S done",
+         3: "WG-C: E1 start(n), E1 done(n), du done(n)"}
+cols = {0: 4, 1: 3, 2: 3, 3: 3}
 for role in range(4):
     print(names[role])
     for c in R: print(c, t[role, c, :cols[role]].tolist())
-print("period", np.diff(t[0, 5:60, 1]).mean())
+d = np.diff(t[0, 1:64, 1])
+print("period", d.mean(), "by 8:", [int(d[i:i+8].mean()) for i in range(0, 62, 8)])
