@@ -203,7 +203,7 @@ def kernel_bytes(name, rows, D, e):
     """Algorithmic bytes one launch of `name` must move (reads + writes of its own tensors)."""
     table = {
         "la_fwd_causal": 4 * D * e + 4, "la_bwd_causal": 8 * D * e + 4,
-        "k_fwd_rows": 4 * D * e + 4, "la_fwd_agg": 2 * D * e, "la_bwd_agg": 6 * D * e + 4, "k_bwd_rows_dq": 4 * D * e + 8, "k_bwd_rows_dk": 4 * D * e + 8,
+        "k_fwd_rows": 4 * D * e + 4, "la_fwd_agg": 2 * D * e, "la_bwd_agg": 4 * D * e + 8, "k_bwd_rows_dq": 4 * D * e + 8, "k_bwd_rows_dk": 4 * D * e + 8,
         "k_bwd_rows_dv": 4 * D * e + 4, "k_seg_sums": 2 * D * e, "k_row_s": 2 * D * e + 8,
     }
     for key, per_row in table.items():
@@ -243,6 +243,9 @@ def run_our_arm(args):
     def uni(shape):
         return (torch.rand(shape, device=dev, generator=gen, dtype=torch.float32) * 2 - 1).to(torch.bfloat16)
 
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats(dev)
+    free0 = torch.cuda.mem_get_info(dev)[0]
     q = unit_rows((G, N, D))       # SequenceMajor
     k = unit_rows((G, N, D))       # SequenceMajor
     v = uni((G, D, N))             # FeatureMajor
@@ -296,6 +299,18 @@ def run_our_arm(args):
     if world > 1:
         dist.barrier()
     launches = L.la_launch_count() - launches0
+    # ---- peak HBM: everything the step touches is allocated through torch
+    # (inputs, outputs, workspaces, saved segment states); the library itself allocates
+    # nothing on this path, which the driver-level free-memory delta cross-checks.
+    T_ = G * N * D * e
+    retained = 4 * T_ + 4 * T_ + 4 * G * N  # q, k, v, dO in; o, dq, dk, dv out; g
+    transient = wsf.numel() + wsb.numel() + saved.numel()
+    memory = {"peak_allocated_bytes": int(torch.cuda.max_memory_allocated(dev)),
+              "driver_delta_bytes": int(free0 - torch.cuda.mem_get_info(dev)[0]),
+              "retained_bytes": int(retained), "transient_bytes": int(transient),
+              "minimal_retained_bytes": int(8 * T_ + 4 * G * N),
+              "note": "retained = q,k,v,dO,o,g,dq,dk,dv; transient = fwd/bwd workspaces + per-segment "
+                      "saved prefix states (O(G*P*D^2), independent of N)"}
     L.la_profile_enable(0)
     prof = _abi.profile_read()
     ms = t0.elapsed_time(t1) / args.steps
@@ -390,7 +405,7 @@ def run_our_arm(args):
                 "step_roofline": {"alg_bytes": step_bytes, "achieved_gbs": step_gbs, "frac_hbm": step_gbs / hbm,
                                   "alg_tflops": flops / (ms / 1e3) / 1e12,
                                   "frac_bf16": flops / (ms / 1e3) / 1e12 / tf},
-                "kernels": kstats, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "kernels": kstats, "memory": memory, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clocks}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -21,3 +21,35 @@ def test_shim_compiles_and_links(tmp_path):
     ref = os.path.join(ROOT, "oracle", "_ref", "libla_ref.so")
     subprocess.run(["g++", "-shared", "-o", str(so), str(obj), ref, "-L", lib, "-lla_cuda",
                     f"-Wl,-rpath,{lib}", "-Wl,--no-undefined"], check=True)
+
+
+VERIFY = os.path.join(ROOT, "oracle", "_ref", "verify_gpu")
+
+
+def _verify_binary():
+    if not os.path.exists(VERIFY):
+        if os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libla_ref.so")):
+            pytest.fail("oracle/_ref/verify_gpu missing: run __graft_entry__.build()")
+        pytest.skip("reference build absent")
+    return VERIFY
+
+
+@pytest.mark.gpu
+def test_verify_suites_through_shim_on_gpu():
+    """The reference's verify suites (verify.cpp:57-380) with la::cuda::* as the code
+    under test: every suite passes on the device."""
+    r = subprocess.run([_verify_binary()], capture_output=True, text=True, timeout=900)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert '"suite": "tensorcore", "passed": true' in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("defect", ["beta-k-sign", "causal-off-by-one", "drop-v-a-term"])
+def test_verify_catches_injected_defects_on_gpu(defect):
+    """Mutation sensitivity (acceptance.cpp:193-217): each Fault run on the device makes
+    the verify suites fail (exit 1)."""
+    r = subprocess.run([_verify_binary(), "--fwd-cases", "25", "--bwd-cases", "10", "--norm-cases", "50",
+                        "--tc-cases", "0", "--inject-defect", defect], capture_output=True, text=True, timeout=600)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 1, r.stdout + r.stderr
