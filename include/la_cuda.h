@@ -175,6 +175,34 @@ la_status la_combine_shard_states(const la_problem* p, const float* gathered, in
 
 la_status la_query_status(const void* workspace, void* stream, la_error_info* err);
 
+/* ------------------------------------------- input prologue and diagnostics (device)
+ * The reference's API calls either side of the hot path.
+ * Tensors are (G, N, D) in p->dtype; accumulators are the reference's TermAccumulator
+ * (forward.hpp:44-50): FeatureMajor G*N*D, fp32 on the device. */
+/* normalize_qk (plan.cpp:95-117): every row scaled to unit L2 norm, zero rows left as
+ * they are; outputs keep the input layouts and may alias the inputs. */
+la_status la_normalize_qk(const la_problem* p, const void* q, la_layout lq, const void* k, la_layout lk,
+                          void* q_out, void* k_out, void* stream, la_error_info* err);
+/* relayout (tensor.cpp:101-119): copy of x in layout ly. */
+la_status la_relayout(const la_problem* p, const void* x, la_layout lx, void* y, la_layout ly, void* stream,
+                      la_error_info* err);
+/* make_omega_hat (backward.cpp:74-91): out = omega / g per row, FeatureMajor. */
+la_status la_make_omega_hat(const la_problem* p, const void* omega, la_layout lw, const float* g, void* out,
+                            void* stream, la_error_info* err);
+/* constant_term_pass (forward.cpp:97-107): f_ij = a * sum_{n<=i} v_nj (overwrites f). */
+la_status la_constant_term_pass(const la_problem* p, const void* v, la_layout lv, float* f, void* stream,
+                                la_error_info* err);
+/* linear_term_pass (forward.cpp:109-131): f_ij += sum_m q_im * b * sum_{n<=i} k_nm v_nj. */
+la_status la_linear_term_pass(const la_problem* p, const void* q, la_layout lq, const void* k, la_layout lk,
+                              const void* v, la_layout lv, float* f, void* stream, la_error_info* err);
+/* alpha_term_pass (backward.cpp:103-128), b = p->b: dk_ir = sum_j alphaK_rj v_ij with
+ * alphaK_rj = b * sum_{t>=i} q_tr * omega_hat_tj (overwrites dk). */
+la_status la_alpha_term_pass(const la_problem* p, const void* q, la_layout lq, const void* v, la_layout lv,
+                             const void* omega_hat, la_layout lw, float* dk, void* stream, la_error_info* err);
+/* beta_term_pass (backward.cpp:130-153), b = p->b: dk_ir -= b * sum_{t>=i} q_tr * sum_j o_tj omega_hat_tj. */
+la_status la_beta_term_pass(const la_problem* p, const void* q, la_layout lq, const void* o, la_layout lo,
+                            const void* omega_hat, la_layout lw, float* dk, void* stream, la_error_info* err);
+
 /* ---------------------------------------------------------------- host API */
 /* End-to-end over host buffers: copies inputs to the device, runs, copies the
  * results back (device arena cached per thread). Used by the reference-facing

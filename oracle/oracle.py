@@ -250,3 +250,111 @@ def ref_fwd_bwd_f32(q, k, v, omega, a=1.0, b=1.0, causal=True, workers=1):
     if st:
         raise RuntimeError(f"reference run_backward<float> failed with status {st}")
     return out, g, dq, dk, dv
+
+
+# --------------------------------------------------------------------------- prologue + term passes
+# numpy restatements (logical (G, N, D) arrays, f64) of the reference's API calls
+# either side of the hot path; pinned against the reference library in tests/test_oracle.py.
+def relayout_flat(x, layout):
+    """relayout (tensor.cpp:101-119): the flat buffer of logical x in ``layout``."""
+    return to_flat(np.asarray(x, np.float64), layout)
+
+
+def omega_hat(omega, g):
+    """make_omega_hat (backward.cpp:74-91): omega_ij / g_i."""
+    G, N, _ = omega.shape
+    return np.asarray(omega, np.float64) / np.asarray(g, np.float64).reshape(G, N, 1)
+
+
+def constant_term(v, a):
+    """constant_causal_core (forward_kernels.hpp:22-34): f_ij = running sum of a*v_nj."""
+    return np.cumsum(a * np.asarray(v, np.float64), axis=1)
+
+
+def linear_term(q, k, v, b, f):
+    """linear_causal_core with g_vec = null (forward_kernels.hpp:63-128, forward.cpp:109-131):
+    state[j][m] += b*k_im*v_ij, then f_ij += sum_m q_im * state[j][m]."""
+    q, k, v = (np.asarray(x, np.float64) for x in (q, k, v))
+    G, N, D = q.shape
+    f = np.array(f, np.float64, copy=True)
+    for g in range(G):
+        st = np.zeros((D, D))
+        for i in range(N):
+            st += np.outer(v[g, i], b * k[g, i])
+            f[g, i] += st @ q[g, i]
+    return f
+
+
+def alpha_term(q, v, wh, b):
+    """grad_k_alpha_core at unit g (backward_kernels.hpp:61-91, backward.cpp:103-128):
+    suffix alpha[r][j] += b*q_ir*wh_ij; dk_ir = sum_j alpha[r][j]*v_ij (assign)."""
+    q, v, wh = (np.asarray(x, np.float64) for x in (q, v, wh))
+    G, N, D = q.shape
+    dk = np.zeros((G, N, D))
+    for g in range(G):
+        al = np.zeros((D, D))
+        for i in range(N - 1, -1, -1):
+            al += np.outer(b * q[g, i], wh[g, i])
+            dk[g, i] = al @ v[g, i]
+    return dk
+
+
+def beta_term(q, o, wh, b, dk):
+    """grad_k_beta_core at unit g (backward_kernels.hpp:95-130, backward.cpp:130-153):
+    suffix beta[r][j] += b*q_ir*o_ij*wh_ij; dk_ir -= sum_j beta[r][j]."""
+    q, o, wh = (np.asarray(x, np.float64) for x in (q, o, wh))
+    G, N, D = q.shape
+    dk = np.array(dk, np.float64, copy=True)
+    for g in range(G):
+        be = np.zeros((D, D))
+        for i in range(N - 1, -1, -1):
+            be += np.outer(b * q[g, i], o[g, i] * wh[g, i])
+            dk[g, i] -= be.sum(axis=1)
+    return dk
+
+
+def ref_term_pass(kind, x, y, z, a, b, acc, lx=SEQUENCE_MAJOR, ly=FEATURE_MAJOR, lz=FEATURE_MAJOR, L=0):
+    """The reference's own term pass (kind 0 constant, 1 linear, 2 alpha, 3 beta) on a
+    logical f64 accumulator; returns the logical result."""
+    G, N, D = x.shape
+    fl = [to_flat(np.asarray(t if t is not None else x, np.float64), l) for t, l in ((x, lx), (y, ly), (z, lz))]
+    accf = np.array(to_flat(np.asarray(acc, np.float64), FEATURE_MAJOR), copy=True)  # never alias the caller
+    st = ref_lib().ref_term_pass(C.c_int(kind), _p(fl[0]), lx, _p(fl[1]), ly, _p(fl[2]), lz, C.c_int64(G),
+                                 C.c_int64(N), C.c_int64(D), C.c_double(a), C.c_double(b), C.c_int64(L), _p(accf))
+    if st:
+        raise RuntimeError(f"reference term pass failed with status {st}")
+    return from_flat(accf, G, N, D, FEATURE_MAJOR).copy()
+
+
+def ref_omega_hat(omega, g, lw=FEATURE_MAJOR):
+    G, N, D = omega.shape
+    wf = to_flat(np.asarray(omega, np.float64), lw)
+    gf = np.ascontiguousarray(np.asarray(g, np.float64).reshape(-1))
+    out = np.zeros(G * N * D)
+    st = ref_lib().ref_make_omega_hat(_p(wf), lw, _p(gf), C.c_int64(G), C.c_int64(N), C.c_int64(D), _p(out))
+    if st:
+        raise RuntimeError(f"reference make_omega_hat failed with status {st}")
+    return from_flat(out, G, N, D, FEATURE_MAJOR).copy()
+
+
+def ref_normalize_qk(q, k, lq=SEQUENCE_MAJOR, lk=SEQUENCE_MAJOR):
+    G, N, D = q.shape
+    qf, kf = to_flat(np.asarray(q, np.float64), lq), to_flat(np.asarray(k, np.float64), lk)
+    qo, ko = np.zeros(G * N * D), np.zeros(G * N * D)
+    st = ref_lib().ref_normalize_qk(_p(qf), lq, _p(kf), lk, C.c_int64(G), C.c_int64(N), C.c_int64(D),
+                                    _p(qo), _p(ko))
+    if st:
+        raise RuntimeError(f"reference normalize_qk failed with status {st}")
+    return from_flat(qo, G, N, D, lq).copy(), from_flat(ko, G, N, D, lk).copy()
+
+
+def ref_prefix_advance(k_rows, v_rows, a, b):
+    """make_prefix_state + prefix_advance over the rows; returns (x1, x2, y1, y2)."""
+    k_rows, v_rows = np.ascontiguousarray(k_rows, np.float64), np.ascontiguousarray(v_rows, np.float64)
+    R, D = k_rows.shape
+    st_ = np.zeros(D + D * D + 1 + D)
+    st = ref_lib().ref_prefix_advance(_p(k_rows), _p(v_rows), C.c_int64(R), C.c_int64(D), C.c_double(a),
+                                      C.c_double(b), _p(st_))
+    if st:
+        raise RuntimeError(f"reference prefix_advance failed with status {st}")
+    return st_[:D], st_[D:D + D * D].reshape(D, D), st_[D + D * D], st_[D + D * D + 1:]

@@ -193,4 +193,74 @@ int ref_run_backward_f32(int causal, const float* q, const float* k, const float
   }
 }
 
+// Term passes (forward.cpp:97-131, backward.cpp:103-153) on a FeatureMajor f64
+// accumulator `acc` (in/out, G*N*D). kind 0 constant(v=x), 1 linear(q, k=y, v=z),
+// 2 alpha(q, v=y, omega_hat=z), 3 beta(q, o=y, omega_hat=z). Inputs SequenceMajor
+// or FeatureMajor per their layout codes.
+int ref_term_pass(int kind, const double* x, int lx, const double* y, int ly, const double* z, int lz,
+                  int64_t g, int64_t n, int64_t d, double a, double b, int64_t l, double* acc) {
+  try {
+    la::TermAccumulator f = la::make_accumulator(g, n, d);
+    std::memcpy(f.data.data(), acc, sizeof(double) * f.data.size());
+    const la::BlockPlan plan = plan_of(g, n, d, l, 2);
+    if (kind == 0) {
+      la::constant_term_pass(wrap(x, g, n, d, lx), {a, b}, f);
+    } else if (kind == 1) {
+      la::linear_term_pass(wrap(x, g, n, d, lx), wrap(y, g, n, d, ly), wrap(z, g, n, d, lz), {a, b}, plan, f);
+    } else if (kind == 2) {
+      la::alpha_term_pass(wrap(x, g, n, d, lx), wrap(y, g, n, d, ly), wrap(z, g, n, d, lz), plan, f, b);
+    } else {
+      la::beta_term_pass(wrap(x, g, n, d, lx), wrap(y, g, n, d, ly), wrap(z, g, n, d, lz), plan, f, b);
+    }
+    std::memcpy(acc, f.data.data(), sizeof(double) * f.data.size());
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception(), nullptr, nullptr);
+  }
+}
+
+// la::make_omega_hat (backward.cpp:74-91): out FeatureMajor.
+int ref_make_omega_hat(const double* w, int lw, const double* gvec, int64_t g, int64_t n, int64_t d,
+                       double* out) {
+  try {
+    const std::vector<double> gv(gvec, gvec + g * n);
+    copy_out(la::make_omega_hat(wrap(w, g, n, d, lw), gv), out);
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception(), nullptr, nullptr);
+  }
+}
+
+// la::normalize_qk (plan.cpp:95-117): both outputs keep their input layouts.
+int ref_normalize_qk(const double* q, int lq, const double* k, int lk, int64_t g, int64_t n, int64_t d,
+                     double* qo, double* ko) {
+  try {
+    const auto [a, b] = la::normalize_qk(wrap(q, g, n, d, lq), wrap(k, g, n, d, lk));
+    copy_out(a, qo);
+    copy_out(b, ko);
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception(), nullptr, nullptr);
+  }
+}
+
+// la::make_prefix_state + la::prefix_advance over `rows` rows (forward.cpp:50-83).
+// state = [x1 (d) | x2 (d*d) | y1 | y2 (d)].
+int ref_prefix_advance(const double* k_rows, const double* v_rows, int64_t rows, int64_t d, double a,
+                       double b, double* state) {
+  try {
+    la::PrefixState s = la::make_prefix_state(d);
+    for (int64_t r = 0; r < rows; ++r)
+      s = la::prefix_advance(s, std::span<const double>(k_rows + r * d, d),
+                             std::span<const double>(v_rows + r * d, d), {a, b});
+    std::memcpy(state, s.x1.data(), sizeof(double) * d);
+    std::memcpy(state + d, s.x2.data(), sizeof(double) * d * d);
+    state[d + d * d] = s.y1;
+    std::memcpy(state + d + d * d + 1, s.y2.data(), sizeof(double) * d);
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception(), nullptr, nullptr);
+  }
+}
+
 }  // extern "C"

@@ -7,3 +7,6 @@ from .api import (BlockPlan, DegenerateDenominator, Error, Fault, ForwardArtifac
                   HeadTensor, InvalidArgument, InvalidPlan, InvalidShape, Layout, LinearKernelCoeffs,
                   MissingForwardState, Shape, ShapeMismatch, Unsupported, backward_causal, backward_full,
                   default_plan, forward_causal, forward_full, max_abs_diff, validate_plan)
+from .api import (PrefixState, TermAccumulator, alpha_term_pass, beta_term_pass, constant_term_pass,  # noqa: F401
+                  linear_term_pass, make_accumulator, make_omega_hat, make_prefix_state, normalize_qk,
+                  prefix_advance, relayout)

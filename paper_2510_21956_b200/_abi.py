@@ -27,6 +27,8 @@ EXPORTS = [
     "la_backward_shard_state", "la_combine_shard_states", "la_query_status", "la_host_forward",
     "la_host_backward", "la_host_step", "la_host_release", "la_profile_enable", "la_profile_read",
     "la_saved_state_bytes", "la_forward_save", "la_backward_saved",
+    "la_normalize_qk", "la_relayout", "la_make_omega_hat", "la_constant_term_pass", "la_linear_term_pass",
+    "la_alpha_term_pass", "la_beta_term_pass",
 ]
 
 
@@ -98,6 +100,14 @@ def lib():
                                    vp, E]
         L.la_host_backward.argtypes = [P, vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, C.c_int, vp,
                                        vp, vp, vp, E]
+        ci = C.c_int
+        L.la_normalize_qk.argtypes = [P, vp, ci, vp, ci, vp, vp, vp, E]
+        L.la_relayout.argtypes = [P, vp, ci, vp, ci, vp, E]
+        L.la_make_omega_hat.argtypes = [P, vp, ci, vp, vp, vp, E]
+        L.la_constant_term_pass.argtypes = [P, vp, ci, vp, vp, E]
+        L.la_linear_term_pass.argtypes = [P, vp, ci, vp, ci, vp, ci, vp, vp, E]
+        L.la_alpha_term_pass.argtypes = [P, vp, ci, vp, ci, vp, ci, vp, vp, E]
+        L.la_beta_term_pass.argtypes = [P, vp, ci, vp, ci, vp, ci, vp, vp, E]
         _lib = L
     return _lib
 

@@ -11,6 +11,11 @@ tests port line for line:
     la::backward_full(...)                   backward_full(...)                   backward.cpp:98
     la::default_plan / validate_plan         default_plan / validate_plan         plan.cpp:24-62
     la::Error hierarchy                      Error, InvalidShape, ...             error.hpp:10-75
+    la::normalize_qk / relayout              normalize_qk / relayout              plan.cpp:95, tensor.cpp:101
+    la::make_omega_hat                       make_omega_hat                       backward.cpp:74
+    la::constant_term_pass / linear_term_pass  (same names, TermAccumulator)      forward.cpp:97-131
+    la::alpha_term_pass / beta_term_pass     (same names)                         backward.cpp:103-153
+    la::make_prefix_state / prefix_advance   (same names, host, O(D^2))           forward.cpp:50-83
 
 Tensors are HeadTensor objects holding a flat buffer in a declared layout.
 A buffer that is a CUDA ``torch.Tensor`` runs through the device entry points
@@ -427,3 +432,177 @@ def max_abs_diff(x: HeadTensor, y: HeadTensor) -> float:
 
 def launch_count() -> int:
     return int(_abi.lib().la_launch_count())
+
+
+# ----------------------------------------------------------------------------- prologue + diagnostics
+# The reference's API calls either side of the hot path, on
+# the device through la_normalize_qk / la_relayout / la_make_omega_hat / la_*_term_pass.
+# They take device (CUDA torch) HeadTensors; accumulators are fp32 on the device.
+def _device_tensor(t, what):
+    if t is None or t.empty():
+        raise InvalidShape(what)
+    if not _is_torch(t.data) or not t.data.is_cuda:
+        raise InvalidArgument("device entry point: tensor data must be a CUDA torch.Tensor")
+    return t
+
+
+def _simple_problem(t, c=None, plan=None):
+    c = c or LinearKernelCoeffs()
+    return _abi.make_problem(t.groups(), t.seq_len(), t.dim(), _dtype_of_torch(t.data), c.a, c.b, True, 0,
+                             "auto", plan)
+
+
+def normalize_qk(q: HeadTensor, k: HeadTensor):
+    """la::normalize_qk (plan.cpp:95-117): unit-norm rows, zero rows kept, layouts kept."""
+    import torch
+    _device_tensor(q, "normalize_qk requires non-empty Q and K")
+    _device_tensor(k, "normalize_qk requires non-empty Q and K")
+    if not q.same_shape(k) or q.data.dtype != k.data.dtype:
+        raise ShapeMismatch("Q and K shapes must agree")
+    qo, ko = torch.empty_like(q.data), torch.empty_like(k.data)
+    err = _abi.ErrorInfo()
+    p = _simple_problem(q)
+    _raise(_abi.lib().la_normalize_qk(C.byref(p), q.data.data_ptr(), int(q.layout()), k.data.data_ptr(),
+                                      int(k.layout()), qo.data_ptr(), ko.data_ptr(), _stream_ptr(),
+                                      C.byref(err)), err)
+    return (HeadTensor(q.groups(), q.seq_len(), q.dim(), q.layout(), qo),
+            HeadTensor(k.groups(), k.seq_len(), k.dim(), k.layout(), ko))
+
+
+def relayout(t: HeadTensor, target) -> HeadTensor:
+    """la::relayout (tensor.cpp:101-119): same values in ``target`` layout (shared when equal)."""
+    import torch
+    _device_tensor(t, "relayout of an empty tensor")
+    if Layout(target) == t.layout():
+        return t
+    y = torch.empty_like(t.data)
+    err = _abi.ErrorInfo()
+    p = _simple_problem(t)
+    _raise(_abi.lib().la_relayout(C.byref(p), t.data.data_ptr(), int(t.layout()), y.data_ptr(), int(target),
+                                  _stream_ptr(), C.byref(err)), err)
+    return HeadTensor(t.groups(), t.seq_len(), t.dim(), Layout(target), y)
+
+
+def make_omega_hat(omega: HeadTensor, g) -> HeadTensor:
+    """la::make_omega_hat (backward.cpp:74-91): omega / g per row, FeatureMajor."""
+    import torch
+    _device_tensor(omega, "make_omega_hat requires a non-empty cotangent")
+    if g is None or len(g) != omega.groups() * omega.seq_len():
+        raise MissingForwardState("denominator vector length must equal groups*seq_len")
+    g = g if _is_torch(g) else torch.as_tensor(np.asarray(g, np.float32), device=omega.data.device)
+    g = g.to(torch.float32).contiguous()
+    out = torch.empty_like(omega.data)
+    err = _abi.ErrorInfo()
+    p = _simple_problem(omega)
+    _raise(_abi.lib().la_make_omega_hat(C.byref(p), omega.data.data_ptr(), int(omega.layout()), g.data_ptr(),
+                                        out.data_ptr(), _stream_ptr(), C.byref(err)), err)
+    return HeadTensor(omega.groups(), omega.seq_len(), omega.dim(), Layout.FeatureMajor, out)
+
+
+@dataclass
+class TermAccumulator:
+    """la::TermAccumulator (forward.hpp:44-50): FeatureMajor (G, D, N) numerator, fp32 on the device."""
+    groups: int = 0
+    seq_len: int = 0
+    dim: int = 0
+    data: object = None
+
+    def logical(self):
+        return self.data.double().cpu().numpy().reshape(self.groups, self.dim, self.seq_len).transpose(0, 2, 1)
+
+
+def make_accumulator(groups, seq_len, dim, device="cuda") -> TermAccumulator:
+    """la::make_accumulator (forward.cpp:85-95): zero-initialised."""
+    import torch
+    if groups <= 0 or seq_len <= 0 or dim <= 0:
+        raise InvalidShape("accumulator dimensions must be strictly positive")
+    return TermAccumulator(groups, seq_len, dim, torch.zeros(groups * dim * seq_len, dtype=torch.float32,
+                                                             device=device))
+
+
+def _check_acc(acc, t):
+    if acc.groups != t.groups() or acc.seq_len != t.seq_len() or acc.dim != t.dim():
+        raise ShapeMismatch("accumulator shape must match the inputs")
+
+
+def constant_term_pass(v: HeadTensor, c: LinearKernelCoeffs, f: TermAccumulator) -> None:
+    """la::constant_term_pass (forward.cpp:97-107): f = a * prefix sum of V (overwrites)."""
+    _device_tensor(v, "constant_term_pass requires a non-empty V")
+    if f.groups != v.groups() or f.seq_len != v.seq_len() or f.dim != v.dim():
+        raise ShapeMismatch("accumulator shape must match V")
+    err = _abi.ErrorInfo()
+    p = _simple_problem(v, c)
+    _raise(_abi.lib().la_constant_term_pass(C.byref(p), v.data.data_ptr(), int(v.layout()), f.data.data_ptr(),
+                                            _stream_ptr(), C.byref(err)), err)
+
+
+def linear_term_pass(q, k, v, c: LinearKernelCoeffs, plan, f: TermAccumulator) -> None:
+    """la::linear_term_pass (forward.cpp:109-131): f += q . (b-weighted causal K^T V state)."""
+    for t in (q, k, v):
+        _device_tensor(t, "forward requires non-empty Q, K, V")
+    _check_forward_inputs(q, k, v, c, plan)
+    _check_acc(f, q)
+    err = _abi.ErrorInfo()
+    p = _simple_problem(q, c, plan)
+    _raise(_abi.lib().la_linear_term_pass(C.byref(p), q.data.data_ptr(), int(q.layout()), k.data.data_ptr(),
+                                          int(k.layout()), v.data.data_ptr(), int(v.layout()),
+                                          f.data.data_ptr(), _stream_ptr(), C.byref(err)), err)
+
+
+def _check_pass_inputs(a_, b_, omega_hat, plan, dk):
+    """check_pass_inputs (backward.cpp:58-72)."""
+    for t in (a_, b_, omega_hat):
+        _device_tensor(t, "term passes require non-empty inputs")
+    if not a_.same_shape(b_) or not a_.same_shape(omega_hat):
+        raise ShapeMismatch("term pass input shapes must agree")
+    _check_acc(dk, a_)
+    validate_plan(plan, a_.groups(), a_.dim())
+
+
+def alpha_term_pass(q, v, omega_hat, plan, dk: TermAccumulator, b: float = 1.0) -> None:
+    """la::alpha_term_pass (backward.cpp:103-128): dk = sum_j alphaK_rj v_ij (assigns)."""
+    _check_pass_inputs(q, v, omega_hat, plan, dk)
+    err = _abi.ErrorInfo()
+    p = _simple_problem(q, LinearKernelCoeffs(1.0, b), plan)
+    _raise(_abi.lib().la_alpha_term_pass(C.byref(p), q.data.data_ptr(), int(q.layout()), v.data.data_ptr(),
+                                         int(v.layout()), omega_hat.data.data_ptr(), int(omega_hat.layout()),
+                                         dk.data.data_ptr(), _stream_ptr(), C.byref(err)), err)
+
+
+def beta_term_pass(q, o, omega_hat, plan, dk: TermAccumulator, b: float = 1.0) -> None:
+    """la::beta_term_pass (backward.cpp:130-153): dk -= sum_j betaK_rj."""
+    _check_pass_inputs(q, o, omega_hat, plan, dk)
+    err = _abi.ErrorInfo()
+    p = _simple_problem(q, LinearKernelCoeffs(1.0, b), plan)
+    _raise(_abi.lib().la_beta_term_pass(C.byref(p), q.data.data_ptr(), int(q.layout()), o.data.data_ptr(),
+                                        int(o.layout()), omega_hat.data.data_ptr(), int(omega_hat.layout()),
+                                        dk.data.data_ptr(), _stream_ptr(), C.byref(err)), err)
+
+
+@dataclass
+class PrefixState:
+    """la::PrefixState (forward.hpp:13-25): x1 = a*sum v, x2[j][m] = b*sum k_m v_j, y1 = a*i, y2 = b*sum k.
+    The same quantities as a device state record (S^T scaled by b, sigma by a, z by b, count by a)."""
+    dim: int = 0
+    x1: np.ndarray = None
+    x2: np.ndarray = None
+    y1: float = 0.0
+    y2: np.ndarray = None
+
+
+def make_prefix_state(dim: int) -> PrefixState:
+    """la::make_prefix_state (forward.cpp:50-61)."""
+    if dim <= 0:
+        raise InvalidShape("prefix state dimension must be strictly positive")
+    return PrefixState(dim, np.zeros(dim), np.zeros((dim, dim)), 0.0, np.zeros(dim))
+
+
+def prefix_advance(state: PrefixState, k_row, v_row, c: LinearKernelCoeffs) -> PrefixState:
+    """la::prefix_advance (forward.cpp:63-83): pure one-row update (host, O(D^2), f64 like the reference)."""
+    k_row, v_row = np.asarray(k_row, np.float64), np.asarray(v_row, np.float64)
+    if k_row.shape != (state.dim,) or v_row.shape != (state.dim,):
+        raise ShapeMismatch("prefix_advance rows must match the state dimension")
+    x2 = state.x2.copy()
+    for j in range(state.dim):  # the reference's accumulation order, row j then column m
+        x2[j] += c.b * k_row * v_row[j]
+    return PrefixState(state.dim, state.x1 + c.a * v_row, x2, state.y1 + c.a, state.y2 + c.b * k_row)
