@@ -203,6 +203,7 @@ def kernel_bytes(name, rows, D, e):
     """Algorithmic bytes one launch of `name` must move (reads + writes of its own tensors)."""
     table = {
         "la_fwd_causal": 4 * D * e + 4, "la_bwd_causal": 8 * D * e + 4,
+        "la_bwd_fused": 8 * D * e + 4,  # the whole backward (aggregate units + sweeps) in one grid
         "k_fwd_rows": 4 * D * e + 4, "la_fwd_agg": 2 * D * e, "la_bwd_agg": 4 * D * e + 8, "k_bwd_rows_dq": 4 * D * e + 8, "k_bwd_rows_dk": 4 * D * e + 8,
         "k_bwd_rows_dv": 4 * D * e + 4, "k_seg_sums": 2 * D * e, "k_row_s": 2 * D * e + 8,
     }
