@@ -8,9 +8,13 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <string>
 #include <vector>
 
+#include <fstream>
+
 #include "la/backward.hpp"
+#include "la/bench.hpp"
 #include "la/detail/backward_kernels.hpp"
 #include "la/detail/forward_kernels.hpp"
 #include "la/detail/view.hpp"
@@ -262,5 +266,32 @@ int ref_prefix_advance(const double* k_rows, const double* v_rows, int64_t rows,
     return status_of(std::current_exception(), nullptr, nullptr);
   }
 }
+
+// la::read_csv_file + la::fit_slope (bench.cpp:365-403, 459-503): parses a CSV in the
+// reference schema and fits log(wall_time_s) against log(N) (axis 0) or log(D) (axis 1)
+// over the records with the given pass ("fwd"/"bwd", or "" for all).
+int ref_csv_fit(const char* path, int axis, const char* pass, int64_t* n_records, double* slope,
+                double* intercept, double* r2) {
+  try {
+    std::vector<la::BenchRecord> recs = la::read_csv_file(path);
+    *n_records = static_cast<int64_t>(recs.size());
+    std::vector<la::BenchRecord> sel;
+    for (const auto& r : recs)
+      if (!pass[0] || std::string(la::pass_name(r.pass)) == pass) sel.push_back(r);
+    const la::SlopeFit f = la::fit_slope(sel, axis == 0 ? la::SweepAxis::N : la::SweepAxis::D);
+    *slope = f.slope;
+    *intercept = f.intercept;
+    *r2 = f.r2;
+    return 0;
+  } catch (const la::IoError&) {
+    return 10;
+  } catch (const la::InsufficientData&) {
+    return 11;
+  } catch (...) {
+    return status_of(std::current_exception(), nullptr, nullptr);
+  }
+}
+
+const char* ref_csv_header() { return la::kCsvHeader; }
 
 }  // extern "C"

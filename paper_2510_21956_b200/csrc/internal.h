@@ -19,26 +19,21 @@ inline int64_t state_floats(int64_t d) { return (d * d + 2 * d + 1 + 3) & ~(int6
 
 // Sequence segmentation shared by the tensor-core forward and backward so a
 // forward's saved per-segment states line up with the backward's segments.
-// Segments are whole multiples of 128 rows. The count minimises a simple model
-// of the makespan: waves(P) x (chunks per segment + fixed per-CTA overhead) plus
-// the aggregate pre-pass that P > 1 needs.
+// Segments are whole multiples of 128 rows. Rule: the most segments that still fit
+// the G x P sweep grid in ONE wave of CTAs (one CTA per SM). Measured on B200 (B=4
+// H=16 D=128 bf16, profiles/r01_s3_segments.md): more waves of shorter segments lose
+// to the per-CTA prologue (record combine, TMEM / barrier setup), the partial last
+// wave and the larger aggregate pre-pass; fewer segments leave SMs idle. At the north
+// star (G = 64) this gives P = 2: fwd + bwd 3.26 ms against 3.54 ms at P = 9.
 inline int choose_segments(int64_t G, int64_t N, int num_sms = 148) {
   const int64_t c128 = N / 128;
   if (c128 <= 1) return 1;
-  double best = 1e300;
-  int bestP = 1;
-  for (int64_t P = 1; P <= c128 && P <= 64; ++P) {
-    const int64_t seg = (c128 + P - 1) / P;  // 128-row chunks per segment
-    if (seg * (P - 1) >= c128) continue;     // no empty trailing segment
-    const double waves = (double)((G * P + num_sms - 1) / num_sms);
-    double t = waves * (2.0 * seg + 3.0);    // in 64-row chunk times
-    if (P > 1) t += 0.45 * waves * 2.0 * seg;  // aggregate pre-pass
-    if (t < best * 0.995) {
-      best = t;
-      bestP = (int)P;
-    }
-  }
-  return bestP;
+  int64_t P = G >= num_sms ? 1 : num_sms / G;
+  if (P > c128) P = c128;
+  if (P > 64) P = 64;
+  if (P < 1) P = 1;
+  while (P > 1 && ((c128 + P - 1) / P) * (P - 1) >= c128) --P;  // no empty trailing segment
+  return (int)P;
 }
 
 // Aggregate passes split each segment into A equal units (whole 128-row chunks)

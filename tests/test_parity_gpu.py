@@ -357,3 +357,26 @@ def test_f16_key_sum_beyond_half_range(cuda, causal):
     assert np.isfinite(res["out"]).all() and np.isfinite(res["g"]).all()
     assert max_abs(res["out"], ref["out"]) <= BF16_ABS
     assert rel_err(res["g"], ref["g"]) <= 1e-3
+
+
+@pytest.mark.gpu
+def test_fused_backward_schedule_matches_separate(cuda, monkeypatch):
+    """LA_BWD_FUSED=1 (k_bwd_fused: aggregate units and sweeps in one ticket-scheduled
+    grid) computes bitwise the same gradients as the two-launch default."""
+    import torch
+    import paper_2510_21956_b200 as la
+    from tests._util import fast_inputs
+    G, N, D = 8, 4096, 128
+    q, k, v, w = fast_inputs(G, N, D, seed=7)
+    t = [torch.as_tensor(x).to(torch.bfloat16).to(cuda) for x in (q, k, v, w)]
+    L = la.Layout
+    hq, hk = la.HeadTensor.from_logical(t[0], L.SequenceMajor), la.HeadTensor.from_logical(t[1], L.SequenceMajor)
+    hv, hw = la.HeadTensor.from_logical(t[2], L.FeatureMajor), la.HeadTensor.from_logical(t[3], L.FeatureMajor)
+    art = la.forward_causal(hq, hk, hv)
+    monkeypatch.setenv("LA_BWD_FUSED", "0")
+    g0 = la.backward_causal(art, hw)
+    monkeypatch.setenv("LA_BWD_FUSED", "1")
+    g1 = la.backward_causal(art, hw)
+    torch.cuda.synchronize()
+    for a_, b_ in ((g0.dq, g1.dq), (g0.dk, g1.dk), (g0.dv, g1.dv)):
+        assert torch.equal(a_.data, b_.data)
