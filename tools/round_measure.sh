@@ -1,0 +1,14 @@
+#!/bin/bash
+# Round-end measurement on one GPU: bench line, ncu launch list + full captures,
+# compute-sanitizer over every tcgen05 / fused / prologue kernel. Outputs in gpurun_out/.
+set -u
+TAG=${1:-r01s3}
+mkdir -p gpurun_out
+python bench.py --steps 10 --warmup 3 > gpurun_out/${TAG}_bench.log 2>&1
+bash tools/profile_round.sh $TAG
+for T in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $T --kernel-regex kns=_tc --kernel-regex kns=fused \
+    python tools/sanitize_run.py > gpurun_out/${TAG}_san_${T}.log 2>&1
+done
+timeout 900 compute-sanitizer --tool memcheck python tools/sanitize_run.py > gpurun_out/${TAG}_san_memcheck_all.log 2>&1
+tail -c 400 gpurun_out/${TAG}_bench.log; for f in gpurun_out/${TAG}_san_*.log; do echo "$f: $(tail -2 $f | tr '\n' ' ')"; done

@@ -1,5 +1,6 @@
 """Small causal + non-causal fwd/bwd through the public API, for compute-sanitizer runs:
-compute-sanitizer --tool racecheck --kernel-regex kns=_tc python tools/sanitize_run.py"""
+compute-sanitizer --tool racecheck --kernel-regex kns=_tc python tools/sanitize_run.py
+(also exercises the opt-in fused backward and the prologue / term-pass kernels)"""
 import os
 import sys
 
@@ -17,5 +18,20 @@ for causal in (True, False):
     hv, hw = T(v, la.Layout.FeatureMajor), T(w, la.Layout.FeatureMajor)
     art = (la.forward_causal if causal else la.forward_full)(hq, hk, hv)
     (la.backward_causal if causal else la.backward_full)(art, hw)
+    if causal:  # the opt-in fused backward schedule (k_bwd_fused)
+        os.environ["LA_BWD_FUSED"] = "1"
+        la.backward_causal(art, hw)
+        os.environ.pop("LA_BWD_FUSED")
+# prologue / diagnostics kernels (la_prologue.cu)
+hq2, hk2 = la.normalize_qk(hq, hk)
+hw_hat = la.make_omega_hat(hw, art.g)
+la.relayout(hv, la.Layout.SequenceMajor)
+plan = la.default_plan(la.Shape(1, 2, 1024, 128))
+f = la.make_accumulator(2, 1024, 128)
+la.constant_term_pass(hv, la.LinearKernelCoeffs(), f)
+la.linear_term_pass(hq, hk, hv, la.LinearKernelCoeffs(), plan, f)
+dk = la.make_accumulator(2, 1024, 128)
+la.alpha_term_pass(hq, hv, hw_hat, plan, dk)
+la.beta_term_pass(hq, art.out, hw_hat, plan, dk)
 torch.cuda.synchronize()
 print("ok")
