@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libla_cuda.so")
+LIB_PATH = os.environ.get("LA_CUDA_LIB") or os.path.join(PKG, "libla_cuda.so")  # override: A/B builds
 
 # enums (la_cuda.h)
 LA_OK = 0

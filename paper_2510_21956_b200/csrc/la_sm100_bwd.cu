@@ -132,6 +132,8 @@ struct BwdParams {
   int pf;      // chunks prefetched into L2 ahead of the ring
   int store_w = 0;  // W_hat pass: store W_hat^T (into dv) and s (into dq rows) for the sweep
   uint32_t* flags = nullptr;  // fused schedule: per aggregate unit [G][P * A], set when published
+  int r_unit0 = 0;  // aggregate pass: units below this only produce W_hat^T / s (their R records
+                    // would feed no segment: segment 0 in the causal sweep)
 };
 
 // Cross-CTA publication for the fused schedule (k_bwd_fused): the aggregate unit's
@@ -473,6 +475,7 @@ __device__ __forceinline__ void bwd_aggR_body(const CUtensorMap& tmQ, const CUte
   const int64_t s0 = (int64_t)p * prm.seg_len;
   const int64_t s1 = lmin(prm.N, s0 + prm.seg_len);
   const int nc = (int)((s1 - s0) / kCB);
+  const bool needR = p >= prm.r_unit0;
   const uint32_t warp = warp_id();
   if (warp == 0 && elect_one()) {
     tma_prefetch(&tmQ);
@@ -506,7 +509,7 @@ __device__ __forceinline__ void bwd_aggR_body(const CUtensorMap& tmQ, const CUte
     if (elect_one()) {
       auto l2_prefetch = [&](int c) {
         const int64_t row0 = s0 + (int64_t)c * kCB;
-        tma_prefetch_l2_3d(&tmQ, 0, (int)(grp * prm.N + row0), 0);
+        if (needR) tma_prefetch_l2_3d(&tmQ, 0, (int)(grp * prm.N + row0), 0);
         tma_prefetch_l2_3d(&tmW, 0, (int)(grp * kD), (int)(row0 / 64));
         tma_prefetch_l2_3d(&tmO, 0, (int)(grp * kD), (int)(row0 / 64));
       };
@@ -517,8 +520,8 @@ __device__ __forceinline__ void bwd_aggR_body(const CUtensorMap& tmQ, const CUte
         if (c >= kAStages) mbar_wait(&empty[s], ((c / kAStages) & 1) ^ 1);
         const int64_t row0 = s0 + (int64_t)c * kCB;
         uint8_t* st = smem + s * kAStage;
-        mbar_expect_tx(&full[s], 3 * kT64);
-        tma_load_3d(st, &tmQ, &full[s], 0, (int)(grp * prm.N + row0), 0);
+        mbar_expect_tx(&full[s], (needR ? 3 : 2) * kT64);
+        if (needR) tma_load_3d(st, &tmQ, &full[s], 0, (int)(grp * prm.N + row0), 0);
         tma_load_3d(st + kAOffW, &tmW, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
         tma_load_3d(st + kAOffO, &tmO, &full[s], 0, (int)(grp * kD), (int)(row0 / 64));
       }
@@ -533,12 +536,16 @@ __device__ __forceinline__ void bwd_aggR_body(const CUtensorMap& tmQ, const CUte
       mbar_wait(w_ready, c & 1);
       tc_fence_after();
       if (elect_one()) {
-        for (int ks = 0; ks < 4; ++ks)
-          mma_ss(tmem, kd(st + kAOffW, ks, 128), mn(st, ks, 8192), id_RT, (c > 0 || ks > 0) ? 1u : 0u);
-        for (int ks = 0; ks < 4; ++ks)
-          mma_ss(tmem + 160, mn(st, ks, 8192), kd(st + kAOffS, ks, 16), id_U, (c > 0 || ks > 0) ? 1u : 0u);
-        mma_commit(&empty[s]);
-        if (c == nc - 1) mma_commit(done);
+        if (needR) {
+          for (int ks = 0; ks < 4; ++ks)
+            mma_ss(tmem, kd(st + kAOffW, ks, 128), mn(st, ks, 8192), id_RT, (c > 0 || ks > 0) ? 1u : 0u);
+          for (int ks = 0; ks < 4; ++ks)
+            mma_ss(tmem + 160, mn(st, ks, 8192), kd(st + kAOffS, ks, 16), id_U, (c > 0 || ks > 0) ? 1u : 0u);
+          mma_commit(&empty[s]);
+          if (c == nc - 1) mma_commit(done);
+        } else {
+          mbar_arrive(&empty[s]);  // no MMA reads this stage
+        }
       }
       __syncwarp();
     }
@@ -599,7 +606,7 @@ __device__ __forceinline__ void bwd_aggR_body(const CUtensorMap& tmQ, const CUte
       }
     }
     if (et == 0) tma_store_wait0();
-    if (half == 0) {  // records: R (X[m][j]), u, c, count
+    if (half == 0 && needR) {  // records: R (X[m][j]), u, c, count
       float* rR = prm.stR + (grp * prm.P + p) * state_floats(kD);
       const uint32_t lb = (qd * 32u) << 16;
       if (nc > 0) {
@@ -1576,6 +1583,7 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
   pa.P = P * A;
   pa.p0 = 0;
   pa.store_w = 1;
+  pa.r_unit0 = A;  // segment 0 R records would feed no sweep: its units only write W_hat^T / s
   auto agg = bf ? k_bwd_agg_tc<true> : k_bwd_agg_tc<false>;
   auto main_k = bf ? k_bwd_tc<true> : k_bwd_tc<false>;
   cudaFuncSetAttribute(agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggSmemB);
