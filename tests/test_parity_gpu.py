@@ -360,6 +360,34 @@ def test_f16_key_sum_beyond_half_range(cuda, causal):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("G,N", [(3, 4096), (5, 1280), (64, 2048), (200, 256)])
+def test_segment_partition_matches_oracle(cuda, G, N):
+    """Segment counts from 1 (G = 200 >= 148 SMs) to many (G = 3): carries across
+    segment boundaries, bf16 fwd+bwd against the oracle on sampled groups."""
+    import torch
+    q, k, v, w = fast_inputs(G, N, 128, seed=G + N)
+    t = [torch.as_tensor(x).to(torch.bfloat16) for x in (q, k, v, w)]
+    L = la.Layout
+    hq = la.HeadTensor.from_logical(t[0].to(cuda), L.SequenceMajor)
+    hk = la.HeadTensor.from_logical(t[1].to(cuda), L.SequenceMajor)
+    hv = la.HeadTensor.from_logical(t[2].to(cuda), L.FeatureMajor)
+    hw = la.HeadTensor.from_logical(t[3].to(cuda), L.FeatureMajor)
+    art = la.forward_causal(hq, hk, hv)
+    gr = la.backward_causal(art, hw)
+    torch.cuda.synchronize()
+    o_dev = art.out.logical()
+    g_dev = art.g.cpu().numpy().reshape(G, N)
+    dq_d, dk_d, dv_d = gr.dq.logical(), gr.dk.logical(), gr.dv.logical()
+    for gi in sorted({0, G // 2, G - 1}):
+        rq, rk, rv, rw = (x[gi:gi + 1].double().numpy() for x in t)
+        out, g = O.forward(rq, rk, rv)
+        assert max_abs(o_dev[gi:gi + 1], out) <= 2e-2
+        dq, dk, dv = O.backward(rq, rk, rv, o_dev[gi:gi + 1], rw, g_dev[gi:gi + 1])
+        for a_, b_ in ((dq_d, dq), (dk_d, dk), (dv_d, dv)):
+            assert max_abs(a_[gi:gi + 1], b_) <= 2e-2
+
+
+@pytest.mark.gpu
 def test_fused_backward_schedule_matches_separate(cuda, monkeypatch):
     """LA_BWD_FUSED=1 (k_bwd_fused: aggregate units and sweeps in one ticket-scheduled
     grid) computes bitwise the same gradients as the two-launch default."""
