@@ -115,6 +115,11 @@ size_t tc_forward_ws_floats(int64_t G, int64_t N, int64_t D);
 size_t tc_backward_ws_floats(int64_t G, int64_t N, int64_t D);
 size_t tc_saved_floats(int64_t G, int64_t N, int64_t D);
 int tc_segments(int64_t G, int64_t N);
+
+// Non-causal path for D != 128 (bf16/fp16, canonical layouts): batched GEMMs (la_gemm.cu).
+bool gemm_full_supported(const Launch& L, const Tensors& t);
+cudaError_t gemm_forward_full(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws);
+cudaError_t gemm_backward_full(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv);
 cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws);
 cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv,
                         Workspace ws);

@@ -153,7 +153,7 @@ size_t bwd_floats(const la_problem* p) {
 // scratch (exact: padded key features add nothing to S or z, padded value features
 // are dropped on the way out), run the D = 128 kernels, copy the D columns back.
 bool pad_eligible(const la_problem* p, const la_shard* sh, int lq, int lk, int lv, int lw) {
-  return p->impl != LA_IMPL_SIMT && (p->dtype == LA_BF16 || p->dtype == LA_F16) && p->dim < 128 &&
+  return p->impl != LA_IMPL_SIMT && p->causal && (p->dtype == LA_BF16 || p->dtype == LA_F16) && p->dim < 128 &&
          p->dim % 8 == 0 && p->fault == LA_FAULT_NONE && p->seq_len % 128 == 0 && sh == nullptr &&
          lq == LA_SEQUENCE_MAJOR && lk == LA_SEQUENCE_MAJOR && lv == LA_FEATURE_MAJOR &&
          (lw < 0 || lw == LA_FEATURE_MAJOR) && p->groups * p->seq_len < (1ll << 31);
@@ -265,6 +265,8 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
   }
   if (tc)
     e = tc_forward(L, t, out, g, w);
+  else if (p->impl == LA_IMPL_AUTO && gemm_full_supported(L, t))
+    e = gemm_forward_full(L, t, out, g, w);
   else if (p->impl == LA_IMPL_TCGEN05)
     return fail(err, LA_ERR_UNSUPPORTED, "tcgen05 path needs bf16/fp16, D=128, canonical layouts");
   else
@@ -345,6 +347,8 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
   cudaError_t e;
   if (tc)
     e = tc_backward(L, t, dq, dk, dv, w);
+  else if (p->impl == LA_IMPL_AUTO && gemm_full_supported(L, t))
+    e = gemm_backward_full(L, t, dq, dk, dv);
   else if (p->impl == LA_IMPL_TCGEN05)
     return fail(err, LA_ERR_UNSUPPORTED, "tcgen05 path needs bf16/fp16, D=128, canonical layouts");
   else

@@ -175,12 +175,31 @@ def test_bf16_causal_d128_parity(cuda, impl):
     assert rel_err(res["g"], ref["g"]) <= 1e-3
 
 
-@pytest.mark.parametrize("D", [64, 128, 256])
+@pytest.mark.parametrize("D", [32, 64, 96, 128, 192, 256])
 def test_bf16_noncausal_head_dim_sweep(cuda, D):
-    # BASELINE config 4 shape family (non-causal, D sweep) at reduced N
+    # BASELINE config 4 shape family (non-causal, D sweep) at reduced N; D != 128 runs
+    # the batched-GEMM path (la_gemm.cu), D = 128 the tcgen05 kernels
     q, k, v, w = fast_inputs(2, 2048, D, seed=D)
     res = run_dev(q, k, v, w, "bf16", cuda, causal=False)
     ref = oracle_all(res, False)
+    for key in ("out", "dq", "dk", "dv"):
+        assert max_abs(res[key], ref[key]) <= BF16_ABS, (D, key)
+    assert rel_err(res["g"], ref["g"]) <= 1e-3
+
+
+@pytest.mark.parametrize("D,a,b", [(256, 1.0, 1.0), (64, 0.5, 2.0)])
+def test_noncausal_gemm_path_runs_and_matches(cuda, D, a, b):
+    """The non-causal D != 128 path is the batched-GEMM one (profile scopes), fp16 too."""
+    from paper_2510_21956_b200 import _abi
+    q, k, v, w = fast_inputs(3, 1024, D, seed=D + 1)
+    L = _abi.lib()
+    L.la_profile_enable(1)
+    _abi.profile_read()
+    res = run_dev(q, k, v, w, "f16", cuda, causal=False, a=a, b=b)
+    names = {r["name"] for r in _abi.profile_read()}
+    L.la_profile_enable(0)
+    assert {"la_gemm_fwd_full", "la_gemm_bwd_full"} <= names, names
+    ref = oracle_all(res, False, a=a, b=b)
     for key in ("out", "dq", "dk", "dv"):
         assert max_abs(res[key], ref[key]) <= BF16_ABS, (D, key)
 
