@@ -116,6 +116,10 @@ size_t tc_backward_ws_floats(int64_t G, int64_t N, int64_t D);
 size_t tc_saved_floats(int64_t G, int64_t N, int64_t D);
 int tc_segments(int64_t G, int64_t N);
 
+// Sequence-shard totals on the tensor core (bf16/fp16, D = 128, canonical layouts).
+cudaError_t tc_forward_shard_state(const Launch& L, const Tensors& t, float* out);
+cudaError_t tc_backward_shard_state(const Launch& L, const Tensors& t, float* out);
+
 // Non-causal path for D != 128 (bf16/fp16, canonical layouts): batched GEMMs (la_gemm.cu).
 bool gemm_full_supported(const Launch& L, const Tensors& t);
 cudaError_t gemm_forward_full(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws);

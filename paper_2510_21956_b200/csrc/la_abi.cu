@@ -640,6 +640,12 @@ la_status la_backward_sharded(const la_problem* p, const la_shard* shard, const 
                        ws_bytes, stream, err);
 }
 
+// Shard totals on the tensor core when the tcgen05 kernels take the shape.
+static bool shard_state_tc(const la_problem* p, bool canonical) {
+  return p->impl != LA_IMPL_SIMT && (p->dtype == LA_BF16 || p->dtype == LA_F16) && p->dim == 128 &&
+         p->seq_len % 128 == 0 && p->fault == LA_FAULT_NONE && canonical && p->groups * p->seq_len < (1ll << 31);
+}
+
 la_status la_forward_shard_state(const la_problem* p, const void* k, la_layout lk, const void* v,
                                  la_layout lv, float* state_out, void* stream) {
   la_status s = check_problem(p, nullptr);
@@ -647,6 +653,8 @@ la_status la_forward_shard_state(const la_problem* p, const void* k, la_layout l
   if (!k || !v || !state_out) return LA_ERR_INVALID_SHAPE;
   Launch L = make_launch(p, nullptr, stream);
   Tensors t{nullptr, 0, k, lk, v, lv, nullptr, 0, nullptr, 0, nullptr};
+  if (shard_state_tc(p, lk == LA_SEQUENCE_MAJOR && lv == LA_FEATURE_MAJOR))
+    return tc_forward_shard_state(L, t, state_out) == cudaSuccess ? LA_OK : LA_ERR_CUDA;
   return simt_forward_shard_state(L, t, state_out) == cudaSuccess ? LA_OK : LA_ERR_CUDA;
 }
 
@@ -658,6 +666,8 @@ la_status la_backward_shard_state(const la_problem* p, const void* q, la_layout 
   if (!q || !o || !omega || !g || !state_out) return LA_ERR_MISSING_FORWARD_STATE;
   Launch L = make_launch(p, nullptr, stream);
   Tensors t{q, lq, nullptr, 0, nullptr, 0, o, LA_FEATURE_MAJOR, omega, lw, g};
+  if (shard_state_tc(p, lq == LA_SEQUENCE_MAJOR && lw == LA_FEATURE_MAJOR))
+    return tc_backward_shard_state(L, t, state_out) == cudaSuccess ? LA_OK : LA_ERR_CUDA;
   // scratch for s_i: G*N floats, allocated stream-ordered
   float* scratch = nullptr;
   if (cudaMallocAsync((void**)&scratch, sizeof(float) * p->groups * p->seq_len, L.stream) !=

@@ -195,3 +195,22 @@ def test_sequence_sharding_carries_on_device(cuda, impl, world):
     dv = torch.cat([x[2].view(G, D, -1) for x in grads], 2).transpose(1, 2).double().cpu().numpy()
     oq, ok_, ov = O.backward(rq, rk, rv, out, rw, g)
     assert max_abs(dq, oq) <= 2e-2 and max_abs(dk, ok_) <= 2e-2 and max_abs(dv, ov) <= 2e-2
+
+
+@pytest.mark.gpu
+def test_shard_states_tensor_core_match_simt(cuda):
+    """la_forward_shard_state / la_backward_shard_state: the tcgen05 totals (aggregate
+    kernels + unit sums) equal the CUDA-core totals (same records, fp32)."""
+    G, N, D = 3, 1024, 128
+    q, k, v, w = fast_inputs(G, N, D, seed=11)
+    tb = lambda x: torch.as_tensor(x).to(torch.bfloat16).to(cuda)
+    qs, ks = tb(q), tb(k)
+    vs, ws_ = tb(v.transpose(0, 2, 1)), tb(w.transpose(0, 2, 1))
+    tc, si = S.CudaOps(G, N, D, "bf16", impl="auto"), S.CudaOps(G, N, D, "bf16", impl="simt")
+    f_tc, f_si = tc.forward_shard_state(ks, vs), si.forward_shard_state(ks, vs)
+    out, g = tc.forward_with_carry(qs, ks, vs, torch.zeros_like(f_tc), 0)
+    b_tc, b_si = tc.backward_shard_state(qs, out, ws_, g), si.backward_shard_state(qs, out, ws_, g)
+    torch.cuda.synchronize()
+    for a_, b_ in ((f_tc, f_si), (b_tc, b_si)):
+        a_, b_ = a_.double().cpu().numpy(), b_.double().cpu().numpy()
+        assert np.max(np.abs(a_ - b_)) <= 1e-4 * max(1.0, np.max(np.abs(b_)))
