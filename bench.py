@@ -4,6 +4,7 @@ Default workload = BASELINE.json configs[1], the north star:
 B=4 H=16 N=65536 D=128, bf16, causal, a=b=1, one fwd+bwd per step.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  python bench.py --config 3|5 ...   (the sharded BASELINE configs, see run_sharded_arm)
 
 Our arm: inputs resident in HBM (each input tensor is 1.07 GB, far above the
 126 MB L2, so no flush is needed between steps); K steps timed with CUDA events
@@ -413,6 +414,111 @@ def run_our_arm(args):
         dist.destroy_process_group()
 
 
+# ----------------------------------------------------------------------------- sharded configs
+SHARDED = {
+    # BASELINE configs[2]: 1.4B-LM attention layer, batch x head sharded (no collective)
+    "3": dict(batch=8, heads=16, seq_len=4096, mode="batch_head",
+              metric="causal LA fwd+bwd tokens/s, B=8 H=16 N=4096 D=128 (batch x head sharded)"),
+    # BASELINE configs[4]: long context, sequence-sharded with an all-gather scan of shard states
+    "5": dict(batch=1, heads=16, seq_len=1 << 20, mode="sequence",
+              metric="causal LA fwd+bwd tokens/s, B=1 H=16 N=1M D=128 (sequence sharded)"),
+}
+
+
+def run_sharded_arm(args):
+    """Config 3: the B*H = 128 groups split over ranks (strong scaling of one layer, no
+    collective). Config 5: every rank owns N / world consecutive rows of all 16 heads;
+    one step = shard totals -> NCCL all-gather -> exclusive prefix -> carried forward,
+    then backward shard totals -> all-gather -> exclusive suffix -> carried backward
+    (paper_2510_21956_b200/sharding.py). Same timing rules as the default arm."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_21956_b200 import _abi
+    from paper_2510_21956_b200 import sharding as S
+
+    cfg = SHARDED[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L = _abi.lib()
+    D, G_all, N_all = 128, cfg["batch"] * cfg["heads"], cfg["seq_len"]
+    if cfg["mode"] == "batch_head":
+        g0, g1 = S.batch_head_range(G_all, rank, world)
+        G, N, row0 = g1 - g0, N_all, 0
+    else:
+        sh = S.SequenceShard(N_all, rank, world)
+        G, N, row0 = G_all, sh.row1 - sh.row0, sh.row0
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(99 + rank)
+
+    def unit_rows(shape):
+        x = torch.rand(shape, device=dev, generator=gen) * 2 - 1
+        return (x / x.norm(dim=-1, keepdim=True)).to(torch.bfloat16)
+
+    q, k = unit_rows((G, N, D)), unit_rows((G, N, D))
+    v = (torch.rand((G, D, N), device=dev, generator=gen) * 2 - 1).to(torch.bfloat16)
+    w = (torch.rand((G, D, N), device=dev, generator=gen) * 2 - 1).to(torch.bfloat16)
+    ops = S.CudaOps(G, N, D, "bf16")
+
+    zero = ops._empty_state(q)
+
+    def step():  # the forward's saved segment states feed the backward (no K/V re-read)
+        if cfg["mode"] == "batch_head" or world == 1:
+            out, g, saved = ops.forward_with_carry(q, k, v, zero, row0, save=True)
+            return ops.backward_with_carry(q, k, v, out, w, g, zero, zero, row0, saved=saved)
+        carry = S.exclusive_prefix(S.all_gather_states(ops.forward_shard_state(k, v)), rank)
+        out, g, saved = ops.forward_with_carry(q, k, v, carry, row0, save=True)
+        suffix = S.exclusive_suffix(S.all_gather_states(ops.backward_shard_state(q, out, w, g)), rank)
+        return ops.backward_with_carry(q, k, v, out, w, g, carry, suffix, row0, saved=saved)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = L.la_launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.current_stream(dev)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = L.la_launch_count() - launches0
+    ms = t0.elapsed_time(t1) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    tokens = cfg["batch"] * N_all  # the whole job's tokens per step
+    hbm, tf, src = peaks()
+    alg = G_all * N_all * 3080 / max(1, world)  # per-rank algorithmic bytes (SURVEY 8(d))
+    if rank == 0:
+        print(json.dumps({
+            "metric": cfg["metric"], "value": tokens / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (U(-1,1), unit-norm q/k rows)",
+            "config": {"workload": f"BASELINE config {args.config}", "global_batch": cfg["batch"],
+                       "seq_len": N_all, "heads": cfg["heads"], "dim": D,
+                       "parallelism": f"{cfg['mode']}{world}", "l2": "inputs > L2 at world <= 8; no flush"},
+            "step_roofline": {"alg_bytes_per_rank": alg, "achieved_gbs": alg / (ms / 1e3) / 1e9,
+                              "frac_hbm": alg / (ms / 1e3) / 1e9 / hbm},
+            "e2e": None, "cpu_baseline": None, "gpu_launches": int(launches), "clocks": clk.summary()}),
+            flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -423,10 +529,14 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default="2", choices=["2", "3", "5"],
+                    help="2 = the north star (default); 3 / 5 = the sharded BASELINE configs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":
         run_reference_arm(args)
+    elif args.config != "2":
+        run_sharded_arm(args)
     else:
         run_our_arm(args)
 

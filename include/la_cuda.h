@@ -159,6 +159,17 @@ la_status la_backward_sharded(const la_problem* p, const la_shard* shard, const 
                               la_layout lv, const void* o, const void* omega, la_layout lw,
                               const float* g, void* dq, void* dk, void* dv, void* workspace,
                               size_t ws_bytes, void* stream, la_error_info* err);
+/* The same with the forward's per-segment saved states (see la_forward_save): the
+ * carried backward then skips its K/V aggregate pass. */
+la_status la_forward_sharded_save(const la_problem* p, const la_shard* shard, const void* q, la_layout lq,
+                                  const void* k, la_layout lk, const void* v, la_layout lv, void* out, float* g,
+                                  void* saved, size_t saved_bytes, void* workspace, size_t ws_bytes, void* stream,
+                                  la_error_info* err);
+la_status la_backward_sharded_saved(const la_problem* p, const la_shard* shard, const void* q, la_layout lq,
+                                    const void* k, la_layout lk, const void* v, la_layout lv, const void* o,
+                                    const void* omega, la_layout lw, const float* g, const void* saved,
+                                    size_t saved_bytes, void* dq, void* dk, void* dv, void* workspace,
+                                    size_t ws_bytes, void* stream, la_error_info* err);
 /* Shard totals to exchange: forward (S=sum k^T v, z=sum k, sigma=sum v, count);
  * backward (R=sum q^T w_hat, u=sum s q, c=sum w_hat). Written to `state_out`
  * (la_shard_state_floats(p) fp32 values, device). */

@@ -28,7 +28,7 @@ EXPORTS = [
     "la_host_backward", "la_host_step", "la_host_release", "la_profile_enable", "la_profile_read",
     "la_saved_state_bytes", "la_forward_save", "la_backward_saved",
     "la_normalize_qk", "la_relayout", "la_make_omega_hat", "la_constant_term_pass", "la_linear_term_pass",
-    "la_alpha_term_pass", "la_beta_term_pass",
+    "la_alpha_term_pass", "la_beta_term_pass", "la_forward_sharded_save", "la_backward_sharded_saved",
 ]
 
 
@@ -101,6 +101,10 @@ def lib():
         L.la_host_backward.argtypes = [P, vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, C.c_int, vp,
                                        vp, vp, vp, E]
         ci = C.c_int
+        L.la_forward_sharded_save.argtypes = [P, C.POINTER(Shard), vp, ci, vp, ci, vp, ci, vp, vp, vp, sz, vp, sz,
+                                              vp, E]
+        L.la_backward_sharded_saved.argtypes = [P, C.POINTER(Shard), vp, ci, vp, ci, vp, ci, vp, vp, ci, vp, vp,
+                                                sz, vp, vp, vp, vp, sz, vp, E]
         L.la_normalize_qk.argtypes = [P, vp, ci, vp, ci, vp, vp, vp, E]
         L.la_relayout.argtypes = [P, vp, ci, vp, ci, vp, E]
         L.la_make_omega_hat.argtypes = [P, vp, ci, vp, vp, vp, E]

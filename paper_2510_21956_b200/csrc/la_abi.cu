@@ -631,6 +631,23 @@ la_status la_forward_sharded(const la_problem* p, const la_shard* shard, const v
   return forward_impl(p, shard, q, lq, k, lk, v, lv, out, g, workspace, ws_bytes, stream, err);
 }
 
+la_status la_forward_sharded_save(const la_problem* p, const la_shard* shard, const void* q, la_layout lq,
+                                  const void* k, la_layout lk, const void* v, la_layout lv, void* out, float* g,
+                                  void* saved, size_t saved_bytes, void* workspace, size_t ws_bytes, void* stream,
+                                  la_error_info* err) {
+  if (!saved) return fail(err, LA_ERR_INVALID_ARGUMENT, "null saved-state buffer");
+  return forward_impl(p, shard, q, lq, k, lk, v, lv, out, g, workspace, ws_bytes, stream, err, saved, saved_bytes);
+}
+
+la_status la_backward_sharded_saved(const la_problem* p, const la_shard* shard, const void* q, la_layout lq,
+                                    const void* k, la_layout lk, const void* v, la_layout lv, const void* o,
+                                    const void* omega, la_layout lw, const float* g, const void* saved,
+                                    size_t saved_bytes, void* dq, void* dk, void* dv, void* workspace,
+                                    size_t ws_bytes, void* stream, la_error_info* err) {
+  return backward_impl(p, shard, q, lq, k, lk, v, lv, o, omega, lw, g, dq, dk, dv, workspace, ws_bytes, stream,
+                       err, saved, saved_bytes);
+}
+
 la_status la_backward_sharded(const la_problem* p, const la_shard* shard, const void* q,
                               la_layout lq, const void* k, la_layout lk, const void* v,
                               la_layout lv, const void* o, const void* omega, la_layout lw,

@@ -124,7 +124,9 @@ class CudaOps:
         assert rc == 0, _abi.STATUS_NAMES[rc]
         return st
 
-    def forward_with_carry(self, q, k, v, carry, row0):
+    def forward_with_carry(self, q, k, v, carry, row0, save=False):
+        """Carried forward of this shard; with save=True also returns the per-segment
+        saved states (la_forward_sharded_save) for backward_with_carry."""
         import torch
         from .api import _raise
         out = torch.empty_like(v)
@@ -132,22 +134,37 @@ class CudaOps:
         ws = torch.empty(self.L.la_forward_workspace_bytes(C.byref(self.p)), dtype=torch.uint8, device=q.device)
         sh = _abi.Shard(row0, carry.data_ptr(), None)
         err = _abi.ErrorInfo()
+        if save:
+            saved = torch.empty(self.L.la_saved_state_bytes(C.byref(self.p)), dtype=torch.uint8, device=q.device)
+            rc = self.L.la_forward_sharded_save(C.byref(self.p), C.byref(sh), q.data_ptr(), 1, k.data_ptr(), 1,
+                                                v.data_ptr(), 0, out.data_ptr(), g.data_ptr(), saved.data_ptr(),
+                                                saved.numel(), ws.data_ptr(), ws.numel(), self._stream(),
+                                                C.byref(err))
+            _raise(rc, err)
+            return out, g, saved
         rc = self.L.la_forward_sharded(C.byref(self.p), C.byref(sh), q.data_ptr(), 1, k.data_ptr(), 1,
                                        v.data_ptr(), 0, out.data_ptr(), g.data_ptr(), ws.data_ptr(), ws.numel(),
                                        self._stream(), C.byref(err))
         _raise(rc, err)
         return out, g
 
-    def backward_with_carry(self, q, k, v, o, omega, g, carry_prefix, carry_suffix, row0):
+    def backward_with_carry(self, q, k, v, o, omega, g, carry_prefix, carry_suffix, row0, saved=None):
         import torch
         from .api import _raise
         dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
         ws = torch.empty(self.L.la_backward_workspace_bytes(C.byref(self.p)), dtype=torch.uint8, device=q.device)
         sh = _abi.Shard(row0, carry_prefix.data_ptr(), carry_suffix.data_ptr())
         err = _abi.ErrorInfo()
-        rc = self.L.la_backward_sharded(C.byref(self.p), C.byref(sh), q.data_ptr(), 1, k.data_ptr(), 1,
-                                        v.data_ptr(), 0, o.data_ptr(), omega.data_ptr(), 0, g.data_ptr(),
-                                        dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), ws.data_ptr(), ws.numel(),
-                                        self._stream(), C.byref(err))
+        if saved is not None:
+            rc = self.L.la_backward_sharded_saved(C.byref(self.p), C.byref(sh), q.data_ptr(), 1, k.data_ptr(), 1,
+                                                  v.data_ptr(), 0, o.data_ptr(), omega.data_ptr(), 0, g.data_ptr(),
+                                                  saved.data_ptr(), saved.numel(), dq.data_ptr(), dk.data_ptr(),
+                                                  dv.data_ptr(), ws.data_ptr(), ws.numel(), self._stream(),
+                                                  C.byref(err))
+        else:
+            rc = self.L.la_backward_sharded(C.byref(self.p), C.byref(sh), q.data_ptr(), 1, k.data_ptr(), 1,
+                                            v.data_ptr(), 0, o.data_ptr(), omega.data_ptr(), 0, g.data_ptr(),
+                                            dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), ws.data_ptr(), ws.numel(),
+                                            self._stream(), C.byref(err))
         _raise(rc, err)
         return dq, dk, dv

@@ -147,10 +147,11 @@ def test_sequence_shards_partition_rows():
 
 # ---------------------------------------------------------------------------- GPU
 @pytest.mark.gpu
-@pytest.mark.parametrize("impl", ["auto", "simt"])
+@pytest.mark.parametrize("impl,save", [("auto", False), ("auto", True), ("simt", False)])
 @pytest.mark.parametrize("world", [2, 4])
-def test_sequence_sharding_carries_on_device(cuda, impl, world):
-    """P shards run one after another on one GPU through the C-ABI carries."""
+def test_sequence_sharding_carries_on_device(cuda, impl, save, world):
+    """P shards run one after another on one GPU through the C-ABI carries (save: the
+    carried forward's segment states feed the carried backward)."""
     G, N, D = 4, 2048, 128
     q, k, v, w = fast_inputs(G, N, D, seed=world)
     tb = lambda x: torch.as_tensor(x).to(torch.bfloat16)
@@ -170,11 +171,16 @@ def test_sequence_sharding_carries_on_device(cuda, impl, world):
         ins.append((qs, ks, vs, ws_))
         fstates.append(ops.forward_shard_state(ks, vs))
     gathered = torch.stack(fstates)
-    outs, gs, carries = [], [], []
+    outs, gs, carries, saves = [], [], [], []
     for r, sh in enumerate(shards):
         carry = S.exclusive_prefix(gathered, r)
         qs, ks, vs, _ = ins[r]
-        out, g = opss[r].forward_with_carry(qs, ks, vs, carry, sh.row0)
+        if save:
+            out, g, sv = opss[r].forward_with_carry(qs, ks, vs, carry, sh.row0, save=True)
+            saves.append(sv)
+        else:
+            out, g = opss[r].forward_with_carry(qs, ks, vs, carry, sh.row0)
+            saves.append(None)
         outs.append(out)
         gs.append(g)
         carries.append(carry)
@@ -189,7 +195,7 @@ def test_sequence_sharding_carries_on_device(cuda, impl, world):
     for r, sh in enumerate(shards):
         qs, ks, vs, ws_ = ins[r]
         grads.append(opss[r].backward_with_carry(qs, ks, vs, outs[r], ws_, gs[r], carries[r],
-                                                 S.exclusive_suffix(bg, r), sh.row0))
+                                                 S.exclusive_suffix(bg, r), sh.row0, saved=saves[r]))
     dq = torch.cat([x[0].view(G, -1, D) for x in grads], 1).double().cpu().numpy()
     dk = torch.cat([x[1].view(G, D, -1) for x in grads], 2).transpose(1, 2).double().cpu().numpy()
     dv = torch.cat([x[2].view(G, D, -1) for x in grads], 2).transpose(1, 2).double().cpu().numpy()
