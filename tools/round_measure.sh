@@ -5,6 +5,9 @@ set -u
 TAG=${1:-r01s3}
 mkdir -p gpurun_out
 python bench.py --steps 10 --warmup 3 > gpurun_out/${TAG}_bench.log 2>&1
+python bench.py --config 3 --steps 10 --warmup 3 > gpurun_out/${TAG}_bench_c3.log 2>&1
+python bench.py --config 5 --steps 3 --warmup 3 > gpurun_out/${TAG}_bench_c5.log 2>&1
+python tools/config_sweep.py > gpurun_out/${TAG}_configs.jsonl 2> gpurun_out/${TAG}_configs.err
 bash tools/profile_round.sh $TAG
 for T in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $T --kernel-regex kns=_tc --kernel-regex kns=fused \
