@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/la_cuda.h"
 
@@ -42,6 +43,10 @@ inline int choose_segments(int64_t G, int64_t N, int num_sms = 148) {
 inline int agg_split(int64_t G, int64_t seg_rows, int segs_aggregated, int num_sms = 148) {
   if (segs_aggregated <= 0) return 1;
   const int64_t units = G * segs_aggregated, chunks = seg_rows / 128;
+  if (const char* e = getenv("LA_AGG_SPLIT")) {  // measurement override
+    const int a = atoi(e);
+    if (a >= 1 && chunks % a == 0) return a;
+  }
   int best = 1;
   double best_t = 1e300;
   for (int A = 1; A <= 8; ++A) {
@@ -55,6 +60,20 @@ inline int agg_split(int64_t G, int64_t seg_rows, int segs_aggregated, int num_s
     }
   }
   return best;
+}
+
+// The backward aggregate (W_hat^T / s for every row, R records for segments >= 1): its
+// segment-0 units skip Q and the MMAs, so units are uneven; the finest split (up to 8
+// units per segment, several waves) balances them (0.70 -> 0.64 ms at the north star).
+inline int bwd_agg_split(int64_t seg_rows) {
+  const int64_t chunks = seg_rows / 128;
+  if (const char* e = getenv("LA_AGG_SPLIT")) {
+    const int a = atoi(e);
+    if (a >= 1 && chunks % a == 0) return a;
+  }
+  for (int a = 8; a > 1; --a)
+    if (chunks % a == 0) return a;
+  return 1;
 }
 
 struct Tensors {

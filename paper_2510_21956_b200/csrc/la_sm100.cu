@@ -659,7 +659,8 @@ __global__ void k_sum_units(const float* recs, int U, int64_t SZ, float* tot) {
   if (e >= SZ) return;
   const float* r = recs + grp * U * SZ + e;
   float acc = 0.f;
-  for (int u = 0; u < U; ++u) acc += r[u * SZ];
+  if (e <= (int64_t)kD * kD + 2 * kD)  // record padding: never written by the units, kept zero
+    for (int u = 0; u < U; ++u) acc += r[u * SZ];
   tot[grp * SZ + e] = acc;
 }
 

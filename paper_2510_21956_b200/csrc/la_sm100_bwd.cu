@@ -1486,7 +1486,7 @@ size_t tc_backward_ws_floats(int64_t G, int64_t N, int64_t D) {
   if (D != kD || N % 128) return 0;
   const int P = tcb_segments(G, N);
   const int64_t seg = ((N / 128 + P - 1) / P) * 128;
-  const int A = std::max(agg_split(G, seg, P > 1 ? P - 1 : 1), agg_split(G, seg, P));
+  const int A = std::max(std::max(agg_split(G, seg, P > 1 ? P - 1 : 1), agg_split(G, seg, P)), bwd_agg_split(seg));
   // S, R unit sums + combined records, then the fused schedule's flags and ticket
   const size_t causal = (size_t)((2 * A + 2) * G * P) + (size_t)(G * P * A + 4 + state_floats(kD) - 1) / state_floats(kD);
   const int Af = agg_split(G, seg, P);
@@ -1597,7 +1597,7 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
   // segmentation (no K/V re-read), else computed by the aggregate pass.
   const float* sv = L.saved_in;
   const bool use_saved = sv != nullptr;  // validated by the ABI layer
-  const int A = agg_split(G, seg, P);  // the W_hat pass covers every segment
+  const int A = bwd_agg_split(seg);  // the W_hat pass covers every segment
   float* stS = ws.base;
   float* stR = stS + G * P * A * SZ;
   float* cmb = stR + G * P * A * SZ;

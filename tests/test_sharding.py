@@ -217,6 +217,10 @@ def test_shard_states_tensor_core_match_simt(cuda):
     out, g = tc.forward_with_carry(qs, ks, vs, torch.zeros_like(f_tc), 0)
     b_tc, b_si = tc.backward_shard_state(qs, out, ws_, g), si.backward_shard_state(qs, out, ws_, g)
     torch.cuda.synchronize()
-    for a_, b_ in ((f_tc, f_si), (b_tc, b_si)):
-        a_, b_ = a_.double().cpu().numpy(), b_.double().cpu().numpy()
-        assert np.max(np.abs(a_ - b_)) <= 1e-4 * max(1.0, np.max(np.abs(b_)))
+    SZ = f_tc.numel() // G
+    for name, a_, b_ in (("fwd", f_tc, f_si), ("bwd", b_tc, b_si)):
+        a_, b_ = a_.double().cpu().numpy().reshape(G, SZ), b_.double().cpu().numpy().reshape(G, SZ)
+        d = np.abs(a_ - b_)
+        where = np.unravel_index(np.argmax(d), d.shape)
+        # the tensor-core sums take W_hat in bf16 (the MMA operand): 2e-2 of the record scale
+        assert d.max() <= 2e-2 * max(1.0, np.abs(b_[:, :-4]).max()), (name, d.max(), where, a_[where], b_[where])
