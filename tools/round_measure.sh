@@ -4,6 +4,7 @@
 set -u
 TAG=${1:-r01s3}
 mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1
 python bench.py --steps 10 --warmup 3 > gpurun_out/${TAG}_bench.log 2>&1
 python bench.py --config 3 --steps 10 --warmup 3 > gpurun_out/${TAG}_bench_c3.log 2>&1
 python bench.py --config 5 --steps 3 --warmup 3 > gpurun_out/${TAG}_bench_c5.log 2>&1
