@@ -895,7 +895,9 @@ static cudaError_t tc_forward_full(const Launch& L, const Tensors& t, void* out,
   }
   // apply pass: segments of whole 64-row chunks, about two CTAs per SM
   const int64_t c64 = N / kCF;
-  int64_t P2 = (2 * 148 + G - 1) / G;
+  // independent chunks: ~7 waves (G = 64: 0.24 ms at 2 waves -> 0.19 ms)
+  int64_t P2 = (7 * 148 + G / 2) / G;
+  if (const char* e = getenv("LA_FULL_SEGMENTS_F")) P2 = atoi(e);  // measurement override
   if (P2 > c64) P2 = c64;
   if (P2 < 1) P2 = 1;
   const int64_t seg2 = ((c64 + P2 - 1) / P2) * kCF;
