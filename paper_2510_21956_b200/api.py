@@ -372,7 +372,7 @@ def _run_backward(art, omega, c, plan, causal, fault, dtype, impl):
         dq, dk, dv = (torch.empty(G * N * D, dtype=q.data.dtype, device=dev) for _ in range(3))
         ws = torch.empty(L.la_backward_workspace_bytes(C.byref(p)), dtype=torch.uint8, device=dev)
         g = art.g if _is_torch(art.g) else torch.as_tensor(np.asarray(art.g, np.float32), device=dev)
-        if art.saved is not None and causal:
+        if art.saved is not None:  # per-segment prefixes (causal) or the K/V totals (non-causal)
             st = L.la_backward_saved(C.byref(p), q.data.data_ptr(), int(q.layout()), k.data.data_ptr(),
                                      int(k.layout()), v.data.data_ptr(), int(v.layout()), o.data.data_ptr(),
                                      omega.data.data_ptr(), int(omega.layout()), g.data_ptr(),

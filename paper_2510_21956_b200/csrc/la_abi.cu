@@ -256,7 +256,7 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
   cudaError_t e;
   const bool tc = use_tc(p, tc_forward_supported(L, t));
   if (saved) {
-    if (tc && p->causal) {  // prefix states per segment (the non-causal path keeps no prefixes)
+    if (tc) {  // causal: prefix states per segment; non-causal: the K/V totals
       L.saved_out = (float*)saved;
     } else {  // header only: the backward recomputes its prefix states
       const float hdr[kSavedHeader] = {kSavedMagic, (float)p->groups, (float)p->seq_len, (float)p->dim, 0.f};
@@ -340,7 +340,8 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
     if (hdr[0] != kSavedMagic || hdr[1] != (float)p->groups || hdr[2] != (float)p->seq_len ||
         hdr[3] != (float)p->dim)
       return fail(err, LA_ERR_MISSING_FORWARD_STATE, "saved forward state does not match the problem");
-    if (hdr[4] == (float)P && hdr[5] == (float)seg && saved_bytes >= la_saved_state_bytes(p))
+    if (((p->causal && hdr[4] == (float)P && hdr[5] == (float)seg) || (!p->causal && hdr[4] == -1.f)) &&
+        saved_bytes >= la_saved_state_bytes(p))
       L.saved_in = (const float*)saved;  // else: produced by another path; recompute
   }
   cudaMemsetAsync(w.flag, 0xFF, sizeof(unsigned long long), L.stream);

@@ -877,7 +877,13 @@ static cudaError_t tc_forward_full(const Launch& L, const Tensors& t, void* out,
   const int64_t seg = ((N / kC + P - 1) / P) * kC;
   const int A = agg_split(G, seg, P);
   float* units = ws.base;
-  float* tot = ws.base + G * P * A * SZ;
+  // with a saved-state buffer the totals land there (header P = -1 marks "totals") and
+  // the non-causal backward reuses them instead of re-reading K and V
+  float* tot = L.saved_out ? L.saved_out + kSavedHeader : ws.base + G * P * A * SZ;
+  if (L.saved_out) {
+    const float hdr[kSavedHeader] = {kSavedMagic, (float)G, (float)N, (float)kD, -1.f, 0.f};
+    cudaMemcpyAsync(L.saved_out, hdr, sizeof(hdr), cudaMemcpyHostToDevice, L.stream);
+  }
   CUtensorMap mK, mV, mQ64, mO64;
   if (!make_map(&mK, t.k, bf, (uint64_t)(G * N), kD) || !make_map(&mV, t.v, bf, (uint64_t)(G * kD), (uint64_t)N) ||
       !make_tma_map(&mQ64, t.q, bf, (uint64_t)(G * N), kD, 64, 2) ||

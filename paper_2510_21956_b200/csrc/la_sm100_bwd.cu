@@ -1508,7 +1508,11 @@ static cudaError_t tc_backward_full(const Launch& L, const Tensors& t, void* dq,
   float* totS = unitsS + G * Ukv * SZ;
   float* unitsR = totS + G * SZ;
   float* totR = unitsR + G * P * A * SZ;
-  cudaError_t e = tc_kv_totals(L, t, unitsS, totS);
+  cudaError_t e = cudaSuccess;
+  if (L.saved_in)  // the forward's K/V totals (la_forward_save)
+    totS = const_cast<float*>(L.saved_in) + kSavedHeader;
+  else
+    e = tc_kv_totals(L, t, unitsS, totS);
   if (e != cudaSuccess) return e;
   CUtensorMap mQ, mK, mV, mW, mO;
   if (!make_tma_map(&mO, t.o, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1) ||
