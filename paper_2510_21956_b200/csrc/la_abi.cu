@@ -255,8 +255,9 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
   cudaMemsetAsync(w.flag, 0xFF, sizeof(unsigned long long), L.stream);
   cudaError_t e;
   const bool tc = use_tc(p, tc_forward_supported(L, t));
+  const bool gemm = !tc && p->impl == LA_IMPL_AUTO && gemm_full_supported(L, t);
   if (saved) {
-    if (tc) {  // causal: prefix states per segment; non-causal: the K/V totals
+    if (tc || gemm) {  // causal: prefix states per segment; non-causal: the K/V totals
       L.saved_out = (float*)saved;
     } else {  // header only: the backward recomputes its prefix states
       const float hdr[kSavedHeader] = {kSavedMagic, (float)p->groups, (float)p->seq_len, (float)p->dim, 0.f};
@@ -265,7 +266,7 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
   }
   if (tc)
     e = tc_forward(L, t, out, g, w);
-  else if (p->impl == LA_IMPL_AUTO && gemm_full_supported(L, t))
+  else if (gemm)
     e = gemm_forward_full(L, t, out, g, w);
   else if (p->impl == LA_IMPL_TCGEN05)
     return fail(err, LA_ERR_UNSUPPORTED, "tcgen05 path needs bf16/fp16, D=128, canonical layouts");
@@ -324,11 +325,12 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
   Tensors t{q, lq, k, lk, v, lv, o, LA_FEATURE_MAJOR, omega, lw, g};
   Workspace w = carve(ws, ws_bytes);
   const bool tc = use_tc(p, tc_backward_supported(L, t));
-  if (saved && tc && trust_saved) {
+  const bool gemm = !tc && p->impl == LA_IMPL_AUTO && gemm_full_supported(L, t);
+  if (saved && (tc || gemm) && trust_saved) {
     // written by this library's own forward of the same problem on the same stream
     // (la_host_step): the header is known to match, no synchronous read
     L.saved_in = (const float*)saved;
-  } else if (saved && tc) {
+  } else if (saved && (tc || gemm)) {
     // validate the saved-state header written by la_forward_save
     float hdr[kSavedHeader];
     if (saved_bytes < sizeof(hdr) ||
@@ -348,7 +350,7 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
   cudaError_t e;
   if (tc)
     e = tc_backward(L, t, dq, dk, dv, w);
-  else if (p->impl == LA_IMPL_AUTO && gemm_full_supported(L, t))
+  else if (gemm)
     e = gemm_backward_full(L, t, dq, dk, dv);
   else if (p->impl == LA_IMPL_TCGEN05)
     return fail(err, LA_ERR_UNSUPPORTED, "tcgen05 path needs bf16/fp16, D=128, canonical layouts");

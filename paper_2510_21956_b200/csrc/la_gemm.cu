@@ -138,16 +138,31 @@ __global__ void __launch_bounds__(256) k_qtilde(const T* q, const float* z, floa
 
 // S~ [Dp][D] = [b S ; a sigma ; 0] and (bwd) T_S [Dp][D] = [(b S)^T ; -b z ; 0], bR = b R.
 template <typename T>
-__global__ void k_pack_state(const float* S, const float* vec, float row_scale, float vec_scale, int transpose,
-                             T* out, int D, int Dp) {
+__global__ void k_pack_state(const float* S, int64_t sgs, const float* vec, int64_t vgs, float row_scale,
+                             float vec_scale, int transpose, T* out, int D, int Dp) {
   const int64_t g = blockIdx.y;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)Dp * D) return;
   const int r = (int)(e / D), col = (int)(e % D);
   float v = 0.f;
-  if (r < D) v = row_scale * (transpose ? S[g * D * D + (int64_t)col * D + r] : S[g * D * D + (int64_t)r * D + col]);
-  else if (r == D && vec) v = vec_scale * vec[g * D + col];
+  if (r < D) v = row_scale * (transpose ? S[g * sgs + (int64_t)col * D + r] : S[g * sgs + (int64_t)r * D + col]);
+  else if (r == D && vec) v = vec_scale * vec[g * vgs + col];
   out[g * Dp * D + e] = cvt<T>(v);
+}
+
+// Saved-state record per group: [S (D x D) | z | sigma | count | 0 padding].
+__global__ void k_write_records(const float* S, const float* z, const float* sig, float count, float* rec, int D) {
+  const int64_t g = blockIdx.y;
+  const int64_t SZ = state_floats(D);
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= SZ) return;
+  const int64_t DD = (int64_t)D * D;
+  float v = 0.f;
+  if (e < DD) v = S[g * DD + e];
+  else if (e < DD + D) v = z[g * D + (e - DD)];
+  else if (e < DD + 2 * D) v = sig[g * D + (e - DD - D)];
+  else if (e == DD + 2 * D) v = count;
+  rec[g * SZ + e] = v;
 }
 
 // w_hat^T [Dp][N] = [omega^T / g ; s ; 0] and s_i = sum_j o_ij w_hat_ij (fp32), one thread
@@ -236,7 +251,15 @@ cudaError_t fwd_t(const Launch& L, const Tensors& t, void* out, float* g, Worksp
   k_rowsum<T><<<dim3(D, (unsigned)G), 256, 0, st>>>(v, sig, N, D, N, N * D);
   k_qtilde<T><<<(unsigned)((G * N + 7) / 8), 256, 0, st>>>(q, z, L.a, L.b, (float)L.n_total, Qt, g, G * N, N, D,
                                                             Dp, ws.flag);
-  k_pack_state<T><<<dim3((unsigned)((Dp * D + 255) / 256), (unsigned)G), 256, 0, st>>>(S, sig, L.b, L.a, 0, St, D, Dp);
+  k_pack_state<T><<<dim3((unsigned)((Dp * D + 255) / 256), (unsigned)G), 256, 0, st>>>(S, (int64_t)D * D, sig, D, L.b,
+                                                                                     L.a, 0, St, D, Dp);
+  if (L.saved_out) {  // the K/V totals as state records for the backward (header P = -1)
+    const float hdr[kSavedHeader] = {kSavedMagic, (float)G, (float)N, (float)D, -1.f, 0.f};
+    cudaMemcpyAsync(L.saved_out, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st);
+    const int64_t SZ = state_floats(D);
+    k_write_records<<<dim3((unsigned)((SZ + 255) / 256), (unsigned)G), 256, 0, st>>>(S, z, sig, (float)N,
+                                                                                     L.saved_out + kSavedHeader, D);
+  }
   if (cs == CUBLAS_STATUS_SUCCESS)  // O^T = S~^T Q~^T  (FeatureMajor)
     cs = rm_gemm(st, true, true, D, (int)N, Dp, St, D, (long long)Dp * D, dt, Qt, Dp, N * Dp, dt, out, (int)N,
                  N * D, dt, (int)G);
@@ -282,10 +305,21 @@ cudaError_t bwd_t(const Launch& L, const Tensors& t, void* dq, void* dk, void* d
   const T* v = (const T*)t.v;
   const T* o = (const T*)t.o;
   const T* w = (const T*)t.w;
-  cublasStatus_t cs = rm_gemm(st, true, true, D, D, (int)N, k, D, N * D, dt, v, (int)N, N * D, dt, S, D,
-                              (long long)D * D, CUDA_R_32F, (int)G);  // S = K^T V
-  k_colsum_part<T><<<dim3(nchunk, (unsigned)G), 256, 0, st>>>(k, nullptr, part, N, D, nchunk);
-  k_sum_part<<<(unsigned)G, 256, 0, st>>>(part, z, nchunk, D);
+  // S, z: the forward's saved totals (la_forward_save) or recomputed from K, V
+  const float* Sp = S;
+  const float* zp = z;
+  int64_t sgs = (int64_t)D * D;
+  cublasStatus_t cs = CUBLAS_STATUS_SUCCESS;
+  if (L.saved_in) {
+    sgs = state_floats(D);
+    Sp = L.saved_in + kSavedHeader;
+    zp = Sp + (int64_t)D * D;
+  } else {
+    cs = rm_gemm(st, true, true, D, D, (int)N, k, D, N * D, dt, v, (int)N, N * D, dt, S, D, (long long)D * D,
+                 CUDA_R_32F, (int)G);  // S = K^T V
+    k_colsum_part<T><<<dim3(nchunk, (unsigned)G), 256, 0, st>>>(k, nullptr, part, N, D, nchunk);
+    k_sum_part<<<(unsigned)G, 256, 0, st>>>(part, z, nchunk, D);
+  }
   k_what<T><<<dim3((unsigned)((N + 255) / 256), (unsigned)G), 256, 0, st>>>(w, o, t.g, Wt, s, N, D, Dp);
   k_colsum_part<T><<<dim3(nchunk, (unsigned)G), 256, 0, st>>>(q, s, part, N, D, nchunk);
   k_sum_part<<<(unsigned)G, 256, 0, st>>>(part, u, nchunk, D);                                     // u = Q^T s
@@ -294,8 +328,9 @@ cudaError_t bwd_t(const Launch& L, const Tensors& t, void* dq, void* dk, void* d
     cs = rm_gemm(st, true, true, D, D, (int)N, q, D, N * D, dt, Wt, (int)N, (long long)Dp * N, dt, R, D,
                  (long long)D * D, CUDA_R_32F, (int)G);
   const dim3 pg((unsigned)((Dp * D + 255) / 256), (unsigned)G);
-  k_pack_state<T><<<pg, 256, 0, st>>>(S, z, b, -b, 1, TS, D, Dp);  // [(b S)^T ; -b z]
-  k_pack_state<T><<<dim3((unsigned)((D * D + 255) / 256), (unsigned)G), 256, 0, st>>>(R, nullptr, b, 0.f, 0, bR, D, D);
+  k_pack_state<T><<<pg, 256, 0, st>>>(Sp, sgs, zp, sgs == (int64_t)D * D ? D : sgs, b, -b, 1, TS, D, Dp);  // [(b S)^T ; -b z]
+  k_pack_state<T><<<dim3((unsigned)((D * D + 255) / 256), (unsigned)G), 256, 0, st>>>(R, (int64_t)D * D, nullptr, 0, b,
+                                                                                   0.f, 0, bR, D, D);
   if (cs == CUBLAS_STATUS_SUCCESS)  // dQ = [W_hat | s] T_S  (SequenceMajor)
     cs = rm_gemm(st, true, false, (int)N, D, Dp, Wt, (int)N, (long long)Dp * N, dt, TS, D, (long long)Dp * D, dt,
                  dq, D, N * D, dt, (int)G);
