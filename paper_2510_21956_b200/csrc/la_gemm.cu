@@ -55,29 +55,35 @@ cublasStatus_t rm_gemm(cudaStream_t st, bool ta, bool tb, int M, int N, int K, c
 constexpr int kChunk = 256;  // rows per partial column sum
 
 // partial[g][c][m] = sum over rows [c*kChunk, ...) of x[g][n][m] (* w[g][n]); x SequenceMajor.
-// 256 threads = (256 / D') row lanes x D' features (D' = D rounded up to a power of two
-// <= 256), coalesced along m; the row lanes are reduced through shared memory.
+// A thread owns 8 consecutive features (one 16-byte load per row); the D/8 threads of
+// a row and the 256/(D/8) row lanes are reduced through shared memory.
 template <typename T>
 __global__ void __launch_bounds__(256) k_colsum_part(const T* x, const float* w, float* part, int64_t N, int D,
                                                      int nchunk) {
-  __shared__ float red[256];
+  __shared__ float red[2048];  // [lanes][D], lanes * D <= 2048
   const int64_t g = blockIdx.y;
   const int c = blockIdx.x;
-  int Dw = 1;
-  while (Dw < D) Dw <<= 1;
-  const int lanes = 256 / Dw, m = threadIdx.x % Dw, rl = threadIdx.x / Dw;
+  const int C8 = D / 8, lanes = 256 / C8;
+  const int m8 = threadIdx.x % C8, rl = threadIdx.x / C8;
   const int64_t n0 = (int64_t)c * kChunk, n1 = lmin(N, n0 + kChunk);
-  float acc = 0.f;
-  if (m < D)
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (rl < lanes)
     for (int64_t n = n0 + rl; n < n1; n += lanes) {
-      const float v = ld(x + (g * N + n) * D + m);
-      acc += w ? v * w[g * N + n] : v;
+      const uint4 u = __ldg((const uint4*)(x + (g * N + n) * D) + m8);
+      const T* e = (const T*)&u;
+      const float wn = w ? w[g * N + n] : 1.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] += (float)e[k] * wn;
     }
-  red[threadIdx.x] = acc;
   __syncthreads();
-  if (rl == 0 && m < D) {
+  float* r = red;  // [lanes][D]
+  if (rl < lanes)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[rl * D + 8 * m8 + k] = acc[k];
+  __syncthreads();
+  for (int m = threadIdx.x; m < D; m += blockDim.x) {
     float t = 0.f;
-    for (int l = 0; l < lanes; ++l) t += red[l * Dw + m];
+    for (int l = 0; l < lanes; ++l) t += r[l * D + m];
     part[((int64_t)g * nchunk + c) * D + m] = t;
   }
 }
@@ -111,29 +117,51 @@ __global__ void __launch_bounds__(256) k_rowsum(const T* y, float* out, int64_t 
   }
 }
 
-// g_i = a n_total + b q_i . z and Q~ = [q_i / g_i, 1 / g_i, 0...] (Dp columns), one warp per row.
+// g_i = a n_total + b q_i . z and Q~ = [q_i / g_i, 1 / g_i, 0...] (Dp = D + 8 columns):
+// 8 lanes per row, 16-byte loads / stores (4 rows per warp instruction).
 template <typename T>
 __global__ void __launch_bounds__(256) k_qtilde(const T* q, const float* z, float a, float b, float n_total,
                                                 T* qt, float* gout, int64_t rows, int64_t N, int D, int Dp,
                                                 unsigned long long* flag) {
-  const int64_t r = (int64_t)blockIdx.x * 8 + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  if (r >= rows) return;
-  const int64_t g = r / N;
-  const T* qr = q + r * D;
+  const int64_t r = (int64_t)blockIdx.x * 32 + threadIdx.x / 8;
+  const int l8 = threadIdx.x % 8;
+  const bool ok = r < rows;
+  const int64_t rr = ok ? r : 0;
+  const int64_t g = rr / N;
+  const uint4* qr = (const uint4*)(q + rr * D);
   const float* zg = z + g * D;
+  const int C8 = D / 8;
   float dot = 0.f;
-  for (int m = lane; m < D; m += 32) dot += ld(qr + m) * zg[m];
+  for (int c = l8; c < C8; c += 8) {
+    const uint4 u = __ldg(qr + c);
+    const T* e = (const T*)&u;
 #pragma unroll
-  for (int off = 16; off; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+    for (int k = 0; k < 8; ++k) dot += (float)e[k] * zg[8 * c + k];
+  }
+  dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+  dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+  dot += __shfl_xor_sync(0xffffffffu, dot, 4);
+  if (!ok) return;
   const float gi = a * n_total + b * dot;
-  if (lane == 0) {
+  if (l8 == 0) {
     gout[r] = gi;
     if (fabsf(gi) < kEpsF32) flag_degenerate(flag, g, r - g * N);
   }
   const float inv = 1.f / gi;
-  T* o = qt + r * Dp;
-  for (int m = lane; m < Dp; m += 32) o[m] = cvt<T>(m < D ? ld(qr + m) * inv : (m == D ? inv : 0.f));
+  uint4* o = (uint4*)(qt + r * Dp);
+  for (int c = l8; c <= C8; c += 8) {
+    uint4 u = make_uint4(0, 0, 0, 0);
+    T* e = (T*)&u;
+    if (c < C8) {
+      const uint4 v = __ldg(qr + c);
+      const T* ev = (const T*)&v;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) e[k] = cvt<T>((float)ev[k] * inv);
+    } else {
+      e[0] = cvt<T>(inv);
+    }
+    o[c] = u;
+  }
 }
 
 // S~ [Dp][D] = [b S ; a sigma ; 0] and (bwd) T_S [Dp][D] = [(b S)^T ; -b z ; 0], bR = b R.
@@ -165,28 +193,50 @@ __global__ void k_write_records(const float* S, const float* z, const float* sig
   rec[g * SZ + e] = v;
 }
 
-// w_hat^T [Dp][N] = [omega^T / g ; s ; 0] and s_i = sum_j o_ij w_hat_ij (fp32), one thread
-// per row i (FeatureMajor reads coalesced along i).
+// w_hat^T [Dp][N] = [omega^T / g ; s ; 0] and s_i = sum_j o_ij w_hat_ij (fp32): a thread
+// owns 8 consecutive rows i (16-byte FeatureMajor loads / stores along i).
 template <typename T>
 __global__ void __launch_bounds__(256) k_what(const T* w, const T* o, const float* gv, T* wt, float* s, int64_t N,
                                               int D, int Dp) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i8 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
   const int64_t g = blockIdx.y;
-  if (i >= N) return;
-  const float gi = gv[g * N + i];
-  const T* wg = w + g * N * D + i;
-  const T* og = o + g * N * D + i;
-  T* dst = wt + g * (int64_t)Dp * N + i;
-  float si = 0.f;
-  for (int j = 0; j < D; ++j) {
-    const float wh = ld(wg + (int64_t)j * N) / gi;
-    const T whr = cvt<T>(wh);
-    dst[(int64_t)j * N] = whr;
-    si += ld(og + (int64_t)j * N) * wh;
+  if (i8 >= N) return;
+  float ginv[8], si[8];
+  {
+    const float4 g0 = *(const float4*)(gv + g * N + i8), g1 = *(const float4*)(gv + g * N + i8 + 4);
+    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      ginv[k] = gg[k];
+      si[k] = 0.f;
+    }
   }
-  s[g * N + i] = si;
-  dst[(int64_t)D * N] = cvt<T>(si);
-  for (int j = D + 1; j < Dp; ++j) dst[(int64_t)j * N] = cvt<T>(0.f);
+  const T* wg = w + g * N * D + i8;
+  const T* og = o + g * N * D + i8;
+  T* dst = wt + g * (int64_t)Dp * N + i8;
+  for (int j = 0; j < D; ++j) {
+    const uint4 wu = __ldg((const uint4*)(wg + (int64_t)j * N)), ou = __ldg((const uint4*)(og + (int64_t)j * N));
+    const T* we = (const T*)&wu;
+    const T* oe = (const T*)&ou;
+    uint4 r;
+    T* re = (T*)&r;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float wh = (float)we[k] / ginv[k];
+      re[k] = cvt<T>(wh);
+      si[k] += (float)oe[k] * wh;
+    }
+    *(uint4*)(dst + (int64_t)j * N) = r;
+  }
+  uint4 r;
+  T* re = (T*)&r;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) re[k] = cvt<T>(si[k]);
+  *(uint4*)(dst + (int64_t)D * N) = r;
+  *(float4*)(s + g * N + i8) = make_float4(si[0], si[1], si[2], si[3]);
+  *(float4*)(s + g * N + i8 + 4) = make_float4(si[4], si[5], si[6], si[7]);
+  const uint4 zero = make_uint4(0, 0, 0, 0);
+  for (int j = D + 1; j < Dp; ++j) *(uint4*)(dst + (int64_t)j * N) = zero;
 }
 
 // y[g][j][i] += scale * vec[g][j] (FeatureMajor, in place): 8 values per thread
@@ -249,7 +299,7 @@ cudaError_t fwd_t(const Launch& L, const Tensors& t, void* out, float* g, Worksp
   k_colsum_part<T><<<dim3(nchunk, (unsigned)G), 256, 0, st>>>(k, nullptr, part, N, D, nchunk);
   k_sum_part<<<(unsigned)G, 256, 0, st>>>(part, z, nchunk, D);
   k_rowsum<T><<<dim3(D, (unsigned)G), 256, 0, st>>>(v, sig, N, D, N, N * D);
-  k_qtilde<T><<<(unsigned)((G * N + 7) / 8), 256, 0, st>>>(q, z, L.a, L.b, (float)L.n_total, Qt, g, G * N, N, D,
+  k_qtilde<T><<<(unsigned)((G * N + 31) / 32), 256, 0, st>>>(q, z, L.a, L.b, (float)L.n_total, Qt, g, G * N, N, D,
                                                             Dp, ws.flag);
   k_pack_state<T><<<dim3((unsigned)((Dp * D + 255) / 256), (unsigned)G), 256, 0, st>>>(S, (int64_t)D * D, sig, D, L.b,
                                                                                      L.a, 0, St, D, Dp);
@@ -320,7 +370,7 @@ cudaError_t bwd_t(const Launch& L, const Tensors& t, void* dq, void* dk, void* d
     k_colsum_part<T><<<dim3(nchunk, (unsigned)G), 256, 0, st>>>(k, nullptr, part, N, D, nchunk);
     k_sum_part<<<(unsigned)G, 256, 0, st>>>(part, z, nchunk, D);
   }
-  k_what<T><<<dim3((unsigned)((N + 255) / 256), (unsigned)G), 256, 0, st>>>(w, o, t.g, Wt, s, N, D, Dp);
+  k_what<T><<<dim3((unsigned)((N / 8 + 255) / 256), (unsigned)G), 256, 0, st>>>(w, o, t.g, Wt, s, N, D, Dp);
   k_colsum_part<T><<<dim3(nchunk, (unsigned)G), 256, 0, st>>>(q, s, part, N, D, nchunk);
   k_sum_part<<<(unsigned)G, 256, 0, st>>>(part, u, nchunk, D);                                     // u = Q^T s
   k_rowsum<T><<<dim3(D, (unsigned)G), 256, 0, st>>>(Wt, c, N, D, N, (int64_t)Dp * N);             // c
