@@ -139,6 +139,9 @@ int tc_segments(int64_t G, int64_t N);
 cudaError_t tc_forward_shard_state(const Launch& L, const Tensors& t, float* out);
 cudaError_t tc_backward_shard_state(const Launch& L, const Tensors& t, float* out);
 
+// Stream-ordered scratch (cudaMallocAsync) keeps its freed blocks: call before allocating.
+void keep_pool_memory();
+
 // Non-causal path for D != 128 (bf16/fp16, canonical layouts): batched GEMMs (la_gemm.cu).
 bool gemm_full_supported(const Launch& L, const Tensors& t);
 cudaError_t gemm_forward_full(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws);

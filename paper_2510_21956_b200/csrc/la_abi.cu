@@ -41,6 +41,21 @@ ProfScope::~ProfScope() {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   if (idx < (int)g_prof.size()) cudaEventRecord(g_prof[idx].b, stream);
 }
+
+// Keep the stream-ordered pool's freed blocks for reuse (the padded path allocates
+// per call); without this every call would map fresh pages.
+void keep_pool_memory() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
 }  // namespace lab
 
 using namespace lab;
@@ -196,20 +211,6 @@ void pad_copy(void* dst, const void* src, const la_problem* p, bool seq_major, b
                                                             to_padded ? 1 : 0);
   }
   note_launch(1);
-}
-// Keep the stream-ordered pool's freed blocks for reuse (the padded path allocates
-// per call); without this every call would map fresh pages.
-void keep_pool_memory() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  });
 }
 
 la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, la_layout lq,

@@ -12,8 +12,6 @@
 // CUDA-core sweep for D = 256 and the zero-padding detour for D < 128.
 #include <cublas_v2.h>
 
-#include <mutex>
-
 #include "common.cuh"
 #include "internal.h"
 
@@ -24,19 +22,6 @@ cublasHandle_t handle() {
   static thread_local cublasHandle_t h = nullptr;
   if (!h) cublasCreate(&h);
   return h;
-}
-
-void keep_pool() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  });
 }
 
 // Row-major C[M x N] = op(A) op(B), batched over groups (cuBLAS is column-major:
@@ -274,7 +259,7 @@ cudaError_t fwd_t(const Launch& L, const Tensors& t, void* out, float* g, Worksp
   const cudaDataType dt = L.dtype == LA_BF16 ? CUDA_R_16BF : CUDA_R_16F;
   const int nchunk = (int)((N + kChunk - 1) / kChunk);
   cudaStream_t st = L.stream;
-  keep_pool();
+  keep_pool_memory();
   size_t bytes = 0;
   bytes += ((size_t)G * D * D * 4 + 255) & ~255ull;           // S
   bytes += ((size_t)G * nchunk * D * 4 + 255) & ~255ull;      // partial sums
@@ -328,7 +313,7 @@ cudaError_t bwd_t(const Launch& L, const Tensors& t, void* dq, void* dk, void* d
   const int nchunk = (int)((N + kChunk - 1) / kChunk);
   cudaStream_t st = L.stream;
   const float a = L.a, b = L.b;
-  keep_pool();
+  keep_pool_memory();
   size_t bytes = 0;
   bytes += 2 * (((size_t)G * D * D * 4 + 255) & ~255ull);       // S, R
   bytes += ((size_t)G * nchunk * D * 4 + 255) & ~255ull;         // partial sums

@@ -1555,6 +1555,7 @@ static cudaError_t tc_backward_full(const Launch& L, const Tensors& t, void* dq,
 // sharding.py): forward (S, z, sigma, rows) = the non-causal K/V totals; backward
 // (R, u, c, rows) = the R aggregate units summed per group. Scratch is stream-ordered.
 cudaError_t tc_forward_shard_state(const Launch& L, const Tensors& t, float* out) {
+  keep_pool_memory();
   float* units = nullptr;
   const size_t n = (size_t)L.G * tc_kv_units(L.G, L.N) * state_floats(kD);
   cudaError_t e = cudaMallocAsync((void**)&units, n * sizeof(float), L.stream);
@@ -1575,6 +1576,7 @@ cudaError_t tc_backward_shard_state(const Launch& L, const Tensors& t, float* ou
       !make_tma_map(&mQ, t.q, bf, (uint64_t)(G * N), kD, 64, 2) ||
       !make_tma_map(&mW, t.w, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1))
     return cudaErrorInvalidValue;
+  keep_pool_memory();
   float* units = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&units, (size_t)G * P * A * SZ * sizeof(float), L.stream);
   if (e != cudaSuccess) return e;
