@@ -427,3 +427,16 @@ def test_fused_backward_schedule_matches_separate(cuda, monkeypatch):
     torch.cuda.synchronize()
     for a_, b_ in ((g0.dq, g1.dq), (g0.dk, g1.dk), (g0.dv, g1.dv)):
         assert torch.equal(a_.data, b_.data)
+
+
+@pytest.mark.parametrize("causal", [True, False])
+@pytest.mark.parametrize("a,b", [(0.5, 2.0), (1.0, 0.0), (2.0, 0.25)])
+def test_tcgen05_kernel_coefficients(cuda, causal, a, b):
+    """f(x) = a + b x with b = 0 (pure prefix / full averaging) and unequal a, b on the
+    tensor-core kernels, forward and backward."""
+    q, k, v, w = fast_inputs(2, 512, 128, seed=int(10 * a + 100 * b))
+    res = run_dev(q, k, v, w, "bf16", cuda, causal=causal, a=a, b=b, impl="tcgen05")
+    ref = oracle_all(res, causal, a=a, b=b)
+    for key in ("out", "dq", "dk", "dv"):
+        assert max_abs(res[key], ref[key]) <= BF16_ABS, key
+    assert rel_err(res["g"], ref["g"]) <= 1e-3
