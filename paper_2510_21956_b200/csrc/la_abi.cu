@@ -179,6 +179,38 @@ la_problem padded_problem(const la_problem* p) {
   la_default_plan(q.groups, 128, p->plan.workers > 0 ? p->plan.workers : 1, &q.plan);
   return q;
 }
+// Sequence lengths that are not a multiple of 128 on the tensor-core path: the rows
+// are zero-padded to Np = 128 * ceil(N / 128) in device scratch. Exact for both masks:
+// padded keys / values add nothing to any state, padded cotangent rows (omega = 0)
+// give w_hat = 0, padded rows come after every real row (causal prefixes of real rows
+// are unchanged) and the non-causal normaliser keeps a * N (n_total). Padded rows have
+// g = a (i + 1) or a N, so a >= 1e-3 keeps them away from the degenerate threshold.
+bool padn_eligible(const la_problem* p, const la_shard* sh, int lq, int lk, int lv, int lw) {
+  const int64_t np = (p->seq_len + 127) / 128 * 128;
+  // D <= 128: tcgen05 (D < 128 through the D padding); non-causal D <= 256: batched GEMMs
+  const bool fast_d = p->dim <= 128 || (!p->causal && p->dim <= 256);
+  return p->impl != LA_IMPL_SIMT && (p->dtype == LA_BF16 || p->dtype == LA_F16) && p->seq_len % 128 != 0 &&
+         fast_d && p->dim % 8 == 0 && p->fault == LA_FAULT_NONE && p->a >= 1e-3 && sh == nullptr &&
+         lq == LA_SEQUENCE_MAJOR && lk == LA_SEQUENCE_MAJOR && lv == LA_FEATURE_MAJOR &&
+         (lw < 0 || lw == LA_FEATURE_MAJOR) && p->groups * np * (p->dim + 8) < (1ll << 31);
+}
+la_problem n_padded_problem(const la_problem* p) {
+  la_problem q = *p;
+  q.seq_len = (p->seq_len + 127) / 128 * 128;
+  return q;
+}
+// rows x width bytes between row pitches; zero (or fill) the padded tail of each row
+cudaError_t pitch_copy(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows,
+                       cudaStream_t st) {
+  return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyDeviceToDevice, st);
+}
+__global__ void k_fill_tail(float* g, int64_t G, int64_t N, int64_t Np, float v) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t tail = Np - N;
+  if (e >= G * tail) return;
+  g[(e / tail) * Np + N + e % tail] = v;
+}
+
 // [rows][D] <-> [rows][128] (SequenceMajor) and [G][D][N] <-> [G][128][N] (FeatureMajor),
 // 16-byte vectors, zero fill of the padded part on the way in.
 __global__ void k_pad_seq(uint4* dst, const uint4* src, int64_t rows, int dv, int to_padded) {
@@ -216,7 +248,7 @@ void pad_copy(void* dst, const void* src, const la_problem* p, bool seq_major, b
 la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, la_layout lq,
                        const void* k, la_layout lk, const void* v, la_layout lv, void* out,
                        float* g, void* ws, size_t ws_bytes, void* stream, la_error_info* err,
-                       void* saved = nullptr, size_t saved_bytes = 0) {
+                       void* saved = nullptr, size_t saved_bytes = 0, int64_t n_total = 0) {
   la_status s = check_problem(p, err);
   if (s != LA_OK) return s;
   if (!q || !k || !v || !out || !g)
@@ -227,6 +259,34 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
     return fail(err, LA_ERR_WORKSPACE, "workspace smaller than la_forward_workspace_bytes");
   if (sh && !p->causal && (sh->carry_in || sh->row_offset))
     return fail(err, LA_ERR_UNSUPPORTED, "sequence sharding is defined for the causal mask");
+  if (padn_eligible(p, sh, lq, lk, lv, -1)) {
+    const la_problem pn = n_padded_problem(p);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t G = p->groups, N = p->seq_len, Np = pn.seq_len, D = p->dim;
+    const size_t T = (size_t)G * Np * D * 2, e = 2;
+    char* buf = nullptr;
+    keep_pool_memory();
+    if (cudaMallocAsync((void**)&buf, 4 * T + (size_t)G * Np * 4, st) != cudaSuccess)
+      return cuda_fail(err, cudaErrorMemoryAllocation);
+    cudaMemsetAsync(buf, 0, 3 * T, st);
+    pitch_copy(buf, Np * D * e, q, N * D * e, N * D * e, G, st);            // SequenceMajor rows
+    pitch_copy(buf + T, Np * D * e, k, N * D * e, N * D * e, G, st);
+    pitch_copy(buf + 2 * T, Np * e, v, N * e, N * e, G * D, st);            // FeatureMajor rows
+    float* gp = (float*)(buf + 4 * T);
+    if (saved) {  // no per-segment states on this path: header only, the backward recomputes
+      const float hdr[kSavedHeader] = {kSavedMagic, (float)p->groups, (float)p->seq_len, (float)p->dim, 0.f};
+      cudaMemcpyAsync(saved, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st);
+    }
+    s = forward_impl(&pn, nullptr, buf, LA_SEQUENCE_MAJOR, buf + T, LA_SEQUENCE_MAJOR, buf + 2 * T,
+                     LA_FEATURE_MAJOR, buf + 3 * T, gp, ws, ws_bytes, stream, nullptr, nullptr, 0, N);
+    if (s == LA_OK) {
+      pitch_copy(out, N * e, buf + 3 * T, Np * e, N * e, G * D, st);
+      pitch_copy(g, N * 4, gp, Np * 4, N * 4, G, st);
+    }
+    cudaFreeAsync(buf, st);
+    if (s != LA_OK) return fail(err, s, "sequence-padded forward failed");
+    return finish(ws, st, err);
+  }
   if (pad_eligible(p, sh, lq, lk, lv, -1)) {
     const la_problem p2 = padded_problem(p);
     cudaStream_t st = (cudaStream_t)stream;
@@ -242,13 +302,14 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
       cudaMemcpyAsync(saved, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st);
     }
     s = forward_impl(&p2, nullptr, buf, LA_SEQUENCE_MAJOR, buf + T, LA_SEQUENCE_MAJOR, buf + 2 * T,
-                     LA_FEATURE_MAJOR, buf + 3 * T, g, ws, ws_bytes, stream, nullptr);
+                     LA_FEATURE_MAJOR, buf + 3 * T, g, ws, ws_bytes, stream, nullptr, nullptr, 0, n_total);
     if (s == LA_OK) pad_copy(out, buf + 3 * T, p, false, false, st);
     cudaFreeAsync(buf, st);
     if (s != LA_OK) return fail(err, s, "padded forward failed");
     return finish(ws, st, err);
   }
   Launch L = make_launch(p, sh, stream);
+  if (n_total > 0) L.n_total = n_total;  // padded rows excluded from the non-causal a * N
   Tensors t{q, lq, k, lk, v, lv, nullptr, 0, nullptr, 0, nullptr};
   Workspace w = carve(ws, ws_bytes);
   if (saved && saved_bytes < la_saved_state_bytes(p))
@@ -298,6 +359,37 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
     return fail(err, LA_ERR_WORKSPACE, "workspace smaller than la_backward_workspace_bytes");
   if (sh && !p->causal && (sh->carry_in || sh->carry_suffix || sh->row_offset))
     return fail(err, LA_ERR_UNSUPPORTED, "sequence sharding is defined for the causal mask");
+  if (padn_eligible(p, sh, lq, lk, lv, lw)) {
+    const la_problem pn = n_padded_problem(p);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t G = p->groups, N = p->seq_len, Np = pn.seq_len, D = p->dim;
+    const size_t T = (size_t)G * Np * D * 2, e = 2;
+    char* buf = nullptr;
+    keep_pool_memory();
+    if (cudaMallocAsync((void**)&buf, 8 * T + (size_t)G * Np * 4, st) != cudaSuccess)
+      return cuda_fail(err, cudaErrorMemoryAllocation);
+    cudaMemsetAsync(buf, 0, 5 * T, st);
+    pitch_copy(buf, Np * D * e, q, N * D * e, N * D * e, G, st);
+    pitch_copy(buf + T, Np * D * e, k, N * D * e, N * D * e, G, st);
+    pitch_copy(buf + 2 * T, Np * e, v, N * e, N * e, G * D, st);
+    pitch_copy(buf + 3 * T, Np * e, o, N * e, N * e, G * D, st);
+    pitch_copy(buf + 4 * T, Np * e, omega, N * e, N * e, G * D, st);
+    float* gp = (float*)(buf + 8 * T);
+    pitch_copy(gp, Np * 4, g, N * 4, N * 4, G, st);
+    const int64_t tail = G * (Np - N);
+    k_fill_tail<<<(unsigned)((tail + 255) / 256), 256, 0, st>>>(gp, G, N, Np, 1.f);  // w_hat = 0 / 1 there
+    la_status s2 = backward_impl(&pn, nullptr, buf, LA_SEQUENCE_MAJOR, buf + T, LA_SEQUENCE_MAJOR, buf + 2 * T,
+                                 LA_FEATURE_MAJOR, buf + 3 * T, buf + 4 * T, LA_FEATURE_MAJOR, gp, buf + 5 * T,
+                                 buf + 6 * T, buf + 7 * T, ws, ws_bytes, stream, nullptr);
+    if (s2 == LA_OK) {
+      pitch_copy(dq, N * D * e, buf + 5 * T, Np * D * e, N * D * e, G, st);
+      pitch_copy(dk, N * e, buf + 6 * T, Np * e, N * e, G * D, st);
+      pitch_copy(dv, N * e, buf + 7 * T, Np * e, N * e, G * D, st);
+    }
+    cudaFreeAsync(buf, st);
+    if (s2 != LA_OK) return fail(err, s2, "sequence-padded backward failed");
+    return finish(ws, st, err);
+  }
   if (pad_eligible(p, sh, lq, lk, lv, lw)) {
     const la_problem p2 = padded_problem(p);
     cudaStream_t st = (cudaStream_t)stream;
@@ -550,7 +642,13 @@ size_t la_forward_workspace_bytes(const la_problem* p) {
     const size_t f2 = fwd_floats(&p2);
     if (f2 > f) f = f2;
   }
-  return ws_bytes_for(f);
+  size_t bytes = ws_bytes_for(f);
+  if (padn_eligible(p, nullptr, LA_SEQUENCE_MAJOR, LA_SEQUENCE_MAJOR, LA_FEATURE_MAJOR, -1)) {
+    const la_problem pn = n_padded_problem(p);
+    const size_t b2 = la_forward_workspace_bytes(&pn);
+    if (b2 > bytes) bytes = b2;
+  }
+  return bytes;
 }
 
 size_t la_backward_workspace_bytes(const la_problem* p) {
@@ -561,7 +659,13 @@ size_t la_backward_workspace_bytes(const la_problem* p) {
     const size_t f2 = bwd_floats(&p2);
     if (f2 > f) f = f2;
   }
-  return ws_bytes_for(f);
+  size_t bytes = ws_bytes_for(f);
+  if (padn_eligible(p, nullptr, LA_SEQUENCE_MAJOR, LA_SEQUENCE_MAJOR, LA_FEATURE_MAJOR, LA_FEATURE_MAJOR)) {
+    const la_problem pn = n_padded_problem(p);
+    const size_t b2 = la_backward_workspace_bytes(&pn);
+    if (b2 > bytes) bytes = b2;
+  }
+  return bytes;
 }
 
 // validate_plan (plan.cpp:49-62), same order of checks and messages.
