@@ -199,17 +199,46 @@ la_problem n_padded_problem(const la_problem* p) {
   q.seq_len = (p->seq_len + 127) / 128 * 128;
   return q;
 }
-// rows x width bytes between row pitches; zero (or fill) the padded tail of each row
-cudaError_t pitch_copy(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows,
-                       cudaStream_t st) {
-  return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyDeviceToDevice, st);
+// rows x w elements from a row pitch of sp to dp elements; the tail [w, wd) of every
+// destination row is set to `fill` (wd = w copies back without a tail). One pass, 4
+// consecutive elements per thread (rows are not 16-byte aligned when N is odd).
+template <typename T>
+__global__ void k_pitch_copy(T* dst, int64_t dp, const T* src, int64_t sp, int64_t w, int64_t wd, T fill) {
+  const int64_t r = blockIdx.y;
+  const int64_t c0 = (int64_t)blockIdx.x * 2048 + threadIdx.x;  // element c0 + 256 u: warps stay contiguous
+  T v[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) v[u] = c0 + 256 * u < w ? src[r * sp + c0 + 256 * u] : fill;  // 8 loads in flight
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    if (c0 + 256 * u < wd) dst[r * dp + c0 + 256 * u] = v[u];
 }
-__global__ void k_fill_tail(float* g, int64_t G, int64_t N, int64_t Np, float v) {
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t tail = Np - N;
-  if (e >= G * tail) return;
-  g[(e / tail) * Np + N + e % tail] = v;
+// 16-byte variant: every row start, pitch and w a multiple of 16 bytes.
+template <typename T>
+__global__ void k_pitch_copy16(uint4* dst, int64_t dp, const uint4* src, int64_t sp, int64_t w, int64_t wd,
+                               T fill) {
+  const int64_t r = blockIdx.y;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // 16-byte vector index
+  if (c >= wd) return;
+  uint4 f;
+  T* fe = (T*)&f;
+#pragma unroll
+  for (int u = 0; u < (int)(16 / sizeof(T)); ++u) fe[u] = fill;
+  dst[r * dp + c] = c < w ? src[r * sp + c] : f;
 }
+template <typename T>
+void pitch_copy(T* dst, int64_t dp, const T* src, int64_t sp, int64_t w, int64_t wd, int64_t rows, T fill,
+                cudaStream_t st) {
+  constexpr int64_t V = 16 / sizeof(T);
+  if (dp % V == 0 && sp % V == 0 && w % V == 0 && wd % V == 0 && ((uintptr_t)dst | (uintptr_t)src) % 16 == 0) {
+    const dim3 grid((unsigned)((wd / V + 255) / 256), (unsigned)rows);
+    k_pitch_copy16<T><<<grid, 256, 0, st>>>((uint4*)dst, dp / V, (const uint4*)src, sp / V, w / V, wd / V, fill);
+  } else {
+    const dim3 grid((unsigned)((wd + 2047) / 2048), (unsigned)rows);
+    k_pitch_copy<T><<<grid, 256, 0, st>>>(dst, dp, src, sp, w, wd, fill);
+  }
+}
+using u16 = unsigned short;
 
 // [rows][D] <-> [rows][128] (SequenceMajor) and [G][D][N] <-> [G][128][N] (FeatureMajor),
 // 16-byte vectors, zero fill of the padded part on the way in.
@@ -268,20 +297,19 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
     keep_pool_memory();
     if (cudaMallocAsync((void**)&buf, 4 * T + (size_t)G * Np * 4, st) != cudaSuccess)
       return cuda_fail(err, cudaErrorMemoryAllocation);
-    cudaMemsetAsync(buf, 0, 3 * T, st);
-    pitch_copy(buf, Np * D * e, q, N * D * e, N * D * e, G, st);            // SequenceMajor rows
-    pitch_copy(buf + T, Np * D * e, k, N * D * e, N * D * e, G, st);
-    pitch_copy(buf + 2 * T, Np * e, v, N * e, N * e, G * D, st);            // FeatureMajor rows
+    (void)e;
+    pitch_copy<u16>((u16*)buf, Np * D, (const u16*)q, N * D, N * D, Np * D, G, 0, st);  // SequenceMajor rows
+    pitch_copy<u16>((u16*)(buf + T), Np * D, (const u16*)k, N * D, N * D, Np * D, G, 0, st);
+    pitch_copy<u16>((u16*)(buf + 2 * T), Np, (const u16*)v, N, N, Np, G * D, 0, st);   // FeatureMajor rows
+    note_launch(3);
     float* gp = (float*)(buf + 4 * T);
-    if (saved) {  // no per-segment states on this path: header only, the backward recomputes
-      const float hdr[kSavedHeader] = {kSavedMagic, (float)p->groups, (float)p->seq_len, (float)p->dim, 0.f};
-      cudaMemcpyAsync(saved, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st);
-    }
+    // the saved states are the padded problem's (la_saved_state_bytes sizes them for Np)
     s = forward_impl(&pn, nullptr, buf, LA_SEQUENCE_MAJOR, buf + T, LA_SEQUENCE_MAJOR, buf + 2 * T,
-                     LA_FEATURE_MAJOR, buf + 3 * T, gp, ws, ws_bytes, stream, nullptr, nullptr, 0, N);
+                     LA_FEATURE_MAJOR, buf + 3 * T, gp, ws, ws_bytes, stream, nullptr, saved, saved_bytes, N);
     if (s == LA_OK) {
-      pitch_copy(out, N * e, buf + 3 * T, Np * e, N * e, G * D, st);
-      pitch_copy(g, N * 4, gp, Np * 4, N * 4, G, st);
+      pitch_copy<u16>((u16*)out, N, (const u16*)(buf + 3 * T), Np, N, N, G * D, 0, st);
+      pitch_copy<float>(g, N, gp, Np, N, N, G, 0.f, st);
+      note_launch(2);
     }
     cudaFreeAsync(buf, st);
     if (s != LA_OK) return fail(err, s, "sequence-padded forward failed");
@@ -368,23 +396,24 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
     keep_pool_memory();
     if (cudaMallocAsync((void**)&buf, 8 * T + (size_t)G * Np * 4, st) != cudaSuccess)
       return cuda_fail(err, cudaErrorMemoryAllocation);
-    cudaMemsetAsync(buf, 0, 5 * T, st);
-    pitch_copy(buf, Np * D * e, q, N * D * e, N * D * e, G, st);
-    pitch_copy(buf + T, Np * D * e, k, N * D * e, N * D * e, G, st);
-    pitch_copy(buf + 2 * T, Np * e, v, N * e, N * e, G * D, st);
-    pitch_copy(buf + 3 * T, Np * e, o, N * e, N * e, G * D, st);
-    pitch_copy(buf + 4 * T, Np * e, omega, N * e, N * e, G * D, st);
+    (void)e;
+    pitch_copy<u16>((u16*)buf, Np * D, (const u16*)q, N * D, N * D, Np * D, G, 0, st);
+    pitch_copy<u16>((u16*)(buf + T), Np * D, (const u16*)k, N * D, N * D, Np * D, G, 0, st);
+    pitch_copy<u16>((u16*)(buf + 2 * T), Np, (const u16*)v, N, N, Np, G * D, 0, st);
+    pitch_copy<u16>((u16*)(buf + 3 * T), Np, (const u16*)o, N, N, Np, G * D, 0, st);
+    pitch_copy<u16>((u16*)(buf + 4 * T), Np, (const u16*)omega, N, N, Np, G * D, 0, st);
     float* gp = (float*)(buf + 8 * T);
-    pitch_copy(gp, Np * 4, g, N * 4, N * 4, G, st);
-    const int64_t tail = G * (Np - N);
-    k_fill_tail<<<(unsigned)((tail + 255) / 256), 256, 0, st>>>(gp, G, N, Np, 1.f);  // w_hat = 0 / 1 there
+    pitch_copy<float>(gp, Np, g, N, N, Np, G, 1.f, st);  // padded rows: w_hat = 0 / 1
+    note_launch(6);
     la_status s2 = backward_impl(&pn, nullptr, buf, LA_SEQUENCE_MAJOR, buf + T, LA_SEQUENCE_MAJOR, buf + 2 * T,
                                  LA_FEATURE_MAJOR, buf + 3 * T, buf + 4 * T, LA_FEATURE_MAJOR, gp, buf + 5 * T,
-                                 buf + 6 * T, buf + 7 * T, ws, ws_bytes, stream, nullptr);
+                                 buf + 6 * T, buf + 7 * T, ws, ws_bytes, stream, nullptr, saved, saved_bytes,
+                                 trust_saved);
     if (s2 == LA_OK) {
-      pitch_copy(dq, N * D * e, buf + 5 * T, Np * D * e, N * D * e, G, st);
-      pitch_copy(dk, N * e, buf + 6 * T, Np * e, N * e, G * D, st);
-      pitch_copy(dv, N * e, buf + 7 * T, Np * e, N * e, G * D, st);
+      pitch_copy<u16>((u16*)dq, N * D, (const u16*)(buf + 5 * T), Np * D, N * D, N * D, G, 0, st);
+      pitch_copy<u16>((u16*)dk, N, (const u16*)(buf + 6 * T), Np, N, N, G * D, 0, st);
+      pitch_copy<u16>((u16*)dv, N, (const u16*)(buf + 7 * T), Np, N, N, G * D, 0, st);
+      note_launch(3);
     }
     cudaFreeAsync(buf, st);
     if (s2 != LA_OK) return fail(err, s2, "sequence-padded backward failed");
@@ -613,6 +642,10 @@ size_t la_shard_state_floats(const la_problem* p) {
 
 size_t la_saved_state_bytes(const la_problem* p) {
   if (!p || p->groups <= 0 || p->seq_len <= 0 || p->dim <= 0) return kSavedHeader * sizeof(float);
+  if (padn_eligible(p, nullptr, LA_SEQUENCE_MAJOR, LA_SEQUENCE_MAJOR, LA_FEATURE_MAJOR, LA_FEATURE_MAJOR)) {
+    const la_problem pn = n_padded_problem(p);  // the padded problem's states
+    return tc_saved_floats(pn.groups, pn.seq_len, pn.dim) * sizeof(float);
+  }
   return tc_saved_floats(p->groups, p->seq_len, p->dim) * sizeof(float);
 }
 
