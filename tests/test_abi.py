@@ -121,3 +121,20 @@ def test_workspace_is_flat_in_sequence_length():
         p = _abi.make_problem(G, n, D, "bf16")
         assert lib.la_forward_workspace_bytes(C.byref(p)) <= bound
         assert lib.la_saved_state_bytes(C.byref(p)) <= 64 + 4 * G * 64 * sz
+
+
+def test_unaligned_sequence_sizes_cover_the_padded_problem():
+    """N not a multiple of 128 runs the padded problem (Np = 128 * ceil(N / 128)) on the
+    fast path: saved-state and workspace sizes cover it; a below 1e-3 or fp32 keep the
+    unpadded sizes (those problems stay on the CUDA-core path)."""
+    L = _abi.lib()
+    for N, Np in ((1000, 1024), (65535, 65536), (130, 256)):
+        p = _abi.make_problem(4, N, 128, "bf16")
+        pp = _abi.make_problem(4, Np, 128, "bf16")
+        assert L.la_saved_state_bytes(C.byref(p)) == L.la_saved_state_bytes(C.byref(pp))
+        assert L.la_forward_workspace_bytes(C.byref(p)) >= L.la_forward_workspace_bytes(C.byref(pp))
+        assert L.la_backward_workspace_bytes(C.byref(p)) >= L.la_backward_workspace_bytes(C.byref(pp))
+    small_a = _abi.make_problem(4, 1000, 128, "bf16", a=0.0, b=1.0)
+    f32 = _abi.make_problem(4, 1000, 128, "f32")
+    for p in (small_a, f32):
+        assert L.la_saved_state_bytes(C.byref(p)) < L.la_saved_state_bytes(C.byref(_abi.make_problem(4, 1024, 128, "bf16")))
