@@ -461,3 +461,16 @@ def test_unaligned_sequence_length_on_fast_path(cuda, causal, N, D):
     for key in ("out", "dq", "dk", "dv"):
         assert max_abs(res[key], ref[key]) <= BF16_ABS, key
     assert rel_err(res["g"], ref["g"]) <= 1e-3
+
+
+@pytest.mark.parametrize("causal", [True, False])
+@pytest.mark.parametrize("G,N", [(1, 128), (1, 64), (3, 1), (1, 129), (5, 192)])
+def test_small_and_edge_shapes_bf16(cuda, causal, G, N):
+    """Single chunks, one row, one group, N just past a chunk boundary: whatever path
+    takes them (tensor core, padded, CUDA cores) matches the oracle."""
+    q, k, v, w = fast_inputs(G, N, 128, seed=G * 1000 + N)
+    res = run_dev(q, k, v, w, "bf16", cuda, causal=causal)
+    ref = oracle_all(res, causal)
+    for key in ("out", "dq", "dk", "dv"):
+        assert max_abs(res[key], ref[key]) <= BF16_ABS, key
+    assert rel_err(res["g"], ref["g"]) <= 1e-3
