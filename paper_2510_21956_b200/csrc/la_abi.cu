@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 
 #include "../../include/la_cuda.h"
 #include "internal.h"
@@ -55,6 +56,38 @@ void keep_pool_memory() {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
   });
+}
+// Host-side registry of saved-state buffers written by this library's forwards, so the
+// paired backward can trust a buffer without reading its header back (a device ->
+// host read would synchronise the stream every training step and break graph capture).
+// Buffers written elsewhere fall back to the header check.
+struct SavedMeta {
+  int64_t G, N, D, P, seg;
+  int causal, usable;
+};
+static std::mutex g_saved_mu;
+static std::unordered_map<const void*, SavedMeta> g_saved;
+
+static void saved_expected(const la_problem* p, int64_t* P, int64_t* seg) {
+  *P = p->causal ? tc_segments(p->groups, p->seq_len) : -1;
+  *seg = p->causal ? ((p->seq_len / 128 + *P - 1) / *P) * 128 : 0;
+}
+void saved_note(const void* ptr, const la_problem* p, bool usable) {
+  SavedMeta m{p->groups, p->seq_len, p->dim, 0, 0, p->causal ? 1 : 0, usable ? 1 : 0};
+  saved_expected(p, &m.P, &m.seg);
+  std::lock_guard<std::mutex> lk(g_saved_mu);
+  g_saved[ptr] = m;
+}
+// 1: states for this problem; 0: a header-only buffer for this problem; -1: unknown
+int saved_lookup(const void* ptr, const la_problem* p) {
+  std::lock_guard<std::mutex> lk(g_saved_mu);
+  auto it = g_saved.find(ptr);
+  if (it == g_saved.end()) return -1;
+  const SavedMeta& m = it->second;
+  int64_t P, seg;
+  saved_expected(p, &P, &seg);
+  if (m.G != p->groups || m.N != p->seq_len || m.D != p->dim || m.causal != (p->causal ? 1 : 0)) return -1;
+  return m.usable && m.P == P && m.seg == seg ? 1 : 0;
 }
 }  // namespace lab
 
@@ -328,6 +361,7 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
     if (saved) {  // no per-segment states on this path: header only, the backward recomputes
       const float hdr[kSavedHeader] = {kSavedMagic, (float)p->groups, (float)p->seq_len, (float)p->dim, 0.f};
       cudaMemcpyAsync(saved, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st);
+      saved_note(saved, p, false);
     }
     s = forward_impl(&p2, nullptr, buf, LA_SEQUENCE_MAJOR, buf + T, LA_SEQUENCE_MAJOR, buf + 2 * T,
                      LA_FEATURE_MAJOR, buf + 3 * T, g, ws, ws_bytes, stream, nullptr, nullptr, 0, n_total);
@@ -353,6 +387,7 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
       const float hdr[kSavedHeader] = {kSavedMagic, (float)p->groups, (float)p->seq_len, (float)p->dim, 0.f};
       cudaMemcpyAsync(saved, hdr, sizeof(hdr), cudaMemcpyHostToDevice, L.stream);
     }
+    saved_note(saved, p, tc || gemm);
   }
   if (tc)
     e = tc_forward(L, t, out, g, w);
@@ -452,6 +487,9 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
     // written by this library's own forward of the same problem on the same stream
     // (la_host_step): the header is known to match, no synchronous read
     L.saved_in = (const float*)saved;
+  } else if (saved && (tc || gemm) && saved_lookup(saved, p) >= 0) {
+    // written by this library's forward for this problem (registry): no device read
+    if (saved_lookup(saved, p) == 1 && saved_bytes >= la_saved_state_bytes(p)) L.saved_in = (const float*)saved;
   } else if (saved && (tc || gemm)) {
     // validate the saved-state header written by la_forward_save
     float hdr[kSavedHeader];
