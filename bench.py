@@ -267,6 +267,7 @@ def run_our_arm(args):
     FMj, SMj = 0, 1
 
     def step():
+        sp = torch.cuda.current_stream(dev).cuda_stream  # the capture stream under --graph
         st = L.la_forward_save(C.byref(p), q.data_ptr(), SMj, k.data_ptr(), SMj, v.data_ptr(), FMj,
                                out.data_ptr(), g.data_ptr(), saved.data_ptr(), saved.numel(), wsf.data_ptr(),
                                wsf.numel(), sp, None)
@@ -279,14 +280,29 @@ def run_our_arm(args):
 
     for _ in range(args.warmup):
         step()
+    launches_per_graph = 0
+    if args.graph:
+        # one step captured in a CUDA graph and replayed in the timed region; event records
+        # inside a graph carry no timing, so the per-kernel times come from eager steps run
+        # right after the timed region (`kernels_source` in the line)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        c0 = L.la_launch_count()
+        with torch.cuda.graph(graph):
+            step()
+        launches_per_graph = L.la_launch_count() - c0  # replays do not pass through the host API
+        eager_step, step = step, graph.replay
+        for _ in range(2):
+            step()
     err = _abi.ErrorInfo()
     st = L.la_query_status(wsf.data_ptr(), sp, C.byref(err))
     assert st == 0, f"forward status {_abi.STATUS_NAMES[st]}: {err.message}"
     torch.cuda.synchronize()
 
     # ---- timed region
-    L.la_profile_enable(1)
-    _abi.profile_read()
+    if not args.graph:
+        L.la_profile_enable(1)
+        _abi.profile_read()
     launches0 = L.la_launch_count()
     if world > 1:
         dist.barrier()
@@ -300,7 +316,7 @@ def run_our_arm(args):
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    launches = L.la_launch_count() - launches0
+    launches = L.la_launch_count() - launches0 + launches_per_graph * args.steps
     # ---- peak HBM: everything the step touches is allocated through torch
     # (inputs, outputs, workspaces, saved segment states); the library itself allocates
     # nothing on this path, which the driver-level free-memory delta cross-checks.
@@ -313,6 +329,17 @@ def run_our_arm(args):
               "minimal_retained_bytes": int(8 * T_ + 4 * G * N),
               "note": "retained = q,k,v,dO,o,g,dq,dk,dv; transient = fwd/bwd workspaces + per-segment "
                       "saved prefix states (O(G*P*D^2), independent of N)"}
+    prof_steps = args.steps
+    if args.graph:
+        for _ in range(2):
+            eager_step()
+        torch.cuda.synchronize()
+        L.la_profile_enable(1)
+        _abi.profile_read()
+        prof_steps = 5
+        for _ in range(prof_steps):
+            eager_step()
+        torch.cuda.synchronize()
     L.la_profile_enable(0)
     prof = _abi.profile_read()
     ms = t0.elapsed_time(t1) / args.steps
@@ -328,8 +355,8 @@ def run_our_arm(args):
     per = {}
     for r in prof:
         per.setdefault(r["name"], []).append(r["ms"])
-    kstats = {n: {"ms": sum(v_) / len(v_), "launches_per_step": len(v_) / args.steps,
-                  "share": sum(v_) / args.steps / ms} for n, v_ in per.items()}
+    kstats = {n: {"ms": sum(v_) / len(v_), "launches_per_step": len(v_) / prof_steps,
+                  "share": sum(v_) / prof_steps / ms} for n, v_ in per.items()}
     top = max(kstats, key=lambda n: kstats[n]["ms"] * kstats[n]["launches_per_step"]) if kstats else None
     roof = None
     if top:
@@ -402,12 +429,13 @@ def run_our_arm(args):
                                        "(BASELINE configs[1])",
                            "global_batch": B * world, "seq_len": N, "heads": H, "dim": D,
                            "parallelism": f"batch_head{world}", "l2": "inputs 1.07 GB each >> 126 MB L2; no flush",
-                           "kernel_impl": args.kernel},
+                           "kernel_impl": args.kernel, "cuda_graph": bool(args.graph)},
                 "roofline": roof,
                 "step_roofline": {"alg_bytes": step_bytes, "achieved_gbs": step_gbs, "frac_hbm": step_gbs / hbm,
                                   "alg_tflops": flops / (ms / 1e3) / 1e12,
                                   "frac_bf16": flops / (ms / 1e3) / 1e12 / tf},
-                "kernels": kstats, "memory": memory, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "kernels": kstats, "kernels_source": "eager steps after the graph-replayed timed region"
+                if args.graph else "timed region", "memory": memory, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clocks}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -529,6 +557,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="replay the step as a captured CUDA graph")
     ap.add_argument("--config", default="2", choices=["2", "3", "5"],
                     help="2 = the north star (default); 3 / 5 = the sharded BASELINE configs")
     args = ap.parse_args()

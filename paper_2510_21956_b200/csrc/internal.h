@@ -141,6 +141,8 @@ cudaError_t tc_backward_shard_state(const Launch& L, const Tensors& t, float* ou
 
 // Stream-ordered scratch (cudaMallocAsync) keeps its freed blocks: call before allocating.
 void keep_pool_memory();
+// {magic, G, N, D, P, seg} into a saved-state buffer, stream-ordered and graph-capturable.
+void write_saved_header(void* dst, double g, double n, double d, double p, double seg, cudaStream_t st);
 
 // Non-causal path for D != 128 (bf16/fp16, canonical layouts): batched GEMMs (la_gemm.cu).
 bool gemm_full_supported(const Launch& L, const Tensors& t);

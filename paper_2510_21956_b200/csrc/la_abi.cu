@@ -57,6 +57,22 @@ void keep_pool_memory() {
     }
   });
 }
+// Saved-state header {magic, G, N, D, P, seg} written by a tiny kernel rather than a
+// pageable host copy, so a forward + backward step can be captured in a CUDA graph.
+__global__ void k_saved_header(float* dst, float g, float n, float d, float p, float seg) {
+  if (threadIdx.x == 0) {
+    dst[0] = kSavedMagic;
+    dst[1] = g;
+    dst[2] = n;
+    dst[3] = d;
+    dst[4] = p;
+    dst[5] = seg;
+  }
+}
+void write_saved_header(void* dst, double g, double n, double d, double p, double seg, cudaStream_t st) {
+  k_saved_header<<<1, 32, 0, st>>>((float*)dst, (float)g, (float)n, (float)d, (float)p, (float)seg);
+}
+
 // Host-side registry of saved-state buffers written by this library's forwards, so the
 // paired backward can trust a buffer without reading its header back (a device ->
 // host read would synchronise the stream every training step and break graph capture).
@@ -359,8 +375,7 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
     pad_copy(buf + T, k, p, true, true, st);
     pad_copy(buf + 2 * T, v, p, false, true, st);
     if (saved) {  // no per-segment states on this path: header only, the backward recomputes
-      const float hdr[kSavedHeader] = {kSavedMagic, (float)p->groups, (float)p->seq_len, (float)p->dim, 0.f};
-      cudaMemcpyAsync(saved, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st);
+      write_saved_header(saved, (double)p->groups, (double)p->seq_len, (double)p->dim, 0, 0, st);
       saved_note(saved, p, false);
     }
     s = forward_impl(&p2, nullptr, buf, LA_SEQUENCE_MAJOR, buf + T, LA_SEQUENCE_MAJOR, buf + 2 * T,
@@ -384,8 +399,7 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
     if (tc || gemm) {  // causal: prefix states per segment; non-causal: the K/V totals
       L.saved_out = (float*)saved;
     } else {  // header only: the backward recomputes its prefix states
-      const float hdr[kSavedHeader] = {kSavedMagic, (float)p->groups, (float)p->seq_len, (float)p->dim, 0.f};
-      cudaMemcpyAsync(saved, hdr, sizeof(hdr), cudaMemcpyHostToDevice, L.stream);
+      write_saved_header(saved, (double)p->groups, (double)p->seq_len, (double)p->dim, 0, 0, L.stream);
     }
     saved_note(saved, p, tc || gemm);
   }

@@ -289,8 +289,7 @@ cudaError_t fwd_t(const Launch& L, const Tensors& t, void* out, float* g, Worksp
   k_pack_state<T><<<dim3((unsigned)((Dp * D + 255) / 256), (unsigned)G), 256, 0, st>>>(S, (int64_t)D * D, sig, D, L.b,
                                                                                      L.a, 0, St, D, Dp);
   if (L.saved_out) {  // the K/V totals as state records for the backward (header P = -1)
-    const float hdr[kSavedHeader] = {kSavedMagic, (float)G, (float)N, (float)D, -1.f, 0.f};
-    cudaMemcpyAsync(L.saved_out, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st);
+    write_saved_header(L.saved_out, (double)G, (double)N, (double)D, -1, 0, st);
     const int64_t SZ = state_floats(D);
     k_write_records<<<dim3((unsigned)((SZ + 255) / 256), (unsigned)G), 256, 0, st>>>(S, z, sig, (float)N,
                                                                                      L.saved_out + kSavedHeader, D);

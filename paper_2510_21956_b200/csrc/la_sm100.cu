@@ -881,8 +881,7 @@ static cudaError_t tc_forward_full(const Launch& L, const Tensors& t, void* out,
   // the non-causal backward reuses them instead of re-reading K and V
   float* tot = L.saved_out ? L.saved_out + kSavedHeader : ws.base + G * P * A * SZ;
   if (L.saved_out) {
-    const float hdr[kSavedHeader] = {kSavedMagic, (float)G, (float)N, (float)kD, -1.f, 0.f};
-    cudaMemcpyAsync(L.saved_out, hdr, sizeof(hdr), cudaMemcpyHostToDevice, L.stream);
+    write_saved_header(L.saved_out, (double)G, (double)N, (double)kD, -1, 0, L.stream);
   }
   CUtensorMap mK, mV, mQ64, mO64;
   if (!make_map(&mK, t.k, bf, (uint64_t)(G * N), kD) || !make_map(&mV, t.v, bf, (uint64_t)(G * kD), (uint64_t)N) ||
@@ -990,8 +989,7 @@ cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, W
     launches += 1;
   }
   if (L.saved_out) {
-    const float hdr[kSavedHeader] = {kSavedMagic, (float)G, (float)N, (float)kD, (float)P, (float)seg};
-    cudaMemcpyAsync(L.saved_out, hdr, sizeof(hdr), cudaMemcpyHostToDevice, L.stream);
+    write_saved_header(L.saved_out, (double)G, (double)N, (double)kD, (double)P, (double)seg, L.stream);
   }
   const char* pfe = getenv("LA_PREFETCH");
   FwdParams prm{agg_st, A, L.carry_prefix, cmb, g, ws.flag, N, G, seg, P, L.row_offset, L.a, L.b, saved, out,

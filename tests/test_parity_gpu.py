@@ -474,3 +474,45 @@ def test_small_and_edge_shapes_bf16(cuda, causal, G, N):
     for key in ("out", "dq", "dk", "dv"):
         assert max_abs(res[key], ref[key]) <= BF16_ABS, key
     assert rel_err(res["g"], ref["g"]) <= 1e-3
+
+
+def test_step_is_cuda_graph_capturable(cuda):
+    """la_forward_save + la_backward_saved capture into a CUDA graph (no host syncs, no
+    pageable copies on the path) and a replay reproduces the eager step bitwise."""
+    import ctypes as C
+    import torch
+    from paper_2510_21956_b200 import _abi
+    L = _abi.lib()
+    G, N, D = 4, 2048, 128
+    q, k, v, w = fast_inputs(G, N, D, seed=5)
+    tq, tk = (torch.as_tensor(x).to(torch.bfloat16).to(cuda).contiguous() for x in (q, k))
+    tv, tw = (torch.as_tensor(x.transpose(0, 2, 1)).to(torch.bfloat16).to(cuda).contiguous() for x in (v, w))
+    p = _abi.make_problem(G, N, D, "bf16")
+    out = torch.empty((G, D, N), device=cuda, dtype=torch.bfloat16)
+    g = torch.empty((G, N), device=cuda, dtype=torch.float32)
+    dq, dk, dv = torch.empty_like(tq), torch.empty_like(tv), torch.empty_like(tv)
+    wsf = torch.empty(L.la_forward_workspace_bytes(C.byref(p)), device=cuda, dtype=torch.uint8)
+    wsb = torch.empty(L.la_backward_workspace_bytes(C.byref(p)), device=cuda, dtype=torch.uint8)
+    sv = torch.empty(L.la_saved_state_bytes(C.byref(p)), device=cuda, dtype=torch.uint8)
+
+    def step():
+        s = torch.cuda.current_stream().cuda_stream
+        assert L.la_forward_save(C.byref(p), tq.data_ptr(), 1, tk.data_ptr(), 1, tv.data_ptr(), 0, out.data_ptr(),
+                                 g.data_ptr(), sv.data_ptr(), sv.numel(), wsf.data_ptr(), wsf.numel(), s, None) == 0
+        assert L.la_backward_saved(C.byref(p), tq.data_ptr(), 1, tk.data_ptr(), 1, tv.data_ptr(), 0,
+                                   out.data_ptr(), tw.data_ptr(), 0, g.data_ptr(), sv.data_ptr(), sv.numel(),
+                                   dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), wsb.data_ptr(), wsb.numel(), s,
+                                   None) == 0
+
+    step()
+    torch.cuda.synchronize()
+    ref = [x.clone() for x in (out, g, dq, dk, dv)]
+    for x in (out, g, dq, dk, dv):
+        x.zero_()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    graph.replay()
+    torch.cuda.synchronize()
+    for a_, b_ in zip((out, g, dq, dk, dv), ref):
+        assert torch.equal(a_, b_)
