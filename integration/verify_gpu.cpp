@@ -16,8 +16,9 @@
 //   normalize  normalized draws never give g_i <= 0 or DegenerateDenominator on the device
 //   faults     (clean runs only) every Fault on the device equals the reference's
 //              faulted result, so the injected defects are the reference's defects
-//   tensorcore (--dtype bf16) N = 256, D = 128 cases on the tcgen05 path vs the f64
-//              reference on the bf16-rounded inputs: <= 2e-2 max-abs
+//   tensorcore bf16 through the shim: N = 256 / 512 / 300 (padded), D = 128 / 64 causal and
+//              non-causal, D = 256 non-causal, vs the f64 reference on the bf16-rounded
+//              inputs: <= 2e-2 max-abs
 // Exit 0 when every suite passes, 1 otherwise (--inject-defect makes the device run
 // the named Fault, which the forward or backward suite must then catch).
 #include <algorithm>
@@ -54,7 +55,7 @@ namespace {
 
 struct Opts {
   uint64_t seed = 0;
-  size_t fwd_cases = 200, bwd_cases = 100, norm_cases = 2000, tc_cases = 4;
+  size_t fwd_cases = 200, bwd_cases = 100, norm_cases = 2000, tc_cases = 7;
   Fault fault = Fault::None;
   bool bf16 = false;
 };
@@ -324,9 +325,13 @@ Result tensorcore_suite(const Opts& o) {
   std::mt19937_64 rng(o.seed ^ 0x7c057c05u);
   const LinearKernelCoeffs c{1.0, 1.0};
   setenv("LA_SHIM_DTYPE", "bf16", 1);
+  // tcgen05 (N % 128 == 0, D = 128), the padded-N path, D < 128 (zero-padded D causal,
+  // batched GEMMs non-causal) and D = 256 non-causal
+  const int64_t shapes[][2] = {{256, 128}, {512, 128}, {300, 128}, {300, 128}, {256, 64}, {256, 64}, {200, 256}};
   for (size_t t = 0; t < o.tc_cases; ++t) {
-    const bool causal = t % 2 == 0;
-    const Shape s{1, 2, 256 * (int64_t)(1 + t % 2), 128};
+    const int64_t n = shapes[t % 7][0], d = shapes[t % 7][1];
+    const bool causal = d == 256 ? false : t % 2 == 0;
+    const Shape s{1, 2, n, d};
     const auto [q0, k0] = normalize_qk(seeded(s, Layout::SequenceMajor, rng()),
                                        seeded(s, Layout::SequenceMajor, rng()));
     const HeadTensor q = round_bf16(q0), k = round_bf16(k0);
