@@ -72,33 +72,41 @@ __global__ void __launch_bounds__(256) k_colsum_part(const T* x, const float* w,
     part[((int64_t)g * nchunk + c) * D + m] = t;
   }
 }
-__global__ void k_sum_part(const float* part, float* out, int nchunk, int D) {
-  const int64_t g = blockIdx.x;
-  for (int m = threadIdx.x; m < D; m += blockDim.x) {
-    float acc = 0.f;
-    for (int c = 0; c < nchunk; ++c) acc += part[((int64_t)g * nchunk + c) * D + m];
-    out[g * D + m] = acc;
-  }
+// out[g][m] = sum_c partial[g][c][m]; one thread per (g, m), 256-wide blocks over G * D.
+__global__ void k_sum_part(const float* part, float* out, int nchunk, int D, int64_t GD) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= GD) return;
+  const int64_t g = e / D;
+  const int m = (int)(e % D);
+  float acc = 0.f;
+  for (int c = 0; c < nchunk; ++c) acc += part[((int64_t)g * nchunk + c) * D + m];
+  out[e] = acc;
 }
 
-// out[g][j] = sum_i y[g][j][i] (FeatureMajor rows, row stride ld), one CTA per (j, g).
+// out[g][j] = sum_i y[g][j][i] (FeatureMajor rows of N, row stride rs, N % 8 == 0),
+// one CTA per (j, g), 16-byte loads.
 template <typename T>
 __global__ void __launch_bounds__(256) k_rowsum(const T* y, float* out, int64_t N, int D, int64_t rs,
                                                 int64_t gstride) {
   __shared__ float red[8];
   const int64_t g = blockIdx.y;
   const int j = blockIdx.x;
-  const T* row = y + g * gstride + (int64_t)j * rs;
+  const uint4* row = (const uint4*)(y + g * gstride + (int64_t)j * rs);
   float acc = 0.f;
-  for (int64_t i = threadIdx.x; i < N; i += blockDim.x) acc += ld(row + i);
+  for (int64_t i = threadIdx.x; i < N / 8; i += blockDim.x) {
+    const uint4 u = __ldg(row + i);
+    const T* e = (const T*)&u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += (float)e[k];
+  }
 #pragma unroll
   for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
-    float s = 0.f;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-    out[g * D + j] = s;
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    out[g * D + j] = t;
   }
 }
 
@@ -282,7 +290,7 @@ cudaError_t fwd_t(const Launch& L, const Tensors& t, void* out, float* g, Worksp
   cublasStatus_t cs = rm_gemm(st, true, true, D, D, (int)N, k, D, N * D, dt, v, (int)N, N * D, dt, S, D,
                               (long long)D * D, CUDA_R_32F, (int)G);  // S = K^T V
   k_colsum_part<T><<<dim3(nchunk, (unsigned)G), 256, 0, st>>>(k, nullptr, part, N, D, nchunk);
-  k_sum_part<<<(unsigned)G, 256, 0, st>>>(part, z, nchunk, D);
+  k_sum_part<<<(unsigned)((G * D + 255) / 256), 256, 0, st>>>(part, z, nchunk, D, G * D);
   k_rowsum<T><<<dim3(D, (unsigned)G), 256, 0, st>>>(v, sig, N, D, N, N * D);
   k_qtilde<T><<<(unsigned)((G * N + 31) / 32), 256, 0, st>>>(q, z, L.a, L.b, (float)L.n_total, Qt, g, G * N, N, D,
                                                             Dp, ws.flag);
@@ -352,11 +360,11 @@ cudaError_t bwd_t(const Launch& L, const Tensors& t, void* dq, void* dk, void* d
     cs = rm_gemm(st, true, true, D, D, (int)N, k, D, N * D, dt, v, (int)N, N * D, dt, S, D, (long long)D * D,
                  CUDA_R_32F, (int)G);  // S = K^T V
     k_colsum_part<T><<<dim3(nchunk, (unsigned)G), 256, 0, st>>>(k, nullptr, part, N, D, nchunk);
-    k_sum_part<<<(unsigned)G, 256, 0, st>>>(part, z, nchunk, D);
+    k_sum_part<<<(unsigned)((G * D + 255) / 256), 256, 0, st>>>(part, z, nchunk, D, G * D);
   }
   k_what<T><<<dim3((unsigned)((N / 8 + 255) / 256), (unsigned)G), 256, 0, st>>>(w, o, t.g, Wt, s, N, D, Dp);
   k_colsum_part<T><<<dim3(nchunk, (unsigned)G), 256, 0, st>>>(q, s, part, N, D, nchunk);
-  k_sum_part<<<(unsigned)G, 256, 0, st>>>(part, u, nchunk, D);                                     // u = Q^T s
+  k_sum_part<<<(unsigned)((G * D + 255) / 256), 256, 0, st>>>(part, u, nchunk, D, G * D);                                     // u = Q^T s
   k_rowsum<T><<<dim3(D, (unsigned)G), 256, 0, st>>>(Wt, c, N, D, N, (int64_t)Dp * N);             // c
   if (cs == CUBLAS_STATUS_SUCCESS)  // R = Q^T W_hat
     cs = rm_gemm(st, true, true, D, D, (int)N, q, D, N * D, dt, Wt, (int)N, (long long)Dp * N, dt, R, D,
