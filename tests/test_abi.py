@@ -138,3 +138,16 @@ def test_unaligned_sequence_sizes_cover_the_padded_problem():
     f32 = _abi.make_problem(4, 1000, 128, "f32")
     for p in (small_a, f32):
         assert L.la_saved_state_bytes(C.byref(p)) < L.la_saved_state_bytes(C.byref(_abi.make_problem(4, 1024, 128, "bf16")))
+
+
+def test_sass_has_tcgen05_and_tma_instructions():
+    """The shipped cubin issues 5th-gen tensor-core MMAs (UTCHMMA), TMEM loads / stores
+    (LDTM / STTM) and TMA bulk tensor loads / stores (UTMALDG / UTMASTG)."""
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([exe, "-sass", _abi.LIB_PATH], capture_output=True, text=True).stdout
+    for op in ("UTCHMMA", "LDTM", "STTM", "UTMALDG", "UTMASTG"):
+        assert op in sass, op
