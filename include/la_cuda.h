@@ -137,7 +137,11 @@ la_status la_backward(const la_problem* p, const void* q, la_layout lq, const vo
 /* Forward that also saves, per (group, segment), the prefix state at the
  * segment's last row (la_saved_state_bytes(p) bytes, device memory). Handing it
  * to la_backward_saved spares the backward from re-reading K and V for its
- * prefix states, the way ForwardArtifacts carries (out, g) (forward.hpp:35-41). */
+ * prefix states, the way ForwardArtifacts carries (out, g) (forward.hpp:35-41).
+ * The buffer must come from la_forward_save of the same problem: the library
+ * remembers which buffers its forwards wrote (no device read in the backward, so a
+ * forward + backward step is stream-asynchronous and CUDA-graph capturable); a buffer
+ * it does not know is checked through its header (one synchronising read). */
 size_t la_saved_state_bytes(const la_problem* p);
 la_status la_forward_save(const la_problem* p, const void* q, la_layout lq, const void* k,
                           la_layout lk, const void* v, la_layout lv, void* out, float* g,
