@@ -10,10 +10,15 @@ Our arm: inputs resident in HBM (each input tensor is 1.07 GB, far above the
 126 MB L2, so no flush is needed between steps); K steps timed with CUDA events
 on the launching stream between barriers; max over ranks. N>1 ranks each run
 their own batch x head shard (weak scaling, no collective on the data path).
-`e2e` repeats the step through the host-buffer C-ABI (la_host_forward /
-la_host_backward: pinned host -> HBM -> host every step). `cpu_baseline` and
-`--impl reference` time the reference's own CPU path (oracle/_ref, compiled from
-the reference sources; else the oracle port) on a bounded sample.
+`e2e` repeats the step through the host-buffer C-ABI (la_host_step: pinned host ->
+HBM -> host every step). `cpu_baseline` times the reference's own CPU path
+(oracle/_ref, compiled from the reference sources; else the oracle port) on a
+bounded sample (8 heads x 16384 rows); `--impl reference` runs that CPU path on the
+FULL workload every step (same config object as this arm).
+
+`roofline` is the dominant phase (the backward: W_hat / R aggregate + reverse sweep)
+against its algorithmic bytes 8 D e + 4 per row; `phases` holds both phases,
+`kernels` each kernel's in-region time and ncu DRAM bytes (profiles/ncu_traffic.json).
 """
 from __future__ import annotations
 
@@ -166,11 +171,61 @@ def cpu_tokens_per_s(t):
     return CPU_SAMPLE["groups"] * CPU_SAMPLE["seq_len"] / CFG["heads"] / t
 
 
+def full_cpu_inputs(seed=0):
+    """The whole north-star workload in the reference's f32 layouts (bench.cpp:75-97
+    distribution: U(-1,1), q/k rows normalised; q, k SequenceMajor, v, omega FeatureMajor)."""
+    import numpy as np
+    G, N, D = CFG["batch"] * CFG["heads"], CFG["seq_len"], CFG["dim"]
+    rng = np.random.default_rng(seed)
+
+    def uni(shape):
+        x = rng.random(shape, dtype=np.float32)
+        x *= 2
+        x -= 1
+        return x
+
+    q, k = uni((G, N, D)), uni((G, N, D))
+    for x in (q, k):
+        x /= np.linalg.norm(x, axis=2, keepdims=True)
+    return q, k, uni((G, D, N)), uni((G, D, N))
+
+
+def our_config(world=1, kernel="auto", graph=False):
+    """The `config` object of the default arm; the reference arm reports the same one."""
+    return {"workload": "causal LA fwd+bwd B=4 H=16 N=65536 D=128 a=b=1 per GPU (BASELINE configs[1])",
+            "global_batch": CFG["batch"] * world, "seq_len": CFG["seq_len"], "heads": CFG["heads"],
+            "dim": CFG["dim"], "parallelism": f"batch_head{world}",
+            "l2": "inputs 1.07 GB each >> 126 MB L2; no flush", "kernel_impl": kernel, "cuda_graph": bool(graph)}
+
+
 def run_reference_arm(args):
+    """The reference's own CPU implementation of the path (oracle/_ref: la_core built from
+    /root/reference/proj/src, else the C port) on the FULL workload every step: G = 64
+    heads x N = 65536 x D = 128, run_forward<float> + run_backward<float> with all host
+    threads, exactly the calls bench.cpp:137-139 / 176-179 time."""
+    import numpy as np
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    kind, cores, fn = cpu_runner()
+    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    G, N, D = CFG["batch"] * CFG["heads"], CFG["seq_len"], CFG["dim"]
+    q, k, v, w = full_cpu_inputs()
+    outs = (np.empty(G * N * D, np.float32), np.empty(G * N, np.float32),
+            *(np.empty(G * N * D, np.float32) for _ in range(3)))
+    for x in outs:  # first touch outside the timed steps
+        x.fill(0)
+    v3, w3 = v.reshape(G, N, D), w.reshape(G, N, D)  # flat FeatureMajor buffers, shape only
+    if O.ref_lib() is not None:
+        kind = "reference"
+
+        def fn():
+            O.ref_fwd_bwd_f32(q, k, v3, w3, workers=cores, outs=outs)
+    else:
+        kind, cores = "port", min(cores, G)
+
+        def fn():
+            O.fwd_bwd_f32_threads(q, k, v3, w3, threads=cores)
     for _ in range(args.warmup):
         fn()
     times = []
@@ -179,16 +234,16 @@ def run_reference_arm(args):
         fn()
         times.append(time.perf_counter() - t0)
     t = sum(times) / len(times)
-    val = cpu_tokens_per_s(t)
+    val = CFG["batch"] * N / t
+    src = ("reference la_core detail::run_forward<float> + run_backward<float> (oracle/_ref, built from "
+           "/root/reference/proj/src)" if kind == "reference" else "oracle/oracle.c f32 port")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3 * (
-                CFG["batch"] * CFG["seq_len"]) / (CPU_SAMPLE["groups"] * CPU_SAMPLE["seq_len"] / CFG["heads"]),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": "causal LA fwd+bwd B=4 H=16 N=65536 D=128 (reference CPU path, sampled)",
-                       "global_batch": CFG["batch"], "seq_len": CFG["seq_len"], "parallelism": "cpu"},
+            "data": "synthetic (U(-1,1), unit-norm q/k rows)", "config": our_config(),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": kind,
-                             "sample": cpu_sample_desc(kind)},
+                             "sample": f"{src}; the full workload every step (G=64 x N=65536 x D=128, f32, "
+                                       f"causal, canonical layouts), {cores} worker threads"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -198,20 +253,6 @@ ALG_BYTES = {  # algorithmic bytes per processed row (D, element bytes e), SURVE
     "fwd": lambda D, e: 4 * D * e + 4,
     "bwd": lambda D, e: 8 * D * e + 4,
 }
-
-
-def kernel_bytes(name, rows, D, e):
-    """Algorithmic bytes one launch of `name` must move (reads + writes of its own tensors)."""
-    table = {
-        "la_fwd_causal": 4 * D * e + 4, "la_bwd_causal": 8 * D * e + 4,
-        "la_bwd_fused": 8 * D * e + 4,  # the whole backward (aggregate units + sweeps) in one grid
-        "k_fwd_rows": 4 * D * e + 4, "la_fwd_agg": 2 * D * e, "la_bwd_agg": 4 * D * e + 8, "k_bwd_rows_dq": 4 * D * e + 8, "k_bwd_rows_dk": 4 * D * e + 8,
-        "k_bwd_rows_dv": 4 * D * e + 4, "k_seg_sums": 2 * D * e, "k_row_s": 2 * D * e + 8,
-    }
-    for key, per_row in table.items():
-        if name.startswith(key):
-            return per_row * rows
-    return None
 
 
 def run_our_arm(args):
@@ -350,28 +391,38 @@ def run_our_arm(args):
     tokens_step = B * N * world
     value = tokens_step / (ms / 1e3)
 
-    # ---- per-kernel roofline from the in-region events
+    # ---- roofline per phase from the in-region events. The algorithmic bytes of SURVEY
+    # 8(d) belong to a phase, not to one kernel: the forward (aggregate + sweep) reads
+    # Q, K, V and writes O, g (4 D e + 4 per row); the backward (W_hat / R aggregate +
+    # sweep) reads Q, K, V, O, dO, g and writes dQ, dK, dV (8 D e + 4 per row). The
+    # dominant phase is the `roofline` object; `traffic` is the ncu DRAM bytes of the
+    # same kernels (profiles/ncu_traffic.json, one --set full capture per kernel).
     hbm, tf, src = peaks()
     per = {}
     for r in prof:
         per.setdefault(r["name"], []).append(r["ms"])
     kstats = {n: {"ms": sum(v_) / len(v_), "launches_per_step": len(v_) / prof_steps,
                   "share": sum(v_) / prof_steps / ms} for n, v_ in per.items()}
-    top = max(kstats, key=lambda n: kstats[n]["ms"] * kstats[n]["launches_per_step"]) if kstats else None
-    roof = None
-    if top:
-        rows = G * N
-        alg = kernel_bytes(top, rows, D, e)
-        kms = kstats[top]["ms"]
-        traffic = None
-        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tpath):
-            traffic = json.load(open(tpath)).get(top)
-        if alg:
-            ach = alg / (kms / 1e3) / 1e9
-            roof = {"bound": "hbm", "kernel": top, "achieved": ach, "peak": hbm, "unit": "GB/s",
-                    "frac": ach / hbm, "traffic": traffic, "peak_source": src,
-                    "alg_bytes_per_launch": alg, "kernel_ms": kms}
+    ncu = {}
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        ncu = {k_: v_ for k_, v_ in json.load(open(tpath)).items() if not k_.startswith("_")}
+    for n, st_ in kstats.items():
+        st_["ncu_dram_bytes"] = ncu.get(n)
+    phases = {}
+    for ph, prefix in (("forward", "la_fwd"), ("backward", "la_bwd")):
+        names = sorted(n for n in kstats if n.startswith(prefix))
+        if not names:
+            continue
+        pms = sum(kstats[n]["ms"] * kstats[n]["launches_per_step"] for n in names)
+        alg = G * N * ALG_BYTES["fwd" if ph == "forward" else "bwd"](D, e)
+        traffic = sum(ncu[n] for n in names) if all(n in ncu for n in names) else None
+        ach = alg / (pms / 1e3) / 1e9
+        phases[ph] = {"bound": "hbm", "kernel": " + ".join(names) + f" ({ph} phase)", "achieved": ach,
+                      "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": traffic, "peak_source": src,
+                      "alg_bytes_per_launch": alg, "kernel_ms": pms,
+                      "traffic_over_alg": traffic / alg if traffic else None}
+    roof = max(phases.values(), key=lambda r_: r_["kernel_ms"]) if phases else None
     step_bytes = G * N * (ALG_BYTES["fwd"](D, e) + ALG_BYTES["bwd"](D, e))
     step_gbs = step_bytes / (ms / 1e3) / 1e9
     flops = G * N * 14 * D * D
@@ -425,12 +476,8 @@ def run_our_arm(args):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (U(-1,1), unit-norm q/k rows)",
-                "config": {"workload": "causal LA fwd+bwd B=4 H=16 N=65536 D=128 bf16 a=b=1 per GPU "
-                                       "(BASELINE configs[1])",
-                           "global_batch": B * world, "seq_len": N, "heads": H, "dim": D,
-                           "parallelism": f"batch_head{world}", "l2": "inputs 1.07 GB each >> 126 MB L2; no flush",
-                           "kernel_impl": args.kernel, "cuda_graph": bool(args.graph)},
-                "roofline": roof,
+                "config": our_config(world, args.kernel, args.graph),
+                "roofline": roof, "phases": phases,
                 "step_roofline": {"alg_bytes": step_bytes, "achieved_gbs": step_gbs, "frac_hbm": step_gbs / hbm,
                                   "alg_tflops": flops / (ms / 1e3) / 1e12,
                                   "frac_bf16": flops / (ms / 1e3) / 1e12 / tf},

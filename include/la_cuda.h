@@ -103,6 +103,22 @@ typedef struct {
   const float* carry_suffix; /* backward: exclusive suffix (R, u, c) */
 } la_shard;
 
+/* Measurement overrides of the built-in schedule rules, for benchmark sweeps only
+ * (0 = the built-in rule; results never depend on them beyond fp32 summation order).
+ * Process-wide; set between calls, not while a call is in flight. */
+typedef struct {
+  int32_t segments;      /* causal tensor-core segments per group (choose_segments) */
+  int32_t agg_split;     /* aggregate-pass units per segment (agg_split / bwd_agg_split) */
+  int32_t full_ctas_fwd; /* non-causal forward apply pass: CTAs per group */
+  int32_t full_ctas_bwd; /* non-causal backward pass: CTAs per group */
+  int32_t prefetch;      /* L2 prefetch distance (chunks) ahead of the TMA ring */
+  int32_t bwd_fused;     /* 1: aggregate units + sweeps in one ticket-scheduled grid */
+  int32_t host_blocks;   /* la_host_step: group blocks per step (default 16) */
+  int32_t simt_seg_rows; /* CUDA-core path: minimum rows per segment (default 32) */
+} la_tuning;
+void la_set_tuning(const la_tuning* t); /* NULL restores the built-in rules */
+void la_get_tuning(la_tuning* t);
+
 /* ---------------------------------------------------------------- queries */
 const char* la_version(void);
 const char* la_status_name(la_status s);

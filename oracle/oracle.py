@@ -230,20 +230,24 @@ def ref_finite_diff(q, k, v, omega, a=1.0, b=1.0, causal=True, h=1e-6):
     return tuple(from_flat(x, G, N, D, SEQUENCE_MAJOR).copy() for x in (dq, dk, dv))
 
 
-def ref_fwd_bwd_f32(q, k, v, omega, a=1.0, b=1.0, causal=True, workers=1):
+def ref_fwd_bwd_f32(q, k, v, omega, a=1.0, b=1.0, causal=True, workers=1, outs=None):
     """The reference's own timed fast path: run_forward<float> then run_backward<float>
-    on flat canonical-layout float32 inputs (bench.cpp:137-139, 176-179)."""
+    on flat canonical-layout float32 inputs (bench.cpp:137-139, 176-179). ``outs`` =
+    (out, g, dq, dk, dv) preallocated float32 buffers (reused across timed steps, as the
+    reference bench reuses its own, bench.cpp:111-191)."""
     r = ref_lib()
     G, N, D = q.shape
     q, k, v, omega = (np.ascontiguousarray(x, np.float32) for x in (q, k, v, omega))
-    out = np.empty(G * N * D, np.float32)
-    g = np.empty(G * N, np.float32)
+    if outs is None:
+        outs = (np.empty(G * N * D, np.float32), np.empty(G * N, np.float32),
+                *(np.empty(G * N * D, np.float32) for _ in range(3)))
+    out, g = outs[0], outs[1]
     st = r.ref_run_forward_f32(C.c_int(int(causal)), _p(q), _p(k), _p(v), C.c_int64(G), C.c_int64(N),
                                C.c_int64(D), C.c_double(a), C.c_double(b), C.c_int(workers), _p(out),
                                _p(g))
     if st:
         raise RuntimeError(f"reference run_forward<float> failed with status {st}")
-    dq, dk, dv = (np.empty(G * N * D, np.float32) for _ in range(3))
+    dq, dk, dv = outs[2], outs[3], outs[4]
     st = r.ref_run_backward_f32(C.c_int(int(causal)), _p(q), _p(k), _p(v), _p(out), _p(omega), _p(g),
                                 C.c_int64(G), C.c_int64(N), C.c_int64(D), C.c_double(a),
                                 C.c_double(b), C.c_int(workers), _p(dq), _p(dk), _p(dv))

@@ -29,6 +29,7 @@ EXPORTS = [
     "la_saved_state_bytes", "la_forward_save", "la_backward_saved",
     "la_normalize_qk", "la_relayout", "la_make_omega_hat", "la_constant_term_pass", "la_linear_term_pass",
     "la_alpha_term_pass", "la_beta_term_pass", "la_forward_sharded_save", "la_backward_sharded_saved",
+    "la_set_tuning", "la_get_tuning",
 ]
 
 
@@ -47,6 +48,12 @@ class Problem(C.Structure):
 class ErrorInfo(C.Structure):
     _fields_ = [("code", C.c_int), ("group", C.c_int64), ("position", C.c_int64),
                 ("message", C.c_char * 256)]
+
+
+class Tuning(C.Structure):
+    """la_tuning: measurement overrides of the schedule rules (0 = built-in rule)."""
+    _fields_ = [(n, C.c_int32) for n in ("segments", "agg_split", "full_ctas_fwd", "full_ctas_bwd", "prefetch",
+                                         "bwd_fused", "host_blocks", "simt_seg_rows")]
 
 
 class Shard(C.Structure):
@@ -112,8 +119,20 @@ def lib():
         L.la_linear_term_pass.argtypes = [P, vp, ci, vp, ci, vp, ci, vp, vp, E]
         L.la_alpha_term_pass.argtypes = [P, vp, ci, vp, ci, vp, ci, vp, vp, E]
         L.la_beta_term_pass.argtypes = [P, vp, ci, vp, ci, vp, ci, vp, vp, E]
+        L.la_set_tuning.argtypes = [C.POINTER(Tuning)]
+        L.la_set_tuning.restype = None
+        L.la_get_tuning.argtypes = [C.POINTER(Tuning)]
+        L.la_get_tuning.restype = None
         _lib = L
     return _lib
+
+
+def set_tuning(**fields):
+    """la_set_tuning with the named overrides (no arguments: the built-in rules)."""
+    t = Tuning()
+    for k, v in fields.items():
+        setattr(t, k, int(v))
+    lib().la_set_tuning(C.byref(t) if fields else None)
 
 
 def profile_read():

@@ -9,6 +9,9 @@
 
 namespace lab {
 
+// Measurement overrides (la_set_tuning); every field 0 unless a benchmark set it.
+const la_tuning& tuning();
+
 // Per-(group, segment) state record, fp32:
 //   [X: D*D row-major][vA: D][vB: D][count: 1]
 // forward  (SUM_KV): X[m][j] = sum k_m v_j, vA = sum k (z), vB = sum v (sigma)
@@ -43,8 +46,7 @@ inline int choose_segments(int64_t G, int64_t N, int num_sms = 148) {
 inline int agg_split(int64_t G, int64_t seg_rows, int segs_aggregated, int num_sms = 148) {
   if (segs_aggregated <= 0) return 1;
   const int64_t units = G * segs_aggregated, chunks = seg_rows / 128;
-  if (const char* e = getenv("LA_AGG_SPLIT")) {  // measurement override
-    const int a = atoi(e);
+  if (const int a = tuning().agg_split) {  // measurement override
     if (a >= 1 && chunks % a == 0) return a;
   }
   int best = 1;
@@ -67,8 +69,7 @@ inline int agg_split(int64_t G, int64_t seg_rows, int segs_aggregated, int num_s
 // units per segment, several waves) balances them (0.70 -> 0.64 ms at the north star).
 inline int bwd_agg_split(int64_t seg_rows) {
   const int64_t chunks = seg_rows / 128;
-  if (const char* e = getenv("LA_AGG_SPLIT")) {
-    const int a = atoi(e);
+  if (const int a = tuning().agg_split) {
     if (a >= 1 && chunks % a == 0) return a;
   }
   for (int a = 8; a > 1; --a)
@@ -101,10 +102,41 @@ struct Launch {
 };
 
 // Saved-state buffer (la_forward_save -> la_backward_saved): a 16-float header
-// {magic, G, N, D, P, seg_rows} then G * P state records (inclusive prefix at
-// each segment's last row: S, z, sigma, rows).
+// {magic, G, N, D, P, seg_rows, ckK, ckC0} then G * P state records (inclusive prefix
+// at each segment's last row: S, z, sigma, rows), then G * ckK checkpoint records.
 constexpr float kSavedMagic = 1279348566.0f;  // 'LASV'
 constexpr int kSavedHeader = 16;
+
+// Prefix-state checkpoints (tensor-core causal path). The backward's reverse sweep
+// rebuilds each chunk's exclusive prefix S (and z) by subtracting K^T V from a later
+// exact state. The tensor core's fp32 accumulation truncates every step relative to
+// the accumulator's magnitude, so the absolute error grows with the number of steps
+// times |S| -- and dq_i = b (w_i S_i^T - s_i z_i) with w_i = omega_i / g_i ~ 1/i weighs
+// it most at small global rows (measured 9e-3 max-abs / 2.6e-2 relative on dq at the
+// north star with 32K-row segments). The forward therefore also saves the exact
+// prefix at the global rows C0 * 2^k (k < ckK, inside a segment); the backward
+// reloads S and z there. Steps since the last reload then stay proportional to i,
+// so the error weighed by 1/g_i stays bounded at every row, for O(G log N D^2) bytes.
+constexpr int kCkC0 = 1024;
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline int ck_count(int64_t n) {  // checkpoint rows C0 * 2^k below n
+  int k = 0;
+  while (((int64_t)kCkC0 << k) < n) ++k;
+  return k;
+}
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline int ck_index(int64_t global_row, int K) {  // k with global_row == C0 * 2^k, or -1
+  if (global_row <= 0 || global_row % kCkC0) return -1;
+  const int64_t q = global_row / kCkC0;
+  if (q & (q - 1)) return -1;
+  int k = 0;
+  while (((int64_t)1 << k) < q) ++k;
+  return k < K ? k : -1;
+}
 
 // Workspace carving shared by every path.
 struct Workspace {
@@ -142,7 +174,8 @@ cudaError_t tc_backward_shard_state(const Launch& L, const Tensors& t, float* ou
 // Stream-ordered scratch (cudaMallocAsync) keeps its freed blocks: call before allocating.
 void keep_pool_memory();
 // {magic, G, N, D, P, seg} into a saved-state buffer, stream-ordered and graph-capturable.
-void write_saved_header(void* dst, double g, double n, double d, double p, double seg, cudaStream_t st);
+void write_saved_header(void* dst, double g, double n, double d, double p, double seg, cudaStream_t st,
+                        int ck_k = 0);
 
 // Non-causal path for D != 128 (bf16/fp16, canonical layouts): batched GEMMs (la_gemm.cu).
 bool gemm_full_supported(const Launch& L, const Tensors& t);

@@ -1,6 +1,7 @@
 // C-ABI layer (include/la_cuda.h): argument validation with the reference's
 // error taxonomy, path selection, workspace carving, the device-side
 // degenerate-denominator report, and the host-buffer entry points.
+#include <algorithm>
 #include <atomic>
 #include <climits>
 #include <cstdio>
@@ -15,6 +16,9 @@
 #include <vector>
 
 namespace lab {
+static la_tuning g_tuning{};
+const la_tuning& tuning() { return g_tuning; }
+
 static std::atomic<uint64_t> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
@@ -59,7 +63,7 @@ void keep_pool_memory() {
 }
 // Saved-state header {magic, G, N, D, P, seg} written by a tiny kernel rather than a
 // pageable host copy, so a forward + backward step can be captured in a CUDA graph.
-__global__ void k_saved_header(float* dst, float g, float n, float d, float p, float seg) {
+__global__ void k_saved_header(float* dst, float g, float n, float d, float p, float seg, float ck) {
   if (threadIdx.x == 0) {
     dst[0] = kSavedMagic;
     dst[1] = g;
@@ -67,43 +71,28 @@ __global__ void k_saved_header(float* dst, float g, float n, float d, float p, f
     dst[3] = d;
     dst[4] = p;
     dst[5] = seg;
+    dst[6] = ck;
+    dst[7] = (float)kCkC0;
   }
 }
-void write_saved_header(void* dst, double g, double n, double d, double p, double seg, cudaStream_t st) {
-  k_saved_header<<<1, 32, 0, st>>>((float*)dst, (float)g, (float)n, (float)d, (float)p, (float)seg);
+void write_saved_header(void* dst, double g, double n, double d, double p, double seg, cudaStream_t st,
+                        int ck_k) {
+  k_saved_header<<<1, 32, 0, st>>>((float*)dst, (float)g, (float)n, (float)d, (float)p, (float)seg, (float)ck_k);
 }
 
-// Host-side registry of saved-state buffers written by this library's forwards, so the
-// paired backward can trust a buffer without reading its header back (a device ->
-// host read would synchronise the stream every training step and break graph capture).
-// Buffers written elsewhere fall back to the header check.
-struct SavedMeta {
-  int64_t G, N, D, P, seg;
-  int causal, usable;
-};
-static std::mutex g_saved_mu;
-static std::unordered_map<const void*, SavedMeta> g_saved;
-
-static void saved_expected(const la_problem* p, int64_t* P, int64_t* seg) {
-  *P = p->causal ? tc_segments(p->groups, p->seq_len) : -1;
-  *seg = p->causal ? ((p->seq_len / 128 + *P - 1) / *P) * 128 : 0;
-}
-void saved_note(const void* ptr, const la_problem* p, bool usable) {
-  SavedMeta m{p->groups, p->seq_len, p->dim, 0, 0, p->causal ? 1 : 0, usable ? 1 : 0};
-  saved_expected(p, &m.P, &m.seg);
-  std::lock_guard<std::mutex> lk(g_saved_mu);
-  g_saved[ptr] = m;
-}
-// 1: states for this problem; 0: a header-only buffer for this problem; -1: unknown
-int saved_lookup(const void* ptr, const la_problem* p) {
-  std::lock_guard<std::mutex> lk(g_saved_mu);
-  auto it = g_saved.find(ptr);
-  if (it == g_saved.end()) return -1;
-  const SavedMeta& m = it->second;
-  int64_t P, seg;
-  saved_expected(p, &P, &seg);
-  if (m.G != p->groups || m.N != p->seq_len || m.D != p->dim || m.causal != (p->causal ? 1 : 0)) return -1;
-  return m.usable && m.P == P && m.seg == seg ? 1 : 0;
+// Saved-state validation on the device: the backward checks the header the forward's
+// kernel wrote against the problem's expected segmentation, with no host read (so a
+// forward + backward step stays asynchronous and graph-capturable). A mismatch sets the
+// workspace flag to kFlagSavedMismatch, reported as MissingForwardState by the call
+// (err != NULL) or by la_query_status; the outputs are then unspecified.
+constexpr unsigned long long kFlagSavedMismatch = 0xFFFFFFFFFFFFFFFEull;
+__global__ void k_saved_check(const float* hdr, float g, float n, float d, float p, float seg, float ck,
+                              unsigned long long* flag) {
+  if (threadIdx.x == 0) {
+    const bool match = hdr[0] == kSavedMagic && hdr[1] == g && hdr[2] == n && hdr[3] == d && hdr[4] == p &&
+                       hdr[5] == seg && hdr[6] == ck;
+    if (!match) atomicExch(flag, kFlagSavedMismatch);
+  }
 }
 }  // namespace lab
 
@@ -376,7 +365,6 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
     pad_copy(buf + 2 * T, v, p, false, true, st);
     if (saved) {  // no per-segment states on this path: header only, the backward recomputes
       write_saved_header(saved, (double)p->groups, (double)p->seq_len, (double)p->dim, 0, 0, st);
-      saved_note(saved, p, false);
     }
     s = forward_impl(&p2, nullptr, buf, LA_SEQUENCE_MAJOR, buf + T, LA_SEQUENCE_MAJOR, buf + 2 * T,
                      LA_FEATURE_MAJOR, buf + 3 * T, g, ws, ws_bytes, stream, nullptr, nullptr, 0, n_total);
@@ -401,7 +389,6 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
     } else {  // header only: the backward recomputes its prefix states
       write_saved_header(saved, (double)p->groups, (double)p->seq_len, (double)p->dim, 0, 0, L.stream);
     }
-    saved_note(saved, p, tc || gemm);
   }
   if (tc)
     e = tc_forward(L, t, out, g, w);
@@ -497,30 +484,23 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
   Workspace w = carve(ws, ws_bytes);
   const bool tc = use_tc(p, tc_backward_supported(L, t));
   const bool gemm = !tc && p->impl == LA_IMPL_AUTO && gemm_full_supported(L, t);
-  if (saved && (tc || gemm) && trust_saved) {
-    // written by this library's own forward of the same problem on the same stream
-    // (la_host_step): the header is known to match, no synchronous read
-    L.saved_in = (const float*)saved;
-  } else if (saved && (tc || gemm) && saved_lookup(saved, p) >= 0) {
-    // written by this library's forward for this problem (registry): no device read
-    if (saved_lookup(saved, p) == 1 && saved_bytes >= la_saved_state_bytes(p)) L.saved_in = (const float*)saved;
-  } else if (saved && (tc || gemm)) {
-    // validate the saved-state header written by la_forward_save
-    float hdr[kSavedHeader];
-    if (saved_bytes < sizeof(hdr) ||
-        cudaMemcpyAsync(hdr, saved, sizeof(hdr), cudaMemcpyDeviceToHost, L.stream) != cudaSuccess ||
-        cudaStreamSynchronize(L.stream) != cudaSuccess)
-      return fail(err, LA_ERR_MISSING_FORWARD_STATE, "cannot read the saved forward state");
-    const int P = tc_segments(p->groups, p->seq_len);
-    const int64_t seg = ((p->seq_len / 128 + P - 1) / P) * 128;
-    if (hdr[0] != kSavedMagic || hdr[1] != (float)p->groups || hdr[2] != (float)p->seq_len ||
-        hdr[3] != (float)p->dim)
-      return fail(err, LA_ERR_MISSING_FORWARD_STATE, "saved forward state does not match the problem");
-    if (((p->causal && hdr[4] == (float)P && hdr[5] == (float)seg) || (!p->causal && hdr[4] == -1.f)) &&
-        saved_bytes >= la_saved_state_bytes(p))
-      L.saved_in = (const float*)saved;  // else: produced by another path; recompute
-  }
   cudaMemsetAsync(w.flag, 0xFF, sizeof(unsigned long long), L.stream);
+  if (saved && (tc || gemm)) {
+    // states from la_forward_save of the same problem: causal -> per-segment prefixes
+    // + checkpoints, non-causal -> the K/V totals (header P = -1)
+    if (saved_bytes < la_saved_state_bytes(p))
+      return fail(err, LA_ERR_WORKSPACE, "saved-state buffer smaller than la_saved_state_bytes");
+    L.saved_in = (const float*)saved;
+    if (!trust_saved) {  // la_host_step hands over its own forward's buffer unchecked
+      const bool ct = p->causal && tc;
+      const int P = ct ? tc_segments(p->groups, p->seq_len) : -1;
+      const int64_t seg = ct ? ((p->seq_len / 128 + P - 1) / P) * 128 : 0;
+      k_saved_check<<<1, 32, 0, L.stream>>>((const float*)saved, (float)p->groups, (float)p->seq_len,
+                                            (float)p->dim, (float)P, (float)seg,
+                                            (float)(ct ? ck_count(p->seq_len) : 0), w.flag);
+      note_launch(1);
+    }
+  }
   cudaError_t e;
   if (tc)
     e = tc_backward(L, t, dq, dk, dv, w);
@@ -570,10 +550,7 @@ thread_local Arena t_arena;
 // a ring of device slots, so PCIe traffic in both directions overlaps compute.
 // Up to this many group blocks per step: more blocks shorten the pipeline's fill
 // (first H2D) and drain (last D2H), which are the only unoverlapped copies.
-int kHostBlocks = [] {
-  const char* e = getenv("LA_HOST_BLOCKS");
-  return e ? (atoi(e) > 0 ? atoi(e) : 16) : 16;
-}();
+constexpr int kHostBlocks = 16;
 
 struct HostPipe {
   static constexpr int R = 3;
@@ -659,6 +636,11 @@ const char* la_status_name(la_status s) {
 }
 
 uint64_t la_launch_count(void) { return g_launches.load(); }
+
+void la_set_tuning(const la_tuning* t) { g_tuning = t ? *t : la_tuning{}; }
+void la_get_tuning(la_tuning* t) {
+  if (t) *t = g_tuning;
+}
 
 void la_profile_enable(int32_t on) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
@@ -793,6 +775,9 @@ la_status la_query_status(const void* workspace, void* stream, la_error_info* er
   cudaError_t e = cudaMemcpyAsync(&flag, workspace, sizeof(flag), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(err, e);
+  if (flag == kFlagSavedMismatch)
+    return fail(err, LA_ERR_MISSING_FORWARD_STATE,
+                "saved forward state does not come from la_forward_save of this problem");
   if (flag != ULLONG_MAX) {
     const int64_t grp = (int64_t)(flag >> 32), pos = (int64_t)(flag & 0xFFFFFFFFull);
     char msg[160];
@@ -981,15 +966,23 @@ la_status la_host_step(const la_problem* p, const void* q, la_layout lq, const v
   if (!layout_ok(lq) || !layout_ok(lk) || !layout_ok(lv) || !layout_ok(lw))
     return fail(err, LA_ERR_INVALID_ARGUMENT, "unknown layout");
   const int64_t G = p->groups, N = p->seq_len, D = p->dim;
-  const int64_t Gb = (G + kHostBlocks - 1) / kHostBlocks;  // blocks of whole groups
+  const int64_t hb = tuning().host_blocks > 0 ? tuning().host_blocks : kHostBlocks;
+  const int64_t Gb = (G + hb - 1) / hb;  // blocks of whole groups
   const int nb = (int)((G + Gb - 1) / Gb);
   la_problem pb = *p;
-  pb.groups = Gb;
-  pb.plan.groups = Gb;
   const size_t eb = elem_bytes(p->dtype);
   const size_t tb = align256((size_t)(Gb * N * D) * eb), gbb = align256(sizeof(float) * (size_t)(Gb * N));
-  const size_t sb = align256(la_saved_state_bytes(&pb));
-  const size_t wf = align256(la_forward_workspace_bytes(&pb)), wbk = align256(la_backward_workspace_bytes(&pb));
+  // The ragged last block has fewer groups, hence possibly more segments per group
+  // (choose_segments), so its saved states / workspaces can exceed the full block's:
+  // size every slot for the larger of the two block shapes.
+  size_t sb = 0, wf = 0, wbk = 0;
+  for (const int64_t gs : {Gb, G - (int64_t)(nb - 1) * Gb}) {
+    pb.groups = gs;
+    pb.plan.groups = gs;
+    sb = std::max(sb, align256(la_saved_state_bytes(&pb)));
+    wf = std::max(wf, align256(la_forward_workspace_bytes(&pb)));
+    wbk = std::max(wbk, align256(la_backward_workspace_bytes(&pb)));
+  }
   const size_t per_slot = 8 * tb + gbb + sb + wf + wbk;
   cudaError_t e = t_pipe.reserve(per_slot, nb);
   if (e != cudaSuccess) return cuda_fail(err, e);

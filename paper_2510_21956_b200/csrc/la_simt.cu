@@ -595,8 +595,8 @@ cudaError_t backward_t(const Launch& L, const Tensors& t, void* dq, void* dk, vo
 int simt_segments(int64_t G, int64_t N, int fault) {
   if (fault != LA_FAULT_NONE) return 1;  // fault variants are defined on the unsplit sweep
   int64_t want = (2 * 148 + G - 1) / G;
-  const char* e = getenv("LA_SIMT_SEG_ROWS");  // measurement override of the minimum segment
-  const int64_t min_rows = e && atoi(e) > 0 ? atoi(e) : 32;  // config 1 (G=4, N=2048): 1.93 -> 0.46 ms vs 256
+  const int e = tuning().simt_seg_rows;  // measurement override of the minimum segment
+  const int64_t min_rows = e > 0 ? e : 32;  // config 1 (G=4, N=2048): 1.93 -> 0.46 ms vs 256
   int64_t cap = (N + min_rows - 1) / min_rows;
   return (int)std::max<int64_t>(1, std::min(want, cap));
 }

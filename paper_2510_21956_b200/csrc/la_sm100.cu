@@ -72,6 +72,8 @@ struct FwdParams {
   float* st_out;        // per-(group, segment) end state (S, z, sigma, rows) for the backward, or null
   void* out;            // o, FeatureMajor [G][D][N]
   int pf;               // chunks prefetched into L2 ahead of the ring
+  float* ck_out;        // [G][ck_K] prefix checkpoints at global rows C0 * 2^k (internal.h), or null
+  int ck_K;
 };
 
 // ================================================================ forward main
@@ -377,6 +379,24 @@ __global__ void __launch_bounds__(448, 1)
       if (es == 0) trace(1, c, 0);
       if (c >= 1) mbar_wait(st_full, (c - 1) & 1);
       tc_fence_after();
+      // exact prefix at this chunk's first row when it is a checkpoint row (internal.h);
+      // kept out of the conversion loop below, which is I-cache sensitive
+      if (prm.ck_out && c >= 1) {
+        const int k = ck_index(prm.row_offset + s0 + (int64_t)c * kCF, prm.ck_K);
+        if (k >= 0) {
+          float* ck = prm.ck_out + (grp * prm.ck_K + k) * state_floats(kD);
+          ck[kD * kD + r] = zr;
+          if (r == 0) ck[kD * kD + 2 * kD] = (float)(prm.row_offset + s0 + (int64_t)c * kCF);
+#pragma unroll 1
+          for (int m0 = 0; m0 < kD; m0 += 32) {  // record X[m][j] = S[m][j]; S^T row j = r here
+            uint32_t x[32];
+            tmem_ld32(tmem + lane_base + kF_ST + m0, x);
+            tmem_ld_wait();
+#pragma unroll
+            for (int u = 0; u < 32; ++u) ck[(m0 + u) * kD + r] = __uint_as_float(x[u]);
+          }
+        }
+      }
 #pragma unroll 1
       for (int half = 0; half < 2; ++half) {
         uint32_t x0[32], x1[32], pk[32];
@@ -841,8 +861,7 @@ __global__ void __launch_bounds__(192, 1)
 }  // namespace
 
 int tc_segments(int64_t G, int64_t N) {
-  const char* e = getenv("LA_SEGMENTS");
-  if (e) return (int)lmax(1, atoi(e));
+  if (const int e = tuning().segments) return (int)lmax(1, e);
   return choose_segments(G, N);
 }
 
@@ -902,7 +921,7 @@ static cudaError_t tc_forward_full(const Launch& L, const Tensors& t, void* out,
   const int64_t c64 = N / kCF;
   // independent chunks: ~7 waves (G = 64: 0.24 ms at 2 waves -> 0.19 ms)
   int64_t P2 = (7 * 148 + G / 2) / G;
-  if (const char* e = getenv("LA_FULL_SEGMENTS_F")) P2 = atoi(e);  // measurement override
+  if (tuning().full_ctas_fwd > 0) P2 = tuning().full_ctas_fwd;  // measurement override
   if (P2 > c64) P2 = c64;
   if (P2 < 1) P2 = 1;
   const int64_t seg2 = ((c64 + P2 - 1) / P2) * kCF;
@@ -921,7 +940,7 @@ static cudaError_t tc_forward_full(const Launch& L, const Tensors& t, void* out,
 size_t tc_saved_floats(int64_t G, int64_t N, int64_t D) {
   if (D != kD && D <= 256) return (size_t)(kSavedHeader + G * state_floats(D));  // la_gemm.cu: K/V totals
   if (D != kD || N % kC) return kSavedHeader;
-  return (size_t)(kSavedHeader + G * tc_segments(G, N) * state_floats(kD));
+  return (size_t)(kSavedHeader + G * (tc_segments(G, N) + ck_count(N)) * state_floats(kD));
 }
 
 // One CTA per (group, segment). P = 1 walks whole sequences (no carries, no
@@ -988,12 +1007,12 @@ cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, W
     agg<<<dim3(A * (P - 1), G), 192, kAggSmem, L.stream>>>(mK, mV, agg_st, N, seg / A, P * A);
     launches += 1;
   }
+  const int ckK = ck_count(N);
   if (L.saved_out) {
-    write_saved_header(L.saved_out, (double)G, (double)N, (double)kD, (double)P, (double)seg, L.stream);
+    write_saved_header(L.saved_out, (double)G, (double)N, (double)kD, (double)P, (double)seg, L.stream, ckK);
   }
-  const char* pfe = getenv("LA_PREFETCH");
   FwdParams prm{agg_st, A, L.carry_prefix, cmb, g, ws.flag, N, G, seg, P, L.row_offset, L.a, L.b, saved, out,
-                pfe ? atoi(pfe) : kFPrefetch};
+                tuning().prefetch > 0 ? tuning().prefetch : kFPrefetch, saved ? saved + G * P * SZ : nullptr, ckK};
   {
     ProfScope ps("la_fwd_causal", L.stream);
     main_k<<<dim3(P, G), 448, kFwdSmem, L.stream>>>(mQ64, mK64, mV64, mO64, prm);

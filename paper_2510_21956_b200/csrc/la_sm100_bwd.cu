@@ -134,6 +134,11 @@ struct BwdParams {
   uint32_t* flags = nullptr;  // fused schedule: per aggregate unit [G][P * A], set when published
   int r_unit0 = 0;  // aggregate pass: units below this only produce W_hat^T / s (their R records
                     // would feed no segment: segment 0 in the causal sweep)
+  const float* ck = nullptr;  // exact prefix (S, z) records the sweep reloads (internal.h, kCkC0):
+  int ck_K = 0;               //   ck_unit == 0: [G][ck_K] at global rows C0 * 2^k (the forward's)
+  int64_t row_offset = 0;     // global index of row 0 (sequence shards)
+  int64_t ck_unit = 0;        //   ck_unit > 0: [G][P][A] at the segment's unit boundaries, built by
+                              //   the sweep's prologue from the aggregate's unit sums (la_backward)
 };
 
 // Cross-CTA publication for the fused schedule (k_bwd_fused): the aggregate unit's
@@ -696,6 +701,17 @@ __device__ __forceinline__ void bwd_main_body(const CUtensorMap& tmQ, const CUte
   const int64_t s1 = lmin(prm.N, s0 + prm.seg_len);
   const int nc = (int)((s1 - s0) / kCB);
   auto row_of = [&](int m) -> int64_t { return s0 + (int64_t)(nc - 1 - m) * kCB; };  // reverse sweep
+  // the forward's exact prefix at chunk m's first row when that row is an interior checkpoint
+  auto ck_record = [&](int m) -> const float* {
+    if (!prm.ck || m >= nc - 1) return nullptr;
+    if (prm.ck_unit > 0) {
+      const int64_t off = row_of(m) - s0;
+      if (off % prm.ck_unit) return nullptr;
+      return prm.ck + ((grp * prm.P + p) * prm.A + off / prm.ck_unit) * state_floats(kD);
+    }
+    const int k = ck_index(prm.row_offset + row_of(m), prm.ck_K);
+    return k < 0 ? nullptr : prm.ck + (grp * prm.ck_K + k) * state_floats(kD);
+  };
   const uint32_t warp = warp_id();
   if (threadIdx.x == 0) traceb(0, 63, 8);
   if (warp == 0 && elect_one()) {
@@ -739,6 +755,14 @@ __device__ __forceinline__ void bwd_main_body(const CUtensorMap& tmQ, const CUte
                         (p + 1) * prm.A, SZ, ct, cn);
       combine_records(cS + SZ, prm.carry_suf ? prm.carry_suf + grp * SZ : nullptr, prm.stR + grp * U * SZ,
                       (p + 1) * prm.A, U, SZ, ct, cn);
+      if (!prm.skipS && prm.ck_unit > 0) {  // exclusive prefix at each unit boundary of the segment
+        float* ck = const_cast<float*>(prm.ck) + (grp * prm.P + p) * prm.A * SZ;
+        combine_records(ck, prm.carry_pre ? prm.carry_pre + grp * SZ : nullptr, prm.stS + grp * U * SZ, 0,
+                        p * prm.A, SZ, ct, cn);
+        for (int j = 1; j < prm.A; ++j)  // each thread re-reads only the elements it wrote
+          combine_records(ck + j * SZ, ck + (j - 1) * SZ, prm.stS + grp * U * SZ, p * prm.A + j - 1,
+                          p * prm.A + j, SZ, ct, cn);
+      }
     }
   }
   tc_fence_before();
@@ -1061,11 +1085,27 @@ __device__ __forceinline__ void bwd_main_body(const CUtensorMap& tmQ, const CUte
       if (n < nc) er_half(n, 64);
       if (n >= 1) dq_out(n - 1);
       if (n == nc) break;
-      // ---- E_S: b S_prev -> sS (after every warp's dQ staging in sS: gq_empty)
+      // ---- E_S: b S_prev -> sS (after every warp's dQ staging in sS: gq_empty). At a
+      //      checkpoint row the forward's exact prefix replaces the rebuilt one, in TMEM
+      //      too, so the later subtractions start from it (internal.h, kCkC0).
       mbar_wait(s_full, n & 1);
       if (n >= 1) mbar_wait(gq_empty, (n - 1) & 1);
       if (eb == 0) traceb(2, n, 1);
       tc_fence_after();
+      if (const float* ck = ck_record(n)) {  // out of line: the loop below is I-cache sensitive
+#pragma unroll 1
+        for (int j0 = 0; j0 < kD; j0 += 32) {
+          uint32_t x[32];
+#pragma unroll
+          for (int q = 0; q < 32; q += 4) {
+            const float4 f4 = *(const float4*)(ck + r * kD + j0 + q);
+            x[q] = __float_as_uint(f4.x); x[q + 1] = __float_as_uint(f4.y);
+            x[q + 2] = __float_as_uint(f4.z); x[q + 3] = __float_as_uint(f4.w);
+          }
+          tmem_st32(tmem + lb + kS + j0, x);
+        }
+        tmem_st_wait();
+      }
 #pragma unroll 1
       for (int j0 = 0; j0 < kD; j0 += 32) {
         uint32_t x[32];
@@ -1136,7 +1176,9 @@ __device__ __forceinline__ void bwd_main_body(const CUtensorMap& tmQ, const CUte
           }
         }
         const int m = 8 * mg + tg;
-        zbuf[(n & 3) * kD + m] = zbuf[((n - 1) & 3) * kD + m] - reduce_scatter8(zs, tg);
+        const float zn = zbuf[((n - 1) & 3) * kD + m] - reduce_scatter8(zs, tg);
+        const float* ck = ck_record(n);
+        zbuf[(n & 3) * kD + m] = ck ? ck[kD * kD + m] : zn;
       }
       mbar_arrive(sS_ready);  // publishes z(n), s(n) for dq_out(n) (dQ(n) waits sS_ready)
       // ---- du_m = sum_i q_im s_i of this chunk -> du_s[n & 3] (read by dk_out(n + 1))
@@ -1487,8 +1529,10 @@ size_t tc_backward_ws_floats(int64_t G, int64_t N, int64_t D) {
   const int P = tcb_segments(G, N);
   const int64_t seg = ((N / 128 + P - 1) / P) * 128;
   const int A = std::max(std::max(agg_split(G, seg, P > 1 ? P - 1 : 1), agg_split(G, seg, P)), bwd_agg_split(seg));
-  // S, R unit sums + combined records, then the fused schedule's flags and ticket
-  const size_t causal = (size_t)((2 * A + 2) * G * P) + (size_t)(G * P * A + 4 + state_floats(kD) - 1) / state_floats(kD);
+  // S, R unit sums + combined records, then the fused schedule's flags and ticket or the
+  // unit-boundary prefixes of the recomputing sweep (never both)
+  const size_t causal = (size_t)((2 * A + 2) * G * P) +
+                        std::max((size_t)(G * P * A), (size_t)(G * P * A + 4 + state_floats(kD) - 1) / state_floats(kD));
   const int Af = agg_split(G, seg, P);
   const size_t full = (size_t)(tc_kv_units(G, N) * G + Af * P * G + 2 * G);  // non-causal unit sums + totals
   return (causal > full ? causal : full) * state_floats(kD);
@@ -1535,7 +1579,7 @@ static cudaError_t tc_backward_full(const Launch& L, const Tensors& t, void* dq,
   // independent chunks: ~4 waves of CTAs balance the tail against the per-CTA setup
   // of the constant bS / bR operands (G = 64: 1.19 ms at 1.3 waves -> 0.85 ms at 3.9)
   int64_t P2 = (4 * 148 + G / 2) / G;
-  if (const char* e = getenv("LA_FULL_SEGMENTS")) P2 = atoi(e);  // measurement override
+  if (tuning().full_ctas_bwd > 0) P2 = tuning().full_ctas_bwd;  // measurement override
   if (P2 > c64) P2 = c64;
   if (P2 < 1) P2 = 1;
   const int64_t seg2 = ((c64 + P2 - 1) / P2) * kCB;
@@ -1618,15 +1662,22 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
       !make_tma_map(&mW, t.w, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1) ||
       !make_tma_map(&mWh, dv, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1))  // W_hat^T staged in dV
     return cudaErrorInvalidValue;
-  const char* dbg = getenv("LA_BWD_DEBUG");
   // The W_hat pass + R aggregate runs over every unit of seg / A rows (the sweep
   // reads W_hat^T and s from it; the R sums of segments 1..P-1 feed the earlier
   // segments' suffix). Without the forward's saved S records a second aggregate
   // sums S per unit for the inclusive prefix. The main kernel's prologue sums the
   // unit records.
   BwdParams prm{t.o, t.g, dq, dk, dv, use_saved ? const_cast<float*>(sv + kSavedHeader) : stS, stR, N, seg, P,
-                L.a, L.b, dbg ? atoi(dbg) : 0, use_saved ? 1 : 0, 0, A, L.carry_prefix, L.carry_suffix, cmb,
-                getenv("LA_PREFETCH") ? atoi(getenv("LA_PREFETCH")) : kBPrefetch};
+                L.a, L.b, 0, use_saved ? 1 : 0, 0, A, L.carry_prefix, L.carry_suffix, cmb,
+                tuning().prefetch > 0 ? tuning().prefetch : kBPrefetch};
+  prm.row_offset = L.row_offset;
+  if (use_saved) {  // checkpoints follow the G * P segment records (la_sm100.cu, tc_forward)
+    prm.ck = sv + kSavedHeader + G * P * SZ;
+    prm.ck_K = ck_count(N);
+  } else if (A > 1) {  // unit-boundary prefixes from the S aggregate (after cmb)
+    prm.ck = cmb + G * P * 2 * SZ;
+    prm.ck_unit = seg / A;
+  }
   BwdParams pa = prm;  // aggregate launch: unit geometry
   pa.stS = stS;
   pa.seg_len = seg / A;
@@ -1639,13 +1690,12 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
   cudaFuncSetAttribute(agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggSmemB);
   cudaFuncSetAttribute(main_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmemB);
   int launches = 2;
-  // LA_BWD_FUSED=1: one grid with the aggregate units beside the sweeps (k_bwd_fused;
+  // tuning().bwd_fused = 1: one grid with the aggregate units beside the sweeps (k_bwd_fused;
   // flags + ticket zeroed first). Measured slower at the north star (2.48 vs 0.72 + 1.62
   // ms: the aggregate CTAs take HBM bandwidth from the sweeps rather than filling
   // idle bandwidth), faster only when the sweep grid is a poor fit for the SMs (P = 5:
   // 2.54 vs 2.79 ms); kept as an opt-in schedule, profiles/r01_s3_fused.md.
-  const char* fz = getenv("LA_BWD_FUSED");
-  if (use_saved && fz && atoi(fz) == 1) {
+  if (use_saved && tuning().bwd_fused == 1) {
     uint32_t* flags = (uint32_t*)(cmb + G * P * 2 * SZ);
     const size_t nflag = (size_t)(G * P * A);
     cudaError_t e = cudaMemsetAsync(flags, 0, (nflag + 4) * sizeof(uint32_t), L.stream);

@@ -156,3 +156,33 @@ def test_finite_difference_goldens_from_reference():
     an = O.backward(q, k, v, out, w, g)
     for a_, f_ in zip(an, fd):
         assert np.all(np.abs(a_ - f_) <= 1e-7 + 1e-5 * np.abs(f_))
+
+
+@pytest.mark.parametrize("causal", [True, False])
+@pytest.mark.parametrize("N,D,a,b", [(1300, 24, 1.0, 1.0), (515, 16, 0.7, 1.3), (3, 2, 1.0, 1.0)])
+def test_chunked_oracle_matches_restatement(causal, N, D, a, b):
+    """oracle/chunked.py (BLAS-chunked f64, used for full-N parity) equals the loop-for-loop
+    restatement, chunk tails included (CHUNK = 512), and its sequence-shard carries
+    reproduce the unsharded result ('Sequence shards')."""
+    from oracle import chunked as CH
+    q = O.normalize_rows(O.seeded(1, N, D, 31, SM))
+    k = O.normalize_rows(O.seeded(1, N, D, 32, SM))
+    v = O.seeded(1, N, D, 33, FM)
+    w = O.seeded(1, N, D, 34, FM)
+    out, g = O.forward(q, k, v, a, b, causal=causal)
+    dq, dk, dv = O.backward(q, k, v, out, w, g, a, b, causal=causal)
+    co, cg = CH.forward(q[0], k[0], v[0], a, b, causal)
+    assert np.max(np.abs(co - out[0])) <= 1e-11 and np.max(np.abs(cg - g[0])) <= 1e-10
+    cq, ck, cv = CH.backward(q[0], k[0], v[0], out[0], w[0], g[0], a, b, causal)
+    for x, y in ((cq, dq[0]), (ck, dk[0]), (cv, dv[0])):
+        assert np.max(np.abs(x - y)) <= 1e-10 * max(1.0, np.max(np.abs(y)))
+    if causal and N > 8:
+        cut = N // 3
+        pre = CH.shard_totals_forward(k[0, :cut], v[0, :cut])
+        o2, g2 = CH.forward(q[0, cut:], k[0, cut:], v[0, cut:], a, b, True, prefix=pre, row0=cut)
+        assert np.max(np.abs(o2 - out[0, cut:])) <= 1e-11
+        suf = CH.shard_totals_backward(q[0, cut:], out[0, cut:], w[0, cut:], g[0, cut:])
+        q1, k1, v1 = CH.backward(q[0, :cut], k[0, :cut], v[0, :cut], out[0, :cut], w[0, :cut], g[0, :cut],
+                                 a, b, True, suffix=suf)
+        for x, y in ((q1, dq[0, :cut]), (k1, dk[0, :cut]), (v1, dv[0, :cut])):
+            assert np.max(np.abs(x - y)) <= 1e-10 * max(1.0, np.max(np.abs(y)))

@@ -283,7 +283,9 @@ def test_backward_with_saved_forward_state_matches_recompute(cuda):
     torch.cuda.synchronize()
 
 
-@pytest.mark.parametrize("dtype,G,N,D", [("bf16", 10, 1024, 128), ("f32", 3, 300, 64)])
+# (bf16, 69, 8192): blocks of 5 groups (P = 29 segments each) and a ragged last block of
+# 4 (P = 37): the last block needs more saved-state / workspace bytes than a full one
+@pytest.mark.parametrize("dtype,G,N,D", [("bf16", 10, 1024, 128), ("f32", 3, 300, 64), ("bf16", 69, 8192, 128)])
 def test_host_step_pipeline_matches_oracle(cuda, dtype, G, N, D):
     # la_host_step: forward + backward over host buffers, groups pipelined in blocks
     # (ragged last block at G=10) through the H2D / compute / D2H streams
@@ -407,8 +409,8 @@ def test_segment_partition_matches_oracle(cuda, G, N):
 
 
 @pytest.mark.gpu
-def test_fused_backward_schedule_matches_separate(cuda, monkeypatch):
-    """LA_BWD_FUSED=1 (k_bwd_fused: aggregate units and sweeps in one ticket-scheduled
+def test_fused_backward_schedule_matches_separate(cuda):
+    """la_tuning.bwd_fused = 1 (k_bwd_fused: aggregate units and sweeps in one ticket-scheduled
     grid) computes bitwise the same gradients as the two-launch default."""
     import torch
     import paper_2510_21956_b200 as la
@@ -420,10 +422,13 @@ def test_fused_backward_schedule_matches_separate(cuda, monkeypatch):
     hq, hk = la.HeadTensor.from_logical(t[0], L.SequenceMajor), la.HeadTensor.from_logical(t[1], L.SequenceMajor)
     hv, hw = la.HeadTensor.from_logical(t[2], L.FeatureMajor), la.HeadTensor.from_logical(t[3], L.FeatureMajor)
     art = la.forward_causal(hq, hk, hv)
-    monkeypatch.setenv("LA_BWD_FUSED", "0")
+    from paper_2510_21956_b200 import _abi
     g0 = la.backward_causal(art, hw)
-    monkeypatch.setenv("LA_BWD_FUSED", "1")
-    g1 = la.backward_causal(art, hw)
+    _abi.set_tuning(bwd_fused=1)
+    try:
+        g1 = la.backward_causal(art, hw)
+    finally:
+        _abi.set_tuning()
     torch.cuda.synchronize()
     for a_, b_ in ((g0.dq, g1.dq), (g0.dk, g1.dk), (g0.dv, g1.dv)):
         assert torch.equal(a_.data, b_.data)
@@ -516,3 +521,42 @@ def test_step_is_cuda_graph_capturable(cuda):
     torch.cuda.synchronize()
     for a_, b_ in zip((out, g, dq, dk, dv), ref):
         assert torch.equal(a_, b_)
+
+
+def test_saved_state_mismatch_reported(cuda):
+    """la_backward_saved validates the saved-state header on the device (no host read):
+    a buffer that does not come from la_forward_save of this problem is reported as
+    MissingForwardState (backward.cpp:15-20's error class), synchronously with err."""
+    import ctypes as C
+    import torch
+    from paper_2510_21956_b200 import _abi
+    L = _abi.lib()
+    G, N, D = 2, 2048, 128
+    q, k, v, w = fast_inputs(G, N, D, seed=12)
+    tq, tk = (torch.as_tensor(x).to(torch.bfloat16).to(cuda).contiguous() for x in (q, k))
+    tv, tw = (torch.as_tensor(x.transpose(0, 2, 1)).to(torch.bfloat16).to(cuda).contiguous() for x in (v, w))
+    p = _abi.make_problem(G, N, D, "bf16")
+    p2 = _abi.make_problem(G, N // 2, D, "bf16")
+    out = torch.empty((G, D, N), device=cuda, dtype=torch.bfloat16)
+    g = torch.empty((G, N), device=cuda, dtype=torch.float32)
+    dq, dk, dv = torch.empty_like(tq), torch.empty_like(tv), torch.empty_like(tv)
+    wsf = torch.empty(L.la_forward_workspace_bytes(C.byref(p)), device=cuda, dtype=torch.uint8)
+    wsb = torch.empty(L.la_backward_workspace_bytes(C.byref(p)), device=cuda, dtype=torch.uint8)
+    sv = torch.empty(L.la_saved_state_bytes(C.byref(p)), device=cuda, dtype=torch.uint8)
+    s = torch.cuda.current_stream().cuda_stream
+    err = _abi.ErrorInfo()
+
+    def bwd():
+        return L.la_backward_saved(C.byref(p), tq.data_ptr(), 1, tk.data_ptr(), 1, tv.data_ptr(), 0, out.data_ptr(),
+                                   tw.data_ptr(), 0, g.data_ptr(), sv.data_ptr(), sv.numel(), dq.data_ptr(),
+                                   dk.data_ptr(), dv.data_ptr(), wsb.data_ptr(), wsb.numel(), s, C.byref(err))
+
+    assert L.la_forward_save(C.byref(p), tq.data_ptr(), 1, tk.data_ptr(), 1, tv.data_ptr(), 0, out.data_ptr(),
+                             g.data_ptr(), sv.data_ptr(), sv.numel(), wsf.data_ptr(), wsf.numel(), s, C.byref(err)) == 0
+    assert bwd() == 0
+    sv.zero_()                                          # not a saved state
+    assert bwd() == 5 and b"la_forward_save" in err.message
+    # states of another problem (half the rows) in a large-enough buffer
+    assert L.la_forward_save(C.byref(p2), tq.data_ptr(), 1, tk.data_ptr(), 1, tv.data_ptr(), 0, out.data_ptr(),
+                             g.data_ptr(), sv.data_ptr(), sv.numel(), wsf.data_ptr(), wsf.numel(), s, C.byref(err)) == 0
+    assert bwd() == 5

@@ -19,9 +19,10 @@ for causal in (True, False):
     art = (la.forward_causal if causal else la.forward_full)(hq, hk, hv)
     (la.backward_causal if causal else la.backward_full)(art, hw)
     if causal:  # the opt-in fused backward schedule (k_bwd_fused)
-        os.environ["LA_BWD_FUSED"] = "1"
+        from paper_2510_21956_b200 import _abi
+        _abi.set_tuning(bwd_fused=1)
         la.backward_causal(art, hw)
-        os.environ.pop("LA_BWD_FUSED")
+        _abi.set_tuning()
 # prologue / diagnostics kernels (la_prologue.cu)
 hq2, hk2 = la.normalize_qk(hq, hk)
 hw_hat = la.make_omega_hat(hw, art.g)
