@@ -177,10 +177,11 @@ void keep_pool_memory();
 void write_saved_header(void* dst, double g, double n, double d, double p, double seg, cudaStream_t st,
                         int ck_k = 0);
 
-// Non-causal path for D != 128 (bf16/fp16, canonical layouts): batched GEMMs (la_gemm.cu).
-bool gemm_full_supported(const Launch& L, const Tensors& t);
-cudaError_t gemm_forward_full(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws);
-cudaError_t gemm_backward_full(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv);
+// Non-causal tensor-core path for D = 64, 192, 256 (bf16/fp16, canonical layouts; la_full.cu).
+bool full_tc_supported(const Launch& L, const Tensors& t);
+size_t full_ws_floats(int64_t G, int64_t N, int64_t D);
+cudaError_t full_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws);
+cudaError_t full_backward(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv, Workspace ws);
 cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws);
 cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv,
                         Workspace ws);

@@ -191,12 +191,14 @@ la_status finish(void* ws, cudaStream_t s, la_error_info* err) {
 
 size_t fwd_floats(const la_problem* p) {
   size_t a = simt_forward_ws_floats(p->groups, p->seq_len, p->dim, p->fault);
-  size_t b = tc_forward_ws_floats(p->groups, p->seq_len, p->dim);
+  size_t b = std::max(tc_forward_ws_floats(p->groups, p->seq_len, p->dim),
+                      full_ws_floats(p->groups, p->seq_len, p->dim));
   return a > b ? a : b;
 }
 size_t bwd_floats(const la_problem* p) {
   size_t a = simt_backward_ws_floats(p->groups, p->seq_len, p->dim, p->fault);
-  size_t b = tc_backward_ws_floats(p->groups, p->seq_len, p->dim);
+  size_t b = std::max(tc_backward_ws_floats(p->groups, p->seq_len, p->dim),
+                      full_ws_floats(p->groups, p->seq_len, p->dim));
   size_t c = (size_t)(p->groups * p->seq_len);  // backward shard state scratch
   size_t m = a > b ? a : b;
   return m > c ? m : c;
@@ -205,8 +207,10 @@ size_t bwd_floats(const la_problem* p) {
 // Head dimensions below 128 on the tensor-core path: zero-pad D to 128 in device
 // scratch (exact: padded key features add nothing to S or z, padded value features
 // are dropped on the way out), run the D = 128 kernels, copy the D columns back.
+// (non-causal D = 64 has its own kernels, la_full.cu)
 bool pad_eligible(const la_problem* p, const la_shard* sh, int lq, int lk, int lv, int lw) {
-  return p->impl != LA_IMPL_SIMT && p->causal && (p->dtype == LA_BF16 || p->dtype == LA_F16) && p->dim < 128 &&
+  return p->impl != LA_IMPL_SIMT && (p->causal || p->dim != 64) && (p->dtype == LA_BF16 || p->dtype == LA_F16) &&
+         p->dim < 128 &&
          p->dim % 8 == 0 && p->fault == LA_FAULT_NONE && p->seq_len % 128 == 0 && sh == nullptr &&
          lq == LA_SEQUENCE_MAJOR && lk == LA_SEQUENCE_MAJOR && lv == LA_FEATURE_MAJOR &&
          (lw < 0 || lw == LA_FEATURE_MAJOR) && p->groups * p->seq_len < (1ll << 31);
@@ -225,8 +229,8 @@ la_problem padded_problem(const la_problem* p) {
 // g = a (i + 1) or a N, so a >= 1e-3 keeps them away from the degenerate threshold.
 bool padn_eligible(const la_problem* p, const la_shard* sh, int lq, int lk, int lv, int lw) {
   const int64_t np = (p->seq_len + 127) / 128 * 128;
-  // D <= 128: tcgen05 (D < 128 through the D padding); non-causal D <= 256: batched GEMMs
-  const bool fast_d = p->dim <= 128 || (!p->causal && p->dim <= 256);
+  // D <= 128: tcgen05 (D < 128 through the D padding); non-causal D = 192, 256: la_full.cu
+  const bool fast_d = p->dim <= 128 || (!p->causal && (p->dim == 192 || p->dim == 256));
   return p->impl != LA_IMPL_SIMT && (p->dtype == LA_BF16 || p->dtype == LA_F16) && p->seq_len % 128 != 0 &&
          fast_d && p->dim % 8 == 0 && p->fault == LA_FAULT_NONE && p->a >= 1e-3 && sh == nullptr &&
          lq == LA_SEQUENCE_MAJOR && lk == LA_SEQUENCE_MAJOR && lv == LA_FEATURE_MAJOR &&
@@ -382,9 +386,9 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
   cudaMemsetAsync(w.flag, 0xFF, sizeof(unsigned long long), L.stream);
   cudaError_t e;
   const bool tc = use_tc(p, tc_forward_supported(L, t));
-  const bool gemm = !tc && p->impl == LA_IMPL_AUTO && gemm_full_supported(L, t);
+  const bool full = !tc && p->impl != LA_IMPL_SIMT && full_tc_supported(L, t);
   if (saved) {
-    if (tc || gemm) {  // causal: prefix states per segment; non-causal: the K/V totals
+    if (tc || full) {  // causal: prefix states per segment; non-causal: the K/V totals
       L.saved_out = (float*)saved;
     } else {  // header only: the backward recomputes its prefix states
       write_saved_header(saved, (double)p->groups, (double)p->seq_len, (double)p->dim, 0, 0, L.stream);
@@ -392,10 +396,11 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
   }
   if (tc)
     e = tc_forward(L, t, out, g, w);
-  else if (gemm)
-    e = gemm_forward_full(L, t, out, g, w);
+  else if (full)
+    e = full_forward(L, t, out, g, w);
   else if (p->impl == LA_IMPL_TCGEN05)
-    return fail(err, LA_ERR_UNSUPPORTED, "tcgen05 path needs bf16/fp16, D=128, canonical layouts");
+    return fail(err, LA_ERR_UNSUPPORTED,
+                "tcgen05 path needs bf16/fp16, canonical layouts, D = 128 (causal) or 64/128/192/256 (non-causal)");
   else
     e = simt_forward(L, t, out, g, w);
   if (e != cudaSuccess) return cuda_fail(err, e);
@@ -483,9 +488,9 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
   Tensors t{q, lq, k, lk, v, lv, o, LA_FEATURE_MAJOR, omega, lw, g};
   Workspace w = carve(ws, ws_bytes);
   const bool tc = use_tc(p, tc_backward_supported(L, t));
-  const bool gemm = !tc && p->impl == LA_IMPL_AUTO && gemm_full_supported(L, t);
+  const bool full = !tc && p->impl != LA_IMPL_SIMT && full_tc_supported(L, t);
   cudaMemsetAsync(w.flag, 0xFF, sizeof(unsigned long long), L.stream);
-  if (saved && (tc || gemm)) {
+  if (saved && (tc || full)) {
     // states from la_forward_save of the same problem: causal -> per-segment prefixes
     // + checkpoints, non-causal -> the K/V totals (header P = -1)
     if (saved_bytes < la_saved_state_bytes(p))
@@ -504,10 +509,11 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
   cudaError_t e;
   if (tc)
     e = tc_backward(L, t, dq, dk, dv, w);
-  else if (gemm)
-    e = gemm_backward_full(L, t, dq, dk, dv);
+  else if (full)
+    e = full_backward(L, t, dq, dk, dv, w);
   else if (p->impl == LA_IMPL_TCGEN05)
-    return fail(err, LA_ERR_UNSUPPORTED, "tcgen05 path needs bf16/fp16, D=128, canonical layouts");
+    return fail(err, LA_ERR_UNSUPPORTED,
+                "tcgen05 path needs bf16/fp16, canonical layouts, D = 128 (causal) or 64/128/192/256 (non-causal)");
   else
     e = simt_backward(L, t, dq, dk, dv, w);
   if (e != cudaSuccess) return cuda_fail(err, e);

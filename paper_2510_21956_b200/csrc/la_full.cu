@@ -1,0 +1,802 @@
+// sm_100a tensor-core non-causal linear attention for head dims D = 64, 192, 256
+// (forward_full / backward_full: forward_kernels.hpp:133-206, backward_kernels.hpp:173-288;
+// D = 128 keeps the kernels of la_sm100.cu / la_sm100_bwd.cu).
+//
+// Without the mask the algebra is two kinds of contraction:
+//   totals over rows  T = X^T Y      k_full_totals: S = K^T V, z = sum k, sigma = sum v (forward)
+//                                                    R = Q^T W_hat, u = Q^T s, c = sum w_hat (backward)
+//   apply per row     Out^T = W Y^T  k_full_apply:  O^T  = (b S)^T Q^T,  o = (O^T + a sigma) / g
+//                                                    dQ^T = (b S) W_hat^T - b z s^T
+//                                                    dK^T = (b R) V^T - b u 1^T
+//                                                    dV^T = (b R)^T K^T + a c 1^T
+// with w_hat_i = omega_i / g_i, s_i = o_i . w_hat_i and g_i = a N + b q_i . z.
+//
+// Layout: every accumulator has the output features on the 128 TMEM lanes (M = 128, in
+// NH = ceil(D / 128) halves; D = 64 and the second half of D = 192 leave lanes unused) and
+// rows on the columns. The constant W (D x D) is built once per CTA from the fp32 totals,
+// converted to bf16 / fp16 and stored in TMEM as the MMA's A operand; the row tiles arrive
+// by TMA (128B swizzle) and serve as the B operand K-major (Q, K: SequenceMajor) or
+// MN-major (V^T, Omega^T: FeatureMajor) without any transpose. Warp roles (192 threads):
+// 0 TMA producer, 1 MMA issuer + TMEM owner, 2-5 CUDA-core work (g, W_hat, s, the
+// vector sums) and the epilogue (TMEM -> registers -> swizzled staging -> TMA store).
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+#include "sm100.cuh"
+#include "tma_host.h"
+
+namespace lab {
+
+using namespace sm100;
+
+namespace {
+
+template <int D>
+struct FG {
+  static constexpr int NH = (D + 127) / 128;     // 128-lane halves of the feature dimension
+  static constexpr int CR = D <= 64 ? 128 : 64;  // rows per chunk (MMA N of the apply pass)
+  static constexpr int KS = D / 16;              // MMA k-steps over the feature dimension
+  static constexpr int T = CR * D * 2;           // one [CR][D] or [D][CR] 16-bit tile
+  static constexpr int64_t SZ = (D * D + 2 * D + 1 + 3) & ~3;  // state_floats(D)
+};
+
+// K-major SW128 tile of `rows` 128-byte rows per 64-element panel: k-step ks.
+__device__ __forceinline__ uint64_t kmaj(uint32_t tile, int ks, uint32_t rows) {
+  return sdesc_sw128(tile, 16, 1024) + (uint64_t)(((ks >> 2) * rows * 128 + (ks & 3) * 32) >> 4);
+}
+// MN-major SW128 tile (K rows of 128 B, 64-element MN panels `panel` bytes apart): k-step ks.
+__device__ __forceinline__ uint64_t mnmaj(uint32_t tile, int ks, uint32_t panel) {
+  return sdesc_sw128(tile, panel, 1024) + (uint64_t)((ks * 2048) >> 4);
+}
+
+template <bool kBF16>
+__device__ __forceinline__ float ld16(const uint8_t* p) {
+  const uint16_t h = *(const uint16_t*)p;
+  return kBF16 ? __bfloat162float(__ushort_as_bfloat16(h)) : __half2float(__ushort_as_half(h));
+}
+template <bool kBF16>
+__device__ __forceinline__ void st16(uint8_t* p, float x) {
+  *(uint16_t*)p = kBF16 ? __bfloat16_as_ushort(__float2bfloat16_rn(x)) : __half_as_ushort(__float2half_rn(x));
+}
+
+// Sum over the 128 CUDA-core threads (4 warps) of per-thread values v[0..n) -> out[0..n):
+// a warp reduce-scatter (lane k ends with the warp sum of value k of each 32-block), then
+// the 4 warp partials through shared memory. `part` holds 4 * n floats.
+template <int kN>
+__device__ __forceinline__ void block_colsum(float (&v)[kN], float* part, float* out, int et) {
+  static_assert(kN % 32 == 0, "multiple of 32 values");
+  const int lane = et & 31, wq = et >> 5;
+#pragma unroll
+  for (int b = 0; b < kN; b += 32) {
+    float* x = v + b;
+    // recursive halving: after the step with offset o, lane keeps the half selected by its bit
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int k = 0; k < o; ++k) {
+        const float send = up ? x[k] : x[k + o];
+        const float keep = up ? x[k + o] : x[k];
+        x[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    // lane now holds the sum of value b + (bit-reversed position) -> x[0]: value index = lane
+    part[wq * kN + b + lane] = x[0];
+  }
+  named_bar(1, 128);
+  for (int i = et; i < kN; i += 128) out[i] = part[i] + part[kN + i] + part[2 * kN + i] + part[3 * kN + i];
+  named_bar(1, 128);
+}
+
+// ================================================================ totals over row units
+struct TotParams {
+  const float* g;   // [G][N] (QW)
+  float* s_out;     // [G][N] s_i (QW), consumed by the dQ apply
+  float* recs;      // [G][U] records
+  int64_t N, unit_rows;
+  int U;
+};
+
+// kQW = false: X = K [rows][D] (SequenceMajor), Y^T = V^T [D][rows]: S[m][j], z, sigma.
+// kQW = true:  X = Q, Y^T = W_hat^T = Omega^T / g (scaled in place), third tile O^T:
+//              R[m][j], u = sum s_i q_i, c = sum w_hat; s_i = o_i . w_hat_i -> s_out.
+template <int D, bool kBF16, bool kQW>
+__global__ void __launch_bounds__(192, 1)
+    k_full_totals(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY,
+                  const __grid_constant__ CUtensorMap tmO, TotParams prm) {
+  using F = FG<D>;
+  constexpr int CR = F::CR, T = F::T, NT = kQW ? 3 : 2;
+  constexpr int STAGE = (NT * T + CR * 4 + 1023) & ~1023;  // tiles + g of the chunk (QW), 1 KB aligned
+  constexpr int NS = (STAGE <= 56 * 1024) ? 3 : 2;
+  constexpr int RPT = (D + 127) / 128;  // feature rows per CUDA-core thread
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  float* ginv = (float*)(smem + NS * STAGE);        // [CR]
+  float* sv = ginv + CR;                            // [CR] s of the chunk
+  float* part = sv + CR;                            // [4][CR]
+  uint64_t* bars = (uint64_t*)(part + 4 * CR);
+  uint64_t* full = bars;            // [NS]
+  uint64_t* empty = bars + 4;       // [NS]
+  uint64_t* wready = bars + 8;      // [NS] (QW: W_hat^T written)
+  uint64_t* done = bars + 12;
+  uint32_t* tslot = (uint32_t*)(bars + 14);
+
+  const int u = blockIdx.x;
+  const int64_t grp = blockIdx.y;
+  const int64_t r0 = (int64_t)u * prm.unit_rows;
+  const int64_t r1 = lmin(prm.N, r0 + prm.unit_rows);
+  const int nc = r1 > r0 ? (int)((r1 - r0) / CR) : 0;
+  const uint32_t warp = warp_id();
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&tmX);
+    tma_prefetch(&tmY);
+    if (kQW) tma_prefetch(&tmO);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1 + 128);
+      mbar_init(&wready[s], 128);
+    }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int c = 0; c < nc; ++c) {
+        const int s = c % NS;
+        if (c >= NS) mbar_wait(&empty[s], ((c / NS) & 1) ^ 1);
+        const int64_t row0 = r0 + (int64_t)c * CR;
+        uint8_t* st = smem + s * STAGE;
+        mbar_expect_tx(&full[s], NT * T + (kQW ? CR * 4 : 0));
+        tma_load_3d(st, &tmX, &full[s], 0, (int)(grp * prm.N + row0), 0);
+        tma_load_3d(st + T, &tmY, &full[s], 0, (int)(grp * D), (int)(row0 / 64));
+        if (kQW) {
+          tma_load_3d(st + 2 * T, &tmO, &full[s], 0, (int)(grp * D), (int)(row0 / 64));
+          bulk_load(st + NT * T, prm.g + grp * prm.N + row0, CR * 4, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // T[m][j] (+)= sum_rows X[i][m] Y[i][j]: A = X^T (MN-major over m), B = Y (K-major: the
+    // Y^T tile's rows are j with the rows i contiguous); one M = 128 accumulator per half of m
+    constexpr uint32_t fmt = kBF16 ? 1 : 0;
+    const uint32_t id_T = idesc_f16(128, D, fmt, 1, 0);
+    for (int c = 0; c < nc; ++c) {
+      const int s = c % NS;
+      const uint32_t aX = smem_u32(smem + s * STAGE), aY = aX + T;
+      mbar_wait(&full[s], (c / NS) & 1);
+      if (kQW) mbar_wait(&wready[s], (c / NS) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int h = 0; h < F::NH; ++h)
+          for (int ks = 0; ks < CR / 16; ++ks)
+            mma_ss(tmem + h * 256, mnmaj(aX + h * 2 * CR * 128, ks, CR * 128), kmaj(aY, ks, D), id_T,
+                   (c > 0 || ks > 0) ? 1u : 0u);
+        mma_commit(&empty[s]);
+        if (c == nc - 1) mma_commit(done);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ CUDA cores (128 threads)
+    const int et = (int)threadIdx.x - 64;
+    const uint32_t qd = warp & 3;
+    const int r = (int)(qd * 32 + lane_id());  // TMEM lane of this thread's warp quadrant
+    // thread et owns feature rows f = et + 128 q (q < RPT) for the row-wise sums, and the
+    // feature columns m = et + 128 q for the column-wise ones
+    float va[RPT], vb[RPT];  // z or u (columns m) ; sigma or c (rows j)
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) va[q] = vb[q] = 0.f;
+    for (int c = 0; c < nc; ++c) {
+      const int s = c % NS;
+      uint8_t* st = smem + s * STAGE;
+      mbar_wait(&full[s], (c / NS) & 1);
+      const uint8_t* xt = st;  // [CR][D] K-major panels of CR rows
+      uint8_t* yt = st + T;    // [D][CR] panels of D rows (64 row-elements each)
+      if (kQW) {
+        const float* gg = (const float*)(st + NT * T);
+        if (et < CR) ginv[et] = 1.f / gg[et];
+        named_bar(1, 128);
+        // W_hat^T = Omega^T / g in place; c_j += w_hat; s_i = sum_j o_ij w_hat_ij, 32
+        // columns at a time (bounded registers)
+        const uint8_t* ot = st + 2 * T;
+#pragma unroll 1
+        for (int ib = 0; ib < CR; ib += 32) {
+          float ps[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) ps[i] = 0.f;
+#pragma unroll
+          for (int q = 0; q < RPT; ++q) {
+            const int f = et + 128 * q;
+            if (f < D) {
+#pragma unroll
+              for (int i8 = 0; i8 < 32; i8 += 8) {
+                const uint32_t off = sw128_off(f, ib + i8, D);
+                uint4 w4 = *(const uint4*)(yt + off);
+                const uint4 o4 = *(const uint4*)(ot + off);
+                uint32_t* wp = (uint32_t*)&w4;
+                const uint32_t* op = (const uint32_t*)&o4;
+#pragma unroll
+                for (int h2 = 0; h2 < 4; ++h2) {
+                  const float2 w2 = unpack2<kBF16>(wp[h2]), o2 = unpack2<kBF16>(op[h2]);
+                  const int i = i8 + 2 * h2;
+                  const float w0 = w2.x * ginv[ib + i], w1 = w2.y * ginv[ib + i + 1];
+                  vb[q] += w0 + w1;
+                  ps[i] += o2.x * w0;
+                  ps[i + 1] += o2.y * w1;
+                  wp[h2] = pack2<kBF16>(w0, w1);
+                }
+                *(uint4*)(yt + off) = w4;
+              }
+            }
+          }
+          block_colsum<32>(ps, part, sv + ib, et);
+        }
+        fence_proxy_async();
+        mbar_arrive(&wready[s]);
+        if (et < CR) prm.s_out[grp * prm.N + r0 + (int64_t)c * CR + et] = sv[et];
+        // u_m += sum_i s_i q_im (column m of the Q tile)
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+          const int m = et + 128 * q;
+          if (m < D) {
+            float acc = 0.f;
+#pragma unroll 8
+            for (int i = 0; i < CR; ++i) acc += sv[i] * ld16<kBF16>(xt + sw128_off(i, m, CR));
+            va[q] += acc;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+          const int f = et + 128 * q;
+          if (f < D) {
+            float zs = 0.f, ss = 0.f;
+#pragma unroll 8
+            for (int i = 0; i < CR; ++i) zs += ld16<kBF16>(xt + sw128_off(i, f, CR));  // z_m: column of K
+#pragma unroll
+            for (int i8 = 0; i8 < CR; i8 += 8) {  // sigma_j: row of V^T
+              const uint4 v4 = *(const uint4*)(yt + sw128_off(f, i8, D));
+              const uint32_t* vp = (const uint32_t*)&v4;
+#pragma unroll
+              for (int h2 = 0; h2 < 4; ++h2) {
+                const float2 v2 = unpack2<kBF16>(vp[h2]);
+                ss += v2.x + v2.y;
+              }
+            }
+            va[q] += zs;
+            vb[q] += ss;
+          }
+        }
+      }
+      mbar_arrive(&empty[s]);
+    }
+    // ---- the unit's record: X[m][j] (lanes m), vA (z | u), vB (sigma | c), rows
+    float* rec = prm.recs + (grp * prm.U + u) * F::SZ;
+    if (nc > 0) {
+      mbar_wait(done, 0);
+      tc_fence_after();
+#pragma unroll 1
+      for (int h = 0; h < F::NH; ++h) {
+        const int m = 128 * h + r;
+#pragma unroll 1
+        for (int j0 = 0; j0 < D; j0 += 32) {
+          uint32_t x[32];
+          tmem_ld32(tmem + ((qd * 32u) << 16) + h * 256 + j0, x);
+          tmem_ld_wait();
+          if (m < D) {
+#pragma unroll
+            for (int k = 0; k < 32; k += 4)
+              *(float4*)(rec + (int64_t)m * D + j0 + k) =
+                  make_float4(__uint_as_float(x[k]), __uint_as_float(x[k + 1]), __uint_as_float(x[k + 2]),
+                              __uint_as_float(x[k + 3]));
+          }
+        }
+      }
+    } else {
+      for (int e = et; e < D * D; e += 128) rec[e] = 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int f = et + 128 * q;
+      if (f < D) {
+        rec[D * D + f] = va[q];
+        rec[D * D + D + f] = vb[q];
+      }
+    }
+    if (et == 0) rec[D * D + 2 * D] = (float)(r1 > r0 ? r1 - r0 : 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// Per-group totals: tot[g] = sum_u recs[g][u] (elements D*D + 2D + 1; padding zero).
+__global__ void k_full_sum(const float* recs, int U, int64_t SZ, int64_t used, float* tot) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t grp = blockIdx.y;
+  if (e >= SZ) return;
+  float acc = 0.f;
+  if (e < used)
+    for (int u = 0; u < U; ++u) acc += recs[(grp * U + u) * SZ + e];
+  tot[grp * SZ + e] = acc;
+}
+
+// ================================================================ apply passes
+enum ApplyMode { kFwd = 0, kDQ = 1, kDK = 2, kDV = 3 };
+
+struct ApplyParams {
+  const float* tot;     // per-group fp32 totals record: S (kFwd, kDQ) or R (kDK, kDV)
+  const float* totS;    // kDQ: z comes from the S record (same as tot); kFwd: S record
+  const float* g;       // [G][N]: kDQ (w_hat = omega / g)
+  const float* s;       // [G][N]: kDQ
+  float* gout;          // kFwd: g_i
+  unsigned long long* flag;
+  int64_t N, n_total, seg_len;
+  float a, b;
+};
+
+// Out^T = W Y^T per chunk of CR rows, W = the constant D x D operand in TMEM:
+//   kFwd: W[j][m] = b S[m][j],  Y = Q  (K-major),          o^T = (acc + a sigma_j) / g_i
+//   kDQ:  W[m][j] = b S[m][j],  Y^T = Omega^T / g (MN-major), dQ = acc - b z_m s_i (transposed store)
+//   kDK:  W[m][j] = b R[m][j],  Y^T = V^T (MN-major),       dK^T = acc - b u_m
+//   kDV:  W[j][m] = b R[m][j],  Y = K (K-major),            dV^T = acc + a c_j
+template <int D, bool kBF16, int kMode>
+__global__ void __launch_bounds__(192, 1)
+    k_full_apply(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmOut,
+                 ApplyParams prm) {
+  using F = FG<D>;
+  constexpr int CR = F::CR, T = F::T, NH = F::NH;
+  constexpr bool kSeqIn = kMode == kFwd || kMode == kDV;  // Y tile [CR][D] (else [D][CR])
+  constexpr bool kPre = kMode == kFwd || kMode == kDQ;    // CUDA-core pass over the tile first
+  constexpr int STAGE = (T + (kMode == kDQ ? 2 * CR * 4 : 0) + 1023) & ~1023;  // + g, s of the chunk
+  constexpr int NS = 3;
+  constexpr int RPT = (D + 127) / 128;
+  constexpr uint32_t kAcc = 256;  // accumulators: [256, 512) = 2 buffers x NH halves x CR columns
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* stg = smem + NS * STAGE;              // [2][T] output staging
+  float* zf = (float*)(stg + 2 * T);             // [D] z (kFwd)
+  float* ginv = zf + D;                          // [2][CR] 1 / g_i (kFwd, kDQ)
+  float* sbuf = ginv + 2 * CR;                   // [2][CR] s_i (kDQ)
+  float* part = sbuf + 2 * CR;                   // [4][CR] (kFwd: partial q.z)
+  uint64_t* bars = (uint64_t*)(part + 4 * CR);
+  uint64_t* full = bars;        // [NS]
+  uint64_t* empty = bars + 4;   // [NS]
+  uint64_t* pre = bars + 8;     // [NS] CUDA-core pass done (kDQ: W_hat^T ready)
+  uint64_t* acc_full = bars + 12;   // [2]
+  uint64_t* acc_empty = bars + 14;  // [2]
+  uint32_t* tslot = (uint32_t*)(bars + 16);
+
+  const int p = blockIdx.x;
+  const int64_t grp = blockIdx.y;
+  const int64_t s0 = (int64_t)p * prm.seg_len;
+  const int64_t s1 = lmin(prm.N, s0 + prm.seg_len);
+  const int nc = s1 > s0 ? (int)((s1 - s0) / CR) : 0;
+  const uint32_t warp = warp_id();
+  const float* tot = prm.tot + grp * F::SZ;
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&tmY);
+    tma_prefetch(&tmOut);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1 + (kPre ? 128 : 0));
+      mbar_init(&pre[s], 128);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const int et = (int)threadIdx.x - 64;
+  const uint32_t qd = warp & 3;
+  const int r = (int)(qd * 32 + lane_id());
+  const uint32_t lb = (qd * 32u) << 16;
+  if (warp >= 2) {
+    // W (bf16 / fp16) into TMEM columns [h * D / 2, (h + 1) * D / 2): lane = output feature
+    // f = 128 h + r, column c = input features (2c, 2c + 1)
+    constexpr bool kTrans = kMode == kFwd || kMode == kDV;  // W[f][k] = b X[k][f]
+    const float b = prm.b;
+#pragma unroll 1
+    for (int h = 0; h < NH; ++h) {
+      const int f = 128 * h + r;
+#pragma unroll 1
+      for (int k0 = 0; k0 < D; k0 += 64) {
+        uint32_t pk[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          float w0 = 0.f, w1 = 0.f;
+          if (f < D) {
+            const int k = k0 + 2 * c;
+            w0 = b * (kTrans ? tot[(int64_t)k * D + f] : tot[(int64_t)f * D + k]);
+            w1 = b * (kTrans ? tot[(int64_t)(k + 1) * D + f] : tot[(int64_t)f * D + k + 1]);
+          }
+          pk[c] = pack2<kBF16>(w0, w1);
+        }
+        tmem_st32(tmem + lb + h * (D / 2) + k0 / 2, pk);
+      }
+    }
+    tmem_st_wait();
+    if (kMode == kFwd)
+      for (int m = et; m < D; m += 128) zf[m] = tot[D * D + m];
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int c = 0; c < nc; ++c) {
+        const int s = c % NS;
+        if (c >= NS) mbar_wait(&empty[s], ((c / NS) & 1) ^ 1);
+        const int64_t row0 = s0 + (int64_t)c * CR;
+        uint8_t* st = smem + s * STAGE;
+        mbar_expect_tx(&full[s], T + (kMode == kDQ ? 2 * CR * 4 : 0));
+        if (kSeqIn)
+          tma_load_3d(st, &tmY, &full[s], 0, (int)(grp * prm.N + row0), 0);
+        else
+          tma_load_3d(st, &tmY, &full[s], 0, (int)(grp * D), (int)(row0 / 64));
+        if (kMode == kDQ) {
+          bulk_load(st + T, prm.g + grp * prm.N + row0, CR * 4, &full[s]);
+          bulk_load(st + T + CR * 4, prm.s + grp * prm.N + row0, CR * 4, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t fmt = kBF16 ? 1 : 0;
+    const uint32_t id = idesc_f16(128, CR, fmt, 0, kSeqIn ? 0 : 1);
+    for (int c = 0; c < nc; ++c) {
+      const int s = c % NS, bb = c & 1;
+      const uint32_t aY = smem_u32(smem + s * STAGE);
+      mbar_wait(&full[s], (c / NS) & 1);
+      if (kMode == kDQ) mbar_wait(&pre[s], (c / NS) & 1);
+      if (c >= 2) mbar_wait(&acc_empty[bb], ((c - 2) >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+          for (int ks = 0; ks < F::KS; ++ks)
+            mma_ts(tmem + kAcc + (bb * NH + h) * CR, tmem + h * (D / 2) + ks * 8,
+                   kSeqIn ? kmaj(aY, ks, CR) : mnmaj(aY, ks, D * 128), id, ks > 0);
+        mma_commit(&acc_full[bb]);
+        mma_commit(&empty[s]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ CUDA cores + epilogue
+    const float a = prm.a, b = prm.b;
+    float bias[RPT];  // per output feature of this thread's lanes: a sigma_j, -b u_m, a c_j, b z_m
+#pragma unroll
+    for (int h = 0; h < RPT; ++h) {
+      const int f = 128 * h + r;
+      float x = 0.f;
+      if (f < D) {
+        if (kMode == kFwd) x = a * tot[D * D + D + f];
+        if (kMode == kDK) x = -b * tot[D * D + f];
+        if (kMode == kDV) x = a * tot[D * D + D + f];
+        if (kMode == kDQ) x = b * tot[D * D + f];
+      }
+      bias[h] = x;
+    }
+    // pass over chunk c's tile before its MMA / epilogue
+    auto pre_pass = [&](int c) {
+      const int s = c % NS;
+      uint8_t* st = smem + s * STAGE;
+      mbar_wait(&full[s], (c / NS) & 1);
+      const int64_t row0 = s0 + (int64_t)c * CR;
+      if (kMode == kFwd) {  // g_i = a N + b q_i . z; 128 / CR threads per row
+        constexpr int TPR = 128 / CR;
+        const int i = et / TPR, part_k = et % TPR;
+        float acc = 0.f;
+#pragma unroll
+        for (int m8 = part_k * (D / TPR); m8 < (part_k + 1) * (D / TPR); m8 += 8) {
+          const uint4 q4 = *(const uint4*)(st + sw128_off(i, m8, CR));
+          const uint32_t* qp = (const uint32_t*)&q4;
+#pragma unroll
+          for (int h2 = 0; h2 < 4; ++h2) {
+            const float2 q2 = unpack2<kBF16>(qp[h2]);
+            acc += q2.x * zf[m8 + 2 * h2] + q2.y * zf[m8 + 2 * h2 + 1];
+          }
+        }
+#pragma unroll
+        for (int o = 1; o < TPR; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (part_k == 0) {
+          const float gi = a * (float)prm.n_total + b * acc;
+          if (fabsf(gi) < kEpsF32) flag_degenerate(prm.flag, grp, row0 + i);
+          ginv[(c & 1) * CR + i] = 1.f / gi;
+          prm.gout[grp * prm.N + row0 + i] = gi;
+        }
+        mbar_arrive(&empty[s]);  // Q tile no longer read by the CUDA cores
+      } else {  // kDQ: W_hat^T = Omega^T / g in place; keep 1/g, s for the epilogue
+        const float* gg = (const float*)(st + T);
+        const float* ss = gg + CR;
+        if (et < CR) {
+          ginv[(c & 1) * CR + et] = 1.f / gg[et];
+          sbuf[(c & 1) * CR + et] = ss[et];
+        }
+        named_bar(1, 128);
+        const float* gi = ginv + (c & 1) * CR;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+          const int f = et + 128 * q;
+          if (f < D) {
+#pragma unroll
+            for (int i8 = 0; i8 < CR; i8 += 8) {
+              const uint32_t off = sw128_off(f, i8, D);
+              uint4 w4 = *(const uint4*)(st + off);
+              uint32_t* wp = (uint32_t*)&w4;
+#pragma unroll
+              for (int h2 = 0; h2 < 4; ++h2) {
+                const float2 w2 = unpack2<kBF16>(wp[h2]);
+                wp[h2] = pack2<kBF16>(w2.x * gi[i8 + 2 * h2], w2.y * gi[i8 + 2 * h2 + 1]);
+              }
+              *(uint4*)(st + off) = w4;
+            }
+          }
+        }
+        fence_proxy_async();
+        mbar_arrive(&pre[s]);
+        mbar_arrive(&empty[s]);
+      }
+    };
+    auto epilogue = [&](int c) {
+      const int bb = c & 1;
+      const int64_t row0 = s0 + (int64_t)c * CR;
+      mbar_wait(&acc_full[bb], (c >> 1) & 1);
+      tc_fence_after();
+      if (et == 0) tma_store_wait_read1();  // the store that used staging bb two chunks ago
+      named_bar(1, 128);
+      uint8_t* so = stg + bb * T;
+#pragma unroll 1
+      for (int h = 0; h < NH; ++h) {
+        const int f = 128 * h + r;
+        const float bh = h == 0 ? bias[0] : bias[RPT - 1];
+#pragma unroll 1
+        for (int c0 = 0; c0 < CR; c0 += 32) {
+          uint32_t x[32];
+          tmem_ld32(tmem + lb + kAcc + (bb * NH + h) * CR + c0, x);
+          tmem_ld_wait();
+          if (f < D) {
+            if (kMode == kDQ) {  // dQ[i][f]: SequenceMajor staging [CR][D]
+              const float* sv = sbuf + bb * CR + c0;
+#pragma unroll
+              for (int k = 0; k < 32; ++k)
+                st16<kBF16>(so + sw128_off(c0 + k, f, CR), __uint_as_float(x[k]) - bh * sv[k]);
+            } else {  // FeatureMajor staging [D][CR]: row f
+              const float* gv = ginv + bb * CR + c0;
+#pragma unroll
+              for (int k8 = 0; k8 < 32; k8 += 8) {
+                uint32_t pk[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  float v0 = __uint_as_float(x[k8 + 2 * q]) + bh;
+                  float v1 = __uint_as_float(x[k8 + 2 * q + 1]) + bh;
+                  if (kMode == kFwd) {
+                    v0 *= gv[k8 + 2 * q];
+                    v1 *= gv[k8 + 2 * q + 1];
+                  }
+                  pk[q] = pack2<kBF16>(v0, v1);
+                }
+                *(uint4*)(so + sw128_off(f, c0 + k8, D)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[bb]);
+      fence_proxy_async();
+      named_bar(1, 128);
+      if (et == 0) {
+        if (kMode == kDQ)
+          tma_store_3d(&tmOut, so, 0, (int)(grp * prm.N + row0), 0);
+        else
+          tma_store_3d(&tmOut, so, 0, (int)(grp * D), (int)(row0 / 64));
+        tma_store_commit();
+      }
+    };
+    for (int c = 0; c <= nc; ++c) {
+      if (kPre && c < nc) pre_pass(c);
+      if (c >= 1) epilogue(c - 1);
+    }
+    if (et == 0) tma_store_wait0();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+template <int D>
+constexpr size_t totals_smem(bool qw) {
+  using F = FG<D>;
+  const int stage = ((qw ? 3 : 2) * F::T + F::CR * 4 + 1023) & ~1023;
+  const int ns = stage <= 56 * 1024 ? 3 : 2;
+  return (size_t)ns * stage + 6 * F::CR * 4 + 16 * 8 + 1024;
+}
+template <int D>
+constexpr size_t apply_smem(int mode) {
+  using F = FG<D>;
+  const int stage = (F::T + (mode == kDQ ? 2 * F::CR * 4 : 0) + 1023) & ~1023;
+  return (size_t)3 * stage + 2 * F::T + (D + 8 * F::CR) * 4 + 17 * 8 + 1024;
+}
+
+// geometry of the totals units and the apply segments
+template <int D>
+struct Plan {
+  int U;
+  int64_t unit_rows;
+  int P;
+  int64_t seg_rows;
+  Plan(int64_t G, int64_t N) {
+    const int64_t CR = FG<D>::CR, chunks = std::max<int64_t>(1, N / CR);  // sizing queries: any N
+    int64_t u = std::max<int64_t>(1, std::min<int64_t>(chunks, (2 * 148 + G - 1) / G));
+    unit_rows = ((chunks + u - 1) / u) * CR;
+    U = (int)((N + unit_rows - 1) / unit_rows);
+    int64_t p2 = std::max<int64_t>(1, std::min<int64_t>(chunks, (4 * 148 + G / 2) / G));
+    if (tuning().full_ctas_fwd > 0) p2 = std::min<int64_t>(chunks, tuning().full_ctas_fwd);
+    seg_rows = ((chunks + p2 - 1) / p2) * CR;
+    P = (int)((N + seg_rows - 1) / seg_rows);
+  }
+};
+
+bool maps_seq(CUtensorMap* m, const void* base, bool bf, int64_t G, int64_t N, int D, int CR) {
+  return make_tma_map(m, base, bf, (uint64_t)(G * N), (uint64_t)D, (uint32_t)CR, (uint32_t)(D / 64));
+}
+bool maps_feat(CUtensorMap* m, const void* base, bool bf, int64_t G, int64_t N, int D, int CR) {
+  return make_tma_map(m, base, bf, (uint64_t)(G * D), (uint64_t)N, (uint32_t)D, (uint32_t)(CR / 64));
+}
+
+template <int D, bool kBF16>
+cudaError_t totals(const Launch& L, const Tensors& t, bool qw, float* units, float* tot, float* s_out) {
+  using F = FG<D>;
+  const Plan<D> pl(L.G, L.N);
+  CUtensorMap mX, mY, mO;
+  const void* x = qw ? t.q : t.k;
+  const void* y = qw ? t.w : t.v;
+  if (!maps_seq(&mX, x, kBF16, L.G, L.N, D, F::CR) || !maps_feat(&mY, y, kBF16, L.G, L.N, D, F::CR) ||
+      !maps_feat(&mO, qw ? t.o : t.v, kBF16, L.G, L.N, D, F::CR))
+    return cudaErrorInvalidValue;
+  TotParams prm{t.g, s_out, units, L.N, pl.unit_rows, pl.U};
+  const size_t smem = totals_smem<D>(qw);
+  const dim3 grid((unsigned)pl.U, (unsigned)L.G);
+  if (qw) {
+    auto k = k_full_totals<D, kBF16, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ProfScope ps("la_full_totals_r", L.stream);
+    k<<<grid, 192, smem, L.stream>>>(mX, mY, mO, prm);
+  } else {
+    auto k = k_full_totals<D, kBF16, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ProfScope ps("la_full_totals_s", L.stream);
+    k<<<grid, 192, smem, L.stream>>>(mX, mY, mO, prm);
+  }
+  k_full_sum<<<dim3((unsigned)((F::SZ + 255) / 256), (unsigned)L.G), 256, 0, L.stream>>>(
+      units, pl.U, F::SZ, (int64_t)D * D + 2 * D + 1, tot);
+  note_launch(2);
+  return cudaGetLastError();
+}
+
+template <int D, bool kBF16, int kMode>
+cudaError_t apply(const Launch& L, const CUtensorMap& mY, const CUtensorMap& mOut, const ApplyParams& prm,
+                  const char* name) {
+  const Plan<D> pl(L.G, L.N);
+  auto k = k_full_apply<D, kBF16, kMode>;
+  const size_t smem = apply_smem<D>(kMode);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    ProfScope ps(name, L.stream);
+    k<<<dim3((unsigned)pl.P, (unsigned)L.G), 192, smem, L.stream>>>(mY, mOut, prm);
+  }
+  note_launch(1);
+  return cudaGetLastError();
+}
+
+template <int D, bool kBF16>
+cudaError_t forward_d(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws) {
+  using F = FG<D>;
+  const Plan<D> pl(L.G, L.N);
+  float* units = ws.base;
+  // with a saved-state buffer the totals land there (header P = -1 marks "totals") and the
+  // backward reuses them instead of re-reading K and V
+  float* tot = L.saved_out ? L.saved_out + kSavedHeader : units + L.G * pl.U * F::SZ;
+  if (L.saved_out) write_saved_header(L.saved_out, (double)L.G, (double)L.N, (double)D, -1, 0, L.stream);
+  cudaError_t e = totals<D, kBF16>(L, t, false, units, tot, nullptr);
+  if (e != cudaSuccess) return e;
+  CUtensorMap mQ, mO;
+  if (!maps_seq(&mQ, t.q, kBF16, L.G, L.N, D, F::CR) || !maps_feat(&mO, out, kBF16, L.G, L.N, D, F::CR))
+    return cudaErrorInvalidValue;
+  ApplyParams prm{tot, tot, nullptr, nullptr, g, ws.flag, L.N, L.n_total > 0 ? L.n_total : L.N, pl.seg_rows,
+                  L.a, L.b};
+  return apply<D, kBF16, kFwd>(L, mQ, mO, prm, "la_full_fwd");
+}
+
+template <int D, bool kBF16>
+cudaError_t backward_d(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv, Workspace ws) {
+  using F = FG<D>;
+  const Plan<D> pl(L.G, L.N);
+  float* units = ws.base;                         // [G][U] records (S, then R)
+  float* totR = units + L.G * pl.U * F::SZ;       // [G]
+  float* totS = totR + L.G * F::SZ;               // [G] (when not saved)
+  float* s = totS + L.G * F::SZ;                  // [G][N]
+  cudaError_t e = cudaSuccess;
+  if (L.saved_in)
+    totS = const_cast<float*>(L.saved_in) + kSavedHeader;
+  else
+    e = totals<D, kBF16>(L, t, false, units, totS, nullptr);
+  if (e != cudaSuccess) return e;
+  e = totals<D, kBF16>(L, t, true, units, totR, s);
+  if (e != cudaSuccess) return e;
+  CUtensorMap mW, mV, mK, mdQ, mdK, mdV;
+  if (!maps_feat(&mW, t.w, kBF16, L.G, L.N, D, F::CR) || !maps_feat(&mV, t.v, kBF16, L.G, L.N, D, F::CR) ||
+      !maps_seq(&mK, t.k, kBF16, L.G, L.N, D, F::CR) || !maps_seq(&mdQ, dq, kBF16, L.G, L.N, D, F::CR) ||
+      !maps_feat(&mdK, dk, kBF16, L.G, L.N, D, F::CR) || !maps_feat(&mdV, dv, kBF16, L.G, L.N, D, F::CR))
+    return cudaErrorInvalidValue;
+  ApplyParams pq{totS, totS, t.g, s, nullptr, nullptr, L.N, L.N, pl.seg_rows, L.a, L.b};
+  if ((e = apply<D, kBF16, kDQ>(L, mW, mdQ, pq, "la_full_dq")) != cudaSuccess) return e;
+  ApplyParams pr{totR, totR, nullptr, nullptr, nullptr, nullptr, L.N, L.N, pl.seg_rows, L.a, L.b};
+  if ((e = apply<D, kBF16, kDK>(L, mV, mdK, pr, "la_full_dk")) != cudaSuccess) return e;
+  return apply<D, kBF16, kDV>(L, mK, mdV, pr, "la_full_dv");
+}
+
+template <int D>
+size_t ws_floats_d(int64_t G, int64_t N) {
+  const Plan<D> pl(G, N);
+  return (size_t)(G * pl.U * FG<D>::SZ + 2 * G * FG<D>::SZ + G * N);
+}
+
+}  // namespace
+
+bool full_tc_supported(const Launch& L, const Tensors& t) {
+  const int64_t cr = L.D <= 64 ? 128 : 64;
+  return !L.causal && (L.dtype == LA_BF16 || L.dtype == LA_F16) && (L.D == 64 || L.D == 192 || L.D == 256) &&
+         L.fault == LA_FAULT_NONE && L.carry_prefix == nullptr && L.carry_suffix == nullptr && L.row_offset == 0 &&
+         L.N % cr == 0 && t.lq == LA_SEQUENCE_MAJOR && t.lk == LA_SEQUENCE_MAJOR && t.lv == LA_FEATURE_MAJOR &&
+         (t.w == nullptr || t.lw == LA_FEATURE_MAJOR) && L.G * L.N < (1ll << 31) && L.G * L.D < (1ll << 31);
+}
+
+size_t full_ws_floats(int64_t G, int64_t N, int64_t D) {
+  switch (D) {
+    case 64: return ws_floats_d<64>(G, N);
+    case 192: return ws_floats_d<192>(G, N);
+    case 256: return ws_floats_d<256>(G, N);
+  }
+  return 0;
+}
+
+cudaError_t full_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws) {
+  const bool bf = L.dtype == LA_BF16;
+  switch (L.D) {
+    case 64: return bf ? forward_d<64, true>(L, t, out, g, ws) : forward_d<64, false>(L, t, out, g, ws);
+    case 192: return bf ? forward_d<192, true>(L, t, out, g, ws) : forward_d<192, false>(L, t, out, g, ws);
+    case 256: return bf ? forward_d<256, true>(L, t, out, g, ws) : forward_d<256, false>(L, t, out, g, ws);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t full_backward(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv, Workspace ws) {
+  const bool bf = L.dtype == LA_BF16;
+  switch (L.D) {
+    case 64: return bf ? backward_d<64, true>(L, t, dq, dk, dv, ws) : backward_d<64, false>(L, t, dq, dk, dv, ws);
+    case 192:
+      return bf ? backward_d<192, true>(L, t, dq, dk, dv, ws) : backward_d<192, false>(L, t, dq, dk, dv, ws);
+    case 256:
+      return bf ? backward_d<256, true>(L, t, dq, dk, dv, ws) : backward_d<256, false>(L, t, dq, dk, dv, ws);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace lab

@@ -938,7 +938,7 @@ static cudaError_t tc_forward_full(const Launch& L, const Tensors& t, void* out,
 }
 
 size_t tc_saved_floats(int64_t G, int64_t N, int64_t D) {
-  if (D != kD && D <= 256) return (size_t)(kSavedHeader + G * state_floats(D));  // la_gemm.cu: K/V totals
+  if (D != kD && D <= 256) return (size_t)(kSavedHeader + G * state_floats(D));  // la_full.cu: K/V totals
   if (D != kD || N % kC) return kSavedHeader;
   return (size_t)(kSavedHeader + G * (tc_segments(G, N) + ck_count(N)) * state_floats(kD));
 }

@@ -177,8 +177,8 @@ def test_bf16_causal_d128_parity(cuda, impl):
 
 @pytest.mark.parametrize("D", [32, 64, 96, 128, 192, 256])
 def test_bf16_noncausal_head_dim_sweep(cuda, D):
-    # BASELINE config 4 shape family (non-causal, D sweep) at reduced N; D != 128 runs
-    # the batched-GEMM path (la_gemm.cu), D = 128 the tcgen05 kernels
+    # BASELINE config 4 shape family (non-causal, D sweep) at reduced N; D = 64 / 192 / 256
+    # run la_full.cu, D = 128 the la_sm100 kernels, D = 32 / 96 those on a zero-padded copy
     q, k, v, w = fast_inputs(2, 2048, D, seed=D)
     res = run_dev(q, k, v, w, "bf16", cuda, causal=False)
     ref = oracle_all(res, False)
@@ -187,9 +187,10 @@ def test_bf16_noncausal_head_dim_sweep(cuda, D):
     assert rel_err(res["g"], ref["g"]) <= 1e-3
 
 
-@pytest.mark.parametrize("D,a,b", [(256, 1.0, 1.0), (64, 0.5, 2.0)])
-def test_noncausal_gemm_path_runs_and_matches(cuda, D, a, b):
-    """The non-causal D != 128 path is the batched-GEMM one (profile scopes), fp16 too."""
+@pytest.mark.parametrize("D,a,b", [(256, 1.0, 1.0), (64, 0.5, 2.0), (192, 2.0, 0.25)])
+def test_noncausal_full_tc_path_runs_and_matches(cuda, D, a, b):
+    """Non-causal D = 64 / 192 / 256 runs the tcgen05 kernels of la_full.cu (profile scopes:
+    totals, forward apply, dQ / dK / dV applies), fp16 here, unequal coefficients."""
     from paper_2510_21956_b200 import _abi
     q, k, v, w = fast_inputs(3, 1024, D, seed=D + 1)
     L = _abi.lib()
@@ -198,7 +199,8 @@ def test_noncausal_gemm_path_runs_and_matches(cuda, D, a, b):
     res = run_dev(q, k, v, w, "f16", cuda, causal=False, a=a, b=b)
     names = {r["name"] for r in _abi.profile_read()}
     L.la_profile_enable(0)
-    assert {"la_gemm_fwd_full", "la_gemm_bwd_full"} <= names, names
+    assert {"la_full_totals_s", "la_full_totals_r", "la_full_fwd", "la_full_dq", "la_full_dk",
+            "la_full_dv"} <= names, names
     ref = oracle_all(res, False, a=a, b=b)
     for key in ("out", "dq", "dk", "dv"):
         assert max_abs(res[key], ref[key]) <= BF16_ABS, (D, key)
@@ -363,20 +365,23 @@ def test_bf16_small_head_dim_padded_tcgen05(cuda, causal, D):
     assert rel_err(res["g"], ref["g"]) <= 1e-3
 
 
-@pytest.mark.parametrize("causal", [True, False])
-def test_f16_key_sum_beyond_half_range(cuda, causal):
+@pytest.mark.parametrize("causal,D", [(True, 128), (False, 128), (False, 64), (False, 256)])
+def test_f16_key_sum_beyond_half_range(cuda, causal, D):
     # every key is e_0, so z_0 = N = 131072 > 65504 (the fp16 maximum): the q.z term
-    # must not overflow on the fp16 tensor-core path
-    G, N, D = 1, 131072, 128
+    # must not overflow on the fp16 tensor-core paths (la_sm100 D = 128, la_full D = 64 / 256)
+    G, N = 1, 131072
     rng = np.random.default_rng(11)
     q = O.normalize_rows(rng.uniform(-1, 1, (G, N, D)))
     k = np.zeros((G, N, D))
     k[..., 0] = 1.0
     v = rng.uniform(-1, 1, (G, N, D))
-    res = run_dev(q, k, v, None, "f16", cuda, causal=causal)
+    w = rng.uniform(-1, 1, (G, N, D))
+    res = run_dev(q, k, v, w, "f16", cuda, causal=causal)
     ref = oracle_all(res, causal, dtype=np.float32)
-    assert np.isfinite(res["out"]).all() and np.isfinite(res["g"]).all()
-    assert max_abs(res["out"], ref["out"]) <= BF16_ABS
+    for key in ("out", "g", "dq", "dk", "dv"):
+        assert np.isfinite(res[key]).all(), key
+    for key in ("out", "dq", "dk", "dv"):
+        assert max_abs(res[key], ref[key]) <= BF16_ABS, key
     assert rel_err(res["g"], ref["g"]) <= 1e-3
 
 
