@@ -504,8 +504,9 @@ def run_sharded_arm(args):
     """Config 3: the B*H = 128 groups split over ranks (strong scaling of one layer, no
     collective). Config 5: every rank owns N / world consecutive rows of all 16 heads;
     one step = shard totals -> NCCL all-gather -> exclusive prefix -> carried forward,
-    then backward shard totals -> all-gather -> exclusive suffix -> carried backward
-    (paper_2510_21956_b200/sharding.py). Same timing rules as the default arm."""
+    then backward shard totals -> all-gather -> exclusive suffix -> carried backward,
+    all inside the C-ABI's la_sharded_forward / la_sharded_backward (csrc/la_dist.cu;
+    sharding.DistStep is the ctypes wrapper). Same timing rules as the default arm."""
     import torch
     import torch.distributed as dist
 
@@ -538,18 +539,20 @@ def run_sharded_arm(args):
     q, k = unit_rows((G, N, D)), unit_rows((G, N, D))
     v = (torch.rand((G, D, N), device=dev, generator=gen) * 2 - 1).to(torch.bfloat16)
     w = (torch.rand((G, D, N), device=dev, generator=gen) * 2 - 1).to(torch.bfloat16)
-    ops = S.CudaOps(G, N, D, "bf16")
-
-    zero = ops._empty_state(q)
+    # the C-ABI multi-GPU entry points: shard totals, ncclAllGather and the prefix / suffix
+    # combine run inside la_sharded_forward / la_sharded_backward (la_dist.cu)
+    if world > 1:
+        comm = S.nccl_comm(rank, world)
+    else:  # one rank: the library's single-shard exchange (a record copy), no communicator
+        comm = None
+    dstep = S.DistStep(G, N, D, cfg["mode"], rank, world, row_offset=row0, comm=comm)
+    out, g = torch.empty_like(v), torch.empty(G * N, device=dev)
+    saved = torch.empty(dstep.saved_bytes, dtype=torch.uint8, device=dev)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(v), torch.empty_like(v)
 
     def step():  # the forward's saved segment states feed the backward (no K/V re-read)
-        if cfg["mode"] == "batch_head" or world == 1:
-            out, g, saved = ops.forward_with_carry(q, k, v, zero, row0, save=True)
-            return ops.backward_with_carry(q, k, v, out, w, g, zero, zero, row0, saved=saved)
-        carry = S.exclusive_prefix(S.all_gather_states(ops.forward_shard_state(k, v)), rank)
-        out, g, saved = ops.forward_with_carry(q, k, v, carry, row0, save=True)
-        suffix = S.exclusive_suffix(S.all_gather_states(ops.backward_shard_state(q, out, w, g)), rank)
-        return ops.backward_with_carry(q, k, v, out, w, g, carry, suffix, row0, saved=saved)
+        dstep.forward(q, k, v, out=out, g=g, saved=saved, check=False)
+        dstep.backward(q, k, v, out, w, g, saved, dq=dq, dk=dk, dv=dv, check=False)
 
     for _ in range(args.warmup):
         step()

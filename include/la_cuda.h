@@ -18,6 +18,8 @@
  * la_forward_shard_state           (new) per-shard (S,z,sigma,count) totals for
  * la_backward_shard_state          (new) sequence sharding, exchanged by the
  *                                  caller over NCCL, fed back as carry-in/out
+ * la_sharded_forward / _backward   (new) multi-GPU: batch x head or sequence shards,
+ *                                  the state exchange over NCCL inside the call
  * la_validate_plan                 la::validate_plan    src/plan.cpp:49-62
  * la_default_plan                  la::default_plan     src/plan.cpp:24-47
  *
@@ -192,12 +194,15 @@ la_status la_backward_sharded_saved(const la_problem* p, const la_shard* shard, 
                                     size_t ws_bytes, void* stream, la_error_info* err);
 /* Shard totals to exchange: forward (S=sum k^T v, z=sum k, sigma=sum v, count);
  * backward (R=sum q^T w_hat, u=sum s q, c=sum w_hat). Written to `state_out`
- * (la_shard_state_floats(p) fp32 values, device). */
+ * (la_shard_state_floats(p) fp32 values, device); `workspace` is device scratch of
+ * la_shard_state_workspace_bytes(p) bytes. */
+size_t la_shard_state_workspace_bytes(const la_problem* p);
 la_status la_forward_shard_state(const la_problem* p, const void* k, la_layout lk, const void* v,
-                                 la_layout lv, float* state_out, void* stream);
+                                 la_layout lv, float* state_out, void* workspace, size_t ws_bytes,
+                                 void* stream);
 la_status la_backward_shard_state(const la_problem* p, const void* q, la_layout lq,
                                   const void* o, const void* omega, la_layout lw, const float* g,
-                                  float* state_out, void* stream);
+                                  float* state_out, void* workspace, size_t ws_bytes, void* stream);
 /* Exclusive prefix (forward) / suffix (backward) of `nshards` gathered shard
  * states for shard `rank`, in fp32 on the device: the local step of the
  * NCCL all-gather scan. */
@@ -205,6 +210,52 @@ la_status la_combine_shard_states(const la_problem* p, const float* gathered, in
                                   int32_t rank, int32_t suffix, float* carry_out, void* stream);
 
 la_status la_query_status(const void* workspace, void* stream, la_error_info* err);
+
+/* ---------------------------------------------------------------- multi-GPU
+ * One process per GPU. The reference has no multi-device path; these entries shard
+ * the groups-independent work of run_forward / run_backward (forward_kernels.hpp:
+ * 221-235, backward_kernels.hpp:292-396) across ranks:
+ *   LA_SHARD_BATCH_HEAD  each rank owns whole groups (p->groups = its local count);
+ *                        no collective at all.
+ *   LA_SHARD_SEQUENCE    each rank owns rows [row_offset, row_offset + p->seq_len) of
+ *                        every group (causal). Forward: shard totals (S, z, sigma, rows)
+ *                        -> one all-gather -> exclusive prefix as the carry. Backward:
+ *                        (R, u, c, rows) -> all-gather -> exclusive suffix.
+ * The all-gather is ncclAllGather on `nccl_comm` (an ncclComm_t over the nranks
+ * processes, e.g. from la_nccl_comm_init) on the call's stream; when nccl_comm is
+ * NULL the caller's `allgather` callback performs it instead (tests use this to run
+ * several ranks on one device). */
+typedef enum { LA_SHARD_BATCH_HEAD = 0, LA_SHARD_SEQUENCE = 1 } la_shard_mode;
+/* recv[r * count .. (r+1) * count) = rank r's send[0 .. count), device fp32 buffers,
+ * stream-ordered on `stream`; returns 0 on success. */
+typedef int (*la_allgather_fn)(const float* send, float* recv, size_t count, void* ctx, void* stream);
+typedef struct {
+  la_shard_mode mode;
+  int32_t rank, nranks;
+  int64_t row_offset;      /* SEQUENCE: global index of this rank's first row */
+  void* nccl_comm;         /* ncclComm_t, or NULL to use `allgather` */
+  la_allgather_fn allgather;
+  void* allgather_ctx;
+} la_dist;
+/* `saved`: the forward's artifacts for the backward (per-segment states + the
+ * forward carry), la_dist_saved_bytes; `workspace`: la_dist_workspace_bytes, for
+ * either pass. Both device, caller-owned. */
+size_t la_dist_saved_bytes(const la_problem* p, const la_dist* d);
+size_t la_dist_workspace_bytes(const la_problem* p, const la_dist* d);
+la_status la_sharded_forward(const la_problem* p, const la_dist* d, const void* q, la_layout lq, const void* k,
+                             la_layout lk, const void* v, la_layout lv, void* out, float* g, void* saved,
+                             size_t saved_bytes, void* workspace, size_t ws_bytes, void* stream,
+                             la_error_info* err);
+la_status la_sharded_backward(const la_problem* p, const la_dist* d, const void* q, la_layout lq, const void* k,
+                              la_layout lk, const void* v, la_layout lv, const void* o, const void* omega,
+                              la_layout lw, const float* g, const void* saved, size_t saved_bytes, void* dq,
+                              void* dk, void* dv, void* workspace, size_t ws_bytes, void* stream,
+                              la_error_info* err);
+/* NCCL bootstrap without linking NCCL into the caller (libnccl.so.2 is loaded at
+ * first use; LA_ERR_UNSUPPORTED when absent). id: 128 bytes (ncclUniqueId). */
+la_status la_nccl_get_unique_id(char* id);
+la_status la_nccl_comm_init(void** comm, int32_t nranks, const char* id, int32_t rank);
+la_status la_nccl_comm_destroy(void* comm);
 
 /* ------------------------------------------- input prologue and diagnostics (device)
  * The reference's API calls either side of the hot path.

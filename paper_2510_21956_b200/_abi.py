@@ -29,7 +29,9 @@ EXPORTS = [
     "la_saved_state_bytes", "la_forward_save", "la_backward_saved",
     "la_normalize_qk", "la_relayout", "la_make_omega_hat", "la_constant_term_pass", "la_linear_term_pass",
     "la_alpha_term_pass", "la_beta_term_pass", "la_forward_sharded_save", "la_backward_sharded_saved",
-    "la_set_tuning", "la_get_tuning",
+    "la_set_tuning", "la_get_tuning", "la_shard_state_workspace_bytes", "la_dist_saved_bytes",
+    "la_dist_workspace_bytes", "la_sharded_forward", "la_sharded_backward", "la_nccl_get_unique_id",
+    "la_nccl_comm_init", "la_nccl_comm_destroy",
 ]
 
 
@@ -58,6 +60,17 @@ class Tuning(C.Structure):
 
 class Shard(C.Structure):
     _fields_ = [("row_offset", C.c_int64), ("carry_in", C.c_void_p), ("carry_suffix", C.c_void_p)]
+
+
+SHARD_BATCH_HEAD, SHARD_SEQUENCE = 0, 1
+# int (*)(const float* send, float* recv, size_t count, void* ctx, void* stream)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+
+
+class Dist(C.Structure):
+    """la_dist: the multi-GPU entry points' sharding description."""
+    _fields_ = [("mode", C.c_int), ("rank", C.c_int32), ("nranks", C.c_int32), ("row_offset", C.c_int64),
+                ("nccl_comm", C.c_void_p), ("allgather", ALLGATHER_FN), ("allgather_ctx", C.c_void_p)]
 
 
 _lib = None
@@ -93,8 +106,22 @@ def lib():
                                          vp, vp, vp, sz, vp, E]
         L.la_backward_sharded.argtypes = [P, C.POINTER(Shard), vp, C.c_int, vp, C.c_int, vp, C.c_int,
                                           vp, vp, C.c_int, vp, vp, vp, vp, vp, sz, vp, E]
-        L.la_forward_shard_state.argtypes = [P, vp, C.c_int, vp, C.c_int, vp, vp]
-        L.la_backward_shard_state.argtypes = [P, vp, C.c_int, vp, vp, C.c_int, vp, vp, vp]
+        L.la_shard_state_workspace_bytes.restype = sz
+        L.la_shard_state_workspace_bytes.argtypes = [P]
+        L.la_forward_shard_state.argtypes = [P, vp, C.c_int, vp, C.c_int, vp, vp, sz, vp]
+        L.la_backward_shard_state.argtypes = [P, vp, C.c_int, vp, vp, C.c_int, vp, vp, vp, sz, vp]
+        Dp = C.POINTER(Dist)
+        L.la_dist_saved_bytes.restype = sz
+        L.la_dist_saved_bytes.argtypes = [P, Dp]
+        L.la_dist_workspace_bytes.restype = sz
+        L.la_dist_workspace_bytes.argtypes = [P, Dp]
+        L.la_sharded_forward.argtypes = [P, Dp, vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, vp, sz, vp, sz,
+                                         vp, E]
+        L.la_sharded_backward.argtypes = [P, Dp, vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, C.c_int, vp, vp,
+                                          sz, vp, vp, vp, vp, sz, vp, E]
+        L.la_nccl_get_unique_id.argtypes = [C.c_char_p]
+        L.la_nccl_comm_init.argtypes = [C.POINTER(vp), C.c_int32, C.c_char_p, C.c_int32]
+        L.la_nccl_comm_destroy.argtypes = [vp]
         L.la_combine_shard_states.argtypes = [P, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp]
         L.la_query_status.argtypes = [vp, vp, E]
         L.la_saved_state_bytes.restype = sz

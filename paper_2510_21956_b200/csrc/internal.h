@@ -167,12 +167,11 @@ size_t tc_backward_ws_floats(int64_t G, int64_t N, int64_t D);
 size_t tc_saved_floats(int64_t G, int64_t N, int64_t D);
 int tc_segments(int64_t G, int64_t N);
 
-// Sequence-shard totals on the tensor core (bf16/fp16, D = 128, canonical layouts).
-cudaError_t tc_forward_shard_state(const Launch& L, const Tensors& t, float* out);
-cudaError_t tc_backward_shard_state(const Launch& L, const Tensors& t, float* out);
-
-// Stream-ordered scratch (cudaMallocAsync) keeps its freed blocks: call before allocating.
-void keep_pool_memory();
+// Sequence-shard totals on the tensor core (bf16/fp16, D = 128, canonical layouts);
+// unit records in caller scratch of tc_shard_state_scratch_floats floats.
+size_t tc_shard_state_scratch_floats(int64_t G, int64_t N);
+cudaError_t tc_forward_shard_state(const Launch& L, const Tensors& t, float* out, float* units);
+cudaError_t tc_backward_shard_state(const Launch& L, const Tensors& t, float* out, float* units);
 // {magic, G, N, D, P, seg} into a saved-state buffer, stream-ordered and graph-capturable.
 void write_saved_header(void* dst, double g, double n, double d, double p, double seg, cudaStream_t st,
                         int ck_k = 0);

@@ -47,20 +47,6 @@ ProfScope::~ProfScope() {
   if (idx < (int)g_prof.size()) cudaEventRecord(g_prof[idx].b, stream);
 }
 
-// Keep the stream-ordered pool's freed blocks for reuse (the padded path allocates
-// per call); without this every call would map fresh pages.
-void keep_pool_memory() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  });
-}
 // Saved-state header {magic, G, N, D, P, seg} written by a tiny kernel rather than a
 // pageable host copy, so a forward + backward step can be captured in a CUDA graph.
 __global__ void k_saved_header(float* dst, float g, float n, float d, float p, float seg, float ck) {
@@ -101,6 +87,7 @@ using namespace lab;
 namespace {
 
 constexpr size_t kFlagBytes = 256;
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 la_status fail(la_error_info* err, la_status code, const char* msg, int64_t grp = -1,
                int64_t pos = -1) {
@@ -199,9 +186,7 @@ size_t bwd_floats(const la_problem* p) {
   size_t a = simt_backward_ws_floats(p->groups, p->seq_len, p->dim, p->fault);
   size_t b = std::max(tc_backward_ws_floats(p->groups, p->seq_len, p->dim),
                       full_ws_floats(p->groups, p->seq_len, p->dim));
-  size_t c = (size_t)(p->groups * p->seq_len);  // backward shard state scratch
-  size_t m = a > b ? a : b;
-  return m > c ? m : c;
+  return a > b ? a : b;
 }
 
 // Head dimensions below 128 on the tensor-core path: zero-pad D to 128 in device
@@ -334,12 +319,9 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
     const la_problem pn = n_padded_problem(p);
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t G = p->groups, N = p->seq_len, Np = pn.seq_len, D = p->dim;
-    const size_t T = (size_t)G * Np * D * 2, e = 2;
-    char* buf = nullptr;
-    keep_pool_memory();
-    if (cudaMallocAsync((void**)&buf, 4 * T + (size_t)G * Np * 4, st) != cudaSuccess)
-      return cuda_fail(err, cudaErrorMemoryAllocation);
-    (void)e;
+    const size_t T = (size_t)G * Np * D * 2;
+    const size_t inner = align256(la_forward_workspace_bytes(&pn));
+    char* buf = (char*)ws + inner;  // the padded copies follow the inner workspace
     pitch_copy<u16>((u16*)buf, Np * D, (const u16*)q, N * D, N * D, Np * D, G, 0, st);  // SequenceMajor rows
     pitch_copy<u16>((u16*)(buf + T), Np * D, (const u16*)k, N * D, N * D, Np * D, G, 0, st);
     pitch_copy<u16>((u16*)(buf + 2 * T), Np, (const u16*)v, N, N, Np, G * D, 0, st);   // FeatureMajor rows
@@ -347,13 +329,12 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
     float* gp = (float*)(buf + 4 * T);
     // the saved states are the padded problem's (la_saved_state_bytes sizes them for Np)
     s = forward_impl(&pn, nullptr, buf, LA_SEQUENCE_MAJOR, buf + T, LA_SEQUENCE_MAJOR, buf + 2 * T,
-                     LA_FEATURE_MAJOR, buf + 3 * T, gp, ws, ws_bytes, stream, nullptr, saved, saved_bytes, N);
+                     LA_FEATURE_MAJOR, buf + 3 * T, gp, ws, inner, stream, nullptr, saved, saved_bytes, N);
     if (s == LA_OK) {
       pitch_copy<u16>((u16*)out, N, (const u16*)(buf + 3 * T), Np, N, N, G * D, 0, st);
       pitch_copy<float>(g, N, gp, Np, N, N, G, 0.f, st);
       note_launch(2);
     }
-    cudaFreeAsync(buf, st);
     if (s != LA_OK) return fail(err, s, "sequence-padded forward failed");
     return finish(ws, st, err);
   }
@@ -361,9 +342,8 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
     const la_problem p2 = padded_problem(p);
     cudaStream_t st = (cudaStream_t)stream;
     const size_t T = (size_t)p->groups * p->seq_len * 128 * 2;
-    char* buf = nullptr;
-    keep_pool_memory();
-    if (cudaMallocAsync((void**)&buf, 4 * T, st) != cudaSuccess) return cuda_fail(err, cudaErrorMemoryAllocation);
+    const size_t inner = align256(la_forward_workspace_bytes(&p2));
+    char* buf = (char*)ws + inner;
     pad_copy(buf, q, p, true, true, st);
     pad_copy(buf + T, k, p, true, true, st);
     pad_copy(buf + 2 * T, v, p, false, true, st);
@@ -371,9 +351,8 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
       write_saved_header(saved, (double)p->groups, (double)p->seq_len, (double)p->dim, 0, 0, st);
     }
     s = forward_impl(&p2, nullptr, buf, LA_SEQUENCE_MAJOR, buf + T, LA_SEQUENCE_MAJOR, buf + 2 * T,
-                     LA_FEATURE_MAJOR, buf + 3 * T, g, ws, ws_bytes, stream, nullptr, nullptr, 0, n_total);
+                     LA_FEATURE_MAJOR, buf + 3 * T, g, ws, inner, stream, nullptr, nullptr, 0, n_total);
     if (s == LA_OK) pad_copy(out, buf + 3 * T, p, false, false, st);
-    cudaFreeAsync(buf, st);
     if (s != LA_OK) return fail(err, s, "padded forward failed");
     return finish(ws, st, err);
   }
@@ -432,12 +411,9 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
     const la_problem pn = n_padded_problem(p);
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t G = p->groups, N = p->seq_len, Np = pn.seq_len, D = p->dim;
-    const size_t T = (size_t)G * Np * D * 2, e = 2;
-    char* buf = nullptr;
-    keep_pool_memory();
-    if (cudaMallocAsync((void**)&buf, 8 * T + (size_t)G * Np * 4, st) != cudaSuccess)
-      return cuda_fail(err, cudaErrorMemoryAllocation);
-    (void)e;
+    const size_t T = (size_t)G * Np * D * 2;
+    const size_t inner = align256(la_backward_workspace_bytes(&pn));
+    char* buf = (char*)ws + inner;  // the padded copies follow the inner workspace
     pitch_copy<u16>((u16*)buf, Np * D, (const u16*)q, N * D, N * D, Np * D, G, 0, st);
     pitch_copy<u16>((u16*)(buf + T), Np * D, (const u16*)k, N * D, N * D, Np * D, G, 0, st);
     pitch_copy<u16>((u16*)(buf + 2 * T), Np, (const u16*)v, N, N, Np, G * D, 0, st);
@@ -448,7 +424,7 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
     note_launch(6);
     la_status s2 = backward_impl(&pn, nullptr, buf, LA_SEQUENCE_MAJOR, buf + T, LA_SEQUENCE_MAJOR, buf + 2 * T,
                                  LA_FEATURE_MAJOR, buf + 3 * T, buf + 4 * T, LA_FEATURE_MAJOR, gp, buf + 5 * T,
-                                 buf + 6 * T, buf + 7 * T, ws, ws_bytes, stream, nullptr, saved, saved_bytes,
+                                 buf + 6 * T, buf + 7 * T, ws, inner, stream, nullptr, saved, saved_bytes,
                                  trust_saved);
     if (s2 == LA_OK) {
       pitch_copy<u16>((u16*)dq, N * D, (const u16*)(buf + 5 * T), Np * D, N * D, N * D, G, 0, st);
@@ -456,7 +432,6 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
       pitch_copy<u16>((u16*)dv, N, (const u16*)(buf + 7 * T), Np, N, N, G * D, 0, st);
       note_launch(3);
     }
-    cudaFreeAsync(buf, st);
     if (s2 != LA_OK) return fail(err, s2, "sequence-padded backward failed");
     return finish(ws, st, err);
   }
@@ -464,9 +439,8 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
     const la_problem p2 = padded_problem(p);
     cudaStream_t st = (cudaStream_t)stream;
     const size_t T = (size_t)p->groups * p->seq_len * 128 * 2;
-    char* buf = nullptr;
-    keep_pool_memory();
-    if (cudaMallocAsync((void**)&buf, 8 * T, st) != cudaSuccess) return cuda_fail(err, cudaErrorMemoryAllocation);
+    const size_t inner = align256(la_backward_workspace_bytes(&p2));
+    char* buf = (char*)ws + inner;
     pad_copy(buf, q, p, true, true, st);
     pad_copy(buf + T, k, p, true, true, st);
     pad_copy(buf + 2 * T, v, p, false, true, st);
@@ -474,13 +448,12 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
     pad_copy(buf + 4 * T, omega, p, false, true, st);
     la_status s2 = backward_impl(&p2, nullptr, buf, LA_SEQUENCE_MAJOR, buf + T, LA_SEQUENCE_MAJOR, buf + 2 * T,
                                  LA_FEATURE_MAJOR, buf + 3 * T, buf + 4 * T, LA_FEATURE_MAJOR, g, buf + 5 * T,
-                                 buf + 6 * T, buf + 7 * T, ws, ws_bytes, stream, nullptr);
+                                 buf + 6 * T, buf + 7 * T, ws, inner, stream, nullptr);
     if (s2 == LA_OK) {
       pad_copy(dq, buf + 5 * T, p, true, false, st);
       pad_copy(dk, buf + 6 * T, p, false, false, st);
       pad_copy(dv, buf + 7 * T, p, false, false, st);
     }
-    cudaFreeAsync(buf, st);
     if (s2 != LA_OK) return fail(err, s2, "padded backward failed");
     return finish(ws, st, err);
   }
@@ -617,8 +590,6 @@ struct HostPipe {
 };
 thread_local HostPipe t_pipe;
 
-size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
-
 }  // namespace
 
 extern "C" {
@@ -707,36 +678,35 @@ la_status la_backward_saved(const la_problem* p, const void* q, la_layout lq, co
                        stream, err, saved, saved_bytes);
 }
 
+// The padded paths run the padded problem in the head of the workspace and keep
+// their zero-padded copies of the inputs / outputs in its tail: the caller's
+// workspace is the only device memory a call uses (no allocation per call).
 size_t la_forward_workspace_bytes(const la_problem* p) {
   if (!p || p->groups <= 0 || p->seq_len <= 0 || p->dim <= 0) return kFlagBytes;
-  size_t f = fwd_floats(p);
-  if (pad_eligible(p, nullptr, LA_SEQUENCE_MAJOR, LA_SEQUENCE_MAJOR, LA_FEATURE_MAJOR, -1)) {
-    const la_problem p2 = padded_problem(p);
-    const size_t f2 = fwd_floats(&p2);
-    if (f2 > f) f = f2;
-  }
-  size_t bytes = ws_bytes_for(f);
+  size_t bytes = ws_bytes_for(fwd_floats(p));
   if (padn_eligible(p, nullptr, LA_SEQUENCE_MAJOR, LA_SEQUENCE_MAJOR, LA_FEATURE_MAJOR, -1)) {
     const la_problem pn = n_padded_problem(p);
-    const size_t b2 = la_forward_workspace_bytes(&pn);
-    if (b2 > bytes) bytes = b2;
+    const size_t T = (size_t)p->groups * pn.seq_len * p->dim * 2;
+    bytes = std::max(bytes, align256(la_forward_workspace_bytes(&pn)) + 4 * T + (size_t)p->groups * pn.seq_len * 4);
+  } else if (pad_eligible(p, nullptr, LA_SEQUENCE_MAJOR, LA_SEQUENCE_MAJOR, LA_FEATURE_MAJOR, -1)) {
+    const la_problem p2 = padded_problem(p);
+    const size_t T = (size_t)p->groups * p->seq_len * 128 * 2;
+    bytes = std::max(bytes, align256(la_forward_workspace_bytes(&p2)) + 4 * T);
   }
   return bytes;
 }
 
 size_t la_backward_workspace_bytes(const la_problem* p) {
   if (!p || p->groups <= 0 || p->seq_len <= 0 || p->dim <= 0) return kFlagBytes;
-  size_t f = bwd_floats(p);
-  if (pad_eligible(p, nullptr, LA_SEQUENCE_MAJOR, LA_SEQUENCE_MAJOR, LA_FEATURE_MAJOR, LA_FEATURE_MAJOR)) {
-    const la_problem p2 = padded_problem(p);
-    const size_t f2 = bwd_floats(&p2);
-    if (f2 > f) f = f2;
-  }
-  size_t bytes = ws_bytes_for(f);
+  size_t bytes = ws_bytes_for(bwd_floats(p));
   if (padn_eligible(p, nullptr, LA_SEQUENCE_MAJOR, LA_SEQUENCE_MAJOR, LA_FEATURE_MAJOR, LA_FEATURE_MAJOR)) {
     const la_problem pn = n_padded_problem(p);
-    const size_t b2 = la_backward_workspace_bytes(&pn);
-    if (b2 > bytes) bytes = b2;
+    const size_t T = (size_t)p->groups * pn.seq_len * p->dim * 2;
+    bytes = std::max(bytes, align256(la_backward_workspace_bytes(&pn)) + 8 * T + (size_t)p->groups * pn.seq_len * 4);
+  } else if (pad_eligible(p, nullptr, LA_SEQUENCE_MAJOR, LA_SEQUENCE_MAJOR, LA_FEATURE_MAJOR, LA_FEATURE_MAJOR)) {
+    const la_problem p2 = padded_problem(p);
+    const size_t T = (size_t)p->groups * p->seq_len * 128 * 2;
+    bytes = std::max(bytes, align256(la_backward_workspace_bytes(&p2)) + 8 * T);
   }
   return bytes;
 }
@@ -847,37 +817,40 @@ static bool shard_state_tc(const la_problem* p, bool canonical) {
          p->seq_len % 128 == 0 && p->fault == LA_FAULT_NONE && canonical && p->groups * p->seq_len < (1ll << 31);
 }
 
+size_t la_shard_state_workspace_bytes(const la_problem* p) {
+  if (!p || p->groups <= 0 || p->seq_len <= 0 || p->dim <= 0) return 256;
+  size_t f = (size_t)(p->groups * p->seq_len);  // CUDA-core backward: s_i per row
+  if (shard_state_tc(p, true)) f = std::max(f, tc_shard_state_scratch_floats(p->groups, p->seq_len));
+  return align256(f * sizeof(float));
+}
+
 la_status la_forward_shard_state(const la_problem* p, const void* k, la_layout lk, const void* v,
-                                 la_layout lv, float* state_out, void* stream) {
+                                 la_layout lv, float* state_out, void* workspace, size_t ws_bytes,
+                                 void* stream) {
   la_status s = check_problem(p, nullptr);
   if (s != LA_OK) return s;
   if (!k || !v || !state_out) return LA_ERR_INVALID_SHAPE;
+  if (!workspace || ws_bytes < la_shard_state_workspace_bytes(p)) return LA_ERR_WORKSPACE;
   Launch L = make_launch(p, nullptr, stream);
   Tensors t{nullptr, 0, k, lk, v, lv, nullptr, 0, nullptr, 0, nullptr};
   if (shard_state_tc(p, lk == LA_SEQUENCE_MAJOR && lv == LA_FEATURE_MAJOR))
-    return tc_forward_shard_state(L, t, state_out) == cudaSuccess ? LA_OK : LA_ERR_CUDA;
+    return tc_forward_shard_state(L, t, state_out, (float*)workspace) == cudaSuccess ? LA_OK : LA_ERR_CUDA;
   return simt_forward_shard_state(L, t, state_out) == cudaSuccess ? LA_OK : LA_ERR_CUDA;
 }
 
 la_status la_backward_shard_state(const la_problem* p, const void* q, la_layout lq,
                                   const void* o, const void* omega, la_layout lw, const float* g,
-                                  float* state_out, void* stream) {
+                                  float* state_out, void* workspace, size_t ws_bytes, void* stream) {
   la_status s = check_problem(p, nullptr);
   if (s != LA_OK) return s;
   if (!q || !o || !omega || !g || !state_out) return LA_ERR_MISSING_FORWARD_STATE;
+  if (!workspace || ws_bytes < la_shard_state_workspace_bytes(p)) return LA_ERR_WORKSPACE;
   Launch L = make_launch(p, nullptr, stream);
   Tensors t{q, lq, nullptr, 0, nullptr, 0, o, LA_FEATURE_MAJOR, omega, lw, g};
   if (shard_state_tc(p, lq == LA_SEQUENCE_MAJOR && lw == LA_FEATURE_MAJOR))
-    return tc_backward_shard_state(L, t, state_out) == cudaSuccess ? LA_OK : LA_ERR_CUDA;
-  // scratch for s_i: G*N floats, allocated stream-ordered
-  float* scratch = nullptr;
-  if (cudaMallocAsync((void**)&scratch, sizeof(float) * p->groups * p->seq_len, L.stream) !=
-      cudaSuccess)
-    return LA_ERR_CUDA;
-  Workspace w{nullptr, scratch, (size_t)(p->groups * p->seq_len)};
-  cudaError_t e = simt_backward_shard_state(L, t, state_out, w);
-  cudaFreeAsync(scratch, L.stream);
-  return e == cudaSuccess ? LA_OK : LA_ERR_CUDA;
+    return tc_backward_shard_state(L, t, state_out, (float*)workspace) == cudaSuccess ? LA_OK : LA_ERR_CUDA;
+  Workspace w{nullptr, (float*)workspace, (size_t)(p->groups * p->seq_len)};  // s_i scratch
+  return simt_backward_shard_state(L, t, state_out, w) == cudaSuccess ? LA_OK : LA_ERR_CUDA;
 }
 
 la_status la_combine_shard_states(const la_problem* p, const float* gathered, int32_t nshards,

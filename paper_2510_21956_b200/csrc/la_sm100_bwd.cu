@@ -1596,22 +1596,24 @@ static cudaError_t tc_backward_full(const Launch& L, const Tensors& t, void* dq,
 }
 
 // Sequence-shard totals on the tensor core (the inputs of the NCCL all-gather scan,
-// sharding.py): forward (S, z, sigma, rows) = the non-causal K/V totals; backward
-// (R, u, c, rows) = the R aggregate units summed per group. Scratch is stream-ordered.
-cudaError_t tc_forward_shard_state(const Launch& L, const Tensors& t, float* out) {
-  keep_pool_memory();
-  float* units = nullptr;
-  const size_t n = (size_t)L.G * tc_kv_units(L.G, L.N) * state_floats(kD);
-  cudaError_t e = cudaMallocAsync((void**)&units, n * sizeof(float), L.stream);
-  if (e != cudaSuccess) return e;
-  e = tc_kv_totals(L, t, units, out);
-  cudaFreeAsync(units, L.stream);
-  return e;
+// la_sharded_forward / sharding.py): forward (S, z, sigma, rows) = the non-causal K/V
+// totals; backward (R, u, c, rows) = the R aggregate units summed per group. The unit
+// records go to caller scratch (tc_shard_state_scratch_floats), no allocation.
+size_t tc_shard_state_scratch_floats(int64_t G, int64_t N) {
+  const int P = tcb_segments(G, N);
+  const int64_t seg = ((N / 128 + P - 1) / P) * 128;
+  const int A = agg_split(G, seg, P);
+  const size_t f = (size_t)G * tc_kv_units(G, N), b = (size_t)G * P * A;
+  return (f > b ? f : b) * state_floats(kD);
 }
 
-cudaError_t tc_backward_shard_state(const Launch& L, const Tensors& t, float* out) {
+cudaError_t tc_forward_shard_state(const Launch& L, const Tensors& t, float* out, float* units) {
+  return tc_kv_totals(L, t, units, out);
+}
+
+cudaError_t tc_backward_shard_state(const Launch& L, const Tensors& t, float* out, float* units) {
   const bool bf = L.dtype == LA_BF16;
-  const int64_t G = L.G, N = L.N, SZ = state_floats(kD);
+  const int64_t G = L.G, N = L.N;
   const int P = tcb_segments(G, N);
   const int64_t seg = ((N / 128 + P - 1) / P) * 128;
   const int A = agg_split(G, seg, P);
@@ -1620,10 +1622,6 @@ cudaError_t tc_backward_shard_state(const Launch& L, const Tensors& t, float* ou
       !make_tma_map(&mQ, t.q, bf, (uint64_t)(G * N), kD, 64, 2) ||
       !make_tma_map(&mW, t.w, bf, (uint64_t)(G * kD), (uint64_t)N, 128, 1))
     return cudaErrorInvalidValue;
-  keep_pool_memory();
-  float* units = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&units, (size_t)G * P * A * SZ * sizeof(float), L.stream);
-  if (e != cudaSuccess) return e;
   BwdParams pa{t.o, t.g, nullptr, nullptr, nullptr, nullptr, units, N, seg / A, P * A, L.a, L.b, 0, 1, 0, A,
                nullptr, nullptr, nullptr, 0};
   auto aggR = bf ? k_bwd_aggR_tc<true> : k_bwd_aggR_tc<false>;
@@ -1633,9 +1631,7 @@ cudaError_t tc_backward_shard_state(const Launch& L, const Tensors& t, float* ou
     aggR<<<dim3(A * P, G), 320, kAggRSmem, L.stream>>>(mQ, mW, mO, mW, pa);
   }
   note_launch(1);
-  e = tc_sum_units(units, G, P * A, out, L.stream);
-  cudaFreeAsync(units, L.stream);
-  return e;
+  return tc_sum_units(units, G, P * A, out, L.stream);
 }
 
 cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv, Workspace ws) {
