@@ -66,7 +66,7 @@ typedef enum { /* fault.hpp:7-15 */
 typedef enum { /* device path selection; AUTO picks tcgen05 when the shape allows */
   LA_IMPL_AUTO = 0,
   LA_IMPL_SIMT = 1,   /* CUDA-core fp32 path: every dtype/D, exact sweep order */
-  LA_IMPL_TCGEN05 = 2 /* sm_100a tensor-core chunked path (bf16/fp16) */
+  LA_IMPL_TCGEN05 = 2 /* sm_100a tensor-core chunked path (bf16/fp16; fp32 as 3xTF32) */
 } la_impl;
 
 typedef struct { /* la::BlockPlan, plan.hpp:15-21 */

@@ -176,6 +176,13 @@ cudaError_t tc_backward_shard_state(const Launch& L, const Tensors& t, float* ou
 void write_saved_header(void* dst, double g, double n, double d, double p, double seg, cudaStream_t st,
                         int ck_k = 0);
 
+// fp32 inputs on the tensor core (3xTF32, la_f32tc.cu): canonical layouts, D <= 128,
+// N a multiple of 64, causal and non-causal, no shard carries / faults.
+bool f32tc_supported(const Launch& L, const Tensors& t);
+size_t f32tc_ws_floats(int64_t G, int64_t N, int64_t D);
+cudaError_t f32tc_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws);
+cudaError_t f32tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv, Workspace ws);
+
 // Non-causal tensor-core path for D = 64, 192, 256 (bf16/fp16, canonical layouts; la_full.cu).
 bool full_tc_supported(const Launch& L, const Tensors& t);
 size_t full_ws_floats(int64_t G, int64_t N, int64_t D);

@@ -180,12 +180,14 @@ size_t fwd_floats(const la_problem* p) {
   size_t a = simt_forward_ws_floats(p->groups, p->seq_len, p->dim, p->fault);
   size_t b = std::max(tc_forward_ws_floats(p->groups, p->seq_len, p->dim),
                       full_ws_floats(p->groups, p->seq_len, p->dim));
+  if (p->dtype == LA_F32) b = std::max(b, f32tc_ws_floats(p->groups, p->seq_len, p->dim));
   return a > b ? a : b;
 }
 size_t bwd_floats(const la_problem* p) {
   size_t a = simt_backward_ws_floats(p->groups, p->seq_len, p->dim, p->fault);
   size_t b = std::max(tc_backward_ws_floats(p->groups, p->seq_len, p->dim),
                       full_ws_floats(p->groups, p->seq_len, p->dim));
+  if (p->dtype == LA_F32) b = std::max(b, f32tc_ws_floats(p->groups, p->seq_len, p->dim));
   return a > b ? a : b;
 }
 
@@ -366,6 +368,7 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
   cudaError_t e;
   const bool tc = use_tc(p, tc_forward_supported(L, t));
   const bool full = !tc && p->impl != LA_IMPL_SIMT && full_tc_supported(L, t);
+  const bool f32 = !tc && !full && p->impl != LA_IMPL_SIMT && f32tc_supported(L, t);
   if (saved) {
     if (tc || full) {  // causal: prefix states per segment; non-causal: the K/V totals
       L.saved_out = (float*)saved;
@@ -377,9 +380,12 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
     e = tc_forward(L, t, out, g, w);
   else if (full)
     e = full_forward(L, t, out, g, w);
+  else if (f32)
+    e = f32tc_forward(L, t, out, g, w);
   else if (p->impl == LA_IMPL_TCGEN05)
     return fail(err, LA_ERR_UNSUPPORTED,
-                "tcgen05 path needs bf16/fp16, canonical layouts, D = 128 (causal) or 64/128/192/256 (non-causal)");
+                "tcgen05 path needs canonical layouts and bf16/fp16 with D = 128 (causal) or 64/128/192/256 "
+                "(non-causal), or fp32 with D <= 128 and N a multiple of 64");
   else
     e = simt_forward(L, t, out, g, w);
   if (e != cudaSuccess) return cuda_fail(err, e);
@@ -462,6 +468,7 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
   Workspace w = carve(ws, ws_bytes);
   const bool tc = use_tc(p, tc_backward_supported(L, t));
   const bool full = !tc && p->impl != LA_IMPL_SIMT && full_tc_supported(L, t);
+  const bool f32 = !tc && !full && p->impl != LA_IMPL_SIMT && f32tc_supported(L, t);
   cudaMemsetAsync(w.flag, 0xFF, sizeof(unsigned long long), L.stream);
   if (saved && (tc || full)) {
     // states from la_forward_save of the same problem: causal -> per-segment prefixes
@@ -484,9 +491,12 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
     e = tc_backward(L, t, dq, dk, dv, w);
   else if (full)
     e = full_backward(L, t, dq, dk, dv, w);
+  else if (f32)
+    e = f32tc_backward(L, t, dq, dk, dv, w);
   else if (p->impl == LA_IMPL_TCGEN05)
     return fail(err, LA_ERR_UNSUPPORTED,
-                "tcgen05 path needs bf16/fp16, canonical layouts, D = 128 (causal) or 64/128/192/256 (non-causal)");
+                "tcgen05 path needs canonical layouts and bf16/fp16 with D = 128 (causal) or 64/128/192/256 "
+                "(non-causal), or fp32 with D <= 128 and N a multiple of 64");
   else
     e = simt_backward(L, t, dq, dk, dv, w);
   if (e != cudaSuccess) return cuda_fail(err, e);
