@@ -176,12 +176,21 @@ cudaError_t tc_backward_shard_state(const Launch& L, const Tensors& t, float* ou
 void write_saved_header(void* dst, double g, double n, double d, double p, double seg, cudaStream_t st,
                         int ck_k = 0);
 
-// fp32 inputs on the tensor core (3xTF32, la_f32tc.cu): canonical layouts, D <= 128,
-// N a multiple of 64, causal and non-causal, no shard carries / faults.
+// fp32 inputs on the tensor core (3xTF32, la_f32tc.cu): any layouts, D <= 128 (D % 4 == 0),
+// N a multiple of 64, causal and non-causal, the Fault mutations, no shard carries.
 bool f32tc_supported(const Launch& L, const Tensors& t);
 size_t f32tc_ws_floats(int64_t G, int64_t N, int64_t D);
 cudaError_t f32tc_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws);
 cudaError_t f32tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv, Workspace ws);
+
+// Generic 16-bit tensor-core path (la_g16.cu): any layouts, D <= 256 (D % 8 == 0), the
+// Fault mutations, N a multiple of 64, causal and non-causal, no shard carries.
+bool g16_supported(const Launch& L, const Tensors& t);
+size_t g16_ws_floats(int64_t G, int64_t N, int64_t D);
+cudaError_t g16_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws);
+cudaError_t g16_backward(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv, Workspace ws);
+// Fault::CausalPrefixOffByOne: the generic paths' chunk-boundary term (la_g16.cu).
+cudaError_t offbyone_fix(const Launch& L, const Tensors& t, void* out, const float* g);
 
 // Non-causal tensor-core path for D = 64, 192, 256 (bf16/fp16, canonical layouts; la_full.cu).
 bool full_tc_supported(const Launch& L, const Tensors& t);

@@ -69,6 +69,7 @@ struct F32Params {
   float alphk_s;
   const float* alphk_v;  // alpha'_t = alphk_s * alphk_v[t] (null: 0)
   float beta;
+  int shift;    // Fault::CausalPrefixOffByOne: the beta window of row i ends at i + 1
   float* recs;  // [G][U][kSZ] aggregate-unit records (A units per segment, U = P * A)
   int A, U;        // units per segment, unit records per group
   int unit_chunks; // chunks per aggregate unit
@@ -463,8 +464,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int u = 0; u < 4; ++u) {
               const int t = 32 * half + 4 * c8 + u;
               const bool on = prm.dir == kCausal ? t <= i : t >= i;
-              pv[u] = on ? ai + vap[t] + beta * __uint_as_float(x[4 * c8 + u]) : 0.f;
-              rs += pv[u];
+              const bool on_b = prm.shift ? t <= i + 1 : on;
+              const float bt = beta * __uint_as_float(x[4 * c8 + u]);
+              pv[u] = (on ? ai + vap[t] : 0.f) + (on_b ? bt : 0.f);
+              rs += on ? ai + vap[t] + bt : 0.f;
             }
             float4 a, b;
             a.x = __uint_as_float(tf32_hi(pv[0])); b.x = pv[0] - a.x;
@@ -621,15 +624,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // w_hat = omega / g (FeatureMajor, into `wh`), s_i = sum_j o_ij w_hat_ij (make_omega_hat
 // backward.cpp:74-91; backward_kernels.hpp:33-38). Thread per row i, loop over j.
-__global__ void k_f32_what(const float* o, const float* w, const float* g, float* wh, float* s, int64_t N, int D) {
+__global__ void k_f32_what(const float* o, const float* w, int lw, const float* g, float* wh, float* s, int64_t N,
+                           int D) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t grp = blockIdx.y;
   if (i >= N) return;
   const float gi = g[grp * N + i];
+  const Strides sw = strides_of(lw, N, D);
+  const float* wg = w + grp * N * D;
   float acc = 0.f;
   for (int j = 0; j < D; ++j) {
     const int64_t ix = (grp * D + j) * N + i;
-    const float wv = w[ix] / gi;
+    const float wv = wg[i * sw.is + j * sw.js] / gi;
     wh[ix] = wv;
     acc += o[ix] * wv;
   }
@@ -725,7 +731,7 @@ struct Operand {
 // non-causal, the apply pass over every chunk with the totals).
 cudaError_t f32_pass(const Launch& L, Operand X, Operand K, Operand Y, void* out, int lo, int dir, float alpha_c,
                      float alpha_s, const float* alpha_v, float alphk_s, const float* alphk_v, bool normalize,
-                     float* g, unsigned long long* flag, float* recs, const char* name) {
+                     int shift, float* g, unsigned long long* flag, float* recs, const char* name) {
   const int64_t G = L.G, N = L.N;
   const int D = (int)L.D;
   CUtensorMap mX, mK, mY, mO;
@@ -739,7 +745,7 @@ cudaError_t f32_pass(const Launch& L, Operand X, Operand K, Operand Y, void* out
   const int seg = (int)((nc + P - 1) / P);
   const int A = f32_units(G, P, seg, dir);
   F32Params prm{N, D, seg, P, dir, kAgg, X.lay, K.lay, Y.lay, lo, alpha_c, alpha_s, alpha_v, alphk_s, alphk_v, L.b,
-                recs, A, P * A, seg / A, 0, normalize ? 1 : 0, 0, g, flag};
+                shift, recs, A, P * A, seg / A, 0, normalize ? 1 : 0, 0, g, flag};
   cudaFuncSetAttribute(k_f32_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
   if (P > 1 || dir == kFull) {
     // only the segments whose sums some sweep needs: causal 0..P-2, anticausal 1..P-1
@@ -766,10 +772,10 @@ cudaError_t f32_pass(const Launch& L, Operand X, Operand K, Operand Y, void* out
 }  // namespace
 
 bool f32tc_supported(const Launch& L, const Tensors& t) {
-  return L.dtype == LA_F32 && L.fault == LA_FAULT_NONE && L.D % 4 == 0 && L.D <= kT && L.N % kC == 0 &&
-         L.carry_prefix == nullptr && L.carry_suffix == nullptr && L.row_offset == 0 && L.n_total == L.N &&
-         t.lq == LA_SEQUENCE_MAJOR && t.lk == LA_SEQUENCE_MAJOR && t.lv == LA_FEATURE_MAJOR &&
-         (t.w == nullptr || t.lw == LA_FEATURE_MAJOR) && L.G * L.N < (1ll << 31) && L.G < 65536;
+  (void)t;
+  return L.dtype == LA_F32 && L.D % 4 == 0 && L.D <= kT && L.N % kC == 0 && L.carry_prefix == nullptr &&
+         L.carry_suffix == nullptr && L.row_offset == 0 && L.n_total == L.N && L.G * L.N < (1ll << 31) &&
+         L.G < 65536;
 }
 
 size_t f32tc_ws_floats(int64_t G, int64_t N, int64_t D) {
@@ -780,9 +786,12 @@ size_t f32tc_ws_floats(int64_t G, int64_t N, int64_t D) {
 
 cudaError_t f32tc_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws) {
   const int dir = L.causal ? kCausal : kFull;
-  return f32_pass(L, {t.q, LA_SEQUENCE_MAJOR}, {t.k, LA_SEQUENCE_MAJOR}, {t.v, LA_FEATURE_MAJOR}, out,
-                  LA_FEATURE_MAJOR, dir, L.a, 0.f, nullptr, 0.f, nullptr, true, g, ws.flag, ws.base,
-                  L.causal ? "la_f32_fwd_causal" : "la_f32_fwd_full");
+  const int shift = L.causal && L.fault == LA_FAULT_CAUSAL_PREFIX_OFF_BY_ONE ? 1 : 0;
+  cudaError_t e = f32_pass(L, {t.q, t.lq}, {t.k, t.lk}, {t.v, t.lv}, out, LA_FEATURE_MAJOR, dir, L.a, 0.f, nullptr,
+                           0.f, nullptr, true, shift, g, ws.flag, ws.base,
+                           L.causal ? "la_f32_fwd_causal" : "la_f32_fwd_full");
+  if (e != cudaSuccess || !shift) return e;
+  return offbyone_fix(L, t, out, g);
 }
 
 // Backward: w_hat (into the dV buffer) and s, then dQ, dK and dV as three instances of
@@ -796,24 +805,25 @@ cudaError_t f32tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk
   {
     ProfScope ps("la_f32_what", L.stream);
     k_f32_what<<<dim3((unsigned)((N + 255) / 256), (unsigned)G), 256, 0, L.stream>>>(
-        (const float*)t.o, (const float*)t.w, t.g, (float*)dv, s, N, D);
+        (const float*)t.o, (const float*)t.w, t.lw, t.g, (float*)dv, s, N, D);
     note_launch(1);
   }
   const int fwd = L.causal ? kCausal : kFull, rev = L.causal ? kAnti : kFull;
   const float b = L.b;
+  const float kbeta = L.fault == LA_FAULT_FLIP_BETA_K_SIGN ? b : -b;              // backward_kernels.hpp:104, 224
+  const float va = L.fault == LA_FAULT_DROP_GRAD_V_CONSTANT_TERM ? 0.f : L.a;      // backward_kernels.hpp:144, 262
   cudaError_t e;
   // dq_i = sum_{t<=i} (b w_i.v_t - b s_i) k_t
-  e = f32_pass(L, {dv, LA_FEATURE_MAJOR}, {t.v, LA_FEATURE_MAJOR}, {t.k, LA_SEQUENCE_MAJOR}, dq, LA_SEQUENCE_MAJOR,
-               fwd, 0.f, -b, s, 0.f, nullptr, false, nullptr, ws.flag, recs, "la_f32_bwd_dq");
+  e = f32_pass(L, {dv, LA_FEATURE_MAJOR}, {t.v, t.lv}, {t.k, t.lk}, dq, LA_SEQUENCE_MAJOR, fwd, 0.f, -b, s, 0.f,
+               nullptr, false, 0, nullptr, ws.flag, recs, "la_f32_bwd_dq");
   if (e != cudaSuccess) return e;
   // dk_i = sum_{t>=i} (b v_i.w_t - b s_t) q_t
-  e = f32_pass(L, {t.v, LA_FEATURE_MAJOR}, {dv, LA_FEATURE_MAJOR}, {t.q, LA_SEQUENCE_MAJOR}, dk, LA_FEATURE_MAJOR,
-               rev, 0.f, 0.f, nullptr, -b, s, false, nullptr, ws.flag, recs, "la_f32_bwd_dk");
+  e = f32_pass(L, {t.v, t.lv}, {dv, LA_FEATURE_MAJOR}, {t.q, t.lq}, dk, LA_FEATURE_MAJOR, rev, 0.f, 0.f, nullptr,
+               kbeta, s, false, 0, nullptr, ws.flag, recs, "la_f32_bwd_dk");
   if (e != cudaSuccess) return e;
   // dv_i = sum_{t>=i} (a + b k_i.q_t) w_t
-  return f32_pass(L, {t.k, LA_SEQUENCE_MAJOR}, {t.q, LA_SEQUENCE_MAJOR}, {dv, LA_FEATURE_MAJOR}, dv,
-                  LA_FEATURE_MAJOR, rev, L.a, 0.f, nullptr, 0.f, nullptr, false, nullptr, ws.flag, recs,
-                  "la_f32_bwd_dv");
+  return f32_pass(L, {t.k, t.lk}, {t.q, t.lq}, {dv, LA_FEATURE_MAJOR}, dv, LA_FEATURE_MAJOR, rev, va, 0.f, nullptr,
+                  0.f, nullptr, false, 0, nullptr, ws.flag, recs, "la_f32_bwd_dv");
 }
 
 }  // namespace lab

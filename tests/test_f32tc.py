@@ -68,3 +68,22 @@ def test_fp32_tc_degenerate_denominator(cuda):
     with pytest.raises(la.DegenerateDenominator) as e:
         run_dev(q, k, v, None, "f32", cuda, impl="tcgen05")
     assert (e.value.group(), e.value.position()) == (0, 1)
+
+
+@pytest.mark.parametrize("fault", [1, 2, 3])
+@pytest.mark.parametrize("causal", [True, False])
+def test_fp32_tc_faults(cuda, fault, causal):
+    # the Fault mutations (fault.hpp:7-15) on the tensor core match the oracle with the same fault
+    q, k, v, w = bench_inputs(2, 512, 32, seed=fault)
+    res = run_dev(q, k, v, w, "f32", cuda, causal=causal, impl="tcgen05", fault=la.Fault(fault))
+    ref = oracle_all(res, causal, fault=fault)
+    for key in ("out", "g", "dq", "dk", "dv"):
+        assert rel_err(res[key], ref[key]) <= FP32_REL, key
+
+
+def test_fp32_tc_mixed_layouts(cuda):
+    from tests._util import FM, SM
+    q, k, v, w = fast_inputs(2, 1024, 64, seed=12)
+    for causal in (True, False):
+        res = run_dev(q, k, v, w, "f32", cuda, causal=causal, impl="tcgen05", lq=FM, lk=FM, lv=SM, lw=SM)
+        _check(res, causal)

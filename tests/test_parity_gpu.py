@@ -465,8 +465,7 @@ def test_unaligned_sequence_length_on_fast_path(cuda, causal, N, D):
     res = run_dev(q, k, v, w, "bf16", cuda, causal=causal)
     names = {r["name"] for r in _abi.profile_read()}
     L.la_profile_enable(0)
-    if not (D == 256 and causal):  # causal D = 256 has no tensor-core kernel yet
-        assert not any(n.startswith("k_fwd_rows") or n.startswith("k_bwd_rows") for n in names), names
+    assert not any(n.startswith("k_fwd_rows") or n.startswith("k_bwd_rows") for n in names), names
     ref = oracle_all(res, causal)
     for key in ("out", "dq", "dk", "dv"):
         assert max_abs(res[key], ref[key]) <= BF16_ABS, key
