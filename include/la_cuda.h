@@ -117,6 +117,7 @@ typedef struct {
   int32_t bwd_fused;     /* 1: aggregate units + sweeps in one ticket-scheduled grid */
   int32_t host_blocks;   /* la_host_step: group blocks per step (default 16) */
   int32_t simt_seg_rows; /* CUDA-core path: minimum rows per segment (default 32) */
+  int32_t bwd_pair;      /* causal backward as 2-CTA clusters: 1 force, -1 never, 0 rule */
 } la_tuning;
 void la_set_tuning(const la_tuning* t); /* NULL restores the built-in rules */
 void la_get_tuning(la_tuning* t);

@@ -77,6 +77,16 @@ inline int bwd_agg_split(int64_t seg_rows) {
   return 1;
 }
 
+// Causal backward as 2-CTA clusters (la_bwd_pair.cu): one pair sweeps a whole group, the
+// W_hat pass fused in, one launch. Used with the forward's saved states when the pairs
+// fill the GPU in about one wave; otherwise the segmented single-CTA sweep.
+inline bool bwd_pair_rule(int64_t G, int num_sms = 148) {
+  if (const int t = tuning().bwd_pair) return t > 0;
+  (void)G;
+  (void)num_sms;
+  return false;  // opt-in until it beats the segmented sweep
+}
+
 struct Tensors {
   const void* q; int lq;
   const void* k; int lk;
@@ -200,6 +210,7 @@ cudaError_t full_backward(const Launch& L, const Tensors& t, void* dq, void* dk,
 cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws);
 cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv,
                         Workspace ws);
+cudaError_t tc_backward_pair(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv);
 // Non-causal helpers shared by the forward and backward files.
 int tc_kv_units(int64_t G, int64_t N);
 cudaError_t tc_sum_units(const float* recs, int64_t G, int U, float* tot, cudaStream_t st);
