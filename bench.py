@@ -192,7 +192,9 @@ def full_cpu_inputs(seed=0):
 
 def our_config(world=1, kernel="auto", graph=False):
     """The `config` object of the default arm; the reference arm reports the same one."""
-    return {"workload": "causal LA fwd+bwd B=4 H=16 N=65536 D=128 a=b=1 per GPU (BASELINE configs[1])",
+    wl = ("causal LA fwd+bwd B=4 H=16 N=65536 D=128 a=b=1 per GPU (BASELINE configs[1])" if CFG["causal"] else
+          f"non-causal LA fwd+bwd B=2 H=32 N=32768 D={CFG['dim']} a=b=1 (BASELINE configs[3])")
+    return {"workload": wl,
             "global_batch": CFG["batch"] * world, "seq_len": CFG["seq_len"], "heads": CFG["heads"],
             "dim": CFG["dim"], "parallelism": f"batch_head{world}",
             "l2": "inputs 1.07 GB each >> 126 MB L2; no flush", "kernel_impl": kernel, "cuda_graph": bool(graph)}
@@ -608,13 +610,20 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action="store_true", help="replay the step as a captured CUDA graph")
-    ap.add_argument("--config", default="2", choices=["2", "3", "5"],
-                    help="2 = the north star (default); 3 / 5 = the sharded BASELINE configs")
+    ap.add_argument("--config", default="2", choices=["2", "3", "4", "5"],
+                    help="2 = the north star (default); 3 / 5 = the sharded BASELINE configs; "
+                         "4 = the non-causal head-dim sweep (one D per run, --dim)")
+    ap.add_argument("--dim", type=int, default=128, choices=[64, 128, 256], help="config 4 head dim")
     args = ap.parse_args()
+    if args.config == "4":  # BASELINE configs[3]: same single-GPU arm, non-causal B2 H32 N32768
+        global METRIC
+        CFG.update(batch=2, heads=32, seq_len=32768, dim=args.dim, causal=False)
+        METRIC = f"non-causal LA fwd+bwd tokens/s, B=2 H=32 N=32768 D={args.dim}"
+        args.no_cpu_baseline = True  # the CPU sample above is the causal D=128 path
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":
         run_reference_arm(args)
-    elif args.config != "2":
+    elif args.config in ("3", "5"):
         run_sharded_arm(args)
     else:
         run_our_arm(args)

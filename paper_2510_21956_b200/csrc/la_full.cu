@@ -676,12 +676,12 @@ cudaError_t totals(const Launch& L, const Tensors& t, bool qw, float* units, flo
   if (qw) {
     auto k = k_full_totals<D, kBF16, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    ProfScope ps("la_full_totals_r", L.stream);
+    ProfScope ps("la_bwd_full_r", L.stream);
     k<<<grid, 192, smem, L.stream>>>(mX, mY, mO, prm);
   } else {
     auto k = k_full_totals<D, kBF16, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    ProfScope ps("la_full_totals_s", L.stream);
+    ProfScope ps("la_fwd_full_kv", L.stream);
     k<<<grid, 192, smem, L.stream>>>(mX, mY, mO, prm);
   }
   k_full_sum<<<dim3((unsigned)((F::SZ + 255) / 256), (unsigned)L.G), 256, 0, L.stream>>>(
@@ -721,7 +721,7 @@ cudaError_t forward_d(const Launch& L, const Tensors& t, void* out, float* g, Wo
     return cudaErrorInvalidValue;
   ApplyParams prm{tot, tot, nullptr, nullptr, g, ws.flag, L.N, L.n_total > 0 ? L.n_total : L.N, pl.seg_rows,
                   L.a, L.b};
-  return apply<D, kBF16, kFwd>(L, mQ, mO, prm, "la_full_fwd");
+  return apply<D, kBF16, kFwd>(L, mQ, mO, prm, "la_fwd_full_apply");
 }
 
 template <int D, bool kBF16>
@@ -746,10 +746,10 @@ cudaError_t backward_d(const Launch& L, const Tensors& t, void* dq, void* dk, vo
       !maps_feat(&mdK, dk, kBF16, L.G, L.N, D, F::CR) || !maps_feat(&mdV, dv, kBF16, L.G, L.N, D, F::CR))
     return cudaErrorInvalidValue;
   ApplyParams pq{totS, totS, t.g, s, nullptr, nullptr, L.N, L.N, pl.seg_rows, L.a, L.b};
-  if ((e = apply<D, kBF16, kDQ>(L, mW, mdQ, pq, "la_full_dq")) != cudaSuccess) return e;
+  if ((e = apply<D, kBF16, kDQ>(L, mW, mdQ, pq, "la_bwd_full_dq")) != cudaSuccess) return e;
   ApplyParams pr{totR, totR, nullptr, nullptr, nullptr, nullptr, L.N, L.N, pl.seg_rows, L.a, L.b};
-  if ((e = apply<D, kBF16, kDK>(L, mV, mdK, pr, "la_full_dk")) != cudaSuccess) return e;
-  return apply<D, kBF16, kDV>(L, mK, mdV, pr, "la_full_dv");
+  if ((e = apply<D, kBF16, kDK>(L, mV, mdK, pr, "la_bwd_full_dk")) != cudaSuccess) return e;
+  return apply<D, kBF16, kDV>(L, mK, mdV, pr, "la_bwd_full_dv");
 }
 
 template <int D>

@@ -199,8 +199,8 @@ def test_noncausal_full_tc_path_runs_and_matches(cuda, D, a, b):
     res = run_dev(q, k, v, w, "f16", cuda, causal=False, a=a, b=b)
     names = {r["name"] for r in _abi.profile_read()}
     L.la_profile_enable(0)
-    assert {"la_full_totals_s", "la_full_totals_r", "la_full_fwd", "la_full_dq", "la_full_dk",
-            "la_full_dv"} <= names, names
+    assert {"la_fwd_full_kv", "la_bwd_full_r", "la_fwd_full_apply", "la_bwd_full_dq", "la_bwd_full_dk",
+            "la_bwd_full_dv"} <= names, names
     ref = oracle_all(res, False, a=a, b=b)
     for key in ("out", "dq", "dk", "dv"):
         assert max_abs(res[key], ref[key]) <= BF16_ABS, (D, key)
