@@ -35,7 +35,13 @@ namespace {
 template <int D>
 struct FG {
   static constexpr int NH = (D + 127) / 128;     // 128-lane halves of the feature dimension
-  static constexpr int CR = D <= 64 ? 128 : 64;  // rows per chunk (MMA N of the apply pass)
+  static constexpr int CR = 64;                  // rows per chunk (MMA N of the apply pass)
+  // D = 64 needs few TMEM columns and little shared memory: two CTAs per SM (the passes
+  // are latency-bound with one: 4 CUDA-core warps, half of the 128 lanes used).
+  static constexpr int kCtas = D <= 64 ? 2 : 1;
+  static constexpr uint32_t kTmemTot = D <= 64 ? 128 : 512;  // totals: NH x 256-column blocks
+  static constexpr uint32_t kTmemApp = D <= 64 ? 256 : 512;  // apply: W + 2 x NH x CR
+  static constexpr uint32_t kAccApp = D <= 64 ? 64 : 256;
   static constexpr int KS = D / 16;              // MMA k-steps over the feature dimension
   static constexpr int T = CR * D * 2;           // one [CR][D] or [D][CR] 16-bit tile
   static constexpr int64_t SZ = (D * D + 2 * D + 1 + 3) & ~3;  // state_floats(D)
@@ -102,7 +108,7 @@ struct TotParams {
 // kQW = true:  X = Q, Y^T = W_hat^T = Omega^T / g (scaled in place), third tile O^T:
 //              R[m][j], u = sum s_i q_i, c = sum w_hat; s_i = o_i . w_hat_i -> s_out.
 template <int D, bool kBF16, bool kQW>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(192, FG<D>::kCtas)
     k_full_totals(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY,
                   const __grid_constant__ CUtensorMap tmO, TotParams prm) {
   using F = FG<D>;
@@ -140,7 +146,7 @@ __global__ void __launch_bounds__(192, 1)
     mbar_init(done, 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<512>(tslot);
+  if (warp == 1) tmem_alloc<F::kTmemTot>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -315,7 +321,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<512>(tmem);
+  if (warp == 1) tmem_dealloc<F::kTmemTot>(tmem);
 }
 
 // Per-group totals: tot[g] = sum_u recs[g][u] (elements D*D + 2D + 1; padding zero).
@@ -349,7 +355,7 @@ struct ApplyParams {
 //   kDK:  W[m][j] = b R[m][j],  Y^T = V^T (MN-major),       dK^T = acc - b u_m
 //   kDV:  W[j][m] = b R[m][j],  Y = K (K-major),            dV^T = acc + a c_j
 template <int D, bool kBF16, int kMode>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(192, FG<D>::kCtas)
     k_full_apply(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmOut,
                  ApplyParams prm) {
   using F = FG<D>;
@@ -359,7 +365,7 @@ __global__ void __launch_bounds__(192, 1)
   constexpr int STAGE = (T + (kMode == kDQ ? 2 * CR * 4 : 0) + 1023) & ~1023;  // + g, s of the chunk
   constexpr int NS = 3;
   constexpr int RPT = (D + 127) / 128;
-  constexpr uint32_t kAcc = 256;  // accumulators: [256, 512) = 2 buffers x NH halves x CR columns
+  constexpr uint32_t kAcc = F::kAccApp;  // accumulators: 2 buffers x NH halves x CR columns after W
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* stg = smem + NS * STAGE;              // [2][T] output staging
@@ -396,7 +402,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<512>(tslot);
+  if (warp == 1) tmem_alloc<F::kTmemApp>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -617,7 +623,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<512>(tmem);
+  if (warp == 1) tmem_dealloc<F::kTmemApp>(tmem);
 }
 
 template <int D>
