@@ -95,6 +95,38 @@ __device__ __forceinline__ void block_colsum(float (&v)[kN], float* part, float*
   named_bar(1, 128);
 }
 
+// Column sums of a [CR][D] K-major tile (optionally weighted per row): thread (mg, tg) =
+// (et >> 3, et & 7) sums rows tg + 8 k of the 8 columns of group cg = mg + 16 q with 16-byte
+// loads (a quarter-warp reads 8 rows of one 16-byte column chunk: distinct swizzle chunks),
+// then a reduce-scatter over the 8 tg lanes leaves column 8 cg + tg in lane tg.
+template <int D, bool kBF16, bool kW>
+__device__ __forceinline__ void col_sums(const uint8_t* xt, const float* w, float (&ucol)[(D + 127) / 128], int et) {
+  constexpr int CR = FG<D>::CR;
+  const int mg = et >> 3, tg = et & 7;
+#pragma unroll
+  for (int q = 0; q < (D + 127) / 128; ++q) {
+    const int cg = mg + 16 * q;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (cg < D / 8) {
+#pragma unroll
+      for (int k = 0; k < CR / 8; ++k) {
+        const int i = tg + 8 * k;
+        const uint4 v4 = *(const uint4*)(xt + sw128_off(i, 8 * cg, CR));
+        const float wi = kW ? w[i] : 1.f;
+        const uint32_t vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const float2 f2 = unpack2<kBF16>(vv[h]);
+          acc[2 * h] += wi * f2.x;
+          acc[2 * h + 1] += wi * f2.y;
+        }
+      }
+    }
+    const float tot = reduce_scatter8(acc, tg);  // whole warp: the shuffles need every lane
+    if (cg < D / 8) ucol[q] += tot;
+  }
+}
+
 // ================================================================ totals over row units
 struct TotParams {
   const float* g;   // [G][N] (QW)
@@ -197,9 +229,10 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
     const int r = (int)(qd * 32 + lane_id());  // TMEM lane of this thread's warp quadrant
     // thread et owns feature rows f = et + 128 q (q < RPT) for the row-wise sums, and the
     // feature columns m = et + 128 q for the column-wise ones
-    float va[RPT], vb[RPT];  // z or u (columns m) ; sigma or c (rows j)
+    float vb[RPT];  // sigma or c (rows j of the Y^T tile)
 #pragma unroll
-    for (int q = 0; q < RPT; ++q) va[q] = vb[q] = 0.f;
+    for (int q = 0; q < RPT; ++q) vb[q] = 0.f;
+    float ucol[(D + 127) / 128] = {};  // z or u: column sums in col_sums' (mg, tg) layout
     for (int c = 0; c < nc; ++c) {
       const int s = c % NS;
       uint8_t* st = smem + s * STAGE;
@@ -248,25 +281,16 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
         fence_proxy_async();
         mbar_arrive(&wready[s]);
         if (et < CR) prm.s_out[grp * prm.N + r0 + (int64_t)c * CR + et] = sv[et];
-        // u_m += sum_i s_i q_im (column m of the Q tile)
-#pragma unroll
-        for (int q = 0; q < RPT; ++q) {
-          const int m = et + 128 * q;
-          if (m < D) {
-            float acc = 0.f;
-#pragma unroll 8
-            for (int i = 0; i < CR; ++i) acc += sv[i] * ld16<kBF16>(xt + sw128_off(i, m, CR));
-            va[q] += acc;
-          }
-        }
+        // u_m += sum_i s_i q_im: thread (mg, tg) sums rows tg + 8 k of columns
+        // [8 mg, 8 mg + 8) with 16-byte loads, then a reduce-scatter over the 8 tg lanes
+        col_sums<D, kBF16, true>(xt, sv, ucol, et);
       } else {
+        col_sums<D, kBF16, false>(xt, nullptr, ucol, et);  // z_m: column sums of K
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
           const int f = et + 128 * q;
           if (f < D) {
-            float zs = 0.f, ss = 0.f;
-#pragma unroll 8
-            for (int i = 0; i < CR; ++i) zs += ld16<kBF16>(xt + sw128_off(i, f, CR));  // z_m: column of K
+            float ss = 0.f;
 #pragma unroll
             for (int i8 = 0; i8 < CR; i8 += 8) {  // sigma_j: row of V^T
               const uint4 v4 = *(const uint4*)(yt + sw128_off(f, i8, D));
@@ -277,7 +301,6 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
                 ss += v2.x + v2.y;
               }
             }
-            va[q] += zs;
             vb[q] += ss;
           }
         }
@@ -312,10 +335,9 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const int f = et + 128 * q;
-      if (f < D) {
-        rec[D * D + f] = va[q];
-        rec[D * D + D + f] = vb[q];
-      }
+      if (f < D) rec[D * D + D + f] = vb[q];
+      const int cg = (et >> 3) + 16 * q;  // z / u: col_sums' layout
+      if (cg < D / 8) rec[D * D + 8 * cg + (et & 7)] = ucol[q];
     }
     if (et == 0) rec[D * D + 2 * D] = (float)(r1 > r0 ? r1 - r0 : 0);
   }
@@ -577,11 +599,16 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
           tmem_ld32(tmem + lb + kAcc + (bb * NH + h) * CR + c0, x);
           tmem_ld_wait();
           if (f < D) {
-            if (kMode == kDQ) {  // dQ[i][f]: SequenceMajor staging [CR][D]
-              const float* sv = sbuf + bb * CR + c0;
+            if (kMode == kDQ) {  // dQ[i][f]: SequenceMajor staging [CR][D]; lanes f, f ^ 1 trade
+              const float* sv = sbuf + bb * CR + c0;  // values: even lanes store (f, f+1) of row i,
+              const bool odd = (lane_id() & 1) != 0;   // odd lanes (f-1, f) of row i + 1
 #pragma unroll
-              for (int k = 0; k < 32; ++k)
-                st16<kBF16>(so + sw128_off(c0 + k, f, CR), __uint_as_float(x[k]) - bh * sv[k]);
+              for (int k = 0; k < 32; k += 2) {
+                const float v0 = __uint_as_float(x[k]) - bh * sv[k], v1 = __uint_as_float(x[k + 1]) - bh * sv[k + 1];
+                const float got = __shfl_xor_sync(0xffffffffu, odd ? v0 : v1, 1);
+                const uint32_t w2 = odd ? pack2<kBF16>(got, v1) : pack2<kBF16>(v0, got);
+                *(uint32_t*)(so + sw128_off(c0 + k + (odd ? 1 : 0), f & ~1, CR)) = w2;
+              }
             } else {  // FeatureMajor staging [D][CR]: row f
               const float* gv = ginv + bb * CR + c0;
 #pragma unroll
