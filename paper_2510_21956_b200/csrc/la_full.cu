@@ -376,8 +376,11 @@ struct ApplyParams {
 //   kDQ:  W[m][j] = b S[m][j],  Y^T = Omega^T / g (MN-major), dQ = acc - b z_m s_i (transposed store)
 //   kDK:  W[m][j] = b R[m][j],  Y^T = V^T (MN-major),       dK^T = acc - b u_m
 //   kDV:  W[j][m] = b R[m][j],  Y = K (K-major),            dV^T = acc + a c_j
+template <int D>
+constexpr int apply_wgs(int mode) { return mode == 1 ? FG<D>::NH : 1; }  // kDQ: a warpgroup per half
+
 template <int D, bool kBF16, int kMode>
-__global__ void __launch_bounds__(192, FG<D>::kCtas)
+__global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
     k_full_apply(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmOut,
                  ApplyParams prm) {
   using F = FG<D>;
@@ -387,6 +390,7 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
   constexpr int STAGE = (T + (kMode == kDQ ? 2 * CR * 4 : 0) + 1023) & ~1023;  // + g, s of the chunk
   constexpr int NS = 3;
   constexpr int RPT = (D + 127) / 128;
+  constexpr int kWG = apply_wgs<D>(kMode), kCT = 128 * kWG;  // compute warpgroups (kDQ: one per half)
   constexpr uint32_t kAcc = F::kAccApp;  // accumulators: 2 buffers x NH halves x CR columns after W
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
@@ -415,12 +419,12 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
     tma_prefetch(&tmOut);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1 + (kPre ? 128 : 0));
-      mbar_init(&pre[s], 128);
+      mbar_init(&empty[s], 1 + (kPre ? kCT : 0));
+      mbar_init(&pre[s], kCT);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 128);
+      mbar_init(&acc_empty[b], kCT);
     }
     fence_barrier_init();
   }
@@ -430,6 +434,7 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
   tc_fence_after();
   const uint32_t tmem = *tslot;
   const int et = (int)threadIdx.x - 64;
+  const int wg = kWG > 1 ? (et >> 7) : 0;  // compute warpgroup: feature half h = wg (+ kWG ...)
   const uint32_t qd = warp & 3;
   const int r = (int)(qd * 32 + lane_id());
   const uint32_t lb = (qd * 32u) << 16;
@@ -439,7 +444,7 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
     constexpr bool kTrans = kMode == kFwd || kMode == kDV;  // W[f][k] = b X[k][f]
     const float b = prm.b;
 #pragma unroll 1
-    for (int h = 0; h < NH; ++h) {
+    for (int h = wg; h < NH; h += kWG) {
       const int f = 128 * h + r;
 #pragma unroll 1
       for (int k0 = 0; k0 < D; k0 += 64) {
@@ -459,7 +464,7 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
     }
     tmem_st_wait();
     if (kMode == kFwd)
-      for (int m = et; m < D; m += 128) zf[m] = tot[D * D + m];
+      for (int m = et; m < D; m += kCT) zf[m] = tot[D * D + m];
   }
   tc_fence_before();
   __syncthreads();
@@ -526,8 +531,8 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
       uint8_t* st = smem + s * STAGE;
       mbar_wait(&full[s], (c / NS) & 1);
       const int64_t row0 = s0 + (int64_t)c * CR;
-      if (kMode == kFwd) {  // g_i = a N + b q_i . z; 128 / CR threads per row
-        constexpr int TPR = 128 / CR;
+      if (kMode == kFwd) {  // g_i = a N + b q_i . z; kCT / CR threads per row
+        constexpr int TPR = kCT / CR;
         const int i = et / TPR, part_k = et % TPR;
         float acc = 0.f;
 #pragma unroll
@@ -556,11 +561,11 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
           ginv[(c & 1) * CR + et] = 1.f / gg[et];
           sbuf[(c & 1) * CR + et] = ss[et];
         }
-        named_bar(1, 128);
+        named_bar(1, kCT);
         const float* gi = ginv + (c & 1) * CR;
 #pragma unroll
-        for (int q = 0; q < RPT; ++q) {
-          const int f = et + 128 * q;
+        for (int q = wg; q < RPT; q += kWG) {
+          const int f = (et & 127) + 128 * q;
           if (f < D) {
 #pragma unroll
             for (int i8 = 0; i8 < CR; i8 += 8) {
@@ -587,10 +592,10 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
       mbar_wait(&acc_full[bb], (c >> 1) & 1);
       tc_fence_after();
       if (et == 0) tma_store_wait_read1();  // the store that used staging bb two chunks ago
-      named_bar(1, 128);
+      named_bar(1, kCT);
       uint8_t* so = stg + bb * T;
 #pragma unroll 1
-      for (int h = 0; h < NH; ++h) {
+      for (int h = wg; h < NH; h += kWG) {
         const int f = 128 * h + r;
         const float bh = h == 0 ? bias[0] : bias[RPT - 1];
 #pragma unroll 1
@@ -633,7 +638,7 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
       tc_fence_before();
       mbar_arrive(&acc_empty[bb]);
       fence_proxy_async();
-      named_bar(1, 128);
+      named_bar(1, kCT);
       if (et == 0) {
         if (kMode == kDQ)
           tma_store_3d(&tmOut, so, 0, (int)(grp * prm.N + row0), 0);
@@ -732,7 +737,7 @@ cudaError_t apply(const Launch& L, const CUtensorMap& mY, const CUtensorMap& mOu
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   {
     ProfScope ps(name, L.stream);
-    k<<<dim3((unsigned)pl.P, (unsigned)L.G), 192, smem, L.stream>>>(mY, mOut, prm);
+    k<<<dim3((unsigned)pl.P, (unsigned)L.G), 64 + 128 * apply_wgs<D>(kMode), smem, L.stream>>>(mY, mOut, prm);
   }
   note_launch(1);
   return cudaGetLastError();
