@@ -38,9 +38,11 @@ struct FG {
   static constexpr int CR = 64;                  // rows per chunk (MMA N of the apply pass)
   // D = 64 needs few TMEM columns and little shared memory: two CTAs per SM (the passes
   // are latency-bound with one: 4 CUDA-core warps, half of the 128 lanes used).
-  static constexpr int kCtas = D <= 64 ? 2 : 1;
+  static constexpr int kCtas = D <= 64 ? 3 : 1;
+  static constexpr int kTotStages = D <= 64 ? 2 : 0;         // 0: the stage-size rule of k_full_totals
+  static constexpr int kAccBufs = D <= 64 ? 1 : 2;           // apply accumulators (D = 64: CTAs overlap)
   static constexpr uint32_t kTmemTot = D <= 64 ? 128 : 512;  // totals: NH x 256-column blocks
-  static constexpr uint32_t kTmemApp = D <= 64 ? 256 : 512;  // apply: W + 2 x NH x CR
+  static constexpr uint32_t kTmemApp = D <= 64 ? 128 : 512;  // apply: W + kAccBufs x NH x CR
   static constexpr uint32_t kAccApp = D <= 64 ? 64 : 256;
   static constexpr int KS = D / 16;              // MMA k-steps over the feature dimension
   static constexpr int T = CR * D * 2;           // one [CR][D] or [D][CR] 16-bit tile
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
   using F = FG<D>;
   constexpr int CR = F::CR, T = F::T, NT = kQW ? 3 : 2;
   constexpr int STAGE = (NT * T + CR * 4 + 1023) & ~1023;  // tiles + g of the chunk (QW), 1 KB aligned
-  constexpr int NS = (STAGE <= 56 * 1024) ? 3 : 2;
+  constexpr int NS = F::kTotStages ? F::kTotStages : (STAGE <= 56 * 1024) ? 3 : 2;
   constexpr int RPT = (D + 127) / 128;  // feature rows per CUDA-core thread
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
@@ -492,11 +494,11 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
     constexpr uint32_t fmt = kBF16 ? 1 : 0;
     const uint32_t id = idesc_f16(128, CR, fmt, 0, kSeqIn ? 0 : 1);
     for (int c = 0; c < nc; ++c) {
-      const int s = c % NS, bb = c & 1;
+      const int s = c % NS, bb = c % F::kAccBufs;
       const uint32_t aY = smem_u32(smem + s * STAGE);
       mbar_wait(&full[s], (c / NS) & 1);
       if (kMode == kDQ) mbar_wait(&pre[s], (c / NS) & 1);
-      if (c >= 2) mbar_wait(&acc_empty[bb], ((c - 2) >> 1) & 1);
+      if (c >= F::kAccBufs) mbar_wait(&acc_empty[bb], ((c / F::kAccBufs) & 1) ^ 1);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
@@ -587,13 +589,13 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
       }
     };
     auto epilogue = [&](int c) {
-      const int bb = c & 1;
+      const int bb = c % F::kAccBufs, sb = c & 1;  // accumulator buffer, staging buffer
       const int64_t row0 = s0 + (int64_t)c * CR;
-      mbar_wait(&acc_full[bb], (c >> 1) & 1);
+      mbar_wait(&acc_full[bb], (c / F::kAccBufs) & 1);
       tc_fence_after();
-      if (et == 0) tma_store_wait_read1();  // the store that used staging bb two chunks ago
+      if (et == 0) tma_store_wait_read1();  // the store that used staging sb two chunks ago
       named_bar(1, kCT);
-      uint8_t* so = stg + bb * T;
+      uint8_t* so = stg + sb * T;
 #pragma unroll 1
       for (int h = wg; h < NH; h += kWG) {
         const int f = 128 * h + r;
@@ -605,7 +607,7 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
           tmem_ld_wait();
           if (f < D) {
             if (kMode == kDQ) {  // dQ[i][f]: SequenceMajor staging [CR][D]; lanes f, f ^ 1 trade
-              const float* sv = sbuf + bb * CR + c0;  // values: even lanes store (f, f+1) of row i,
+              const float* sv = sbuf + sb * CR + c0;  // values: even lanes store (f, f+1) of row i,
               const bool odd = (lane_id() & 1) != 0;   // odd lanes (f-1, f) of row i + 1
 #pragma unroll
               for (int k = 0; k < 32; k += 2) {
@@ -615,7 +617,7 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
                 *(uint32_t*)(so + sw128_off(c0 + k + (odd ? 1 : 0), f & ~1, CR)) = w2;
               }
             } else {  // FeatureMajor staging [D][CR]: row f
-              const float* gv = ginv + bb * CR + c0;
+              const float* gv = ginv + sb * CR + c0;
 #pragma unroll
               for (int k8 = 0; k8 < 32; k8 += 8) {
                 uint32_t pk[4];
