@@ -228,19 +228,27 @@ def run_reference_arm(args):
 
         def fn():
             O.fwd_bwd_f32_threads(q, k, v3, w3, threads=cores)
-    for _ in range(args.warmup):
+    # one full fwd+bwd takes ~16-20 s on 16 cores: at most one warm-up step (it only pages in
+    # the buffers), and the timed steps stop once --ref-budget-s is spent (at least 2), so the
+    # arm ends within a few minutes; `steps` / `warmup` report what actually ran
+    warm = min(args.warmup, 1)
+    for _ in range(warm):
         fn()
     times = []
-    for _ in range(args.steps):
+    t_start = time.perf_counter()
+    for i in range(args.steps):
         t0 = time.perf_counter()
         fn()
         times.append(time.perf_counter() - t0)
+        if i + 1 >= 2 and time.perf_counter() - t_start > args.ref_budget_s:
+            break
     t = sum(times) / len(times)
     val = CFG["batch"] * N / t
     src = ("reference la_core detail::run_forward<float> + run_backward<float> (oracle/_ref, built from "
            "/root/reference/proj/src)" if kind == "reference" else "oracle/oracle.c f32 port")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "steps": len(times), "warmup": warm, "steps_requested": args.steps, "warmup_requested": args.warmup,
+            "ms_per_step": t * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (U(-1,1), unit-norm q/k rows)", "config": our_config(),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": kind,
@@ -607,6 +615,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "tcgen05"])
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="--impl reference: stop timing full-workload CPU steps after this many seconds")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action="store_true", help="replay the step as a captured CUDA graph")

@@ -58,45 +58,6 @@ __device__ __forceinline__ uint64_t mnmaj(uint32_t tile, int ks, uint32_t panel)
   return sdesc_sw128(tile, panel, 1024) + (uint64_t)((ks * 2048) >> 4);
 }
 
-template <bool kBF16>
-__device__ __forceinline__ float ld16(const uint8_t* p) {
-  const uint16_t h = *(const uint16_t*)p;
-  return kBF16 ? __bfloat162float(__ushort_as_bfloat16(h)) : __half2float(__ushort_as_half(h));
-}
-template <bool kBF16>
-__device__ __forceinline__ void st16(uint8_t* p, float x) {
-  *(uint16_t*)p = kBF16 ? __bfloat16_as_ushort(__float2bfloat16_rn(x)) : __half_as_ushort(__float2half_rn(x));
-}
-
-// Sum over the 128 CUDA-core threads (4 warps) of per-thread values v[0..n) -> out[0..n):
-// a warp reduce-scatter (lane k ends with the warp sum of value k of each 32-block), then
-// the 4 warp partials through shared memory. `part` holds 4 * n floats.
-template <int kN>
-__device__ __forceinline__ void block_colsum(float (&v)[kN], float* part, float* out, int et) {
-  static_assert(kN % 32 == 0, "multiple of 32 values");
-  const int lane = et & 31, wq = et >> 5;
-#pragma unroll
-  for (int b = 0; b < kN; b += 32) {
-    float* x = v + b;
-    // recursive halving: after the step with offset o, lane keeps the half selected by its bit
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      const bool up = (lane & o) != 0;
-#pragma unroll
-      for (int k = 0; k < o; ++k) {
-        const float send = up ? x[k] : x[k + o];
-        const float keep = up ? x[k + o] : x[k];
-        x[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-      }
-    }
-    // lane now holds the sum of value b + (bit-reversed position) -> x[0]: value index = lane
-    part[wq * kN + b + lane] = x[0];
-  }
-  named_bar(1, 128);
-  for (int i = et; i < kN; i += 128) out[i] = part[i] + part[kN + i] + part[2 * kN + i] + part[3 * kN + i];
-  named_bar(1, 128);
-}
-
 // Column sums of a [CR][D] K-major tile (optionally weighted per row): thread (mg, tg) =
 // (et >> 3, et & 7) sums rows tg + 8 k of the 8 columns of group cg = mg + 16 q with 16-byte
 // loads (a quarter-warp reads 8 rows of one 16-byte column chunk: distinct swizzle chunks),
@@ -152,10 +113,8 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
   constexpr int RPT = (D + 127) / 128;  // feature rows per CUDA-core thread
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  float* ginv = (float*)(smem + NS * STAGE);        // [CR]
-  float* sv = ginv + CR;                            // [CR] s of the chunk
-  float* part = sv + CR;                            // [4][CR]
-  uint64_t* bars = (uint64_t*)(part + 4 * CR);
+  float* sv = (float*)(smem + NS * STAGE);          // [CR] s of the chunk
+  uint64_t* bars = (uint64_t*)(sv + 6 * CR);
   uint64_t* full = bars;            // [NS]
   uint64_t* empty = bars + 4;       // [NS]
   uint64_t* wready = bars + 8;      // [NS] (QW: W_hat^T written)
@@ -226,14 +185,20 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
     }
   } else {
     // ------------------------------------------------------------ CUDA cores (128 threads)
+    // Y^T tile [D rows j][CR = 64 columns i]: thread (jg, ig) = (et & 15, et >> 4) owns the
+    // 16-byte column chunk ig (columns 8 ig .. 8 ig + 7) of rows j = jg + 16 rr (every lane
+    // busy for any D; a quarter-warp reads 8 consecutive rows: distinct swizzle chunks).
+    // Row sums (sigma / c) stay per thread until the unit ends; column sums of X (z / u)
+    // go through col_sums.
+    static_assert(CR == 64, "the (jg, ig) tiling covers 64 columns");
+    constexpr int RR = D / 16;
     const int et = (int)threadIdx.x - 64;
     const uint32_t qd = warp & 3;
     const int r = (int)(qd * 32 + lane_id());  // TMEM lane of this thread's warp quadrant
-    // thread et owns feature rows f = et + 128 q (q < RPT) for the row-wise sums, and the
-    // feature columns m = et + 128 q for the column-wise ones
-    float vb[RPT];  // sigma or c (rows j of the Y^T tile)
+    const int jg = et & 15, ig = et >> 4;
+    float crow[RR];  // sigma_j or c_j partials of this thread's 8 columns, rows jg + 16 rr
 #pragma unroll
-    for (int q = 0; q < RPT; ++q) vb[q] = 0.f;
+    for (int q = 0; q < RR; ++q) crow[q] = 0.f;
     float ucol[(D + 127) / 128] = {};  // z or u: column sums in col_sums' (mg, tg) layout
     for (int c = 0; c < nc; ++c) {
       const int s = c % NS;
@@ -242,77 +207,70 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
       const uint8_t* xt = st;  // [CR][D] K-major panels of CR rows
       uint8_t* yt = st + T;    // [D][CR] panels of D rows (64 row-elements each)
       if (kQW) {
+        // W_hat^T = Omega^T / g in place; c_j += w_hat; s_i = sum_j o_ij w_hat_ij
         const float* gg = (const float*)(st + NT * T);
-        if (et < CR) ginv[et] = 1.f / gg[et];
-        named_bar(1, 128);
-        // W_hat^T = Omega^T / g in place; c_j += w_hat; s_i = sum_j o_ij w_hat_ij, 32
-        // columns at a time (bounded registers)
+        const float4 g0 = *(const float4*)(gg + 8 * ig), g1 = *(const float4*)(gg + 8 * ig + 4);
+        const float gi[8] = {1.f / g0.x, 1.f / g0.y, 1.f / g0.z, 1.f / g0.w, 1.f / g1.x, 1.f / g1.y, 1.f / g1.z, 1.f / g1.w};
         const uint8_t* ot = st + 2 * T;
-#pragma unroll 1
-        for (int ib = 0; ib < CR; ib += 32) {
-          float ps[32];
+        float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int i = 0; i < 32; ++i) ps[i] = 0.f;
+        for (int rr = 0; rr < RR; ++rr) {
+          const uint32_t off = sw128_off(jg + 16 * rr, 8 * ig, D);
+          uint4 w4 = *(const uint4*)(yt + off);
+          const uint4 o4 = *(const uint4*)(ot + off);
+          uint32_t* wp = (uint32_t*)&w4;
+          const uint32_t* op = (const uint32_t*)&o4;
 #pragma unroll
-          for (int q = 0; q < RPT; ++q) {
-            const int f = et + 128 * q;
-            if (f < D) {
-#pragma unroll
-              for (int i8 = 0; i8 < 32; i8 += 8) {
-                const uint32_t off = sw128_off(f, ib + i8, D);
-                uint4 w4 = *(const uint4*)(yt + off);
-                const uint4 o4 = *(const uint4*)(ot + off);
-                uint32_t* wp = (uint32_t*)&w4;
-                const uint32_t* op = (const uint32_t*)&o4;
-#pragma unroll
-                for (int h2 = 0; h2 < 4; ++h2) {
-                  const float2 w2 = unpack2<kBF16>(wp[h2]), o2 = unpack2<kBF16>(op[h2]);
-                  const int i = i8 + 2 * h2;
-                  const float w0 = w2.x * ginv[ib + i], w1 = w2.y * ginv[ib + i + 1];
-                  vb[q] += w0 + w1;
-                  ps[i] += o2.x * w0;
-                  ps[i + 1] += o2.y * w1;
-                  wp[h2] = pack2<kBF16>(w0, w1);
-                }
-                *(uint4*)(yt + off) = w4;
-              }
-            }
+          for (int h2 = 0; h2 < 4; ++h2) {
+            const float2 w2 = unpack2<kBF16>(wp[h2]), o2 = unpack2<kBF16>(op[h2]);
+            const float w0 = w2.x * gi[2 * h2], w1 = w2.y * gi[2 * h2 + 1];
+            crow[rr] += w0 + w1;
+            sp[2 * h2] += o2.x * w0;
+            sp[2 * h2 + 1] += o2.y * w1;
+            wp[h2] = pack2<kBF16>(w0, w1);
           }
-          block_colsum<32>(ps, part, sv + ib, et);
+          *(uint4*)(yt + off) = w4;
+        }
+        // s_i: sum over the 16 jg lanes of each column chunk
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+          for (int o = 1; o < 16; o <<= 1) sp[k] += __shfl_xor_sync(0xffffffffu, sp[k], o);
+        if (jg == 0) {
+          *(float4*)(sv + 8 * ig) = make_float4(sp[0], sp[1], sp[2], sp[3]);
+          *(float4*)(sv + 8 * ig + 4) = make_float4(sp[4], sp[5], sp[6], sp[7]);
         }
         fence_proxy_async();
         mbar_arrive(&wready[s]);
+        named_bar(1, 128);  // s of the chunk complete
         if (et < CR) prm.s_out[grp * prm.N + r0 + (int64_t)c * CR + et] = sv[et];
-        // u_m += sum_i s_i q_im: thread (mg, tg) sums rows tg + 8 k of columns
-        // [8 mg, 8 mg + 8) with 16-byte loads, then a reduce-scatter over the 8 tg lanes
-        col_sums<D, kBF16, true>(xt, sv, ucol, et);
+        col_sums<D, kBF16, true>(xt, sv, ucol, et);  // u_m += sum_i s_i q_im
+        named_bar(1, 128);  // sv is rewritten by the next chunk
       } else {
         col_sums<D, kBF16, false>(xt, nullptr, ucol, et);  // z_m: column sums of K
 #pragma unroll
-        for (int q = 0; q < RPT; ++q) {
-          const int f = et + 128 * q;
-          if (f < D) {
-            float ss = 0.f;
+        for (int rr = 0; rr < RR; ++rr) {  // sigma_j: rows of V^T
+          const uint4 v4 = *(const uint4*)(yt + sw128_off(jg + 16 * rr, 8 * ig, D));
+          const uint32_t vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-            for (int i8 = 0; i8 < CR; i8 += 8) {  // sigma_j: row of V^T
-              const uint4 v4 = *(const uint4*)(yt + sw128_off(f, i8, D));
-              const uint32_t* vp = (const uint32_t*)&v4;
-#pragma unroll
-              for (int h2 = 0; h2 < 4; ++h2) {
-                const float2 v2 = unpack2<kBF16>(vp[h2]);
-                ss += v2.x + v2.y;
-              }
-            }
-            vb[q] += ss;
+          for (int h2 = 0; h2 < 4; ++h2) {
+            const float2 v2 = unpack2<kBF16>(vv[h2]);
+            crow[rr] += v2.x + v2.y;
           }
         }
       }
       mbar_arrive(&empty[s]);
     }
+    // row sums: the 8 ig partials of each row j -> vrow (shared scratch: the stages are idle
+    // once the unit's MMAs have retired)
+    if (nc > 0) mbar_wait(done, 0);
+    float* red = (float*)smem;  // [8 ig][D]
+#pragma unroll
+    for (int rr = 0; rr < RR; ++rr) red[ig * D + jg + 16 * rr] = crow[rr];
+    named_bar(1, 128);
     // ---- the unit's record: X[m][j] (lanes m), vA (z | u), vB (sigma | c), rows
     float* rec = prm.recs + (grp * prm.U + u) * F::SZ;
     if (nc > 0) {
-      mbar_wait(done, 0);
       tc_fence_after();
 #pragma unroll 1
       for (int h = 0; h < F::NH; ++h) {
@@ -337,7 +295,12 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const int f = et + 128 * q;
-      if (f < D) rec[D * D + D + f] = vb[q];
+      if (f < D) {  // sigma | c: the 8 column-chunk partials of row f
+        float v = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v += red[k * D + f];
+        rec[D * D + D + f] = v;
+      }
       const int cg = (et >> 3) + 16 * q;  // z / u: col_sums' layout
       if (cg < D / 8) rec[D * D + 8 * cg + (et & 7)] = ucol[q];
     }
@@ -564,24 +527,22 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
           sbuf[(c & 1) * CR + et] = ss[et];
         }
         named_bar(1, kCT);
+        // (jg, ig) tiling: rows j = jg + 16 rr (rr = wg mod kWG), the 16-byte column chunk ig
         const float* gi = ginv + (c & 1) * CR;
+        const int e = et & 127, jg = e & 15, ig = e >> 4;
+        const float4 ga = *(const float4*)(gi + 8 * ig), gb = *(const float4*)(gi + 8 * ig + 4);
+        const float g8[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
 #pragma unroll
-        for (int q = wg; q < RPT; q += kWG) {
-          const int f = (et & 127) + 128 * q;
-          if (f < D) {
+        for (int rr = wg; rr < D / 16; rr += kWG) {
+          const uint32_t off = sw128_off(jg + 16 * rr, 8 * ig, D);
+          uint4 w4 = *(const uint4*)(st + off);
+          uint32_t* wp = (uint32_t*)&w4;
 #pragma unroll
-            for (int i8 = 0; i8 < CR; i8 += 8) {
-              const uint32_t off = sw128_off(f, i8, D);
-              uint4 w4 = *(const uint4*)(st + off);
-              uint32_t* wp = (uint32_t*)&w4;
-#pragma unroll
-              for (int h2 = 0; h2 < 4; ++h2) {
-                const float2 w2 = unpack2<kBF16>(wp[h2]);
-                wp[h2] = pack2<kBF16>(w2.x * gi[i8 + 2 * h2], w2.y * gi[i8 + 2 * h2 + 1]);
-              }
-              *(uint4*)(st + off) = w4;
-            }
+          for (int h2 = 0; h2 < 4; ++h2) {
+            const float2 w2 = unpack2<kBF16>(wp[h2]);
+            wp[h2] = pack2<kBF16>(w2.x * g8[2 * h2], w2.y * g8[2 * h2 + 1]);
           }
+          *(uint4*)(st + off) = w4;
         }
         fence_proxy_async();
         mbar_arrive(&pre[s]);
