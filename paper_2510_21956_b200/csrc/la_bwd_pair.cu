@@ -319,10 +319,10 @@ __device__ __forceinline__ void kv_role(const CUtensorMap& tmQ, const CUtensorMa
         fence_proxy_async();  // the st.async-written W_hat^T is read by the tensor core
         tc_fence_after();
         if (elect_one()) {
-          #pragma unroll 1
+          #pragma unroll
           for (int ks = 0; ks < 8; ++ks)
             mma_ss(tmem + kTD(s) + kHalf, kd(bQ, ks, 64), kd(bK, ks, 64), id_T1, ks > 0);
-          #pragma unroll 1
+          #pragma unroll
           for (int ks = 0; ks < 8; ++ks)
             mma_ss(tmem + kTD(s), mn(bW, ks, 8192), mn(bV, ks, 8192), id_dPt, ks > 0);
           mma_commit(&td_full[s]);
@@ -344,7 +344,7 @@ __device__ __forceinline__ void kv_role(const CUtensorMap& tmQ, const CUtensorMa
         mbar_wait_h(sR_ready, n & 1);  // E_R(n) has read R: R += of chunk n may go now
         tc_fence_after();
         if (elect_one()) {
-          #pragma unroll 1
+          #pragma unroll
           for (int ks = 0; ks < 4; ++ks)  // R += Q^T W_hat (E_R(n + 1) then overlaps dK / dV(n))
             mma_ss(tmem + kR, mn(aQ, ks, 8192), kd(aW, ks, 128), id_R, 1);
           mma_commit(r_full);
@@ -357,16 +357,16 @@ __device__ __forceinline__ void kv_role(const CUtensorMap& tmQ, const CUtensorMa
         trp(0, 0, n, 1);
         tc_fence_after();
         if (elect_one()) {
-          #pragma unroll 1
+          #pragma unroll
           for (int ks = 0; ks < 4; ++ks)  // dK^T = Q^T dS^T
             mma_ss(tmem + kDK(s), mn(aQ, ks, 8192), mn(adS, ks, 8192), id_dK1, ks > 0);
-          #pragma unroll 1
+          #pragma unroll
           for (int ks = 0; ks < 8; ++ks)  //      + (b R) V^T
             mma_ss(tmem + kDK(s), kd(aR, ks, 128), mn(aV, ks, 8192), id_dK2, 1);
-          #pragma unroll 1
+          #pragma unroll
           for (int ks = 0; ks < 4; ++ks)  // dV^T = W_hat^T P
             mma_ss(tmem + kDV(s), kd(aW, ks, 128), mn(aP, ks, 8192), id_dV1, ks > 0);
-          #pragma unroll 1
+          #pragma unroll
           for (int ks = 0; ks < 8; ++ks)  //      + (b R)^T K^T
             mma_ss(tmem + kDV(s), mn(aR, ks, 16384), kd(aK, ks, 64), id_dV2, 1);
           mma_commit(&dkv_full[s]);
@@ -609,9 +609,9 @@ __device__ __forceinline__ void q_role(const CUtensorMap& tmK, const CUtensorMap
         const uint32_t bK = smem_u32(smem + s * kQStage), bV = bK + kT64;
         tc_fence_after();
         if (elect_one()) {
-          #pragma unroll 1
+          #pragma unroll
           for (int ks = 0; ks < 4; ++ks) mma_ss(tmem + kS, mn(bK, ks, 8192), kd(bV, ks, 128), id_Sneg, 1);
-          #pragma unroll 1
+          #pragma unroll
           for (int ks = 0; ks < 4; ++ks)  // column sums of K (z_prev update, read by E_S)
             mma_ss(tmem + kZC(n & 1), mn(bK, ks, 8192), kd(aOnes, ks, 16), id_Z, ks > 0);
           mma_commit(s_full);
@@ -626,7 +626,7 @@ __device__ __forceinline__ void q_role(const CUtensorMap& tmK, const CUtensorMap
         tc_fence_after();
         if (elect_one()) {
           const uint32_t d = tmem + kDP + ((n & 1) ? kHalf : 0u);
-          #pragma unroll 1
+          #pragma unroll
           for (int ks = 0; ks < 8; ++ks) mma_ss(d, mn(bW, ks, 8192), mn(bV, ks, 8192), id_dPt, ks > 0);
           mma_commit(&dpt_full[n & 1]);
         }
@@ -654,10 +654,10 @@ __device__ __forceinline__ void q_role(const CUtensorMap& tmK, const CUtensorMap
         trp(1, 0, n, 1);
         tc_fence_after();
         if (elect_one()) {
-          #pragma unroll 1
+          #pragma unroll
           for (int ks = 0; ks < 4; ++ks)  // dQ^T = K^T dS^T
             mma_ss(tmem + kDQ(bb), mn(aK, ks, 8192), kd(adS, ks, 64), id_dQ1, ks > 0);
-          #pragma unroll 1
+          #pragma unroll
           for (int ks = 0; ks < 8; ++ks)  //      + (b S) W_hat^T   (A from TMEM)
             mma_ts(tmem + kDQ(bb), tmem + kBS(bb) + ks * 8, mn(aW, ks, 8192), id_dQ2, 1);
           mma_commit(&dq_full[bb]);
