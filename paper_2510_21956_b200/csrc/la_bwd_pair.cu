@@ -68,14 +68,18 @@ constexpr uint32_t kHalf = 16u << 16;  // TMEM lane offset of the upper M=64 hal
 // ---- KV CTA (rank 0) shared memory
 constexpr int kKvStages = 2;
 constexpr int kKvStage = 3 * kT64;                 // Q | K | V^T
-constexpr int kWSlots = 2;                         // W_hat^T tiles written by the Q CTA
+#ifndef LA_PAIR_WSLOTS
+#define LA_PAIR_WSLOTS 2
+#endif
+constexpr int kWSlots = LA_PAIR_WSLOTS;             // W_hat^T tiles written by the Q CTA
+constexpr int kPSBufs = kWSlots > 2 ? 1 : 2;       // P / dS buffers (smem: a third W slot or a second P / dS)
 constexpr int kKvOffW = kKvStages * kKvStage;      // 96 KB
 #ifndef LA_KV_PREFETCH
 #define LA_KV_PREFETCH 2
 #endif
 constexpr int kKvPrefetch = LA_KV_PREFETCH;        // chunks the KV CTA prefetches into L2 ahead
-constexpr int kKvOffP = kKvOffW + kWSlots * kT64;  // x2: P [64 i][64 t] | dS [64 i][64 t]
-constexpr int kKvOffR = kKvOffP + 2 * 16384;       // b R [128 m][128 j]
+constexpr int kKvOffP = kKvOffW + kWSlots * kT64;  // x kPSBufs: P [64 i][64 t] | dS [64 i][64 t]
+constexpr int kKvOffR = kKvOffP + kPSBufs * 16384; // b R [128 m][128 j]
 constexpr int kKvOffStg = kKvOffR + 32768;         // 8 warps x 2 KB drain staging
 constexpr int kKvEnd = kKvOffStg + 16384;
 // ---- Q CTA (rank 1) shared memory
@@ -339,7 +343,7 @@ __device__ __forceinline__ void kv_role(const CUtensorMap& tmQ, const CUtensorMa
       for (int n = 0; n < nc; ++n) {
         const int s = n & 1, w = n % kWSlots;
         const uint32_t aQ = smem_u32(smem + s * kKvStage), aK = aQ + kT64, aV = aQ + 2 * kT64,
-                       aW = smem_u32(sW + w * kT64), aP = aPdS + s * 16384, adS = aP + 8192;
+                       aW = smem_u32(sW + w * kT64), aP = aPdS + (s % kPSBufs) * 16384, adS = aP + 8192;
         trp(0, 0, n, 0);
         mbar_wait_h(sR_ready, n & 1);  // E_R(n) has read R: R += of chunk n may go now
         tc_fence_after();
@@ -394,11 +398,13 @@ __device__ __forceinline__ void kv_role(const CUtensorMap& tmQ, const CUtensorMa
     if (t0) trp(0, 1, n, 0);
     mbar_wait_cluster(&wfull[w], (n / kWSlots) & 1);  // s of the chunk (pushed)
     mbar_wait_h(&td_full[s], (n >> 1) & 1);
-    if (n >= 2) mbar_wait_h(&dkv_full[s], ((n - 2) >> 1) & 1);  // dK / dV(n-2) has read P / dS buffer s
+    if (n >= kPSBufs)  // dK / dV(n - kPSBufs) has read this P / dS buffer
+      mbar_wait_h(&dkv_full[(n - kPSBufs) & 1], ((n - kPSBufs) >> 1) & 1);
     if (t0) trp(0, 1, n, 1);
     tc_fence_after();
     const float si = s_w[w * kCB + ih];
-    e1_cols<kBF16>(tmem + lb + kTD(s) + t0, sPdS + s * 16384 + (upper ? 0 : 8192), ih, t0, b, upper ? a : -b * si, true);
+    e1_cols<kBF16>(tmem + lb + kTD(s) + t0, sPdS + (s % kPSBufs) * 16384 + (upper ? 0 : 8192), ih, t0, b,
+                   upper ? a : -b * si, true);
     fence_proxy_async();
     tc_fence_before();
     mbar_arrive(&td_empty[s]);
