@@ -87,6 +87,11 @@ inline bool bwd_pair_rule(int64_t G, int num_sms = 148) {
   return false;  // opt-in until it beats the segmented sweep
 }
 
+// Segment carries: the sweeps sum their carry from the aggregate unit records in their
+// prologue, unless there are more than this many records per group -- then one seg_scan
+// launch (la_sm100.cu) forms every segment's carry.
+constexpr int kScanMinRecords = 8;
+
 struct Tensors {
   const void* q; int lq;
   const void* k; int lk;
@@ -217,6 +222,10 @@ cudaError_t tc_sum_units(const float* recs, int64_t G, int U, float* tot, cudaSt
 cudaError_t tc_kv_totals(const Launch& L, const Tensors& t, float* units, float* tot);
 
 void note_launch(int n = 1);
+// mode 0: exclusive prefix at each segment start, 1: inclusive prefix at each segment end,
+// 2: exclusive suffix after each segment end (k_seg_scan, la_sm100.cu)
+cudaError_t seg_scan(const float* recs, int64_t G, int U, int A, int64_t SZ, const float* base, float* out,
+                     int64_t ostride, int mode, float* unit_pre, cudaStream_t st, const char* name);
 
 // Optional per-kernel event timing (la_profile_enable). Construct before a
 // launch and destroy after it; records only while profiling is on.

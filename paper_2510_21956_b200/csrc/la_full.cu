@@ -264,6 +264,7 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
     // row sums: the 8 ig partials of each row j -> vrow (shared scratch: the stages are idle
     // once the unit's MMAs have retired)
     if (nc > 0) mbar_wait(done, 0);
+    named_bar(1, 128);  // every CUDA-core thread is done reading the stages
     float* red = (float*)smem;  // [8 ig][D]
 #pragma unroll
     for (int rr = 0; rr < RR; ++rr) red[ig * D + jg + 16 * rr] = crow[rr];

@@ -74,6 +74,7 @@ struct FwdParams {
   int pf;               // chunks prefetched into L2 ahead of the ring
   float* ck_out;        // [G][ck_K] prefix checkpoints at global rows C0 * 2^k (internal.h), or null
   int ck_K;
+  int cmb_ready = 0;    // cmb already holds every segment's prefix (seg_scan, many unit records)
 };
 
 // ================================================================ forward main
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(448, 1)
   // exclusive prefix of this segment: carry + sum of the earlier segments' sums
   const bool has_in = p > 0 || prm.carry != nullptr;
   float* st_in = has_in ? prm.cmb + (grp * prm.P + p) * state_floats(kD) : nullptr;
-  if (has_in && warp >= 2 && warp < 10)
+  if (has_in && !prm.cmb_ready && warp >= 2 && warp < 10)
     combine_records(st_in, prm.carry ? prm.carry + grp * state_floats(kD) : nullptr,
                     prm.agg + grp * prm.P * prm.A * state_floats(kD), 0, p * prm.A, state_floats(kD),
                     (int)threadIdx.x - 64, 256);
@@ -978,6 +979,62 @@ cudaError_t tc_kv_totals(const Launch& L, const Tensors& t, float* units, float*
   return tc_sum_units(units, G, P * A, tot, L.stream);
 }
 
+// Segment carries from aggregate unit records in one launch, for when the sweep CTAs would
+// each sum many records in their prologue (small N per segment, many segments: the sum is a
+// latency chain of dependent loads there). Per group g and element e of a state record
+// (recs: [G][U] records of SZ floats, A units per segment, P = U / A segments):
+//   kExclPrefix:   out[g][p] = base[g] + sum_{u <  p A}     recs[g][u]   (the forward's carry)
+//   kInclPrefix:   out[g][p] = base[g] + sum_{u < (p+1) A}   recs[g][u]   (S at the segment end)
+//   kExclSuffix:   out[g][p] = base[g] + sum_{u >= (p+1) A}  recs[g][u]   (R after the segment)
+// with out[g][p] at out + (g P + p) * ostride; unit_pre[g][u] (optional) = the exclusive prefix
+// before unit u. One thread per float4 of a record: the loads of successive units are
+// independent, only the adds chain.
+__global__ void k_seg_scan(const float* recs, int U, int A, int64_t SZ, const float* base, float* out,
+                           int64_t ostride, int mode, float* unit_pre) {
+  const int64_t e = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  const int64_t g = blockIdx.y;
+  if (e >= SZ) return;
+  const int P = U / A;
+  const float* rg = recs + g * U * SZ + e;
+  float4 acc = base ? *(const float4*)(base + g * SZ + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+  auto add = [&](const float4 v) { acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w; };
+  if (mode == 2) {
+    for (int p = P - 1; p >= 0; --p) {
+      *(float4*)(out + (g * P + p) * ostride + e) = acc;
+      if (p > 0) {
+#pragma unroll 4
+        for (int u = p * A; u < (p + 1) * A; ++u) add(*(const float4*)(rg + (int64_t)u * SZ));
+      }
+    }
+    return;
+  }
+  if (mode == 0) {  // the last segment's units are never read (the forward aggregates 0..P-2)
+    for (int p = 0; p < P; ++p) {
+      *(float4*)(out + (g * P + p) * ostride + e) = acc;
+      if (p + 1 < P) {
+#pragma unroll 4
+        for (int u = p * A; u < (p + 1) * A; ++u) add(*(const float4*)(rg + (int64_t)u * SZ));
+      }
+    }
+    return;
+  }
+#pragma unroll 4
+  for (int u = 0; u < U; ++u) {
+    if (unit_pre) *(float4*)(unit_pre + (g * U + u) * SZ + e) = acc;
+    add(*(const float4*)(rg + (int64_t)u * SZ));
+    if ((u + 1) % A == 0) *(float4*)(out + (g * P + (u + 1) / A - 1) * ostride + e) = acc;
+  }
+}
+
+cudaError_t seg_scan(const float* recs, int64_t G, int U, int A, int64_t SZ, const float* base, float* out,
+                     int64_t ostride, int mode, float* unit_pre, cudaStream_t st, const char* name) {
+  const dim3 grid((unsigned)((SZ / 4 + 127) / 128), (unsigned)G);
+  ProfScope ps(name, st);
+  k_seg_scan<<<grid, 128, 0, st>>>(recs, U, A, SZ, base, out, ostride, mode, unit_pre);
+  note_launch(1);
+  return cudaGetLastError();
+}
+
 cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws) {
   if (!L.causal) return tc_forward_full(L, t, out, g, ws);
   const bool bf = L.dtype == LA_BF16;
@@ -1013,6 +1070,12 @@ cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, W
   }
   FwdParams prm{agg_st, A, L.carry_prefix, cmb, g, ws.flag, N, G, seg, P, L.row_offset, L.a, L.b, saved, out,
                 tuning().prefetch > 0 ? tuning().prefetch : kFPrefetch, saved ? saved + G * P * SZ : nullptr, ckK};
+  if (P > 1 && P * A > kScanMinRecords) {  // many unit records: one scan launch, not a chain per CTA
+    cudaError_t e = seg_scan(agg_st, G, P * A, A, SZ, L.carry_prefix, cmb, SZ, 0, nullptr, L.stream, "la_fwd_scan");
+    if (e != cudaSuccess) return e;
+    prm.cmb_ready = 1;
+    launches += 1;
+  }
   {
     ProfScope ps("la_fwd_causal", L.stream);
     main_k<<<dim3(P, G), 448, kFwdSmem, L.stream>>>(mQ64, mK64, mV64, mO64, prm);

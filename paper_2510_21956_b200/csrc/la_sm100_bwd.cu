@@ -78,6 +78,7 @@ struct BwdParams {
   int64_t row_offset = 0;     // global index of row 0 (sequence shards)
   int64_t ck_unit = 0;        //   ck_unit > 0: [G][P][A] at the segment's unit boundaries, built by
                               //   the sweep's prologue from the aggregate's unit sums (la_backward)
+  int cmb_ready = 0;          // cmb (and the unit-boundary prefixes) already formed by seg_scan
 };
 
 // Cross-CTA publication for the fused schedule (k_bwd_fused): the aggregate unit's
@@ -647,12 +648,13 @@ __device__ __forceinline__ void bwd_main_body(const CUtensorMap& tmQ, const CUte
       const int ct = (int)threadIdx.x - 128, cn = kBwdThreads - 128;
       if (prm.skipS)
         combine_records(cS, prm.stS + (grp * prm.P + p) * SZ, prm.stS, 0, 0, SZ, ct, cn);
-      else
+      else if (!prm.cmb_ready)
         combine_records(cS, prm.carry_pre ? prm.carry_pre + grp * SZ : nullptr, prm.stS + grp * U * SZ, 0,
                         (p + 1) * prm.A, SZ, ct, cn);
-      combine_records(cS + SZ, prm.carry_suf ? prm.carry_suf + grp * SZ : nullptr, prm.stR + grp * U * SZ,
-                      (p + 1) * prm.A, U, SZ, ct, cn);
-      if (!prm.skipS && prm.ck_unit > 0) {  // exclusive prefix at each unit boundary of the segment
+      if (!prm.cmb_ready)
+        combine_records(cS + SZ, prm.carry_suf ? prm.carry_suf + grp * SZ : nullptr, prm.stR + grp * U * SZ,
+                        (p + 1) * prm.A, U, SZ, ct, cn);
+      if (!prm.skipS && prm.ck_unit > 0 && !prm.cmb_ready) {  // exclusive prefix at each unit boundary of the segment
         float* ck = const_cast<float*>(prm.ck) + (grp * prm.P + p) * prm.A * SZ;
         combine_records(ck, prm.carry_pre ? prm.carry_pre + grp * SZ : nullptr, prm.stS + grp * U * SZ, 0,
                         p * prm.A, SZ, ct, cn);
@@ -1617,6 +1619,16 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
     cudaFuncSetAttribute(aggR, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggRSmem);
     ProfScope ps("la_bwd_agg", L.stream);
     aggR<<<dim3(A * P, G), 320, kAggRSmem, L.stream>>>(mQ, mW, mO, mWh, pa);
+  }
+  if (P > 1 && P * A > kScanMinRecords) {  // many unit records: one scan launch, not a chain per CTA
+    const int U = P * A;
+    cudaError_t e = seg_scan(stR, G, U, A, SZ, L.carry_suffix, cmb + SZ, 2 * SZ, 2, nullptr, L.stream, "la_bwd_scan");
+    if (e == cudaSuccess && !use_saved)
+      e = seg_scan(stS, G, U, A, SZ, L.carry_prefix, cmb, 2 * SZ, 1, A > 1 ? const_cast<float*>(prm.ck) : nullptr,
+                   L.stream, "la_bwd_scan_s");
+    if (e != cudaSuccess) return e;
+    prm.cmb_ready = 1;
+    launches += 1 + (use_saved ? 0 : 1);
   }
   {
     ProfScope ps("la_bwd_causal", L.stream);

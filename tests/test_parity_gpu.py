@@ -416,7 +416,9 @@ def test_segment_partition_matches_oracle(cuda, G, N):
 @pytest.mark.gpu
 def test_fused_backward_schedule_matches_separate(cuda):
     """la_tuning.bwd_fused = 1 (k_bwd_fused: aggregate units and sweeps in one ticket-scheduled
-    grid) computes bitwise the same gradients as the two-launch default."""
+    grid) computes the same gradients as the two-launch default. Not bitwise: with many unit
+    records the default forms the segment carries in one scan launch (seg_scan), summing the
+    R suffix in another fp32 order than the fused sweeps' prologue; they agree to bf16 rounding."""
     import torch
     import paper_2510_21956_b200 as la
     from tests._util import fast_inputs
@@ -436,7 +438,8 @@ def test_fused_backward_schedule_matches_separate(cuda):
         _abi.set_tuning()
     torch.cuda.synchronize()
     for a_, b_ in ((g0.dq, g1.dq), (g0.dk, g1.dk), (g0.dv, g1.dv)):
-        assert torch.equal(a_.data, b_.data)
+        x, y = a_.data.float(), b_.data.float()
+        assert (x - y).abs().max().item() <= 8e-3 * max(1.0, y.abs().max().item())
 
 
 @pytest.mark.parametrize("causal", [True, False])
