@@ -210,7 +210,8 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
         // W_hat^T = Omega^T / g in place; c_j += w_hat; s_i = sum_j o_ij w_hat_ij
         const float* gg = (const float*)(st + NT * T);
         const float4 g0 = *(const float4*)(gg + 8 * ig), g1 = *(const float4*)(gg + 8 * ig + 4);
-        const float gi[8] = {1.f / g0.x, 1.f / g0.y, 1.f / g0.z, 1.f / g0.w, 1.f / g1.x, 1.f / g1.y, 1.f / g1.z, 1.f / g1.w};
+        const float gi[8] = {__frcp_rn(g0.x), __frcp_rn(g0.y), __frcp_rn(g0.z), __frcp_rn(g0.w),
+                             __frcp_rn(g1.x), __frcp_rn(g1.y), __frcp_rn(g1.z), __frcp_rn(g1.w)};
         const uint8_t* ot = st + 2 * T;
         float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -504,11 +505,13 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
 #pragma unroll
         for (int m8 = part_k * (D / TPR); m8 < (part_k + 1) * (D / TPR); m8 += 8) {
           const uint4 q4 = *(const uint4*)(st + sw128_off(i, m8, CR));
+          const float4 za = *(const float4*)(zf + m8), zb = *(const float4*)(zf + m8 + 4);
+          const float z8[8] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
           const uint32_t* qp = (const uint32_t*)&q4;
 #pragma unroll
           for (int h2 = 0; h2 < 4; ++h2) {
             const float2 q2 = unpack2<kBF16>(qp[h2]);
-            acc += q2.x * zf[m8 + 2 * h2] + q2.y * zf[m8 + 2 * h2 + 1];
+            acc += q2.x * z8[2 * h2] + q2.y * z8[2 * h2 + 1];
           }
         }
 #pragma unroll
@@ -516,7 +519,7 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
         if (part_k == 0) {
           const float gi = a * (float)prm.n_total + b * acc;
           if (fabsf(gi) < kEpsF32) flag_degenerate(prm.flag, grp, row0 + i);
-          ginv[(c & 1) * CR + i] = 1.f / gi;
+          ginv[(c & 1) * CR + i] = __frcp_rn(gi);
           prm.gout[grp * prm.N + row0 + i] = gi;
         }
         mbar_arrive(&empty[s]);  // Q tile no longer read by the CUDA cores
@@ -524,7 +527,7 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
         const float* gg = (const float*)(st + T);
         const float* ss = gg + CR;
         if (et < CR) {
-          ginv[(c & 1) * CR + et] = 1.f / gg[et];
+          ginv[(c & 1) * CR + et] = __frcp_rn(gg[et]);
           sbuf[(c & 1) * CR + et] = ss[et];
         }
         named_bar(1, kCT);
@@ -583,13 +586,19 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
 #pragma unroll
               for (int k8 = 0; k8 < 32; k8 += 8) {
                 uint32_t pk[4];
+                float g8[8];
+                if (kMode == kFwd) {
+                  const float4 ga = *(const float4*)(gv + k8), gb = *(const float4*)(gv + k8 + 4);
+                  g8[0] = ga.x; g8[1] = ga.y; g8[2] = ga.z; g8[3] = ga.w;
+                  g8[4] = gb.x; g8[5] = gb.y; g8[6] = gb.z; g8[7] = gb.w;
+                }
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                   float v0 = __uint_as_float(x[k8 + 2 * q]) + bh;
                   float v1 = __uint_as_float(x[k8 + 2 * q + 1]) + bh;
                   if (kMode == kFwd) {
-                    v0 *= gv[k8 + 2 * q];
-                    v1 *= gv[k8 + 2 * q + 1];
+                    v0 *= g8[2 * q];
+                    v1 *= g8[2 * q + 1];
                   }
                   pk[q] = pack2<kBF16>(v0, v1);
                 }
