@@ -88,7 +88,7 @@ inline bool bwd_pair_rule(int64_t G, int num_sms = 148) {
 }
 
 // Segment carries: the sweeps sum their carry from the aggregate unit records in their
-// prologue, unless there are more than this many records per group -- then one seg_scan
+// prologue, unless the longest such chain ((P - 1) A records) exceeds this -- then one seg_scan
 // launch (la_sm100.cu) forms every segment's carry.
 constexpr int kScanMinRecords = 8;
 

@@ -1070,7 +1070,7 @@ cudaError_t tc_forward(const Launch& L, const Tensors& t, void* out, float* g, W
   }
   FwdParams prm{agg_st, A, L.carry_prefix, cmb, g, ws.flag, N, G, seg, P, L.row_offset, L.a, L.b, saved, out,
                 tuning().prefetch > 0 ? tuning().prefetch : kFPrefetch, saved ? saved + G * P * SZ : nullptr, ckK};
-  if (P > 1 && P * A > kScanMinRecords) {  // many unit records: one scan launch, not a chain per CTA
+  if (P > 1 && (P - 1) * A > kScanMinRecords) {  // many unit records: one scan launch, not a chain per CTA
     cudaError_t e = seg_scan(agg_st, G, P * A, A, SZ, L.carry_prefix, cmb, SZ, 0, nullptr, L.stream, "la_fwd_scan");
     if (e != cudaSuccess) return e;
     prm.cmb_ready = 1;

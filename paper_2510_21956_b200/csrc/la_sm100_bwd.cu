@@ -1620,7 +1620,7 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
     ProfScope ps("la_bwd_agg", L.stream);
     aggR<<<dim3(A * P, G), 320, kAggRSmem, L.stream>>>(mQ, mW, mO, mWh, pa);
   }
-  if (P > 1 && P * A > kScanMinRecords) {  // many unit records: one scan launch, not a chain per CTA
+  if (P > 1 && (P - 1) * A > kScanMinRecords) {  // many unit records: one scan launch, not a chain per CTA
     const int U = P * A;
     cudaError_t e = seg_scan(stR, G, U, A, SZ, L.carry_suffix, cmb + SZ, 2 * SZ, 2, nullptr, L.stream, "la_bwd_scan");
     if (e == cudaSuccess && !use_saved)
