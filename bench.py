@@ -491,6 +491,7 @@ def run_our_arm(args):
                 "step_roofline": {"alg_bytes": step_bytes, "achieved_gbs": step_gbs, "frac_hbm": step_gbs / hbm,
                                   "alg_tflops": flops / (ms / 1e3) / 1e12,
                                   "frac_bf16": flops / (ms / 1e3) / 1e12 / tf},
+                "library": L.la_version().decode(),
                 "kernels": kstats, "kernels_source": "eager steps after the graph-replayed timed region"
                 if args.graph else "timed region", "memory": memory, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clocks}

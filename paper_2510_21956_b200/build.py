@@ -26,6 +26,20 @@ if os.environ.get("LA_TRACE"):  # clock64 pipeline traces (diagnostics, la_inter
         FLAGS.append("-DLA_TRACE_G=" + os.environ["LA_TRACE_G"])
 
 
+def build_id() -> str:
+    """git revision of the sources (+ "-dirty" with local edits) and the UTC build time."""
+    import datetime
+    try:
+        rev = subprocess.run(["git", "-C", ROOT, "rev-parse", "--short=12", "HEAD"], capture_output=True,
+                             text=True, check=True).stdout.strip()
+        dirty = subprocess.run(["git", "-C", ROOT, "status", "--porcelain", "--", "paper_2510_21956_b200/csrc",
+                                "include"], capture_output=True, text=True).stdout.strip()
+        rev += "-dirty" if dirty else ""
+    except Exception:
+        rev = "nogit"
+    return rev + " " + datetime.datetime.now(datetime.timezone.utc).strftime("%Y-%m-%dT%H:%MZ")
+
+
 def _newest(paths):
     return max(os.path.getmtime(p) for p in paths)
 
@@ -47,6 +61,12 @@ def build(verbose: bool = False) -> str:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < _newest(objs):
+        # build provenance (la_version): one C object with the revision and link time
+        stamp_c, stamp_o = os.path.join(ROOT, "build", "la_build_id.c"), os.path.join(OBJ, "la_build_id.o")
+        with open(stamp_c, "w") as f:
+            f.write(f'const char la_build_id_str[] = "{build_id()}";\n')
+        subprocess.run(["gcc", "-c", "-fPIC", "-o", stamp_o, stamp_c], check=True)
+        objs = objs + [stamp_o]
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "shared",
                "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
         if verbose:

@@ -617,7 +617,14 @@ thread_local HostPipe t_pipe;
 
 extern "C" {
 
-const char* la_version(void) { return "la-b200 0.1 (sm_100a)"; }
+// Build provenance: build.py links a one-line object holding the source tree's git revision
+// and the link time, so a log shows which build a process loaded.
+extern "C" const char la_build_id_str[];
+const char* la_version(void) {
+  static char v[160];
+  std::snprintf(v, sizeof(v), "la-b200 0.2 (sm_100a) build %s", la_build_id_str);
+  return v;
+}
 
 const char* la_status_name(la_status s) {
   switch (s) {
