@@ -568,6 +568,17 @@ def run_sharded_arm(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    per_graph = 0
+    if args.graph:  # small shards are launch-bound: replay one captured step (no host gaps)
+        graph = torch.cuda.CUDAGraph()
+        c0 = L.la_launch_count()
+        with torch.cuda.graph(graph):
+            step()
+        per_graph = L.la_launch_count() - c0  # replays do not pass through the host API
+        step = graph.replay
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
     launches0 = L.la_launch_count()
     if world > 1:
         dist.barrier()
@@ -582,7 +593,7 @@ def run_sharded_arm(args):
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    launches = L.la_launch_count() - launches0
+    launches = L.la_launch_count() - launches0 + per_graph * args.steps
     ms = t0.elapsed_time(t1) / args.steps
     if world > 1:
         tt = torch.tensor([ms], device=dev)
@@ -599,7 +610,8 @@ def run_sharded_arm(args):
             "data": "synthetic (U(-1,1), unit-norm q/k rows)",
             "config": {"workload": f"BASELINE config {args.config}", "global_batch": cfg["batch"],
                        "seq_len": N_all, "heads": cfg["heads"], "dim": D,
-                       "parallelism": f"{cfg['mode']}{world}", "l2": "inputs > L2 at world <= 8; no flush"},
+                       "parallelism": f"{cfg['mode']}{world}", "l2": "inputs > L2 at world <= 8; no flush",
+                       "cuda_graph": bool(args.graph)},
             "step_roofline": {"alg_bytes_per_rank": alg, "achieved_gbs": alg / (ms / 1e3) / 1e9,
                               "frac_hbm": alg / (ms / 1e3) / 1e9 / hbm},
             "e2e": None, "cpu_baseline": None, "gpu_launches": int(launches), "clocks": clk.summary()}),
