@@ -1,5 +1,6 @@
 // Internal host-side interfaces between the C-ABI layer and the kernel files.
 #pragma once
+#include <algorithm>
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
@@ -64,15 +65,25 @@ inline int agg_split(int64_t G, int64_t seg_rows, int segs_aggregated, int num_s
   return best;
 }
 
+// Segment carries: the sweeps sum their carry from the aggregate unit records in their
+// prologue, unless the longest such chain ((P - 1) A records) exceeds this -- then one seg_scan
+// launch (la_sm100.cu) forms every segment's carry.
+constexpr int kScanMinRecords = 8;
+
 // The backward aggregate (W_hat^T / s for every row, R records for segments >= 1): its
 // segment-0 units skip Q and the MMAs, so units are uneven; the finest split (up to 8
 // units per segment, several waves) balances them (0.70 -> 0.64 ms at the north star).
-inline int bwd_agg_split(int64_t seg_rows) {
+inline int bwd_agg_split(int64_t seg_rows, int P, bool saved) {
   const int64_t chunks = seg_rows / 128;
   if (const int a = tuning().agg_split) {
     if (a >= 1 && chunks % a == 0) return a;
   }
-  for (int a = 8; a > 1; --a)
+  // with several segments, a sweep CTA sums (P - 1) A unit records for its R carry: keep that
+  // within the in-kernel combine's reach (no scan launch; tiny units cost more than they
+  // balance: config-3 shard 0.142 -> 0.119 ms at A = 1). Without the forward's saved states
+  // the unit boundaries are also the S rebuild's exact reload points, so keep them fine.
+  const int amax = (P > 1 && saved) ? std::max(1, kScanMinRecords / (P - 1)) : 8;
+  for (int a = std::min(8, amax); a > 1; --a)
     if (chunks % a == 0) return a;
   return 1;
 }
@@ -87,10 +98,6 @@ inline bool bwd_pair_rule(int64_t G, int num_sms = 148) {
   return false;  // opt-in until it beats the segmented sweep
 }
 
-// Segment carries: the sweeps sum their carry from the aggregate unit records in their
-// prologue, unless the longest such chain ((P - 1) A records) exceeds this -- then one seg_scan
-// launch (la_sm100.cu) forms every segment's carry.
-constexpr int kScanMinRecords = 8;
 
 struct Tensors {
   const void* q; int lq;

@@ -998,31 +998,41 @@ __global__ void k_seg_scan(const float* recs, int U, int A, int64_t SZ, const fl
   const float* rg = recs + g * U * SZ + e;
   float4 acc = base ? *(const float4*)(base + g * SZ + e) : make_float4(0.f, 0.f, 0.f, 0.f);
   auto add = [&](const float4 v) { acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w; };
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  // units in blocks of 8: the 8 loads are issued together, only the adds chain
   if (mode == 2) {
-    for (int p = P - 1; p >= 0; --p) {
-      *(float4*)(out + (g * P + p) * ostride + e) = acc;
-      if (p > 0) {
-#pragma unroll 4
-        for (int u = p * A; u < (p + 1) * A; ++u) add(*(const float4*)(rg + (int64_t)u * SZ));
+    *(float4*)(out + (g * P + P - 1) * ostride + e) = acc;
+    for (int u1 = U - 1; u1 >= A; u1 -= 8) {
+      float4 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = u1 - k >= A ? *(const float4*)(rg + (int64_t)(u1 - k) * SZ) : zero;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int u = u1 - k;
+        if (u >= A) {
+          add(v[k]);
+          if (u % A == 0) *(float4*)(out + (g * P + u / A - 1) * ostride + e) = acc;
+        }
       }
     }
     return;
   }
-  if (mode == 0) {  // the last segment's units are never read (the forward aggregates 0..P-2)
-    for (int p = 0; p < P; ++p) {
-      *(float4*)(out + (g * P + p) * ostride + e) = acc;
-      if (p + 1 < P) {
-#pragma unroll 4
-        for (int u = p * A; u < (p + 1) * A; ++u) add(*(const float4*)(rg + (int64_t)u * SZ));
+  // mode 0 never reads the last segment's units (the forward aggregates segments 0..P-2)
+  const int u_read = mode == 0 ? (P - 1) * A : U;
+  for (int u0 = 0; u0 < U; u0 += 8) {
+    float4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = u0 + k < u_read ? *(const float4*)(rg + (int64_t)(u0 + k) * SZ) : zero;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int u = u0 + k;
+      if (u < U) {
+        if (mode == 0 && u % A == 0) *(float4*)(out + (g * P + u / A) * ostride + e) = acc;
+        if (unit_pre) *(float4*)(unit_pre + (g * U + u) * SZ + e) = acc;
+        if (u < u_read) add(v[k]);
+        if (mode == 1 && (u + 1) % A == 0) *(float4*)(out + (g * P + (u + 1) / A - 1) * ostride + e) = acc;
       }
     }
-    return;
-  }
-#pragma unroll 4
-  for (int u = 0; u < U; ++u) {
-    if (unit_pre) *(float4*)(unit_pre + (g * U + u) * SZ + e) = acc;
-    add(*(const float4*)(rg + (int64_t)u * SZ));
-    if ((u + 1) % A == 0) *(float4*)(out + (g * P + (u + 1) / A - 1) * ostride + e) = acc;
   }
 }
 

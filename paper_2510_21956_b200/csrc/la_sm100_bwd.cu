@@ -1427,7 +1427,7 @@ size_t tc_backward_ws_floats(int64_t G, int64_t N, int64_t D) {
   if (D != kD || N % 128) return 0;
   const int P = tcb_segments(G, N);
   const int64_t seg = ((N / 128 + P - 1) / P) * 128;
-  const int A = std::max(std::max(agg_split(G, seg, P > 1 ? P - 1 : 1), agg_split(G, seg, P)), bwd_agg_split(seg));
+  const int A = std::max(std::max(agg_split(G, seg, P > 1 ? P - 1 : 1), agg_split(G, seg, P)), bwd_agg_split(seg, P, false));  // the larger of the two
   // S, R unit sums + combined records, then the fused schedule's flags and ticket or the
   // unit-boundary prefixes of the recomputing sweep (never both)
   const size_t causal = (size_t)((2 * A + 2) * G * P) +
@@ -1546,7 +1546,7 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
   const float* sv = L.saved_in;
   const bool use_saved = sv != nullptr;  // validated by the ABI layer
   if (use_saved && bwd_pair_rule(G) && G % 2 == 0) return tc_backward_pair(L, t, dq, dk, dv);
-  const int A = bwd_agg_split(seg);  // the W_hat pass covers every segment
+  const int A = bwd_agg_split(seg, P, sv != nullptr);  // the W_hat pass covers every segment
   float* stS = ws.base;
   float* stR = stS + G * P * A * SZ;
   float* cmb = stR + G * P * A * SZ;
