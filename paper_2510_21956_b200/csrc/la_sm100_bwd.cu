@@ -700,6 +700,14 @@ __device__ __forceinline__ void bwd_main_body(const CUtensorMap& tmQ, const CUte
 
   if (warp < 4) {
   regs_dec<96>();
+#ifdef LA_TRACE
+  if (warp == 2 && lane_id() == 0) {  // observer: when each chunk's stage lands
+    for (int n = 0; n < nc && n < 64; ++n) {
+      mbar_wait(&full[n & 1], (n >> 1) & 1);
+      traceb(2, n, 4);
+    }
+  }
+#endif
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (reverse)
     if (elect_one()) {
@@ -715,6 +723,7 @@ __device__ __forceinline__ void bwd_main_body(const CUtensorMap& tmQ, const CUte
         const int s = n & 1;
         if (n + prm.pf < nc) l2_prefetch(n + prm.pf);
         if (n >= 2) mbar_wait(&empty[s], ((n >> 1) & 1) ^ 1);
+        traceb(0, n, 4);
         const int64_t row0 = row_of(n);
         uint8_t* st = smem + s * kStage;
         mbar_expect_tx(&full[s], kStage + kCB * 4);
@@ -784,6 +793,7 @@ __device__ __forceinline__ void bwd_main_body(const CUtensorMap& tmQ, const CUte
           mma_commit(&empty[n & 1]);
         }
         __syncwarp();
+        if (lane_id() == 0) traceb(0, n, 5);
       }
       if (n + 1 < nc) {  // T1 and dPt of chunk n+1 (E1(n) has read the previous ones)
         mbar_wait(&full[(n + 1) & 1], ((n + 1) >> 1) & 1);
@@ -798,6 +808,7 @@ __device__ __forceinline__ void bwd_main_body(const CUtensorMap& tmQ, const CUte
           mma_commit(dpt_full);
         }
         __syncwarp();
+        if (lane_id() == 0) traceb(0, n + 1, 6);
       }
       if (n + 1 < nc) {  // S -= K^T V of chunk n+1 (E_S(n) has read S: sS_ready above)
         tc_fence_after();
@@ -849,12 +860,14 @@ __device__ __forceinline__ void bwd_main_body(const CUtensorMap& tmQ, const CUte
     mbar_wait(dpt_full, n & 1);
     if (n >= 1) mbar_wait(gq_full, (n - 1) & 1);  // dK^T/dV^T(n-1) and dQ(n-1) have read sP / sdS
     tc_fence_after();
+    if (threadIdx.x == 384) traceb(3, n, 4);
     const float si = s_s[(n & 1) * kCB + ih];
     const float alpha = upper ? a : -b * si;
     uint8_t* dst = upper ? sP : sdS;
     uint32_t x[32];
     tmem_ld32(tmem + lb + kDP + t0, x);
     tmem_ld_wait();
+    if (threadIdx.x == 384) traceb(3, n, 5);
 #pragma unroll
     for (int w8 = 0; w8 < 4; ++w8) {
       uint32_t pk[4];
@@ -868,7 +881,9 @@ __device__ __forceinline__ void bwd_main_body(const CUtensorMap& tmQ, const CUte
       }
       *(uint4*)(dst + sw128_off(ih, t0 + 8 * w8, kCB)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     }
+    if (threadIdx.x == 384) traceb(3, n, 6);
     fence_proxy_async();
+    if (threadIdx.x == 384) traceb(3, n, 7);
     tc_fence_before();
     mbar_arrive(dpt_empty);
     mbar_arrive(ps_ready);
@@ -1006,12 +1021,13 @@ __device__ __forceinline__ void bwd_main_body(const CUtensorMap& tmQ, const CUte
         tmem_st_wait();
       }
 #pragma unroll 1
-      for (int j0 = 0; j0 < kD; j0 += 32) {
-        uint32_t x[32];
-        tmem_ld32(tmem + lb + kS + j0, x);
+      for (int j0 = 0; j0 < kD; j0 += 64) {  // two loads in flight per wait
+        uint32_t x[64];
+        tmem_ld32(tmem + lb + kS + j0, *reinterpret_cast<uint32_t(*)[32]>(x));
+        tmem_ld32(tmem + lb + kS + j0 + 32, *reinterpret_cast<uint32_t(*)[32]>(x + 32));
         tmem_ld_wait();
 #pragma unroll
-        for (int w8 = 0; w8 < 4; ++w8) {
+        for (int w8 = 0; w8 < 8; ++w8) {
           uint4 v;
           v.x = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 0]), b * __uint_as_float(x[8 * w8 + 1]));
           v.y = pack2<kBF16>(b * __uint_as_float(x[8 * w8 + 2]), b * __uint_as_float(x[8 * w8 + 3]));
@@ -1035,6 +1051,7 @@ __device__ __forceinline__ void bwd_main_body(const CUtensorMap& tmQ, const CUte
       const int s = n & 1;
       uint8_t* st = smem + s * kStage;
       mbar_wait(&full[s], (n >> 1) & 1);
+      if (ec == 0) traceb(3, n, 3);
       {  // row j = r of W_hat^T: 8 conflict-free 16-byte chunks
         const uint8_t* w_t = st + 3 * kT64;
         uint4 wv[8];

@@ -4,6 +4,9 @@ sys.path.insert(0, '.')
 from paper_2510_21956_b200 import _abi
 L = _abi.lib()
 dev = torch.device('cuda')
+import os
+if os.environ.get("PF"):
+    tu = _abi.Tuning(); tu.prefetch = int(os.environ["PF"]); L.la_set_tuning(C.byref(tu))
 G, N, D = 64, 65536, 128
 p = _abi.make_problem(G, N, D, "bf16")
 q = torch.randn(G, N, D, device=dev); q = (q / q.norm(dim=-1, keepdim=True)).bfloat16()
@@ -31,6 +34,6 @@ for r in range(4):
     for c in range(c0, c0 + 4):
         print("  ", c, (t[r, c, :4] - t0).tolist())
 print("period MMA top", np.diff(t[0, 10:60, 0]).mean())
-for r, ev in ((1, 0), (1, 1), (1, 2), (2, 0), (2, 1), (2, 2), (3, 0), (3, 1), (3, 2), (0, 1), (0, 3), (0, 2)):
+for r, ev in ((1, 0), (1, 1), (1, 2), (2, 0), (2, 1), (2, 2), (3, 0), (3, 1), (3, 2), (0, 1), (0, 3), (0, 2), (0, 4), (3, 3), (0, 5), (0, 6), (3, 4), (3, 5), (3, 6), (3, 7), (2, 4)):
     x = t[r, 10:60, ev] - t[0, 10:60, 0]
     print(f"role {r} ev {ev}: mean offset vs MMA top {x.mean():.0f}")
