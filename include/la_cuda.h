@@ -114,7 +114,6 @@ typedef struct {
   int32_t full_ctas_fwd; /* non-causal forward apply pass: CTAs per group */
   int32_t full_ctas_bwd; /* non-causal backward pass: CTAs per group */
   int32_t prefetch;      /* L2 prefetch distance (chunks) ahead of the TMA ring */
-  int32_t bwd_fused;     /* 1: aggregate units + sweeps in one ticket-scheduled grid */
   int32_t host_blocks;   /* la_host_step: group blocks per step (default 16) */
   int32_t simt_seg_rows; /* CUDA-core path: minimum rows per segment (default 32) */
   int32_t bwd_pair;      /* causal backward as 2-CTA clusters: 1 force, -1 never, 0 rule */

@@ -55,7 +55,7 @@ class ErrorInfo(C.Structure):
 class Tuning(C.Structure):
     """la_tuning: measurement overrides of the schedule rules (0 = built-in rule)."""
     _fields_ = [(n, C.c_int32) for n in ("segments", "agg_split", "full_ctas_fwd", "full_ctas_bwd", "prefetch",
-                                         "bwd_fused", "host_blocks", "simt_seg_rows", "bwd_pair")]
+                                         "host_blocks", "simt_seg_rows", "bwd_pair")]
 
 
 class Shard(C.Structure):

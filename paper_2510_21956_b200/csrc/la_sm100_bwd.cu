@@ -70,7 +70,6 @@ struct BwdParams {
   float* cmb;  // per (g, segment) combined [S inclusive prefix | R exclusive suffix]
   int pf;      // chunks prefetched into L2 ahead of the ring
   int store_w = 0;  // W_hat pass: store W_hat^T (into dv) and s (into dq rows) for the sweep
-  uint32_t* flags = nullptr;  // fused schedule: per aggregate unit [G][P * A], set when published
   int r_unit0 = 0;  // aggregate pass: units below this only produce W_hat^T / s (their R records
                     // would feed no segment: segment 0 in the causal sweep)
   const float* ck = nullptr;  // exact prefix (S, z) records the sweep reloads (internal.h, kCkC0):
@@ -80,27 +79,6 @@ struct BwdParams {
                               //   the sweep's prologue from the aggregate's unit sums (la_backward)
   int cmb_ready = 0;          // cmb (and the unit-boundary prefixes) already formed by seg_scan
 };
-
-// Cross-CTA publication for the fused schedule (k_bwd_fused): the aggregate unit's
-// records (generic stores) and W_hat^T / s (TMA stores, completed by wait_group 0)
-// are released at gpu scope; the consumer acquires, then orders its own TMA loads
-// after the acquire with a generic -> async proxy fence.
-__device__ __forceinline__ void flag_release(uint32_t* f) {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-  __threadfence();
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(1u) : "memory");
-}
-__device__ __forceinline__ void flags_acquire(const uint32_t* f, int n) {
-  for (int i = 0; i < n; ++i) {
-    uint32_t v;
-    while (true) {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f + i) : "memory");
-      if (v) break;
-      __nanosleep(128);
-    }
-  }
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
 
 // Half-tile variant: rows j = jbase + 16 rr + jg (rr < 4); the partial s of this
 // half goes to s_half, and rs[rr] returns this thread's partial row sum of W_hat
@@ -359,8 +337,7 @@ constexpr int kAStage = 2 * 8192 + 8192 + kT64 + 2048 + kT64;  // 58 KB
 constexpr int kAOffOnes = 16384, kAOffW = 24576, kAOffS = 24576 + kT64, kAOffO = kAOffS + 2048;
 constexpr size_t kAggRSmem = kAStages * kAStage + 128 + 4 * 2 * kCB * 4 + 1024;
 
-// Body shared by the standalone kernel and the fused schedule: 320 threads (warps
-// 0-9) of the CTA run it; its CTA-wide barriers are named barrier 2 over those 320.
+// 320 threads (warps 0-9); its CTA-wide barriers are named barrier 2 over those 320.
 template <bool kBF16>
 __device__ __forceinline__ void bwd_aggR_body(const CUtensorMap& tmQ, const CUtensorMap& tmW,
                                               const CUtensorMap& tmO, const CUtensorMap& tmWo,
@@ -539,7 +516,6 @@ __device__ __forceinline__ void bwd_aggR_body(const CUtensorMap& tmQ, const CUte
   tc_fence_before();
   named_bar(2, 320);
   if (warp == 1) tmem_dealloc<256>(tmem);
-  if (prm.flags && threadIdx.x == 64) flag_release(prm.flags + grp * prm.P + p);  // W_hat^T stores waited above
 }
 
 template <bool kBF16>
@@ -635,10 +611,6 @@ __device__ __forceinline__ void bwd_main_body(const CUtensorMap& tmQ, const CUte
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
-  if (prm.flags) {  // fused schedule: the aggregate units of segments p..P-1 of this group
-    if (threadIdx.x == 0) flags_acquire(prm.flags + grp * prm.P * prm.A + p * prm.A, (prm.P - p) * prm.A);
-    __syncthreads();
-  }
   {  // carries: S inclusive prefix at s1 (saved by the forward, or carry + segment sums
      // 0..p) and R exclusive suffix after s1 (carry + segment sums p+1..P-1)
     const int64_t SZ = state_floats(kD);
@@ -1140,49 +1112,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   bwd_main_body<kBF16>(tmQ, tmK, tmV, tmW, prm, blockIdx.x, blockIdx.y);
 }
 
-// Fused schedule: the aggregate units (W_hat^T / s + R records) and the reverse sweeps
-// in ONE grid, so the bandwidth-bound aggregate CTAs run beside the latency-bound
-// sweeps instead of before them. Each CTA takes a ticket (the order CTAs actually
-// start) and maps it to a unit in dependency order:
-//   agg(P-1), agg(P-2), main(P-1), agg(P-3), main(P-2), ..., agg(0), main(1), main(0)
-// (agg(s) = the A aggregate units of segment s of every group; main(s) = the sweeps of
-// segment s). A sweep waits only on aggregate units with lower tickets, whose CTAs are
-// already running and never wait, so the schedule cannot deadlock.
-struct FusedSched {
-  int* counter;  // zeroed before the launch, with the flags
-  int G, P, A;
-};
-
-template <bool kBF16>
-__global__ void __launch_bounds__(kBwdThreads, 1)
-    k_bwd_fused(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmWh,
-                const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmO,
-                BwdParams pm, BwdParams pa, FusedSched sc) {
-  __shared__ int s_ticket;
-  if (threadIdx.x == 0) s_ticket = atomicAdd(sc.counter, 1);
-  __syncthreads();
-  int t = s_ticket;
-  const int GA = sc.G * sc.A;
-  for (int st = 0; st <= sc.P; ++st) {
-    if (st < sc.P) {  // agg(P-1-st): unit (group, a) of segment P-1-st
-      if (t < GA) {
-        if (threadIdx.x < 320)
-          bwd_aggR_body<kBF16>(tmQ, tmW, tmO, tmWh, pa, (sc.P - 1 - st) * sc.A + t % sc.A, t / sc.A);
-        return;
-      }
-      t -= GA;
-    }
-    if (st >= 1) {  // main(P-st)
-      if (t < sc.G) {
-        bwd_main_body<kBF16>(tmQ, tmK, tmV, tmWh, pm, sc.P - st, t);
-        return;
-      }
-      t -= sc.G;
-    }
-  }
-}
-
 // ================================================================ non-causal backward
 // backward_full (backward_kernels.hpp:173-288): with the totals S, z (keys/values) and
 // R = sum q^T w_hat, u = sum s q, c = sum w_hat over all N, every 64-row chunk is
@@ -1445,10 +1374,9 @@ size_t tc_backward_ws_floats(int64_t G, int64_t N, int64_t D) {
   const int P = tcb_segments(G, N);
   const int64_t seg = ((N / 128 + P - 1) / P) * 128;
   const int A = std::max(std::max(agg_split(G, seg, P > 1 ? P - 1 : 1), agg_split(G, seg, P)), bwd_agg_split(seg, P, false));  // the larger of the two
-  // S, R unit sums + combined records, then the fused schedule's flags and ticket or the
-  // unit-boundary prefixes of the recomputing sweep (never both)
-  const size_t causal = (size_t)((2 * A + 2) * G * P) +
-                        std::max((size_t)(G * P * A), (size_t)(G * P * A + 4 + state_floats(kD) - 1) / state_floats(kD));
+  // S, R unit sums + combined records, then the unit-boundary prefixes of the recomputing
+  // sweep
+  const size_t causal = (size_t)((2 * A + 2) * G * P) + (size_t)(G * P * A);
   const int Af = agg_split(G, seg, P);
   const size_t full = (size_t)(tc_kv_units(G, N) * G + Af * P * G + 2 * G);  // non-causal unit sums + totals
   return (causal > full ? causal : full) * state_floats(kD);
@@ -1603,29 +1531,6 @@ cudaError_t tc_backward(const Launch& L, const Tensors& t, void* dq, void* dk, v
   cudaFuncSetAttribute(agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAggSmemB);
   cudaFuncSetAttribute(main_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmemB);
   int launches = 2;
-  // tuning().bwd_fused = 1: one grid with the aggregate units beside the sweeps (k_bwd_fused;
-  // flags + ticket zeroed first). Measured slower at the north star (2.48 vs 0.72 + 1.62
-  // ms: the aggregate CTAs take HBM bandwidth from the sweeps rather than filling
-  // idle bandwidth), faster only when the sweep grid is a poor fit for the SMs (P = 5:
-  // 2.54 vs 2.79 ms); kept as an opt-in schedule, profiles/r01_s3_fused.md.
-  if (use_saved && tuning().bwd_fused == 1) {
-    uint32_t* flags = (uint32_t*)(cmb + G * P * 2 * SZ);
-    const size_t nflag = (size_t)(G * P * A);
-    cudaError_t e = cudaMemsetAsync(flags, 0, (nflag + 4) * sizeof(uint32_t), L.stream);
-    if (e != cudaSuccess) return e;
-    prm.flags = flags;
-    pa.flags = flags;
-    FusedSched sc{(int*)(flags + nflag), (int)G, P, A};
-    auto fused = bf ? k_bwd_fused<true> : k_bwd_fused<false>;
-    const size_t smem = kAggRSmem > kMainSmemB ? kAggRSmem : kMainSmemB;
-    cudaFuncSetAttribute(fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    {
-      ProfScope ps("la_bwd_fused", L.stream);
-      fused<<<(unsigned)(G * P * A + G * P), kBwdThreads, smem, L.stream>>>(mQ, mK, mV, mWh, mW, mO, prm, pa, sc);
-    }
-    note_launch(1);
-    return cudaGetLastError();
-  }
   if (!use_saved) {
     ProfScope ps("la_bwd_agg_s", L.stream);
     agg<<<dim3(A * P, G), 192, kAggSmemB, L.stream>>>(mQ, mK, mV, mW, pa);

@@ -413,35 +413,6 @@ def test_segment_partition_matches_oracle(cuda, G, N):
             assert max_abs(a_[gi:gi + 1], b_) <= 2e-2
 
 
-@pytest.mark.gpu
-def test_fused_backward_schedule_matches_separate(cuda):
-    """la_tuning.bwd_fused = 1 (k_bwd_fused: aggregate units and sweeps in one ticket-scheduled
-    grid) computes the same gradients as the two-launch default. Not bitwise: with many unit
-    records the default forms the segment carries in one scan launch (seg_scan), summing the
-    R suffix in another fp32 order than the fused sweeps' prologue; they agree to bf16 rounding."""
-    import torch
-    import paper_2510_21956_b200 as la
-    from tests._util import fast_inputs
-    G, N, D = 8, 4096, 128
-    q, k, v, w = fast_inputs(G, N, D, seed=7)
-    t = [torch.as_tensor(x).to(torch.bfloat16).to(cuda) for x in (q, k, v, w)]
-    L = la.Layout
-    hq, hk = la.HeadTensor.from_logical(t[0], L.SequenceMajor), la.HeadTensor.from_logical(t[1], L.SequenceMajor)
-    hv, hw = la.HeadTensor.from_logical(t[2], L.FeatureMajor), la.HeadTensor.from_logical(t[3], L.FeatureMajor)
-    art = la.forward_causal(hq, hk, hv)
-    from paper_2510_21956_b200 import _abi
-    g0 = la.backward_causal(art, hw)
-    _abi.set_tuning(bwd_fused=1)
-    try:
-        g1 = la.backward_causal(art, hw)
-    finally:
-        _abi.set_tuning()
-    torch.cuda.synchronize()
-    for a_, b_ in ((g0.dq, g1.dq), (g0.dk, g1.dk), (g0.dv, g1.dv)):
-        x, y = a_.data.float(), b_.data.float()
-        assert (x - y).abs().max().item() <= 8e-3 * max(1.0, y.abs().max().item())
-
-
 @pytest.mark.parametrize("causal", [True, False])
 @pytest.mark.parametrize("a,b", [(0.5, 2.0), (1.0, 0.0), (2.0, 0.25)])
 def test_tcgen05_kernel_coefficients(cuda, causal, a, b):

@@ -1,6 +1,6 @@
 """Small causal + non-causal fwd/bwd through the public API, for compute-sanitizer runs:
 compute-sanitizer --tool racecheck --kernel-regex kns=_tc python tools/sanitize_run.py
-(also exercises the opt-in fused backward and the prologue / term-pass kernels)"""
+(also exercises the prologue / term-pass kernels)"""
 import os
 import sys
 
@@ -18,11 +18,6 @@ for causal in (True, False):
     hv, hw = T(v, la.Layout.FeatureMajor), T(w, la.Layout.FeatureMajor)
     art = (la.forward_causal if causal else la.forward_full)(hq, hk, hv)
     (la.backward_causal if causal else la.backward_full)(art, hw)
-    if causal:  # the opt-in fused backward schedule (k_bwd_fused)
-        from paper_2510_21956_b200 import _abi
-        _abi.set_tuning(bwd_fused=1)
-        la.backward_causal(art, hw)
-        _abi.set_tuning()
 # prologue / diagnostics kernels (la_prologue.cu)
 hq2, hk2 = la.normalize_qk(hq, hk)
 hw_hat = la.make_omega_hat(hw, art.g)
