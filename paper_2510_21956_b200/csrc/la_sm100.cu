@@ -94,8 +94,10 @@ constexpr int kCF = 64;                  // forward chunk rows
 constexpr int kFT = 16384;               // 64x128 / 128x64 16-bit tile
 constexpr int kKPanel = 80 * 128;        // K-tile panel: 64 key rows + 16 z rows
 constexpr int kFStages = 3;
-constexpr int kFPrefetch = 0;            // L2 prefetch distance (chunks) ahead of the ring: measured
-                                         // to cost extra DRAM re-reads at 148 CTAs, so off (LA_PREFETCH)
+constexpr int kFPrefetch = 0;            // L2 prefetch distance (chunks). 0: each chunk is prefetched
+                                         // into L2 just before the producer waits for its ring slot
+                                         // (sweep 0.76 -> 0.72 ms, bwd aggregate 0.69 -> 0.64 ms
+                                         // against no prefetch); >= 1 costs extra DRAM re-reads
 constexpr int kFStage = kFT + 2 * kKPanel + kFT;  // Q, K(+z), V^T  = 52 KB
 constexpr int kOffK = kFT, kOffV = kFT + 2 * kKPanel;
 constexpr uint32_t kF_T1 = 0, kF_OT = 128, kF_ST = 256, kF_SB = 384;

@@ -45,7 +45,7 @@ constexpr int kCB = 64;   // chunk rows
 constexpr int kD = 128;   // head dim
 constexpr int kT64 = 16384;  // a 64x128 or 128x64 16-bit tile
 constexpr int kStage = 4 * kT64;  // Q, K, V^T, Omega^T
-constexpr int kBPrefetch = 0;     // L2 prefetch distance (chunks): off by default, see la_sm100.cu
+constexpr int kBPrefetch = 0;     // L2 prefetch distance (chunks); 0 = the chunk itself, before the slot wait (la_sm100.cu)
 constexpr uint32_t kDP = 0, kDQ = 64, kDK = 128, kDV = 192, kR = 256, kS = 384;
 constexpr uint32_t kHalf = 16u << 16;  // TMEM lane offset of the upper M=64 half
 
