@@ -149,8 +149,14 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
     if (elect_one()) {
       for (int c = 0; c < nc; ++c) {
         const int s = c % NS;
-        if (c >= NS) mbar_wait(&empty[s], ((c / NS) & 1) ^ 1);
         const int64_t row0 = r0 + (int64_t)c * CR;
+        if (!kQW || D <= 64) {  // into L2 before the slot wait (measured: helps the K/V pass at
+                                // every D, the Q/W/O pass only at D = 64)
+          tma_prefetch_l2_3d(&tmX, 0, (int)(grp * prm.N + row0), 0);
+          tma_prefetch_l2_3d(&tmY, 0, (int)(grp * D), (int)(row0 / 64));
+          if (kQW) tma_prefetch_l2_3d(&tmO, 0, (int)(grp * D), (int)(row0 / 64));
+        }
+        if (c >= NS) mbar_wait(&empty[s], ((c / NS) & 1) ^ 1);
         uint8_t* st = smem + s * STAGE;
         mbar_expect_tx(&full[s], NT * T + (kQW ? CR * 4 : 0));
         tma_load_3d(st, &tmX, &full[s], 0, (int)(grp * prm.N + row0), 0);
@@ -441,8 +447,8 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
     if (elect_one()) {
       for (int c = 0; c < nc; ++c) {
         const int s = c % NS;
-        if (c >= NS) mbar_wait(&empty[s], ((c / NS) & 1) ^ 1);
         const int64_t row0 = s0 + (int64_t)c * CR;
+        if (c >= NS) mbar_wait(&empty[s], ((c / NS) & 1) ^ 1);
         uint8_t* st = smem + s * STAGE;
         mbar_expect_tx(&full[s], T + (kMode == kDQ ? 2 * CR * 4 : 0));
         if (kSeqIn)

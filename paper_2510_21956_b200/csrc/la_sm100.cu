@@ -599,8 +599,10 @@ __global__ void __launch_bounds__(192, 1)
     if (elect_one()) {
       for (int c = 0; c < nc; ++c) {
         const int s = c & 1;
-        if (c >= 2) mbar_wait(&empty[s], ((c >> 1) & 1) ^ 1);
         const int64_t row0 = s0 + (int64_t)c * kC;
+        tma_prefetch_l2_3d(&tmK, 0, (int)(grp * N + row0), 0);  // before the slot wait (kFPrefetch)
+        tma_prefetch_l2_3d(&tmV, 0, (int)(grp * kD), (int)(row0 / 64));
+        if (c >= 2) mbar_wait(&empty[s], ((c >> 1) & 1) ^ 1);
         uint8_t* st = smem + s * kAggStage;
         mbar_expect_tx(&full[s], 2 * kTile);
         tma_load_3d(st, &tmK, &full[s], 0, (int)(grp * N + row0), 0);
@@ -775,6 +777,7 @@ __global__ void __launch_bounds__(192, 1)
     if (elect_one()) {
       for (int c = 0; c < nc; ++c) {
         const int s = c % kQStages;
+        tma_prefetch_l2_3d(&tmQ, 0, (int)(grp * prm.N + s0 + (int64_t)c * kCF), 0);  // before the slot wait
         if (c >= kQStages) mbar_wait(&empty[s], ((c / kQStages) & 1) ^ 1);
         mbar_expect_tx(&full[s], kFT);
         tma_load_3d(smem + s * kFT, &tmQ, &full[s], 0, (int)(grp * prm.N + s0 + (int64_t)c * kCF), 0);
