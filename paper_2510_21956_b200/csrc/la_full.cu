@@ -641,7 +641,7 @@ template <int D>
 constexpr size_t totals_smem(bool qw) {
   using F = FG<D>;
   const int stage = ((qw ? 3 : 2) * F::T + F::CR * 4 + 1023) & ~1023;
-  const int ns = stage <= 56 * 1024 ? 3 : 2;
+  const int ns = F::kTotStages ? F::kTotStages : stage <= 56 * 1024 ? 3 : 2;  // as k_full_totals
   return (size_t)ns * stage + 6 * F::CR * 4 + 16 * 8 + 1024;
 }
 template <int D>
@@ -649,6 +649,25 @@ constexpr size_t apply_smem(int mode) {
   using F = FG<D>;
   const int stage = (F::T + (mode == kDQ ? 2 * F::CR * 4 : 0) + 1023) & ~1023;
   return (size_t)3 * stage + 2 * F::T + (D + 8 * F::CR) * 4 + 17 * 8 + 1024;
+}
+
+// CTAs of a kernel resident per SM: its __launch_bounds__ minimum and the 228 KB of shared
+// memory (1 KB of it reserved per CTA).
+constexpr int ctas_per_sm(int launch_min, size_t smem) {
+  const int by_smem = (int)(233472 / (smem + 1024));
+  return by_smem < launch_min ? (by_smem < 1 ? 1 : by_smem) : launch_min;
+}
+// Pieces per group for G groups of `chunks` chunks over `slots` resident CTAs: minimises
+// waves x (chunks per piece + 2), the 2 standing for a CTA's fixed cost (prologue, ring
+// fill, records). A grid of 1.3 waves (576 CTAs on 444 slots) costs as much as 2 full ones.
+inline int64_t pieces(int64_t G, int64_t chunks, int64_t slots, int64_t cap) {
+  int64_t best = 1, best_cost = INT64_MAX;
+  for (int64_t u = 1; u <= std::min(chunks, cap); ++u) {
+    const int64_t waves = (G * u + slots - 1) / slots, per = (chunks + u - 1) / u;
+    const int64_t cost = waves * (per + 2);
+    if (cost < best_cost) best = u, best_cost = cost;
+  }
+  return best;
 }
 
 // geometry of the totals units and the apply segments
@@ -659,11 +678,14 @@ struct Plan {
   int P;
   int64_t seg_rows;
   Plan(int64_t G, int64_t N) {
-    const int64_t CR = FG<D>::CR, chunks = std::max<int64_t>(1, N / CR);  // sizing queries: any N
-    int64_t u = std::max<int64_t>(1, std::min<int64_t>(chunks, (2 * 148 + G - 1) / G));
+    using F = FG<D>;
+    const int64_t CR = F::CR, chunks = std::max<int64_t>(1, N / CR);  // sizing queries: any N
+    const int tot_ctas = std::min(ctas_per_sm(F::kCtas, totals_smem<D>(false)), ctas_per_sm(F::kCtas, totals_smem<D>(true)));
+    const int app_ctas = std::min(ctas_per_sm(F::kCtas, apply_smem<D>(kFwd)), ctas_per_sm(F::kCtas, apply_smem<D>(kDQ)));
+    const int64_t u = pieces(G, chunks, 148 * tot_ctas, 64);
     unit_rows = ((chunks + u - 1) / u) * CR;
     U = (int)((N + unit_rows - 1) / unit_rows);
-    int64_t p2 = std::max<int64_t>(1, std::min<int64_t>(chunks, (4 * 148 + G / 2) / G));
+    int64_t p2 = pieces(G, chunks, 148 * app_ctas, 64);
     if (tuning().full_ctas_fwd > 0) p2 = std::min<int64_t>(chunks, tuning().full_ctas_fwd);
     seg_rows = ((chunks + p2 - 1) / p2) * CR;
     P = (int)((N + seg_rows - 1) / seg_rows);
