@@ -50,11 +50,14 @@ def run(name, B, H, N, D, dtype, causal, shard=False, reps=5):
 
     def step():
         if shard:
-            s1 = L.la_forward_sharded(C.byref(p), C.byref(sh), q.data_ptr(), 1, k.data_ptr(), 1, v.data_ptr(), 0,
-                                      out.data_ptr(), g.data_ptr(), wsf.data_ptr(), wsf.numel(), st, None)
-            s2 = L.la_backward_sharded(C.byref(p), C.byref(sh), q.data_ptr(), 1, k.data_ptr(), 1, v.data_ptr(), 0,
-                                       out.data_ptr(), w.data_ptr(), 0, g.data_ptr(), dq.data_ptr(), dk.data_ptr(),
-                                       dv.data_ptr(), wsb.data_ptr(), wsb.numel(), st, None)
+            # as la_sharded_forward / _backward run it (la_dist.cu): the forward's states saved
+            s1 = L.la_forward_sharded_save(C.byref(p), C.byref(sh), q.data_ptr(), 1, k.data_ptr(), 1, v.data_ptr(),
+                                           0, out.data_ptr(), g.data_ptr(), sv.data_ptr(), sv.numel(),
+                                           wsf.data_ptr(), wsf.numel(), st, None)
+            s2 = L.la_backward_sharded_saved(C.byref(p), C.byref(sh), q.data_ptr(), 1, k.data_ptr(), 1,
+                                             v.data_ptr(), 0, out.data_ptr(), w.data_ptr(), 0, g.data_ptr(),
+                                             sv.data_ptr(), sv.numel(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                                             wsb.data_ptr(), wsb.numel(), st, None)
         else:
             s1 = L.la_forward_save(C.byref(p), q.data_ptr(), 1, k.data_ptr(), 1, v.data_ptr(), 0, out.data_ptr(),
                                    g.data_ptr(), sv.data_ptr(), sv.numel(), wsf.data_ptr(), wsf.numel(), st, None)
