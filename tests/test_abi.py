@@ -151,3 +151,26 @@ def test_sass_has_tcgen05_and_tma_instructions():
     sass = subprocess.run([exe, "-sass", _abi.LIB_PATH], capture_output=True, text=True).stdout
     for op in ("UTCHMMA", "LDTM", "STTM", "UTMALDG", "UTMASTG"):
         assert op in sass, op
+
+
+def test_tuning_struct_mirrors_the_header():
+    """_abi.Tuning has la_tuning's fields in the header's order, and la_set_tuning /
+    la_get_tuning round-trip it (host-only calls)."""
+    src = open(os.path.join(ROOT, "include", "la_cuda.h")).read()
+    body = re.search(r"typedef struct \{([^}]*)\} la_tuning;", src).group(1)
+    fields = re.findall(r"int32_t\s+(\w+);", body)
+    assert [f for f, _ in _abi.Tuning._fields_] == fields
+    L = _abi.lib()
+    t = _abi.Tuning()
+    for i, (f, _) in enumerate(_abi.Tuning._fields_):
+        setattr(t, f, i + 1)
+    L.la_set_tuning(C.byref(t))
+    try:
+        r = _abi.Tuning()
+        L.la_get_tuning(C.byref(r))
+        assert [getattr(r, f) for f, _ in r._fields_] == [i + 1 for i in range(len(fields))]
+    finally:
+        L.la_set_tuning(None)
+    r = _abi.Tuning()
+    L.la_get_tuning(C.byref(r))
+    assert all(getattr(r, f) == 0 for f, _ in r._fields_)
