@@ -351,6 +351,20 @@ struct ApplyParams {
 //   kDV:  W[j][m] = b R[m][j],  Y = K (K-major),            dV^T = acc + a c_j
 template <int D>
 constexpr int apply_wgs(int mode) { return mode == 1 ? FG<D>::NH : 1; }  // kDQ: a warpgroup per half
+// D = 64: chunks are applied in pairs, with W block-diagonal in TMEM ([W 0; 0 W], K = 128) so
+// that one M = 128 MMA writes chunk c to lanes 0..63 and chunk c + 1 to lanes 64..127 and
+// every epilogue lane has a row to drain (a single chunk would leave lanes 64..127 empty).
+#ifndef LA_D64_PAIR
+#define LA_D64_PAIR 1
+#endif
+// Measured: the passes with a CUDA-core pre-pass (kFwd 0.119 -> 0.099 ms, kDQ 0.204 -> 0.159 ms
+// at config 4) gain; dK^T (0.102 -> 0.110) does not, so kDK / kDV stay one chunk per MMA.
+template <int D>
+constexpr bool apply_pairs(int mode) { return LA_D64_PAIR && D == 64 && (mode == 0 || mode == 1); }
+template <int D>
+constexpr int apply_stages(int mode) { return apply_pairs<D>(mode) ? 4 : 3; }
+template <int D>
+constexpr int apply_slots(int mode) { return apply_pairs<D>(mode) ? 4 : 2; }  // staging tiles; 1/g, s slots
 
 template <int D, bool kBF16, int kMode>
 __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
@@ -361,17 +375,18 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
   constexpr bool kSeqIn = kMode == kFwd || kMode == kDV;  // Y tile [CR][D] (else [D][CR])
   constexpr bool kPre = kMode == kFwd || kMode == kDQ;    // CUDA-core pass over the tile first
   constexpr int STAGE = (T + (kMode == kDQ ? 2 * CR * 4 : 0) + 1023) & ~1023;  // + g, s of the chunk
-  constexpr int NS = 3;
+  constexpr bool kPair = apply_pairs<D>(kMode);
+  constexpr int NS = apply_stages<D>(kMode), kSl = apply_slots<D>(kMode);
   constexpr int RPT = (D + 127) / 128;
   constexpr int kWG = apply_wgs<D>(kMode), kCT = 128 * kWG;  // compute warpgroups (kDQ: one per half)
   constexpr uint32_t kAcc = F::kAccApp;  // accumulators: 2 buffers x NH halves x CR columns after W
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint8_t* stg = smem + NS * STAGE;              // [2][T] output staging
-  float* zf = (float*)(stg + 2 * T);             // [D] z (kFwd)
-  float* ginv = zf + D;                          // [2][CR] 1 / g_i (kFwd, kDQ)
-  float* sbuf = ginv + 2 * CR;                   // [2][CR] s_i (kDQ)
-  float* part = sbuf + 2 * CR;                   // [4][CR] (kFwd: partial q.z)
+  uint8_t* stg = smem + NS * STAGE;              // [kSl][T] output staging
+  float* zf = (float*)(stg + kSl * T);           // [D] z (kFwd)
+  float* ginv = zf + D;                          // [kSl][CR] 1 / g_i (kFwd, kDQ)
+  float* sbuf = ginv + kSl * CR;                 // [kSl][CR] s_i (kDQ)
+  float* part = sbuf + kSl * CR;                 // [4][CR] (kFwd: partial q.z)
   uint64_t* bars = (uint64_t*)(part + 4 * CR);
   uint64_t* full = bars;        // [NS]
   uint64_t* empty = bars + 4;   // [NS]
@@ -418,7 +433,7 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
     const float b = prm.b;
 #pragma unroll 1
     for (int h = wg; h < NH; h += kWG) {
-      const int f = 128 * h + r;
+      const int f = kPair ? (r & 63) : 128 * h + r;
 #pragma unroll 1
       for (int k0 = 0; k0 < D; k0 += 64) {
         uint32_t pk[32];
@@ -432,7 +447,15 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
           }
           pk[c] = pack2<kBF16>(w0, w1);
         }
-        tmem_st32(tmem + lb + h * (D / 2) + k0 / 2, pk);
+        if (kPair) {  // block-diagonal: lanes 0..63 take K 0..63, lanes 64..127 take K 64..127
+          uint32_t zr[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) zr[c] = 0u;
+          tmem_st32(tmem + lb, r < 64 ? pk : zr);
+          tmem_st32(tmem + lb + 32, r < 64 ? zr : pk);
+        } else {
+          tmem_st32(tmem + lb + h * (D / 2) + k0 / 2, pk);
+        }
       }
     }
     tmem_st_wait();
@@ -464,6 +487,30 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
   } else if (warp == 1) {
     constexpr uint32_t fmt = kBF16 ? 1 : 0;
     const uint32_t id = idesc_f16(128, CR, fmt, 0, kSeqIn ? 0 : 1);
+    if (kPair) {
+      for (int c = 0; c < nc; c += 2) {  // chunks c, c1 (c1 = c for an odd last chunk)
+        const int c1 = c + 1 < nc ? c + 1 : c, sa = c % NS, sb = c1 % NS;
+        const uint32_t aY0 = smem_u32(smem + sa * STAGE), aY1 = smem_u32(smem + sb * STAGE);
+        mbar_wait(&full[sa], (c / NS) & 1);
+        if (kMode == kDQ) mbar_wait(&pre[sa], (c / NS) & 1);
+        mbar_wait(&full[sb], (c1 / NS) & 1);
+        if (kMode == kDQ) mbar_wait(&pre[sb], (c1 / NS) & 1);
+        if (c >= 2) mbar_wait(&acc_empty[0], ((c / 2) & 1) ^ 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < 2 * F::KS; ++ks) {
+            const uint32_t aY = ks < F::KS ? aY0 : aY1;
+            const int kk = ks % F::KS;
+            mma_ts(tmem + kAcc, tmem + ks * 8, kSeqIn ? kmaj(aY, kk, CR) : mnmaj(aY, kk, D * 128), id, ks > 0);
+          }
+          mma_commit(&acc_full[0]);
+          mma_commit(&empty[sa]);
+          if (c1 != c) mma_commit(&empty[sb]);
+        }
+        __syncwarp();
+      }
+    } else
     for (int c = 0; c < nc; ++c) {
       const int s = c % NS, bb = c % F::kAccBufs;
       const uint32_t aY = smem_u32(smem + s * STAGE);
@@ -488,7 +535,7 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
     float bias[RPT];  // per output feature of this thread's lanes: a sigma_j, -b u_m, a c_j, b z_m
 #pragma unroll
     for (int h = 0; h < RPT; ++h) {
-      const int f = 128 * h + r;
+      const int f = kPair ? (r & 63) : 128 * h + r;
       float x = 0.f;
       if (f < D) {
         if (kMode == kFwd) x = a * tot[D * D + D + f];
@@ -525,7 +572,7 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
         if (part_k == 0) {
           const float gi = a * (float)prm.n_total + b * acc;
           if (fabsf(gi) < kEpsF32) flag_degenerate(prm.flag, grp, row0 + i);
-          ginv[(c & 1) * CR + i] = __frcp_rn(gi);
+          ginv[(c % kSl) * CR + i] = __frcp_rn(gi);
           prm.gout[grp * prm.N + row0 + i] = gi;
         }
         mbar_arrive(&empty[s]);  // Q tile no longer read by the CUDA cores
@@ -533,12 +580,12 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
         const float* gg = (const float*)(st + T);
         const float* ss = gg + CR;
         if (et < CR) {
-          ginv[(c & 1) * CR + et] = __frcp_rn(gg[et]);
-          sbuf[(c & 1) * CR + et] = ss[et];
+          ginv[(c % kSl) * CR + et] = __frcp_rn(gg[et]);
+          sbuf[(c % kSl) * CR + et] = ss[et];
         }
         named_bar(1, kCT);
         // (jg, ig) tiling: rows j = jg + 16 rr (rr = wg mod kWG), the 16-byte column chunk ig
-        const float* gi = ginv + (c & 1) * CR;
+        const float* gi = ginv + (c % kSl) * CR;
         const int e = et & 127, jg = e & 15, ig = e >> 4;
         const float4 ga = *(const float4*)(gi + 8 * ig), gb = *(const float4*)(gi + 8 * ig + 4);
         const float g8[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
@@ -559,24 +606,29 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
         mbar_arrive(&empty[s]);
       }
     };
+    // kPair: c is the first chunk of a pair; lanes 64..127 hold chunk c + 1
     auto epilogue = [&](int c) {
-      const int bb = c % F::kAccBufs, sb = c & 1;  // accumulator buffer, staging buffer
+      const int bb = kPair ? 0 : c % F::kAccBufs;
+      const int gi2 = kPair ? c / 2 : c;  // MMA group
+      const int cc = kPair ? c + (r >> 6) : c;  // this lane's chunk
+      const int sb = cc % kSl;  // 1/g, s slot of the chunk
+      const int tb = kPair ? (gi2 & 1) * 2 + (r >> 6) : (c & 1);  // staging tile
       const int64_t row0 = s0 + (int64_t)c * CR;
-      mbar_wait(&acc_full[bb], (c / F::kAccBufs) & 1);
+      mbar_wait(&acc_full[bb], (gi2 / F::kAccBufs) & 1);
       tc_fence_after();
-      if (et == 0) tma_store_wait_read1();  // the store that used staging sb two chunks ago
+      if (et == 0) tma_store_wait_read1();  // the store group that used these staging tiles
       named_bar(1, kCT);
-      uint8_t* so = stg + sb * T;
+      uint8_t* so = stg + tb * T;
 #pragma unroll 1
       for (int h = wg; h < NH; h += kWG) {
-        const int f = 128 * h + r;
+        const int f = kPair ? (r & 63) : 128 * h + r;
         const float bh = h == 0 ? bias[0] : bias[RPT - 1];
 #pragma unroll 1
         for (int c0 = 0; c0 < CR; c0 += 32) {
           uint32_t x[32];
           tmem_ld32(tmem + lb + kAcc + (bb * NH + h) * CR + c0, x);
           tmem_ld_wait();
-          if (f < D) {
+          if (f < D && cc < nc) {
             if (kMode == kDQ) {  // dQ[i][f]: SequenceMajor staging [CR][D]; lanes f, f ^ 1 trade
               const float* sv = sbuf + sb * CR + c0;  // values: even lanes store (f, f+1) of row i,
               const bool odd = (lane_id() & 1) != 0;   // odd lanes (f-1, f) of row i + 1
@@ -619,16 +671,31 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
       fence_proxy_async();
       named_bar(1, kCT);
       if (et == 0) {
-        if (kMode == kDQ)
-          tma_store_3d(&tmOut, so, 0, (int)(grp * prm.N + row0), 0);
-        else
-          tma_store_3d(&tmOut, so, 0, (int)(grp * D), (int)(row0 / 64));
+#pragma unroll 1
+        for (int k = 0; k < (kPair ? 2 : 1) && c + k < nc; ++k) {
+          const uint8_t* sk = kPair ? stg + ((gi2 & 1) * 2 + k) * T : so;
+          if (kMode == kDQ)
+            tma_store_3d(&tmOut, sk, 0, (int)(grp * prm.N + row0 + k * CR), 0);
+          else
+            tma_store_3d(&tmOut, sk, 0, (int)(grp * D), (int)((row0 + k * CR) / 64));
+        }
         tma_store_commit();
       }
     };
-    for (int c = 0; c <= nc; ++c) {
-      if (kPre && c < nc) pre_pass(c);
-      if (c >= 1) epilogue(c - 1);
+    if (kPair) {
+      for (int c = 0; c < nc; c += 2) {
+        if (kPre) {
+          pre_pass(c);
+          if (c + 1 < nc) pre_pass(c + 1);
+        }
+        if (c >= 2) epilogue(c - 2);
+      }
+      if (nc > 0) epilogue((nc - 1) & ~1);
+    } else {
+      for (int c = 0; c <= nc; ++c) {
+        if (kPre && c < nc) pre_pass(c);
+        if (c >= 1) epilogue(c - 1);
+      }
     }
     if (et == 0) tma_store_wait0();
   }
@@ -648,7 +715,8 @@ template <int D>
 constexpr size_t apply_smem(int mode) {
   using F = FG<D>;
   const int stage = (F::T + (mode == kDQ ? 2 * F::CR * 4 : 0) + 1023) & ~1023;
-  return (size_t)3 * stage + 2 * F::T + (D + 8 * F::CR) * 4 + 17 * 8 + 1024;
+  const int sl = apply_slots<D>(mode);
+  return (size_t)apply_stages<D>(mode) * stage + sl * F::T + (D + (2 * sl + 4) * F::CR) * 4 + 17 * 8 + 1024;
 }
 
 // CTAs of a kernel resident per SM: its __launch_bounds__ minimum and the 228 KB of shared

@@ -187,6 +187,23 @@ def test_bf16_noncausal_head_dim_sweep(cuda, D):
     assert rel_err(res["g"], ref["g"]) <= 1e-3
 
 
+@pytest.mark.parametrize("ctas", [5, 3])
+def test_noncausal_d64_paired_chunks_odd_segments(cuda, ctas):
+    """D = 64 applies chunks in pairs (block-diagonal W, la_full.cu apply_pairs): segments of
+    7 and 4 chunks (ctas = 5) or 11 and 10 (ctas = 3) cover odd tails and several pairs."""
+    from paper_2510_21956_b200 import _abi
+    q, k, v, w = fast_inputs(2, 2048, 64, seed=11 + ctas)
+    _abi.set_tuning(full_ctas_fwd=ctas)
+    try:
+        res = run_dev(q, k, v, w, "bf16", cuda, causal=False)
+    finally:
+        _abi.set_tuning()
+    ref = oracle_all(res, False)
+    for key in ("out", "dq", "dk", "dv"):
+        assert max_abs(res[key], ref[key]) <= BF16_ABS, key
+    assert rel_err(res["g"], ref["g"]) <= 1e-3
+
+
 @pytest.mark.parametrize("D,a,b", [(256, 1.0, 1.0), (64, 0.5, 2.0), (192, 2.0, 0.25)])
 def test_noncausal_full_tc_path_runs_and_matches(cuda, D, a, b):
     """Non-causal D = 64 / 192 / 256 runs the tcgen05 kernels of la_full.cu (profile scopes:
