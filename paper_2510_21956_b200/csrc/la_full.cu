@@ -437,15 +437,26 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
 #pragma unroll 1
       for (int k0 = 0; k0 < D; k0 += 64) {
         uint32_t pk[32];
+        if (kTrans) {  // W[f][k] = b X[k][f]: lanes f read consecutive addresses
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          float w0 = 0.f, w1 = 0.f;
-          if (f < D) {
-            const int k = k0 + 2 * c;
-            w0 = b * (kTrans ? tot[(int64_t)k * D + f] : tot[(int64_t)f * D + k]);
-            w1 = b * (kTrans ? tot[(int64_t)(k + 1) * D + f] : tot[(int64_t)f * D + k + 1]);
+          for (int c = 0; c < 32; ++c) {
+            float w0 = 0.f, w1 = 0.f;
+            if (f < D) {
+              const int k = k0 + 2 * c;
+              w0 = b * tot[(int64_t)k * D + f];
+              w1 = b * tot[(int64_t)(k + 1) * D + f];
+            }
+            pk[c] = pack2<kBF16>(w0, w1);
           }
-          pk[c] = pack2<kBF16>(w0, w1);
+        } else {  // W[f][k] = b X[f][k]: row f of the record, 16-byte loads (the scalar ones
+                  // were 14 % of the D = 256 dQ pass)
+#pragma unroll
+          for (int c4 = 0; c4 < 16; ++c4) {
+            float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (f < D) w = *(const float4*)(tot + (int64_t)f * D + k0 + 4 * c4);
+            pk[2 * c4] = pack2<kBF16>(b * w.x, b * w.y);
+            pk[2 * c4 + 1] = pack2<kBF16>(b * w.z, b * w.w);
+          }
         }
         if (kPair) {  // block-diagonal: lanes 0..63 take K 0..63, lanes 64..127 take K 64..127
           uint32_t zr[32];
@@ -630,8 +641,13 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
           tmem_ld_wait();
           if (f < D && cc < nc) {
             if (kMode == kDQ) {  // dQ[i][f]: SequenceMajor staging [CR][D]; lanes f, f ^ 1 trade
-              const float* sv = sbuf + sb * CR + c0;  // values: even lanes store (f, f+1) of row i,
-              const bool odd = (lane_id() & 1) != 0;   // odd lanes (f-1, f) of row i + 1
+              float sv[32];  // s_i of the 32 rows, 16-byte shared loads (not 32 scalar ones)
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const float4 s4 = *(const float4*)(sbuf + sb * CR + c0 + 4 * q);
+                sv[4 * q] = s4.x; sv[4 * q + 1] = s4.y; sv[4 * q + 2] = s4.z; sv[4 * q + 3] = s4.w;
+              }
+              const bool odd = (lane_id() & 1) != 0;  // even lanes store (f, f+1) of row i, odd lanes (f-1, f) of row i + 1
 #pragma unroll
               for (int k = 0; k < 32; k += 2) {
                 const float v0 = __uint_as_float(x[k]) - bh * sv[k], v1 = __uint_as_float(x[k + 1]) - bh * sv[k + 1];
