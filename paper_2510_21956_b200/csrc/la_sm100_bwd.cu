@@ -1186,7 +1186,7 @@ __global__ void __launch_bounds__(320, 1)
     const float* src = t < 128 ? tR : tS;
     uint8_t* dst = t < 128 ? sR : sS;
     const float b = prm.b;
-#pragma unroll 1
+#pragma unroll 4  // 8 loads in flight: the row of each lane is 512 B away from its neighbour's
     for (int j0 = 0; j0 < kD; j0 += 8) {
       const float4 x0 = *(const float4*)(src + r * kD + j0), x1 = *(const float4*)(src + r * kD + j0 + 4);
       *(uint4*)(dst + sw128_off(r, j0, 128)) =
