@@ -9,6 +9,8 @@
 #include <mutex>
 #include <unordered_map>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a tool (nsys / ncu --nvtx) injects
+
 #include "../../include/la_cuda.h"
 #include "internal.h"
 
@@ -30,7 +32,11 @@ static std::mutex g_prof_mu;
 static bool g_prof_on = false;
 static std::vector<ProfRec> g_prof;
 
+// Every kernel scope is also an NVTX range (SURVEY §5 "tracing": the reference's
+// ws::set_phase names, forward_kernels.hpp:218,238 / backward_kernels.hpp:303-372, map
+// to the phase ranges of forward_impl / backward_impl; these are the kernels under them).
 ProfScope::ProfScope(const char* name, cudaStream_t s) : idx(-1), stream(s) {
+  nvtxRangePushA(name);
   std::lock_guard<std::mutex> lk(g_prof_mu);
   if (!g_prof_on) return;
   ProfRec r;
@@ -42,6 +48,7 @@ ProfScope::ProfScope(const char* name, cudaStream_t s) : idx(-1), stream(s) {
   idx = (int)g_prof.size() - 1;
 }
 ProfScope::~ProfScope() {
+  nvtxRangePop();
   if (idx < 0) return;
   std::lock_guard<std::mutex> lk(g_prof_mu);
   if (idx < (int)g_prof.size()) cudaEventRecord(g_prof[idx].b, stream);
@@ -310,10 +317,19 @@ void pad_copy(void* dst, const void* src, const la_problem* p, bool seq_major, b
   note_launch(1);
 }
 
+// Phase range of one public forward / backward call (the reference's ws::set_phase,
+// forward_kernels.hpp:218,238, backward_kernels.hpp:303,327,343,372, one level up: the
+// fused kernels compute those term phases together).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, la_layout lq,
                        const void* k, la_layout lk, const void* v, la_layout lv, void* out,
                        float* g, void* ws, size_t ws_bytes, void* stream, la_error_info* err,
                        void* saved = nullptr, size_t saved_bytes = 0, int64_t n_total = 0) {
+  NvtxRange phase(p && !p->causal ? "forward.full" : "forward.causal");
   la_status s = check_problem(p, err);
   if (s != LA_OK) return s;
   if (!q || !k || !v || !out || !g)
@@ -407,6 +423,7 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
                         const void* omega, la_layout lw, const float* g, void* dq, void* dk,
                         void* dv, void* ws, size_t ws_bytes, void* stream, la_error_info* err,
                         const void* saved = nullptr, size_t saved_bytes = 0, bool trust_saved = false) {
+  NvtxRange phase(p && !p->causal ? "backward.full" : "backward.causal");
   // check_backward_inputs (backward.cpp:13-28)
   if (p && (!o || !q || !k || !v))
     return fail(err, LA_ERR_MISSING_FORWARD_STATE,

@@ -13,6 +13,7 @@
 // path runs) on hosts without it; a caller-supplied all-gather can replace it.
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -100,6 +101,10 @@ DistWs carve(const la_problem* p, const la_dist* d, void* ws) {
 
 la_status all_gather(const la_dist* d, const float* send, float* recv, size_t count, void* stream,
                      la_error_info* err) {
+  struct Range {
+    Range() { nvtxRangePushA("sharded.all_gather"); }
+    ~Range() { nvtxRangePop(); }
+  } range;
   if (d->nccl_comm) {
     const NcclApi* api = nccl();
     if (!api) return fail(err, LA_ERR_UNSUPPORTED, "libnccl.so.2 not found");

@@ -174,3 +174,16 @@ def test_tuning_struct_mirrors_the_header():
     r = _abi.Tuning()
     L.la_get_tuning(C.byref(r))
     assert all(getattr(r, f) == 0 for f, _ in r._fields_)
+
+
+def test_library_carries_nvtx_phase_ranges():
+    # SURVEY §5 "tracing": every public forward / backward call is an NVTX range named
+    # after its phase (the reference's ws::set_phase, forward_kernels.hpp:218,238;
+    # backward_kernels.hpp:303-372), with one range per kernel under it (ProfScope) and one
+    # around the sequence-shard all-gather. NVTX v3 is header-only: the strings and the
+    # push/pop calls are in the library, inert unless a tool injects.
+    blob = open(_abi.LIB_PATH, "rb").read()
+    for name in (b"forward.causal", b"forward.full", b"backward.causal", b"backward.full",
+                 b"sharded.all_gather", b"la_bwd_causal", b"la_fwd_causal"):
+        assert name + b"\0" in blob, name
+    assert b"NVTX_INJECTION64_PATH" in blob
