@@ -266,6 +266,11 @@ __global__ void __launch_bounds__(192, FG<D>::kCtas)
           }
         }
       }
+      // The stage is refilled by TMA (async proxy) once this arrival completes the phase, and
+      // the arrive does not wait for this thread's outstanding shared loads: at D = 64 the last
+      // 16 rows of V^T were still being read when the next chunk landed (sigma_48..63 differed
+      // run to run, scratch/det_probe_c4.py). The proxy fence retires the generic reads first.
+      fence_proxy_async();
       mbar_arrive(&empty[s]);
     }
     // row sums: the 8 ig partials of each row j -> vrow (shared scratch: the stages are idle
@@ -586,6 +591,7 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
           ginv[(c % kSl) * CR + i] = __frcp_rn(gi);
           prm.gout[grp * prm.N + row0 + i] = gi;
         }
+        fence_proxy_async();     // the Q tile reads retire before the refill (see k_full_totals)
         mbar_arrive(&empty[s]);  // Q tile no longer read by the CUDA cores
       } else {  // kDQ: W_hat^T = Omega^T / g in place; keep 1/g, s for the epilogue
         const float* gg = (const float*)(st + T);
@@ -647,13 +653,17 @@ __global__ void __launch_bounds__(64 + 128 * apply_wgs<D>(kMode), FG<D>::kCtas)
                 const float4 s4 = *(const float4*)(sbuf + sb * CR + c0 + 4 * q);
                 sv[4 * q] = s4.x; sv[4 * q + 1] = s4.y; sv[4 * q + 2] = s4.z; sv[4 * q + 3] = s4.w;
               }
-              const bool odd = (lane_id() & 1) != 0;  // even lanes store (f, f+1) of row i, odd lanes (f-1, f) of row i + 1
+              // even lanes store (f, f+1) of row i, odd lanes (f-1, f) of row i + 4: rows whose
+              // indices differ in bit 2 take disjoint 16-byte chunk sets under the 128-byte
+              // swizzle, so the warp's 32 stores hit 32 distinct banks (rows i, i + 1 collide)
+              const bool odd = (lane_id() & 1) != 0;
 #pragma unroll
-              for (int k = 0; k < 32; k += 2) {
-                const float v0 = __uint_as_float(x[k]) - bh * sv[k], v1 = __uint_as_float(x[k + 1]) - bh * sv[k + 1];
+              for (int kk = 0; kk < 16; ++kk) {
+                const int k = (kk & 3) + ((kk >> 2) << 3);  // 0..3, 8..11, 16..19, 24..27
+                const float v0 = __uint_as_float(x[k]) - bh * sv[k], v1 = __uint_as_float(x[k + 4]) - bh * sv[k + 4];
                 const float got = __shfl_xor_sync(0xffffffffu, odd ? v0 : v1, 1);
                 const uint32_t w2 = odd ? pack2<kBF16>(got, v1) : pack2<kBF16>(v0, got);
-                *(uint32_t*)(so + sw128_off(c0 + k + (odd ? 1 : 0), f & ~1, CR)) = w2;
+                *(uint32_t*)(so + sw128_off(c0 + k + (odd ? 4 : 0), f & ~1, CR)) = w2;
               }
             } else {  // FeatureMajor staging [D][CR]: row f
               const float* gv = ginv + sb * CR + c0;

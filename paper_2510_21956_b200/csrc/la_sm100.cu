@@ -489,6 +489,7 @@ __global__ void __launch_bounds__(448, 1)
         const float2 f2 = unpack2<kBF16>(v4.z), f3 = unpack2<kBF16>(v4.w);
         vs += ((f0.x + f0.y) + (f1.x + f1.y)) + ((f2.x + f2.y) + (f3.x + f3.y));
       }
+      pin(vs);                 // the V(c) loads have returned before the stage is released
       mbar_arrive(&empty[s]);  // WG-B is done with V(c)
       const float asig = a * sigma;
       sigma += vs;

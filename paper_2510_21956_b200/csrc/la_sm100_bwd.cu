@@ -282,6 +282,9 @@ __global__ void __launch_bounds__(192, 1)
           cc += f2.x + f2.y;
         }
       }
+      pin(u);  // the stage's loads have returned before it is released
+      pin(z);
+      pin(cc);
       mbar_arrive(&empty[s]);
     }
     float* rS = prm.stS + (grp * prm.P + p) * state_floats(kD);

@@ -44,6 +44,11 @@ __device__ __forceinline__ void fence_barrier_init() {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Pin register values in program order: `pin(x)` before a consumer-release arrive forces the
+// loads that produce x to have returned before the arrive issues (the arrive itself does not
+// wait for outstanding shared loads, and the compiler may otherwise sink their consumers past
+// it, letting the producer's next TMA write land before a load has read the stage).
+__device__ __forceinline__ void pin(float& x) { asm volatile("" : "+f"(x)); }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
