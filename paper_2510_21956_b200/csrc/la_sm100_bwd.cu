@@ -674,7 +674,11 @@ __device__ __forceinline__ void bwd_main_body(const CUtensorMap& tmQ, const CUte
   if (threadIdx.x == 0) traceb(0, 63, 9);
 
   if (warp < 4) {
-  regs_dec<96>();
+#ifndef LA_BWD_REG_LO
+#define LA_BWD_REG_LO 96
+#define LA_BWD_REG_HI 136
+#endif
+  regs_dec<LA_BWD_REG_LO>();
 #ifdef LA_TRACE
   if (warp == 2 && lane_id() == 0) {  // observer: when each chunk's stage lands
     for (int n = 0; n < nc && n < 64; ++n) {
@@ -797,7 +801,7 @@ __device__ __forceinline__ void bwd_main_body(const CUtensorMap& tmQ, const CUte
     }
   }
   } else {
-  regs_inc<136>();
+  regs_inc<LA_BWD_REG_HI>();
   const uint32_t qd = warp & 3;
   const int l = (int)lane_id();
   const int r = (int)(qd * 32) + l;            // lane of the M=128 accumulators (j or m)
