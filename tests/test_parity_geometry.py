@@ -167,13 +167,14 @@ def test_config4_launch_geometry(cuda, D):
     check_groups(f"config4_G64_N32768_D{D}", t, res, [0, 63], causal=False)
 
 
-@pytest.mark.parametrize("D,causal", [(64, False), (256, False), (128, False), (128, True)])
+@pytest.mark.parametrize("D,causal", [(64, False), (256, False), (128, False), (128, True), (64, True), (256, True)])
 def test_run_to_run_bitwise_at_launch_geometry(cuda, D, causal):
     """Every tensor of a fwd+bwd step is bitwise the same over repeats at a full launch
     geometry (G = 64, many CTAs per SM). The small-size determinism test in test_parity_gpu
     cannot see a stage-release race: at D = 64 the non-causal K/V totals pass released its
     TMA stage while the last V^T loads were still outstanding, so sigma_48..63 changed run to
-    run at this geometry (fixed with a proxy fence before the arrive, la_full.cu)."""
+    run at this geometry (fixed with a proxy fence before the arrive, la_full.cu). Causal
+    D = 64 runs the D-padded tensor-core path, causal D = 256 the generic la_g16.cu sweep."""
     import torch
     N = 32768 if not causal else 16384
     t = device_inputs(64, N, D, seed=70 + D, cuda=cuda)
