@@ -215,7 +215,7 @@ cudaError_t g16_backward(const Launch& L, const Tensors& t, void* dq, void* dk, 
 cudaError_t offbyone_fix(const Launch& L, const Tensors& t, void* out, const float* g);
 
 // Non-causal tensor-core path for D = 64, 192, 256 (bf16/fp16, canonical layouts; la_full.cu).
-bool full_tc_supported(const Launch& L, const Tensors& t);
+bool full_tc_supported(const Launch& L, const Tensors& t, bool bwd);
 size_t full_ws_floats(int64_t G, int64_t N, int64_t D);
 cudaError_t full_forward(const Launch& L, const Tensors& t, void* out, float* g, Workspace ws);
 cudaError_t full_backward(const Launch& L, const Tensors& t, void* dq, void* dk, void* dv, Workspace ws);

@@ -389,8 +389,10 @@ la_status forward_impl(const la_problem* p, const la_shard* sh, const void* q, l
     return fail(err, LA_ERR_WORKSPACE, "saved-state buffer smaller than la_saved_state_bytes");
   cudaMemsetAsync(w.flag, 0xFF, sizeof(unsigned long long), L.stream);
   cudaError_t e;
-  const bool tc = use_tc(p, tc_forward_supported(L, t));
-  const bool full = !tc && p->impl != LA_IMPL_SIMT && full_tc_supported(L, t);
+  // la_full.cu first: it takes the non-causal shapes it supports (D = 64 / 128 / 192 / 256);
+  // the D = 128 canonical kernels take the rest of D = 128
+  const bool full = p->impl != LA_IMPL_SIMT && full_tc_supported(L, t, false);
+  const bool tc = !full && use_tc(p, tc_forward_supported(L, t));
   const bool gen = !tc && !full && p->impl != LA_IMPL_SIMT && g16_supported(L, t);
   const bool f32 = !tc && !full && p->impl != LA_IMPL_SIMT && f32tc_supported(L, t);
   if (saved) {
@@ -493,8 +495,10 @@ la_status backward_impl(const la_problem* p, const la_shard* sh, const void* q, 
   Launch L = make_launch(p, sh, stream);
   Tensors t{q, lq, k, lk, v, lv, o, LA_FEATURE_MAJOR, omega, lw, g};
   Workspace w = carve(ws, ws_bytes);
-  const bool tc = use_tc(p, tc_backward_supported(L, t));
-  const bool full = !tc && p->impl != LA_IMPL_SIMT && full_tc_supported(L, t);
+  // la_full.cu first: it takes the non-causal shapes it supports (D = 64 / 128 / 192 / 256);
+  // the D = 128 canonical kernels take the rest of D = 128
+  const bool full = p->impl != LA_IMPL_SIMT && full_tc_supported(L, t, true);
+  const bool tc = !full && use_tc(p, tc_backward_supported(L, t));
   const bool gen = !tc && !full && p->impl != LA_IMPL_SIMT && g16_supported(L, t);
   const bool f32 = !tc && !full && p->impl != LA_IMPL_SIMT && f32tc_supported(L, t);
   cudaMemsetAsync(w.flag, 0xFF, sizeof(unsigned long long), L.stream);

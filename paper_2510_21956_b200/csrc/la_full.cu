@@ -893,9 +893,15 @@ size_t ws_floats_d(int64_t G, int64_t N) {
 
 }  // namespace
 
-bool full_tc_supported(const Launch& L, const Tensors& t) {
+// Non-causal D = 128: the backward runs here (per-pass kernels: config 4 D = 128 backward
+// 1.13 -> 0.98 ms), the forward stays on the fused k_fwd_full_tc (0.37 ms against 0.48 ms for
+// the K/V totals + apply passes). The backward reads the totals that forward saved: the same
+// [S | z | sigma | count] records behind a P = -1 header.
+constexpr bool kFull128 = true;
+bool full_tc_supported(const Launch& L, const Tensors& t, bool bwd) {
   const int64_t cr = L.D <= 64 ? 128 : 64;
-  return !L.causal && (L.dtype == LA_BF16 || L.dtype == LA_F16) && (L.D == 64 || L.D == 192 || L.D == 256) &&
+  return !L.causal && (L.dtype == LA_BF16 || L.dtype == LA_F16) &&
+         (L.D == 64 || (kFull128 && bwd && L.D == 128) || L.D == 192 || L.D == 256) &&
          L.fault == LA_FAULT_NONE && L.carry_prefix == nullptr && L.carry_suffix == nullptr && L.row_offset == 0 &&
          L.N % cr == 0 && t.lq == LA_SEQUENCE_MAJOR && t.lk == LA_SEQUENCE_MAJOR && t.lv == LA_FEATURE_MAJOR &&
          (t.w == nullptr || t.lw == LA_FEATURE_MAJOR) && L.G * L.N < (1ll << 31) && L.G * L.D < (1ll << 31);
@@ -904,6 +910,7 @@ bool full_tc_supported(const Launch& L, const Tensors& t) {
 size_t full_ws_floats(int64_t G, int64_t N, int64_t D) {
   switch (D) {
     case 64: return ws_floats_d<64>(G, N);
+    case 128: return ws_floats_d<128>(G, N);
     case 192: return ws_floats_d<192>(G, N);
     case 256: return ws_floats_d<256>(G, N);
   }
@@ -924,6 +931,8 @@ cudaError_t full_backward(const Launch& L, const Tensors& t, void* dq, void* dk,
   const bool bf = L.dtype == LA_BF16;
   switch (L.D) {
     case 64: return bf ? backward_d<64, true>(L, t, dq, dk, dv, ws) : backward_d<64, false>(L, t, dq, dk, dv, ws);
+    case 128:
+      return bf ? backward_d<128, true>(L, t, dq, dk, dv, ws) : backward_d<128, false>(L, t, dq, dk, dv, ws);
     case 192:
       return bf ? backward_d<192, true>(L, t, dq, dk, dv, ws) : backward_d<192, false>(L, t, dq, dk, dv, ws);
     case 256:
