@@ -42,7 +42,8 @@ struct FG {
   // CTAs fit an SM's 512 columns (dQ pass 0.263 -> 0.192 ms at config 4)
   static constexpr bool k128 = D == 128;
   static constexpr int kCtas = D <= 64 ? 3 : k128 ? 2 : 1;
-  static constexpr int kTotStages = D <= 64 ? 2 : 0;         // 0: the stage-size rule of k_full_totals
+  // D = 128: a 2-stage ring (100 KB) lets two totals CTAs share an SM (R pass 0.324 -> 0.279 ms)
+  static constexpr int kTotStages = D <= 64 || D == 128 ? 2 : 0;  // 0: the stage-size rule of k_full_totals
   static constexpr int kAccBufs = D <= 64 ? 1 : 2;           // apply accumulators (D = 64: CTAs overlap)
   static constexpr uint32_t kTmemTot = D <= 64 ? 128 : k128 ? 256 : 512;  // totals: NH x 256-column blocks
   static constexpr uint32_t kTmemApp = D <= 64 ? 128 : k128 ? 256 : 512;  // apply: W + kAccBufs x NH x CR
