@@ -42,6 +42,9 @@ struct FG {
   // CTAs fit an SM's 512 columns (dQ pass 0.263 -> 0.192 ms at config 4)
   static constexpr bool k128 = D == 128;
   static constexpr int kCtas = D <= 64 ? 3 : k128 ? 2 : 1;
+  // totals CTAs per SM: at D = 64 four (4 x 128 TMEM columns; R pass 0.193 -> 0.173 ms). The
+  // apply passes stay at three: at four they spill and lose more than the totals gain.
+  static constexpr int kCtasTot = D <= 64 ? 4 : kCtas;
   // D = 128: a 2-stage ring (100 KB) lets two totals CTAs share an SM (R pass 0.324 -> 0.279 ms)
   static constexpr int kTotStages = D <= 64 || D == 128 ? 2 : 0;  // 0: the stage-size rule of k_full_totals
   static constexpr int kAccBufs = D <= 64 ? 1 : 2;           // apply accumulators (D = 64: CTAs overlap)
@@ -107,7 +110,7 @@ struct TotParams {
 // kQW = true:  X = Q, Y^T = W_hat^T = Omega^T / g (scaled in place), third tile O^T:
 //              R[m][j], u = sum s_i q_i, c = sum w_hat; s_i = o_i . w_hat_i -> s_out.
 template <int D, bool kBF16, bool kQW>
-__global__ void __launch_bounds__(192, FG<D>::kCtas)
+__global__ void __launch_bounds__(192, FG<D>::kCtasTot)
     k_full_totals(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY,
                   const __grid_constant__ CUtensorMap tmO, TotParams prm) {
   using F = FG<D>;
@@ -778,7 +781,8 @@ struct Plan {
   Plan(int64_t G, int64_t N) {
     using F = FG<D>;
     const int64_t CR = F::CR, chunks = std::max<int64_t>(1, N / CR);  // sizing queries: any N
-    const int tot_ctas = std::min(ctas_per_sm(F::kCtas, totals_smem<D>(false)), ctas_per_sm(F::kCtas, totals_smem<D>(true)));
+    const int tot_ctas =
+        std::min(ctas_per_sm(F::kCtasTot, totals_smem<D>(false)), ctas_per_sm(F::kCtasTot, totals_smem<D>(true)));
     const int app_ctas = std::min(ctas_per_sm(F::kCtas, apply_smem<D>(kFwd)), ctas_per_sm(F::kCtas, apply_smem<D>(kDQ)));
     const int64_t u = pieces(G, chunks, 148 * tot_ctas, 64);
     unit_rows = ((chunks + u - 1) / u) * CR;
